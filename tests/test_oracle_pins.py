@@ -1,0 +1,412 @@
+"""Pins for the CPU oracle (oracle/stree_oracle.c) — CPU only.
+
+Each pin checks the oracle against something other than itself: values the
+paper (or SPEC's worked examples) print, closed forms, the paper's matrix
+form re-derived here in numpy, the textbook Mamba-2 chain
+scan, invariants and brute force over all small trees.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from gen import inputs, trees
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------------------
+# Independent helpers (NOT the oracle): the paper's matrix form.
+# ---------------------------------------------------------------------------
+def mask_by_closure(parent):
+    """L row(i) = row(parent(i)) ∪ {i}  (SPEC.md:35 invariant)."""
+    T = len(parent)
+    L = np.zeros((T, T), dtype=np.int64)
+    for i in range(T):
+        if i > 0:
+            L[i] = L[parent[i]]
+        L[i, i] = 1
+    return L
+
+
+def matrix_form_scan(x, dt, A, Bm, Cm, D, h0, parent):
+    """PAPER.md:86-102 for one tree, per head (Mamba-2 scalar-per-head decay):
+    A_log[t] = dt_t*A_h;  A_tree = L @ A_log  (Eq. a_tree);
+    y_i = C_i (exp(A_tree_i) h0)  +  sum_j L_ij exp(A_tree_i - A_tree_j) (C_i·B_j) dt_j x_j  + D x_i.
+    x[T][H][P], dt[T][H], Bm/Cm[T][N] (G=1), h0[H][P][N]."""
+    T, H, P = x.shape
+    L = mask_by_closure(parent).astype(np.float64)
+    y = np.zeros((T, H, P))
+    G = Cm @ Bm.T                                   # C_i · B_j
+    for h in range(H):
+        alog = dt[:, h] * A[h]
+        atree = L @ alog
+        diff = atree[:, None] - atree[None, :]
+        Mu = L * np.exp(np.where(L > 0, diff, 0.0)) * G * dt[None, :, h]
+        Mx = np.exp(atree)[:, None] * (Cm @ h0[h].T)  # (M_x)_i x0 = C_i diag(e^{A_tree_i}) x0
+        y[:, h, :] = Mx + Mu @ x[:, h, :] + D[h] * x[:, h, :]
+    return y
+
+
+def ssd_chain_textbook(x, dt, A, Bm, Cm, D, h0):
+    """Mamba-2 SSD quadratic ('dual') form on a plain sequence with an initial
+    state: segsum with -inf above the diagonal,
+    Y = (exp(segsum) ∘ C Bᵀ)(dt X) + exp(cumsum) C h0ᵀ + D X;  final state
+    h_T = exp(cs_T) h0 + sum_j exp(cs_T - cs_j) dt_j x_j B_jᵀ."""
+    T, H, P = x.shape
+    y = np.zeros((T, H, P))
+    hT = np.zeros_like(h0)
+    for h in range(H):
+        a = dt[:, h] * A[h]
+        cs = np.cumsum(a)
+        seg = cs[:, None] - cs[None, :]
+        seg = np.where(np.tril(np.ones((T, T), bool)), seg, -np.inf)
+        Lm = np.exp(seg)
+        y[:, h] = (Lm * (Cm @ Bm.T)) @ (dt[:, h, None] * x[:, h]) \
+            + np.exp(cs)[:, None] * (Cm @ h0[h].T) + D[h] * x[:, h]
+        w = np.exp(cs[-1] - cs) * dt[:, h]
+        hT[h] = np.exp(cs[-1]) * h0[h] + np.einsum("t,tp,tn->pn", w, x[:, h], Bm)
+    return y, hT
+
+
+def rand_case(parent, H=2, P=3, N=4, seed=0, dt_hi=1e-1):
+    rng = np.random.default_rng(seed)
+    T = len(parent)
+    x = rng.standard_normal((1, T, H, P))
+    dt = np.exp(rng.uniform(np.log(1e-3), np.log(dt_hi), (1, T, H)))
+    A = -rng.uniform(1, 16, H)
+    Bm = rng.standard_normal((1, T, 1, N))
+    Cm = rng.standard_normal((1, T, 1, N))
+    D = 1 + 0.1 * rng.standard_normal(H)
+    h0 = rng.standard_normal((1, H, P, N))
+    return x, dt, A, Bm, Cm, D, h0, np.asarray(parent, np.int32)[None]
+
+
+def relerr(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------------------
+# Mask
+# ---------------------------------------------------------------------------
+def _rows(mask_b, T):
+    return ["".join("1" if (mask_b[i, j // 32] >> (j % 32)) & 1 else "0" for j in range(T))
+            for i in range(T)]
+
+
+def test_mask_spec_examples():
+    for case in _gold("mask_examples.json")["cases"]:
+        par = np.array(case["parent"], np.int32)[None]
+        m, d, st = oracle.build_mask(par)
+        assert st[0] == 0
+        assert _rows(m[0], par.shape[1]) == case["rows"]
+        assert list(d[0]) == [r.count("1") - 1 for r in case["rows"]]
+
+
+def all_parent_arrays(T):
+    return itertools.product(*[range(i) for i in range(1, T)])
+
+
+def test_mask_bruteforce_all_trees_T_le_7():
+    for T in range(1, 8):
+        for tail in all_parent_arrays(T):
+            par = np.array((-1,) + tail, np.int32)
+            m, d, st = oracle.build_mask(par[None])
+            L = mask_by_closure(par)
+            got = np.array([[(m[0, i, j // 32] >> (j % 32)) & 1 for j in range(T)] for i in range(T)])
+            assert st[0] == 0
+            assert np.array_equal(got, L)
+            assert np.array_equal(d[0], L.sum(1) - 1)
+
+
+def test_mask_chain_is_causal_and_multiword():
+    for T in (33, 64, 100, 256):
+        m, d, st = oracle.build_mask(trees.chain(T)[None])
+        got = np.array([[(m[0, i, j // 32] >> (j % 32)) & 1 for j in range(T)] for i in range(T)])
+        assert np.array_equal(got, np.tril(np.ones((T, T), int)))
+        assert np.array_equal(d[0], np.arange(T))
+
+
+def test_mask_invalid_trees():
+    bad = np.array([[0, 0, 0], [-1, 1, 0], [-1, 0, 5], [-1, -1, 0]], np.int32)
+    _, _, st = oracle.build_mask(bad)
+    assert list(st) == [1, 2, 2, 2]
+
+
+def test_fig3_counts_and_table_shapes():
+    g = _gold("fig3_counts.json")
+    for c in g["cases"]:
+        par = trees.heap_kary(2 ** c["levels"] - 1, 2)
+        m, d, st = oracle.build_mask(par[None])
+        has_child = np.zeros(len(par), bool)
+        has_child[par[1:]] = True
+        leaves = np.flatnonzero(~has_child)
+        assert len(par) == c["packed_tokens"]
+        assert len(leaves) == c["unrolled_states"]
+        assert int((d[0][leaves] + 1).sum()) == c["unrolled_tokens"]
+    for name, (width, depth, tok) in g["static_configs"].items():
+        par = trees.static_tree(name)
+        _, d, _ = oracle.build_mask(par[None])
+        assert len(par) == tok and d[0].max() == depth
+        assert max(np.bincount(d[0])) == width
+    M, N, tok = g["beam"]
+    par = trees.beam(M, N, np.random.default_rng(0))
+    _, d, _ = oracle.build_mask(par[None])
+    assert len(par) == tok and d[0].max() == N and max(np.bincount(d[0])[1:]) == M
+
+
+# ---------------------------------------------------------------------------
+# Scan
+# ---------------------------------------------------------------------------
+def test_matrix_form_helper_atree_spec_example():
+    """parent=[-,0,0,1], a_log=ln .5 -> A_tree = [ln.5, 2ln.5, 2ln.5, 3ln.5]."""
+    L = mask_by_closure([-1, 0, 0, 1])
+    assert np.allclose(L @ np.full(4, math.log(0.5)), np.log(0.5) * np.array([1, 2, 2, 3]))
+
+
+def test_scan_hand_example():
+    g = _gold("hand_example.json")
+    T = len(g["parent"])
+    x = np.array(g["x"]).reshape(1, T, 1, 1)
+    dt = np.array(g["dt"]).reshape(1, T, 1)
+    Bm = np.array(g["B"]).reshape(1, T, 1, 1)
+    Cm = np.array(g["C"]).reshape(1, T, 1, 1)
+    h0 = np.full((1, 1, 1, 1), g["h0"])
+    par = np.array(g["parent"], np.int32)[None]
+    A = np.array(g["A"])
+    for Dv, key in ((0.0, "y_D0"), (1.0, "y_D1")):
+        y, st = oracle.tree_scan(x, dt, A, Bm, Cm, np.array([Dv]), h0, par)
+        assert st[0] == 0
+        np.testing.assert_allclose(y.ravel(), g[key], rtol=1e-14, atol=0)
+    hn, st = oracle.commit(x, dt, A, Bm, h0, np.array([[0, 1, 3, -1]], np.int32), np.array([3], np.int32), par)
+    assert st[0] == 0 and abs(hn.ravel()[0] - g["h_new"]) < 1e-14
+
+
+def test_scan_vs_matrix_form_random_trees():
+    """C1 (per-leaf recurrence) vs C2 over 200 random trees."""
+    rng = np.random.default_rng(1)
+    worst = 0.0
+    for k in range(200):
+        T = int(rng.integers(1, 64))
+        par = trees.random_parent_array(T, rng) if k % 2 else trees.random_recursive(T, 3, rng)
+        x, dt, A, Bm, Cm, D, h0, P = rand_case(par, H=2, P=int(rng.integers(1, 9)),
+                                             N=int(rng.integers(1, 17)), seed=k)
+        y, st = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+        ref = matrix_form_scan(x[0], dt[0], A, Bm[0, :, 0], Cm[0, :, 0], D, h0[0], par)
+        worst = max(worst, relerr(y[0], ref))
+    assert worst < 1e-12, worst
+
+
+def test_scan_bruteforce_all_trees_T_le_6():
+    k = 0
+    for T in range(1, 7):
+        for tail in all_parent_arrays(T):
+            par = np.array((-1,) + tail, np.int32)
+            x, dt, A, Bm, Cm, D, h0, P = rand_case(par, H=2, P=3, N=4, seed=k, dt_hi=1.0)
+            y, st = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+            ref = matrix_form_scan(x[0], dt[0], A, Bm[0, :, 0], Cm[0, :, 0], D, h0[0], par)
+            assert relerr(y[0], ref) < 1e-12, (par, relerr(y[0], ref))
+            k += 1
+
+
+def test_chain_equals_textbook_mamba2_scan():
+    """causal L -> Mamba-2 with a non-zero initial state."""
+    for T in (1, 2, 7, 33, 128):
+        par = trees.chain(T)
+        x, dt, A, Bm, Cm, D, h0, P = rand_case(par, H=3, P=5, N=6, seed=T)
+        y, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+        yr, hT = ssd_chain_textbook(x[0], dt[0], A, Bm[0, :, 0], Cm[0, :, 0], D, h0[0])
+        assert relerr(y[0], yr) < 1e-12
+        path = np.arange(T, dtype=np.int32)[None]
+        hn, st = oracle.commit(x, dt, A, Bm, h0, path, np.array([T], np.int32), P)
+        assert st[0] == 0 and relerr(hn[0], hT) < 1e-12
+
+
+def test_unrolled_paths_reproduce_nodes_bitwise():
+    """Each root-to-leaf path scanned as its own chain reproduces the packed
+    tree's outputs bit-identically (BASELINE north_star invariant 1)."""
+    rng = np.random.default_rng(7)
+    for k in range(20):
+        par = trees.random_recursive(40, 3, rng)
+        x, dt, A, Bm, Cm, D, h0, P = rand_case(par, H=2, P=4, N=5, seed=100 + k)
+        y, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+        has_child = np.zeros(len(par), bool)
+        has_child[par[1:]] = True
+        for leaf in np.flatnonzero(~has_child):
+            path = [int(leaf)]
+            while par[path[-1]] >= 0:
+                path.append(int(par[path[-1]]))
+            path = path[::-1]
+            sub = lambda a: a[:, path]  # noqa: E731
+            yc, _ = oracle.tree_scan(sub(x), sub(dt), A, sub(Bm), sub(Cm), D, h0,
+                                     trees.chain(len(path))[None])
+            assert np.array_equal(yc[0], y[0, path])
+
+
+def test_scan_special_cases():
+    rng = np.random.default_rng(3)
+    # T = 1: y = e^{dt A} C h0ᵀ + dt (C·B) x + D x   (SPEC.md:150 with h0)
+    x, dt, A, Bm, Cm, D, h0, P = rand_case([-1], H=2, P=3, N=4, seed=5)
+    y, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+    for h in range(2):
+        exp = np.exp(dt[0, 0, h] * A[h]) * (h0[0, h] @ Cm[0, 0, 0]) \
+            + dt[0, 0, h] * (Cm[0, 0, 0] @ Bm[0, 0, 0]) * x[0, 0, h] + D[h] * x[0, 0, h]
+        np.testing.assert_allclose(y[0, 0, h], exp, rtol=1e-13)
+    par = trees.random_recursive(20, 3, rng)
+    x, dt, A, Bm, Cm, D, h0, P = rand_case(par, H=2, P=3, N=4, seed=6)
+    # dt = 0: no decay, no input -> y_i = C_i h0ᵀ + D x_i
+    y, _ = oracle.tree_scan(x, 0 * dt, A, Bm, Cm, D, h0, P)
+    exp = np.einsum("tn,hpn->thp", Cm[0, :, 0], h0[0]) + D[None, :, None] * x[0]
+    np.testing.assert_allclose(y[0], exp, rtol=1e-13, atol=1e-13)
+    # linearity in (x, h0) (D = 0)
+    Dz = np.zeros_like(D)
+    y1, _ = oracle.tree_scan(x, dt, A, Bm, Cm, Dz, h0, P)
+    y2, _ = oracle.tree_scan(2 * x, dt, A, Bm, Cm, Dz, 0 * h0, P)
+    y3, _ = oracle.tree_scan(0 * x, dt, A, Bm, Cm, Dz, 3 * h0, P)
+    np.testing.assert_allclose(y1, y2 / 2 + y3 / 3, rtol=1e-11, atol=1e-12)
+    # A = 0: no decay -> y_i = C_i (h0 + sum_{j in path} dt_j x_j B_jᵀ) + D x_i
+    y, _ = oracle.tree_scan(x, dt, 0 * A, Bm, Cm, D, h0, P)
+    L = mask_by_closure(par)
+    for i in range(len(par)):
+        js = np.flatnonzero(L[i])
+        S = h0[0] + np.einsum("j,jhp,jn->hpn", np.ones(len(js)), dt[0, js, :, None] * x[0, js], Bm[0, js, 0])
+        np.testing.assert_allclose(y[0, i], S @ Cm[0, i, 0] + D[:, None] * x[0, i], rtol=1e-12, atol=1e-12)
+
+
+def test_subtree_locality_bitwise():
+    """perturbing x_j for j ∉ path(i) leaves y_i bit-identical."""
+    rng = np.random.default_rng(11)
+    par = trees.random_recursive(48, 4, rng)
+    x, dt, A, Bm, Cm, D, h0, P = rand_case(par, seed=12)
+    y, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, P)
+    L = mask_by_closure(par)
+    j = 17
+    x2 = x.copy()
+    x2[0, j] += 1.0
+    y2, _ = oracle.tree_scan(x2, dt, A, Bm, Cm, D, h0, P)
+    for i in range(len(par)):
+        if L[i, j] == 0:
+            assert np.array_equal(y[0, i], y2[0, i])
+        else:
+            assert not np.array_equal(y[0, i], y2[0, i])
+
+
+def test_scan_invalid_tree_zero_filled():
+    x, dt, A, Bm, Cm, D, h0, P = rand_case([-1, 0, 1], seed=1)
+    bad = np.array([[-1, 2, 0]], np.int32)
+    y, st = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, bad)
+    assert st[0] == 2 and not y.any()
+
+
+# ---------------------------------------------------------------------------
+# Accept
+# ---------------------------------------------------------------------------
+def naive_walk(tokens, parent, vtok):
+    """Independent restatement of PAPER.md:309 (children scanned by a dict)."""
+    kids = {}
+    for c in range(1, len(parent)):
+        kids.setdefault(int(parent[c]), []).append(c)
+    path, cur = [0], 0
+    while True:
+        m = [c for c in kids.get(cur, []) if tokens[c] == vtok[cur]]
+        if not m:
+            return path, int(vtok[cur])
+        cur = min(m)
+        path.append(cur)
+
+
+def test_accept_spec_examples_and_hand_example():
+    for c in _gold("accept_examples.json")["cases"]:
+        path, plen, bonus, st = oracle.accept(np.array([c["tokens"]]), np.array([c["parent"]]),
+                                              np.array([c["vtok"]]))
+        assert st[0] == 0 and plen[0] == c["len"] and bonus[0] == c["bonus"]
+        assert list(path[0][: plen[0]]) == c["path"] and (path[0][plen[0]:] == -1).all()
+    g = _gold("hand_example.json")
+    path, plen, bonus, st = oracle.accept(np.array([g["tokens"]]), np.array([g["parent"]]), np.array([g["vtok"]]))
+    assert list(path[0][: plen[0]]) == g["accept_path"] and plen[0] == g["accept_len"] \
+        and bonus[0] == g["accept_bonus"]
+
+
+def test_accept_chain_full_and_none():
+    T = 10
+    par = trees.chain(T)
+    tok = np.arange(100, 100 + T, dtype=np.int32)
+    vt = np.roll(tok, -1)
+    vt[-1] = 5
+    path, plen, bonus, _ = oracle.accept(tok[None], par[None], vt[None])
+    assert plen[0] == T and bonus[0] == 5 and list(path[0]) == list(range(T))
+    vt2 = np.full(T, 1, np.int32)
+    path, plen, bonus, _ = oracle.accept(tok[None], par[None], vt2[None])
+    assert plen[0] == 1 and bonus[0] == 1
+
+
+def test_accept_bruteforce_with_duplicate_siblings():
+    rng = np.random.default_rng(5)
+    for k in range(300):
+        T = int(rng.integers(1, 80))
+        par = trees.random_recursive(T, 4, rng)
+        p_match = [0.0, 0.5, 0.9, 1.0][k % 4]
+        tok = inputs.make_tokens(par, rng, vocab=50, dup_siblings=(k % 3 == 0))
+        vt = inputs.make_verifier_tokens(par, tok, p_match, rng, vocab=50)
+        path, plen, bonus, st = oracle.accept(tok[None], par[None], vt[None])
+        ep, eb = naive_walk(tok, par, vt)
+        assert list(path[0][: plen[0]]) == ep and bonus[0] == eb
+        _, d, _ = oracle.build_mask(par[None])
+        assert 1 <= plen[0] <= d[0].max() + 1
+        for a, b in zip(ep[:-1], ep[1:]):
+            assert par[b] == a
+
+
+# ---------------------------------------------------------------------------
+# Commit (activation replay)
+# ---------------------------------------------------------------------------
+def test_commit_root_only_closed_form():
+    x, dt, A, Bm, Cm, D, h0, P = rand_case([-1, 0, 0], H=2, P=3, N=4, seed=9)
+    hn, st = oracle.commit(x, dt, A, Bm, h0, np.array([[0, -1, -1]], np.int32), np.array([1], np.int32), P)
+    for h in range(2):
+        exp = np.exp(dt[0, 0, h] * A[h]) * h0[0, h] + dt[0, 0, h] * np.outer(x[0, 0, h], Bm[0, 0, 0])
+        np.testing.assert_allclose(hn[0, h], exp, rtol=1e-14)
+
+
+def test_commit_invalid_paths_keep_h0():
+    x, dt, A, Bm, Cm, D, h0, P = rand_case([-1, 0, 0, 1], seed=2)
+    bad = [([1, 3, -1, -1], 2), ([0, 2, 3, -1], 3), ([0, 1, 3, -1], 0), ([0, 1, 1, -1], 3)]
+    for p, r in bad:
+        hn, st = oracle.commit(x, dt, A, Bm, h0, np.array([p], np.int32), np.array([r], np.int32), P)
+        assert st[0] == 3 and np.array_equal(hn, h0)
+
+
+def test_graft_invariant():
+    """Losslessness across iterations (Alg. 1): scanning
+    tree2 from h0 = commit(tree1, path to k) equals scanning tree1 with tree2
+    grafted below k (tree2's root is the bonus token, a new child of k)."""
+    rng = np.random.default_rng(21)
+    for k in range(10):
+        T1, T2 = 20, 12
+        p1 = trees.random_recursive(T1, 3, rng)
+        p2 = trees.random_recursive(T2, 3, rng)
+        kk = int(rng.integers(T1))
+        path = [kk]
+        while p1[path[-1]] >= 0:
+            path.append(int(p1[path[-1]]))
+        path = path[::-1]
+        pg = np.concatenate([p1, [kk], p2[1:] + T1]).astype(np.int32)
+        x, dt, A, Bm, Cm, D, h0, Pg = rand_case(pg, H=2, P=3, N=4, seed=200 + k)
+        yg, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, Pg)
+        pa = np.full((1, T1), -1, np.int32)
+        pa[0, : len(path)] = path
+        s1 = lambda a: a[:, :T1]  # noqa: E731
+        s2 = lambda a: a[:, T1:]  # noqa: E731
+        hk, st = oracle.commit(s1(x), s1(dt), A, s1(Bm), h0, pa, np.array([len(path)], np.int32), p1[None])
+        assert st[0] == 0
+        y2, _ = oracle.tree_scan(s2(x), s2(dt), A, s2(Bm), s2(Cm), D, hk, p2[None])
+        np.testing.assert_allclose(y2[0], yg[0, T1:], rtol=1e-12, atol=1e-12)
