@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""Benchmark of the STree tree-verify hot path (BASELINE.json metric:
+"tree-verify nodes/s per SSM layer (1/2/4/8 B200); % of roofline").
+
+One STEP = one verify iteration of an L-layer Mamba-2 stack over one batch of
+synthetic drafted trees, i.e. one pass through every §8(a) row:
+    stree_build_mask (once)  ->  L x stree_tree_scan  ->  stree_accept (once)
+    ->  L x stree_commit (in place, the committed state is the next step's h0)
+Workload (default) = BASELINE configs[3] / SURVEY c4 per GPU: 16 random
+recursive trees x 64 nodes, Mamba-2 2.7B layer shape (H=80, P=64, N=128, G=1),
+bf16 x/B/C/y, fp32 dt/A/D/state, L = 64 distinct layers (every layer has its
+own buffers, 4.1 GB in total, > 30x the 126 MB L2, so no L2 flush is needed).
+
+value = B*T*L*world / max-over-ranks(step time)  [nodes/s per layer, whole job].
+Each phase of the step (mask / scans / accept / commits) is one CUDA graph;
+CUDA events between the graph launches on the launching stream give the
+per-kernel average durations used in the roofline object.
+
+--impl reference runs the CPU oracle (oracle/, fp64) as the reference arm on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from gen import inputs  # noqa: E402
+
+METRIC = "tree-verify nodes/s per SSM layer"
+UNIT = "nodes/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="stree", choices=["stree", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4"])
+    ap.add_argument("--layers", type=int, default=64)
+    ap.add_argument("--scan-impl", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--p-match", type=float, default=0.9)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg, prob, L):
+    d = prob.dims
+    return {"workload": f"{cfg}: Mamba-2 2.7B-shaped SSM layer stack, tree verify "
+                        f"(mask + {L} x scan + accept + {L} x commit)" if cfg != "c2" else
+            f"{cfg}: Mamba-2 130M-shaped layer stack, tree verify",
+            "trees_per_gpu": d.batch, "nodes_per_tree": d.n_nodes, "heads": d.n_heads, "head_dim": d.head_dim,
+            "d_state": d.d_state, "n_groups": d.n_groups, "layers": L, "io_dtype": d.io_dtype,
+            "state_dtype": "f32", "tree": "random recursive, branching<=4" if cfg == "c4" else "heap binary",
+            "l2": "inputs larger than L2 (distinct per-layer buffers, no reuse within a step)"}
+
+
+def scan_bytes(d):
+    s_io = 2 if d.io_dtype == "bf16" else 4
+    B, T, H, P, N, G = d.batch, d.n_nodes, d.n_heads, d.head_dim, d.d_state, d.n_groups
+    return B * (T * H * P * (s_io + s_io) + T * H * 4 + 2 * T * G * N * s_io + H * P * N * 4 + T * 4) + H * 8
+
+
+def commit_bytes(d, path_len):
+    s_io = 2 if d.io_dtype == "bf16" else 4
+    H, P, N = d.n_heads, d.head_dim, d.d_state
+    return int(sum(2 * H * P * N * 4 + int(r) * (H * P * s_io + H * 4 + N * s_io) for r in path_len))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def load_traffic(cfg):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling through NVML during the timed region."""
+
+    def __init__(self, index, period=0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (reference arm / cpu_baseline)
+# ---------------------------------------------------------------------------
+def oracle_sample(prob, tok, vt, n_trees):
+    """One bounded oracle 'step' on the first n_trees trees of one layer:
+    mask + scan + accept + commit (fp64, OpenMP over (tree, head))."""
+    import oracle
+    sl = slice(0, n_trees)
+    x, Bm, Cm = prob.io_as_f32("x")[sl], prob.io_as_f32("Bm")[sl], prob.io_as_f32("Cm")[sl]
+    par = prob.parent[sl]
+    t0 = time.perf_counter()
+    oracle.build_mask(par)
+    oracle.tree_scan(x, prob.dt[sl], prob.A, Bm, Cm, prob.D, prob.h0[sl], par)
+    path, plen, _, _ = oracle.accept(tok[sl], par, vt[sl])
+    oracle.commit(x, prob.dt[sl], prob.A, Bm, prob.h0[sl], path, plen, par)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    prob = inputs.config_problem(args.config)
+    tok, vt = inputs.make_accept_inputs(prob.parent, seed=123, p_match=args.p_match)
+    n_trees = 1
+    # calibrate the sample: grow until one step takes >= ~2 s (bounded by the batch)
+    dt_ = oracle_sample(prob, tok, vt, n_trees)
+    while dt_ < 2.0 and n_trees < prob.dims.batch:
+        n_trees = min(prob.dims.batch, n_trees * 2)
+        dt_ = oracle_sample(prob, tok, vt, n_trees)
+    for _ in range(args.warmup):
+        oracle_sample(prob, tok, vt, n_trees)
+    times = [oracle_sample(prob, tok, vt, n_trees) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = n_trees * prob.dims.n_nodes / t
+    cores = oracle.num_threads()
+    sample = (f"{n_trees} of {prob.dims.batch} trees x 1 layer per step (mask+scan+accept+commit), "
+              f"fp64 C oracle, OpenMP {cores} threads")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(args.config, prob, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(prob, tok, vt, budget_s=15.0):
+    import oracle
+    n = 1
+    t = oracle_sample(prob, tok, vt, n)
+    while t * 2 < 4.0 and n < prob.dims.batch:
+        n = min(prob.dims.batch, n * 2)
+        t = oracle_sample(prob, tok, vt, n)
+    reps, tot = 0, 0.0
+    while tot < budget_s and reps < 20:
+        tot += oracle_sample(prob, tok, vt, n)
+        reps += 1
+    cores = oracle.num_threads()
+    return {"value": n * prob.dims.n_nodes * reps / tot, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} trees x 1 layer (mask+scan+accept+commit) x {reps} reps of {args_cfg_name(prob)}, "
+                      f"fp64, {tot:.1f} s, OpenMP {cores} threads"}
+
+
+def args_cfg_name(prob):
+    d = prob.dims
+    return f"B={d.batch} T={d.n_nodes} H={d.n_heads} P={d.head_dim} N={d.d_state}"
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_stree(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2505_14969_b200 import api, binding
+
+    binding.stree_set_scan_impl({"auto": 0, "simt": 1, "tc": 2}[args.scan_impl])
+    L = args.layers
+    # every rank verifies its own batch of trees (weak scaling; no data-path collective)
+    base = inputs.config_problem(args.config)
+    d = base.dims
+    par_np = base.parent
+    if world > 1:
+        rng = np.random.default_rng(inputs.BASE_SEED + 1000 + rank)
+        from gen import trees as _t
+        par_np = np.stack([_t.random_recursive(d.n_nodes, 4, rng) for _ in range(d.batch)]) \
+            if args.config == "c4" else par_np
+    tok, vt = inputs.make_accept_inputs(par_np, seed=inputs.BASE_SEED + 77 + rank, p_match=args.p_match)
+
+    # per-layer inputs: distinct buffers (values generated on device to keep setup fast;
+    # layer 0 is the seeded host problem, the others are seeded device randoms of the same recipe)
+    g = torch.Generator(device=dev)
+    g.manual_seed(inputs.BASE_SEED + 10 * rank)
+    layers = []
+    t0 = api.upload(inputs.make_problem(d, par_np, seed=inputs.BASE_SEED + 3 + 100 * rank), device=dev)
+    io_t = t0["x"].dtype
+    for li in range(L):
+        if li == 0:
+            t = t0
+        else:
+            B, T, H, P, N, G = d.batch, d.n_nodes, d.n_heads, d.head_dim, d.d_state, d.n_groups
+            t = {
+                "x": torch.randn((B, T, H, P), generator=g, device=dev).to(io_t),
+                "dt": torch.exp(torch.empty((B, T, H), device=dev).uniform_(np.log(1e-3), np.log(1e-1),
+                                                                            generator=g)),
+                "A": -torch.empty((H,), device=dev).uniform_(1.0, 16.0, generator=g),
+                "Bm": torch.randn((B, T, G, N), generator=g, device=dev).to(io_t),
+                "Cm": torch.randn((B, T, G, N), generator=g, device=dev).to(io_t),
+                "D": 1 + 0.1 * torch.randn((H,), generator=g, device=dev),
+                "h0": torch.randn((B, H, P, N), generator=g, device=dev),
+                "parent": t0["parent"],
+            }
+        t["y"] = torch.empty_like(t["x"])
+        layers.append(t)
+    parent = t0["parent"]
+    tok_d = torch.from_numpy(tok).to(dev)
+    vt_d = torch.from_numpy(vt).to(dev)
+    W = (d.n_nodes + 31) // 32
+    mask = torch.empty((d.batch, d.n_nodes, W), dtype=torch.int32, device=dev)
+    depth = torch.empty((d.batch, d.n_nodes), dtype=torch.int32, device=dev)
+    path = torch.empty((d.batch, d.n_nodes), dtype=torch.int32, device=dev)
+    plen = torch.empty((d.batch,), dtype=torch.int32, device=dev)
+    bonus = torch.empty((d.batch,), dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    dims = binding.make_dims(layers[0]["x"], layers[0]["Bm"])
+    kernel = binding.stree_scan_kernel_for(dims)
+
+    def ph_mask():
+        binding.stree_build_mask(parent, mask, depth, status)
+
+    def ph_scan():
+        for t in layers:
+            binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"],
+                                    status, dims=dims)
+
+    def ph_accept():
+        binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
+
+    def ph_commit():
+        for t in layers:
+            binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"], status,
+                                 dims=dims)
+
+    phases = [ph_mask, ph_scan, ph_accept, ph_commit]
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for f in phases:      # eager warm-up (loads modules, sets smem attributes)
+            f()
+    torch.cuda.synchronize()
+    graphs = []
+    for f in phases:
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            f()
+        graphs.append(gr)
+    torch.cuda.synchronize()
+    assert status.item() == 0, f"device status {status.item()}"
+    plen_host = plen.cpu().numpy()
+
+    def step(evs=None):
+        for i, gr in enumerate(graphs):
+            if evs is not None:
+                evs[i].record(stream)
+            gr.replay()
+        if evs is not None:
+            evs[len(graphs)].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(graphs) + 1)] for _ in range(K)]
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    with sampler:
+        with torch.cuda.stream(stream):
+            for k in range(K):
+                step(evs[k])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    phase_ms = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(len(graphs))] for k in range(K)])
+    total_ms = float(evs[0][0].elapsed_time(evs[K - 1][len(graphs)]))
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / K
+    nodes_per_step = d.batch * d.n_nodes * L * world
+    value = nodes_per_step / (ms_per_step * 1e-3)
+    ph_mean = phase_ms.mean(0)
+    scan_us = ph_mean[1] * 1e3 / L
+    commit_us = ph_mean[3] * 1e3 / L
+    hbm_peak, bf16_peak, peak_src = load_peaks()
+    sb = scan_bytes(d)
+    cb = commit_bytes(d, plen_host)
+    scan_gbs = sb / (scan_us * 1e-6) / 1e9
+    commit_gbs = cb / (commit_us * 1e-6) / 1e9
+    dominant = "stree_tree_scan" if scan_us >= commit_us else "stree_commit"
+    dom_gbs, dom_bytes = (scan_gbs, sb) if dominant == "stree_tree_scan" else (commit_gbs, cb)
+    traffic = load_traffic(args.config) or {}
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": dom_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": dom_gbs / hbm_peak, "traffic": traffic.get(dominant), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dom_bytes,
+                "kernels": {"stree_tree_scan": {"us": scan_us, "bytes": sb, "GB/s": scan_gbs,
+                                                "frac": scan_gbs / hbm_peak,
+                                                "impl": {1: "simt", 2: "tcgen05"}.get(kernel)},
+                            "stree_commit": {"us": commit_us, "bytes": cb, "GB/s": commit_gbs,
+                                             "frac": commit_gbs / hbm_peak, "mean_path_len":
+                                                 float(plen_host.mean())},
+                            "stree_build_mask": {"us": ph_mean[0] * 1e3},
+                            "stree_accept": {"us": ph_mean[2] * 1e3}}}
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": d.io_dtype, "data": "synthetic", "config": workload_desc(args.config, base, L),
+            "gpu_launches": (2 * L + 2) * K, "roofline": roofline, "e2e": e2e,
+            "clocks": sampler.summary(), "parallelism": f"batch-replicas x{world}" if world > 1 else "single"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(base, tok, vt)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L):
+    """Same step through the public API, inputs copied from pinned host memory
+    every step (x, dt, B, C of every layer + tree + tokens) and the acceptance
+    result (path, path_len, bonus) read back."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_14969_b200 import binding
+
+    host = []
+    for t in layers:
+        host.append({k: t[k].cpu().pin_memory() for k in ("x", "dt", "Bm", "Cm")})
+    hp = parent.cpu().pin_memory()
+    htok, hvt = tok_d.cpu().pin_memory(), vt_d.cpu().pin_memory()
+    out = [torch.empty(path.shape, dtype=torch.int32).pin_memory(),
+           torch.empty(plen.shape, dtype=torch.int32).pin_memory(),
+           torch.empty(bonus.shape, dtype=torch.int32).pin_memory()]
+    h2d = sum(v.numel() * v.element_size() for hh in host for v in hh.values()) + \
+        (hp.numel() + htok.numel() + hvt.numel()) * 4
+    d2h = sum(o.numel() * 4 for o in out)
+
+    def step():
+        with torch.cuda.stream(stream):
+            parent.copy_(hp, non_blocking=True)
+            tok_d.copy_(htok, non_blocking=True)
+            vt_d.copy_(hvt, non_blocking=True)
+            binding.stree_build_mask(parent, torch.empty((d.batch, d.n_nodes, (d.n_nodes + 31) // 32),
+                                                         dtype=torch.int32, device=dev), None, status)
+            for t, hh in zip(layers, host):
+                for k, v in hh.items():
+                    t[k].copy_(v, non_blocking=True)
+                binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent,
+                                        t["y"], status, dims=dims)
+            binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
+            for t in layers:
+                binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"],
+                                     status, dims=dims)
+            for o, s in zip(out, (path, plen, bonus)):
+                o.copy_(s, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(2):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    K = max(3, args.steps // 3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": d.batch * d.n_nodes * L * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": K}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_stree(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

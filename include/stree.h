@@ -1,0 +1,160 @@
+/*
+ * stree.h — C ABI of the B200-native STree tree-verify hot path.
+ *
+ * STree (arXiv 2505.14969) verifies a packed speculative token tree through a
+ * diagonal SSM (Mamba-2/SSD) layer in one pass.  This library exposes the four
+ * steps of that hot path (BASELINE.json north_star):
+ *
+ *   stree_build_mask  tree topology -> ancestor mask L          PAPER.md:62-66 (L_ij = 1_{s_i}{t_j}), :90
+ *   stree_tree_scan   packed-tree SSM outputs y (no state out)   PAPER.md:86-102 (A_tree = L A_log, y = M_x x0 + M_u u), :108-113
+ *   stree_accept      greedy longest accepted path + bonus       PAPER.md:309 (greedy verification), Alg. 1 l.125
+ *   stree_commit      state after the last accepted node         PAPER.md:113, Alg. 1 l.123 (activation replay)
+ *
+ * Conventions (all calls):
+ *  - Every array pointer is a DEVICE pointer owned by the caller.  The library
+ *    never allocates device memory, never synchronises (unless STREE_SYNC_CHECK=1
+ *    is set in the environment, a debug mode), and only enqueues work on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Arrays are dense, row-major, contiguous, in the layouts given below.
+ *  - Host-detectable problems (NULL pointers, bad sizes, unsupported dtype,
+ *    misalignment) return a non-zero stree_status synchronously and launch nothing.
+ *  - Tree and path validity is data-dependent and checked on the device.  The
+ *    first failure is recorded in *dev_status (one caller-zeroed int32 on the
+ *    device) with atomicCAS; the offending tree's outputs are defined below and
+ *    the other trees in the batch proceed normally.  dev_status may be NULL.
+ *      STREE_DEV_BAD_ROOT   = 1   parent[0] != -1
+ *      STREE_DEV_BAD_PARENT = 2   parent[i] outside [0, i) for some i >= 1
+ *      STREE_DEV_BAD_PATH   = 3   path not root-anchored / not parent-linked / bad length
+ *  - batch == 0 or n_nodes == 0 is a successful no-op.
+ *  - Thread safety: calls may be issued concurrently from several host threads.
+ *
+ * Notation: B = batch of trees, T = nodes per tree (1..256), H = SSM heads,
+ * P = head dim, N = d_state, G = groups (G divides H; head h uses group
+ * h / (H/G)).  Node 0 is the root; nodes are in topological order
+ * (parent[i] < i).
+ */
+#ifndef STREE_H_
+#define STREE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    STREE_OK = 0,
+    STREE_ERR_NULL = 1,         /* a required pointer is NULL */
+    STREE_ERR_SHAPE = 2,        /* a size is negative / out of range (e.g. T > 256, H % G) */
+    STREE_ERR_DTYPE = 3,        /* unsupported dtype combination */
+    STREE_ERR_ALIGN = 4,        /* pointer not 16-byte aligned where required */
+    STREE_ERR_UNSUPPORTED = 5,  /* valid request this build cannot serve */
+    STREE_ERR_CUDA = 6,         /* a CUDA runtime error (launch failure, ...) */
+    STREE_ERR_DEVICE = 7        /* only with STREE_SYNC_CHECK=1: *dev_status != 0 after the call */
+} stree_status;
+
+typedef enum { STREE_F32 = 0, STREE_BF16 = 1 } stree_dtype;
+
+enum { STREE_DEV_OK = 0, STREE_DEV_BAD_ROOT = 1, STREE_DEV_BAD_PARENT = 2, STREE_DEV_BAD_PATH = 3 };
+
+enum { STREE_MAX_NODES = 256 };
+
+typedef struct {
+    int32_t batch;        /* B */
+    int32_t n_nodes;      /* T, 0..256 */
+    int32_t n_heads;      /* H (local heads when the caller shards heads) */
+    int32_t head_dim;     /* P */
+    int32_t d_state;      /* N */
+    int32_t n_groups;     /* G, divides H */
+    stree_dtype io_dtype; /* dtype of x, B, C and y */
+} stree_dims;
+
+/* Scan kernel selection (stree_set_scan_impl). */
+typedef enum {
+    STREE_SCAN_AUTO = 0,  /* tcgen05 kernel when supported (bf16 io, P==64, N in {64,128}, T<=128), else SIMT */
+    STREE_SCAN_SIMT = 1,  /* generic FP32-FMA kernel (any shape; the fp32 1e-4 path) */
+    STREE_SCAN_TC = 2     /* force the tcgen05 kernel; STREE_ERR_UNSUPPORTED if the shape is not served */
+} stree_scan_impl;
+
+/*
+ * stree_build_mask — ancestor (tree) mask.
+ *   parent [B][T] int32         parent index, parent[0] = -1.
+ *   mask   [B][T][W] uint32     W = ceil(T/32); bit (j % 32) of word j/32 of row i
+ *                               is 1 iff node j is on the root-to-i path (inclusive).
+ *   depth  [B][T] int32 or NULL depth(i) = |path(i)| - 1.
+ * Invalid tree b: dev_status <- 1/2, mask rows and depth of tree b are zero.
+ */
+stree_status stree_build_mask(const int32_t* parent, int32_t batch, int32_t n_nodes,
+                              uint32_t* mask, int32_t* depth, int32_t* dev_status, void* stream);
+
+/*
+ * stree_tree_scan — outputs of every node of every packed tree, one SSM layer
+ * (PAPER.md:91-102 with the Mamba-2 realisation of SURVEY R1-R3):
+ *   Λ_i  = Σ_{j∈path(i)} dt_j A_h                                  (A_tree, Eq. a_tree)
+ *   y_i  = e^{Λ_i} C_i·h0ᵀ + Σ_{j∈path(i)} e^{Λ_i-Λ_j} dt_j (C_i·B_j) x_j + D_h x_i
+ * which equals the per-node recurrence h_i = e^{dt_i A} h_parent(i) + dt_i x_i B_iᵀ,
+ * y_i = h_i C_i + D x_i started from h0 at the root (the root's own update included).
+ * No state is written.
+ *   x      [B][T][H][P]  io dtype
+ *   dt     [B][T][H]     f32, > 0 (post-softplus)
+ *   A      [H]           f32, < 0
+ *   Bm, Cm [B][T][G][N]  io dtype
+ *   D      [H]           f32 or NULL (= 0)
+ *   h0     [B][H][P][N]  f32 or NULL (= 0)
+ *   parent [B][T]        int32
+ *   y      [B][T][H][P]  io dtype; must not alias any input.
+ * Invalid tree b: dev_status <- 1/2 and y[b] = 0.
+ * Alignment: all pointers 16-byte aligned.
+ */
+stree_status stree_tree_scan(const stree_dims* d, const void* x, const float* dt, const float* A,
+                             const void* Bm, const void* Cm, const float* D, const float* h0,
+                             const int32_t* parent, void* y, int32_t* dev_status, void* stream);
+
+/*
+ * stree_accept — greedy acceptance walk (Alg. 1 FirstRejected):
+ * cur = 0; repeatedly move to the lowest-index child c of cur with
+ * tokens[c] == vtok[cur]; stop when none matches; bonus = vtok[cur].
+ *   tokens, vtok [B][T] int32  draft tokens (tokens[0], the root, is never compared);
+ *                              vtok[i] = verifier argmax (or sample) at node i.
+ *   parent [B][T] int32
+ *   path   [B][T] int32        accepted node indices root-first, -1 padded.
+ *   path_len [B] int32         number of accepted nodes incl. the root (>= 1).
+ *   bonus  [B] int32           verifier token at the last accepted node.
+ * Invalid tree b: dev_status <- 1/2, path_len = 0, path = -1, bonus = -1.
+ */
+stree_status stree_accept(const int32_t* tokens, const int32_t* parent, const int32_t* vtok,
+                          int32_t batch, int32_t n_nodes, int32_t* path, int32_t* path_len,
+                          int32_t* bonus, int32_t* dev_status, void* stream);
+
+/*
+ * stree_commit — activation replay of the accepted path (Alg. 1 l.123):
+ *   h_new = e^{Λ_k} h0 + Σ_{s∈path} e^{Λ_k-Λ_s} dt_s x_s B_sᵀ,  k = path[path_len-1],
+ * i.e. the recurrence above run along the path from h0 (state after k).
+ *   x, dt, A, Bm          as in stree_tree_scan (the cached activations of the verified tree)
+ *   h0     [B][H][P][N]   f32 (NULL = 0)
+ *   parent [B][T] or NULL if given, each path[m] must have parent path[m-1]
+ *   path, path_len        as produced by stree_accept
+ *   h_new  [B][H][P][N]   f32; h_new == h0 (in-place) is allowed, partial overlap is not.
+ * Invalid path for tree b: dev_status <- 3 and h_new[b] = h0[b] (state unchanged).
+ */
+stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, const float* A,
+                          const void* Bm, const float* h0, const int32_t* parent,
+                          const int32_t* path, const int32_t* path_len, float* h_new,
+                          int32_t* dev_status, void* stream);
+
+/* Human-readable name of a status code (static storage). */
+const char* stree_status_string(stree_status s);
+
+/* Select the scan kernel for subsequent stree_tree_scan calls (process-wide). */
+stree_status stree_set_scan_impl(stree_scan_impl impl);
+
+/* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
+int32_t stree_scan_kernel_for(const stree_dims* d);
+
+/* Library version string. */
+const char* stree_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STREE_H_ */

@@ -1,0 +1,149 @@
+"""Thin Python binding of the C ABI in include/stree.h (argument marshalling only).
+
+Every function has the name of the C entry point, takes torch CUDA tensors
+(caller-allocated outputs, exactly like the C call), passes raw device
+pointers and the current torch stream to libstree.so, and raises
+``StreeError`` on a non-zero status.  All computation happens in the CUDA
+kernels of ``csrc/``; there is no CPU or PyTorch fallback: if the library is
+missing or fails to load, import/usage fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libstree.so")
+
+STREE_F32, STREE_BF16 = 0, 1
+STREE_SCAN_AUTO, STREE_SCAN_SIMT, STREE_SCAN_TC = 0, 1, 2
+DEV_BAD_ROOT, DEV_BAD_PARENT, DEV_BAD_PATH = 1, 2, 3
+MAX_NODES = 256
+
+
+class StreeError(RuntimeError):
+    def __init__(self, fn, status):
+        super().__init__(f"{fn}: status {status} ({status_string(status)})")
+        self.status = status
+
+
+class stree_dims(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("d_state", ctypes.c_int32), ("n_groups", ctypes.c_int32),
+                ("io_dtype", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libstree.so (built in-tree by __graft_entry__.build()).  No fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32 = ctypes.c_void_p, ctypes.c_int32
+        sig = {
+            "stree_build_mask": [vp, i32, i32, vp, vp, vp, vp],
+            "stree_tree_scan": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "stree_accept": [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp],
+            "stree_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "stree_set_scan_impl": [ctypes.c_int],
+            "stree_scan_kernel_for": [vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.stree_status_string.argtypes = [ctypes.c_int]
+        L.stree_status_string.restype = ctypes.c_char_p
+        L.stree_version.argtypes = []
+        L.stree_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
+                    "stree_status_string", "stree_set_scan_impl", "stree_scan_kernel_for", "stree_version")
+
+
+def status_string(s: int) -> str:
+    return lib().stree_status_string(int(s)).decode()
+
+
+def version() -> str:
+    return lib().stree_version().decode()
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError("stree: tensors must live on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("stree: tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _check(fn, st):
+    if st != 0:
+        raise StreeError(fn, st)
+
+
+def io_code(dtype) -> int:
+    if dtype == torch.bfloat16:
+        return STREE_BF16
+    if dtype == torch.float32:
+        return STREE_F32
+    raise TypeError(f"stree: unsupported io dtype {dtype}")
+
+
+def make_dims(x: torch.Tensor, Bm: torch.Tensor) -> stree_dims:
+    B, T, H, P = x.shape
+    G, N = Bm.shape[2], Bm.shape[3]
+    return stree_dims(B, T, H, P, N, G, io_code(x.dtype))
+
+
+def stree_build_mask(parent, mask, depth=None, dev_status=None, stream=None):
+    B, T = parent.shape
+    _check("stree_build_mask", lib().stree_build_mask(_ptr(parent), B, T, _ptr(mask), _ptr(depth),
+                                                      _ptr(dev_status), _stream(stream)))
+
+
+def stree_tree_scan(x, dt, A, Bm, Cm, D, h0, parent, y, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_tree_scan", lib().stree_tree_scan(ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm),
+                                                    _ptr(Cm), _ptr(D), _ptr(h0), _ptr(parent), _ptr(y),
+                                                    _ptr(dev_status), _stream(stream)))
+
+
+def stree_accept(tokens, parent, vtok, path, path_len, bonus, dev_status=None, stream=None):
+    B, T = parent.shape
+    _check("stree_accept", lib().stree_accept(_ptr(tokens), _ptr(parent), _ptr(vtok), B, T, _ptr(path),
+                                              _ptr(path_len), _ptr(bonus), _ptr(dev_status), _stream(stream)))
+
+
+def stree_commit(x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_commit", lib().stree_commit(ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(h0),
+                                              _ptr(parent), _ptr(path), _ptr(path_len), _ptr(h_new),
+                                              _ptr(dev_status), _stream(stream)))
+
+
+def stree_set_scan_impl(impl: int):
+    _check("stree_set_scan_impl", lib().stree_set_scan_impl(int(impl)))
+
+
+def stree_scan_kernel_for(dims: stree_dims) -> int:
+    return lib().stree_scan_kernel_for(ctypes.byref(dims))

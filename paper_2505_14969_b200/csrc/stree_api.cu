@@ -1,0 +1,151 @@
+// Host side of the C ABI (include/stree.h): argument validation, kernel
+// selection and launch.  No allocation, no synchronisation on the hot path.
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+
+#include "stree_common.cuh"
+
+extern "C" int stree_launch_build_mask(const int32_t*, int, int, uint32_t*, int32_t*, int32_t*, cudaStream_t);
+extern "C" int stree_launch_accept(const int32_t*, const int32_t*, const int32_t*, int, int, int32_t*, int32_t*,
+                                   int32_t*, int32_t*, cudaStream_t);
+extern "C" int stree_launch_commit(const stree_dims*, const void*, const float*, const float*, const void*,
+                                   const float*, const int32_t*, const int32_t*, const int32_t*, float*, int32_t*,
+                                   cudaStream_t);
+extern "C" int stree_launch_scan_simt(const stree_dims*, const void*, const float*, const float*, const void*,
+                                      const void*, const float*, const float*, const int32_t*, void*, int32_t*,
+                                      cudaStream_t);
+extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*, const float*, const void*,
+                                    const void*, const float*, const float*, const int32_t*, void*, int32_t*,
+                                    cudaStream_t);
+extern "C" int stree_tc_supports(const stree_dims*);
+
+namespace {
+
+std::atomic<int> g_scan_impl{STREE_SCAN_AUTO};
+
+bool sync_check_enabled() {
+    static int v = [] {
+        const char* e = std::getenv("STREE_SYNC_CHECK");
+        return (e && e[0] && e[0] != '0') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
+stree_status finish(int cuda_rc, int32_t* dev_status, cudaStream_t s) {
+    if (cuda_rc != 0) return STREE_ERR_CUDA;
+    if (sync_check_enabled()) {
+        if (cudaStreamSynchronize(s) != cudaSuccess) return STREE_ERR_CUDA;
+        if (dev_status) {
+            int32_t v = 0;
+            if (cudaMemcpy(&v, dev_status, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return STREE_ERR_CUDA;
+            if (v) return STREE_ERR_DEVICE;
+        }
+    }
+    return STREE_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+stree_status check_dims(const stree_dims* d) {
+    if (!d) return STREE_ERR_NULL;
+    if (d->batch < 0 || d->n_nodes < 0 || d->n_nodes > STREE_MAX_NODES) return STREE_ERR_SHAPE;
+    if (d->n_heads < 1 || d->head_dim < 1 || d->d_state < 1 || d->n_groups < 1) return STREE_ERR_SHAPE;
+    if (d->n_heads % d->n_groups) return STREE_ERR_SHAPE;
+    if (d->io_dtype != STREE_F32 && d->io_dtype != STREE_BF16) return STREE_ERR_DTYPE;
+    return STREE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
+
+const char* stree_status_string(stree_status s) {
+    switch (s) {
+        case STREE_OK: return "ok";
+        case STREE_ERR_NULL: return "null pointer";
+        case STREE_ERR_SHAPE: return "bad shape";
+        case STREE_ERR_DTYPE: return "unsupported dtype";
+        case STREE_ERR_ALIGN: return "misaligned pointer";
+        case STREE_ERR_UNSUPPORTED: return "unsupported configuration";
+        case STREE_ERR_CUDA: return "cuda error";
+        case STREE_ERR_DEVICE: return "device-side status set";
+    }
+    return "unknown status";
+}
+
+stree_status stree_set_scan_impl(stree_scan_impl impl) {
+    if (impl != STREE_SCAN_AUTO && impl != STREE_SCAN_SIMT && impl != STREE_SCAN_TC) return STREE_ERR_UNSUPPORTED;
+    g_scan_impl.store((int)impl);
+    return STREE_OK;
+}
+
+int32_t stree_scan_kernel_for(const stree_dims* d) {
+    if (check_dims(d) != STREE_OK) return 0;
+    int impl = g_scan_impl.load();
+    if (impl == STREE_SCAN_SIMT) return 1;
+    if (stree_tc_supports(d)) return 2;
+    return impl == STREE_SCAN_TC ? 0 : 1;
+}
+
+stree_status stree_build_mask(const int32_t* parent, int32_t batch, int32_t n_nodes, uint32_t* mask,
+                              int32_t* depth, int32_t* dev_status, void* stream) {
+    if (batch < 0 || n_nodes < 0 || n_nodes > STREE_MAX_NODES) return STREE_ERR_SHAPE;
+    if (batch == 0 || n_nodes == 0) return STREE_OK;
+    if (!parent || !mask) return STREE_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_build_mask(parent, batch, n_nodes, mask, depth, dev_status, s), dev_status, s);
+}
+
+stree_status stree_tree_scan(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm,
+                             const void* Cm, const float* D, const float* h0, const int32_t* parent, void* y,
+                             int32_t* dev_status, void* stream) {
+    stree_status st = check_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!x || !dt || !A || !Bm || !Cm || !parent || !y) return STREE_ERR_NULL;
+    const void* ptrs[] = {x, dt, A, Bm, Cm, D, h0, parent, y};
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return STREE_ERR_ALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    int which = stree_scan_kernel_for(d);
+    if (which == 0) return STREE_ERR_UNSUPPORTED;
+    int rc = (which == 2) ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
+                          : stree_launch_scan_simt(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s);
+    return finish(rc, dev_status, s);
+}
+
+stree_status stree_accept(const int32_t* tokens, const int32_t* parent, const int32_t* vtok, int32_t batch,
+                          int32_t n_nodes, int32_t* path, int32_t* path_len, int32_t* bonus, int32_t* dev_status,
+                          void* stream) {
+    if (batch < 0 || n_nodes < 0 || n_nodes > STREE_MAX_NODES) return STREE_ERR_SHAPE;
+    if (batch == 0 || n_nodes == 0) return STREE_OK;
+    if (!tokens || !parent || !vtok || !path || !path_len || !bonus) return STREE_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_accept(tokens, parent, vtok, batch, n_nodes, path, path_len, bonus, dev_status, s),
+                  dev_status, s);
+}
+
+stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm,
+                          const float* h0, const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                          float* h_new, int32_t* dev_status, void* stream) {
+    stree_status st = check_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!x || !dt || !A || !Bm || !path || !path_len || !h_new) return STREE_ERR_NULL;
+    if (!aligned16(h_new) || (h0 && !aligned16(h0))) return STREE_ERR_ALIGN;
+    if (h0 && h0 != h_new) {
+        // partial overlap is not allowed (in-place is)
+        const char* a = (const char*)h0;
+        const char* b = (const char*)h_new;
+        size_t bytes = (size_t)d->batch * d->n_heads * d->head_dim * d->d_state * sizeof(float);
+        if (a < b + bytes && b < a + bytes) return STREE_ERR_SHAPE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_commit(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s),
+                  dev_status, s);
+}
+
+}  // extern "C"

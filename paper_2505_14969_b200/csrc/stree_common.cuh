@@ -1,0 +1,83 @@
+// stree_common.cuh — device helpers shared by the STree kernels (CUDA path only).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stree.h"
+
+namespace stree {
+
+constexpr int kMaxNodes = STREE_MAX_NODES;          // T <= 256
+constexpr int kMaxWords = (kMaxNodes + 31) / 32;    // mask words per row
+
+__device__ __forceinline__ void report(int32_t* dev_status, int code) {
+    if (dev_status) atomicCAS(dev_status, 0, code);
+}
+
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Validates one tree (PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i)
+// and builds its ancestor-mask rows L[i] in shared memory by
+// pointer jumping: after round k, row(i) holds the ancestors at distance < 2^k
+// and jmp(i) is the 2^k-th ancestor, so ceil(log2 T) rounds give the full
+// root-to-i path.  All threads of the block must call this.
+//   sp    : parent[T] already in smem (int)
+//   rows  : [T][W] uint32 output; rows2: [T][W] scratch; jmp/jmp2: [T] int scratch
+// Returns 0 or the device status code (1 bad root / 2 bad parent); rows are
+// zero for an invalid tree.
+__device__ __forceinline__ int build_tree_rows(const int* sp, int T, int W, uint32_t* rows,
+                                               uint32_t* rows2, int* jmp, int* jmp2) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    int bad = 0;
+    for (int i = tid; i < T; i += nt) {
+        int p = sp[i];
+        if (i == 0) { if (p != -1) bad = max(bad, 1); }
+        else if (p < 0 || p >= i) bad = max(bad, 2);
+    }
+    // block-wide max of the error code
+    int any1 = __syncthreads_or(bad == 1);
+    int any2 = __syncthreads_or(bad == 2);
+    int code = any1 ? 1 : (any2 ? 2 : 0);
+    if (code) {
+        for (int k = tid; k < T * W; k += nt) rows[k] = 0u;
+        __syncthreads();
+        return code;
+    }
+    for (int i = tid; i < T; i += nt) {
+        for (int w = 0; w < W; ++w) rows[i * W + w] = (w == (i >> 5)) ? (1u << (i & 31)) : 0u;
+        jmp[i] = sp[i];
+    }
+    __syncthreads();
+    uint32_t* ra = rows; uint32_t* rb = rows2;
+    int* ja = jmp; int* jb = jmp2;
+    int rounds = 0;
+    while ((1 << rounds) < T) ++rounds;
+    for (int r = 0; r < rounds; ++r) {
+        for (int i = tid; i < T; i += nt) {
+            int j = ja[i];
+            for (int w = 0; w < W; ++w) rb[i * W + w] = ra[i * W + w] | (j >= 0 ? ra[j * W + w] : 0u);
+            jb[i] = j >= 0 ? ja[j] : -1;
+        }
+        __syncthreads();
+        uint32_t* t = ra; ra = rb; rb = t;
+        int* tj = ja; ja = jb; jb = tj;
+    }
+    if (ra != rows) {
+        for (int k = tid; k < T * W; k += nt) rows[k] = ra[k];
+        __syncthreads();
+    }
+    return 0;
+}
+
+__device__ __forceinline__ bool mask_bit(const uint32_t* rows, int W, int i, int j) {
+    return (rows[i * W + (j >> 5)] >> (j & 31)) & 1u;
+}
+
+}  // namespace stree
