@@ -1,10 +1,649 @@
-// K2 stree_tree_scan on tcgen05 tensor cores (placeholder until the kernel lands).
+// K2 stree_tree_scan on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// The packed-tree SSM output of PAPER.md:91-102 (Mamba-2 realisation):
+//     y_i = e^{Λ_i} C_i·h0_hᵀ  +  Σ_{j∈path(i)} e^{Λ_i-Λ_j} dt_j (C_i·B_j) x_j  +  D_h x_i
+// as three dense contractions per tree / head, all on chip:
+//     G   = C·Bᵀ                 (T x T, K = N)    kind::f16   bf16 x bf16 -> fp32 TMEM   (once per tree)
+//     Y0  = C·h0_hᵀ              (T x P, K = N)    kind::tf32  fp32 state  -> fp32 TMEM   (per head; dominant stream)
+//     Y'  = (L∘G∘c_h)·X_h        (T x P, K = T)    kind::f16   bf16 masked weights x bf16 x   (per head)
+// and an epilogue y = e^{Λ_i} Y0 + e'_i Y' + D x (fp32) -> bf16 -> TMA store.
+// Λ = L·(dt A_h) is the tree segsum (Eq. a_tree) built by pointer
+// jumping over the ancestor chains; the decay mask is applied before any exp
+// (SURVEY R4).  The decay factorises, e^{Λ_i-Λ_j} = e^{Λ_i-ref}·e^{ref-Λ_j},
+// whenever min Λ >= -120 (ref = min Λ / 2 keeps both factors inside e^{±60});
+// the masked weights then need no per-element exp.  Heads with deeper decay use
+// the direct per-element e^{Λ_i-Λ_j}.
+//
+// One CTA = one tree and a range of heads of one group (grid = B x G x chunks),
+// 192 threads, warp-specialised:
+//   warp 0      TMA producer: C, B once; then per head h0_h (4 boxes) + x_h, NSTAGE-deep ring
+//   warp 1      tcgen05.mma issuer (one elected thread) + TMEM allocator
+//   warps 2-5   tree / segsum prologue, C -> tf32 conversion, masked-weight build,
+//               TMEM -> register epilogue, TMA store of y
+// Rows are the tree nodes (M = 128 with rows >= T ignored; every MMA row is
+// independent so the unused rows may read arbitrary shared memory).
+//
+// Served shapes: bf16 io, P = 64, N in {64, 128}, 1 <= T <= 64.  Everything
+// else goes to the SIMT kernel (stree_scan_simt.cu).
+#include <cuda.h>
+
 #include "stree_common.cuh"
 
-extern "C" int stree_tc_supports(const stree_dims* d) { (void)d; return 0; }
+namespace stree {
+namespace tc {
 
-extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*, const float*, const void*,
-                                    const void*, const float*, const float*, const int32_t*, void*, int32_t*,
-                                    cudaStream_t) {
-    return (int)cudaErrorNotSupported;
+constexpr int kT = 64;          // max nodes per tree served
+constexpr int kP = 64;          // head dim
+constexpr int kStages = 3;      // h0/x ring depth
+constexpr int kHPC = 12;        // max heads per CTA
+constexpr int kThreads = 192;
+constexpr int kEpi0 = 64;       // first epilogue thread
+constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
+constexpr uint32_t kTmemCols = 512;
+constexpr int kAccCol0 = 128;   // acc a: Y0 at 128 + 128a, Y' at 128 + 128a + 64
+
+template <int NS>
+struct Smem {
+    static constexpr int kCtAtoms = NS / 32;              // tf32 C: 32 fp32 per 128B row chunk
+    static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
+    static constexpr int CT = 0;                          // C as tf32 (A of Y0)
+    static constexpr int U = CT + kCtAtoms * kAtom;       // union: {C bf16, B bf16} then {M'[2], ystage[2]}
+    static constexpr int CB = U;
+    static constexpr int BB = U + kCbAtoms * kAtom;
+    static constexpr int MB = U;                          // M'[a] at MB + a*kAtom
+    static constexpr int YS = U + 2 * kAtom;              // ystage[a] at YS + a*kAtom
+    static constexpr int UBYTES = (2 * kCbAtoms * kAtom > 4 * kAtom) ? 2 * kCbAtoms * kAtom : 4 * kAtom;
+    static constexpr int H0 = U + UBYTES;                 // h0 stages
+    static constexpr int H0S = kP * NS * 4;               // bytes per stage
+    static constexpr int X = H0 + kStages * H0S;          // x stages
+    static constexpr int XS = kAtom;
+    static constexpr int MISC = X + kStages * XS;
+    // misc (4-byte words unless noted)
+    static constexpr int PAR = MISC;                      // int[64]
+    static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
+    static constexpr int JMP = ROWS + 64 * 8;             // int[7][64]
+    static constexpr int SBUF = JMP + 7 * 64 * 4;         // float[2][kHPC][64]
+    static constexpr int DTS = SBUF + 2 * kHPC * 64 * 4;  // float[kHPC][64]
+    static constexpr int LAM = DTS + kHPC * 64 * 4;       // float[kHPC][64]
+    static constexpr int CJ = LAM + kHPC * 64 * 4;        // float[kHPC][64]
+    static constexpr int EI = CJ + kHPC * 64 * 4;         // float[kHPC][64]
+    static constexpr int E0 = EI + kHPC * 64 * 4;         // float[kHPC][64]
+    static constexpr int MODE = E0 + kHPC * 64 * 4;       // int[kHPC]
+    static constexpr int BAR = (MODE + kHPC * 4 + 7) & ~7;
+    // barriers (u64): tree, ctf32, gdone, full[3], empty[3], mfull[2], mempty[2], accfull[2], accempty[2]
+    static constexpr int NBAR = 3 + 2 * kStages + 8;
+    static constexpr int TMEMP = BAR + NBAR * 8;
+    static constexpr int TOTAL = TMEMP + 16;
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// D[tmem] (+)= A[smem desc] · B[smem desc]ᵀ
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (sm_100 encoding: version 1, layout 2).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;   // version (Blackwell)
+    d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor (kind::f16 / kind::tf32): fp32 accumulate.
+__host__ __device__ constexpr uint32_t idesc(uint32_t ab_fmt, uint32_t b_mn_major, int M, int N) {
+    return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | (b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+constexpr uint32_t kFmtBF16 = 1, kFmtTF32 = 2;
+
+// byte offset of 16-byte chunk c of row r inside a swizzle-128B tile (rows of 128 B)
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct Params {
+    int B, T, H, G, cpg, hpc;  // cpg = head chunks per group, hpc = heads per chunk
+    const float* dt;
+    const float* A;
+    const float* D;
+    const int32_t* parent;
+    __nv_bfloat16* y;
+    int32_t* dev_status;
+    int has_h0;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kThreads, 1)
+    scan_tc_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
+                   const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
+                   const __grid_constant__ CUtensorMap tm_y, const Params prm) {
+    using S = Smem<NS>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t sb = smem_u32(sm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int T = prm.T, H = prm.H;
+    const int b = blockIdx.x / (prm.G * prm.cpg);
+    const int rem = blockIdx.x % (prm.G * prm.cpg);
+    const int g = rem / prm.cpg, chunk = rem % prm.cpg;
+    const int hpg = H / prm.G;
+    const int hbeg = g * hpg + chunk * prm.hpc;
+    const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
+    if (nh <= 0) return;
+    int* sp = (int*)(sm + S::PAR);
+
+    // ---- tree validation (all threads; PAPER.md:90 precondition) ----
+    int bad = 0;
+    for (int i = tid; i < T; i += kThreads) {
+        int p = prm.parent[(size_t)b * T + i];
+        sp[i] = p;
+        if (i == 0) { if (p != -1) bad = 1; }
+        else if (p < 0 || p >= i) bad = 2;
+    }
+    const int any1 = __syncthreads_or(bad == 1), any2 = __syncthreads_or(bad == 2);
+    if (any1 | any2) {
+        if (tid == 0 && chunk == 0 && g == 0) report(prm.dev_status, any1 ? 1 : 2);
+        for (int k = tid; k < T * nh * kP; k += kThreads) {
+            int i = k / (nh * kP), hh = (k / kP) % nh, p = k % kP;
+            prm.y[(((size_t)b * T + i) * H + hbeg + hh) * kP + p] = __float2bfloat16_rn(0.f);
+        }
+        return;
+    }
+
+    const uint32_t bar0 = sb + S::BAR;
+    const uint32_t BAR_TREE = bar0, BAR_CTF = bar0 + 8, BAR_G = bar0 + 16;
+    auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };
+    auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kStages + 8 * s; };
+    auto bar_mfull = [&](int a) { return bar0 + 24 + 16 * kStages + 8 * a; };
+    auto bar_mempty = [&](int a) { return bar0 + 24 + 16 * kStages + 16 + 8 * a; };
+    auto bar_accfull = [&](int a) { return bar0 + 24 + 16 * kStages + 32 + 8 * a; };
+    auto bar_accempty = [&](int a) { return bar0 + 24 + 16 * kStages + 48 + 8 * a; };
+    uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
+
+    if (tid == 0) {
+        mbar_init(BAR_TREE, 1);
+        mbar_init(BAR_CTF, 128);
+        mbar_init(BAR_G, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(bar_full(s), 1);
+            mbar_init(bar_empty(s), 2);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(bar_mfull(a), 4);
+            mbar_init(bar_mempty(a), 1);
+            mbar_init(bar_accfull(a), 1);
+            mbar_init(bar_accempty(a), 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int Tp16 = (T + 15) & ~15;
+    const int xbytes = T * 128;
+
+    if (warp == 0) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
+            mbar_expect_tx(BAR_TREE, 2 * S::kCbAtoms * xbytes);
+            for (int a = 0; a < S::kCbAtoms; ++a) {
+                tma_load_2d(sb + S::CB + a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
+                tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
+            }
+            for (int k = 0; k < nh; ++k) {
+                const int s = k % kStages;
+                mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
+                const int h = hbeg + k;
+                mbar_expect_tx(bar_full(s), (prm.has_h0 ? S::H0S : 0) + xbytes);
+                if (prm.has_h0)
+                    for (int a = 0; a < NS / 32; ++a)
+                        tma_load_2d(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
+                                    ((b * H) + h) * kP);
+                tma_load_2d(sb + S::X + s * S::XS, &tm_x, bar_full(s), h * kP, b * T);
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            mbar_wait(BAR_TREE, 0);
+            tc_fence_after();
+            // G = C·Bᵀ (once per tree), kind::f16 bf16, M=128, N=Tp16, K=NS
+            const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
+            for (int kk = 0; kk < NS / 16; ++kk) {
+                uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+                mma_f16(tmem + 0, sdesc(sb + S::CB + off, 16, 1024), sdesc(sb + S::BB + off, 16, 1024), id_g,
+                        kk > 0);
+            }
+            tc_commit(BAR_G);
+            mbar_wait(BAR_CTF, 0);
+            tc_fence_after();
+            const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
+            const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
+            for (int k = 0; k < nh; ++k) {
+                const int s = k % kStages, a = k & 1;
+                mbar_wait(bar_full(s), (k / kStages) & 1);
+                mbar_wait(bar_accempty(a), ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d0 = tmem + kAccCol0 + 128 * a;
+                if (prm.has_h0) {
+                    // Y0 = C·h0_hᵀ, kind::tf32, K = NS in steps of 8 (32 B)
+                    for (int kk = 0; kk < NS / 8; ++kk) {
+                        uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+                        mma_tf32(d0, sdesc(sb + S::CT + off, 16, 1024), sdesc(sb + S::H0 + s * S::H0S + off, 16, 1024),
+                                 id_y0, kk > 0);
+                    }
+                }
+                mbar_wait(bar_mfull(a), (k >> 1) & 1);
+                tc_fence_after();
+                // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j)
+                for (int kk = 0; kk < Tp16 / 16; ++kk)
+                    mma_f16(d0 + 64, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
+                            sdesc(sb + S::X + s * S::XS + kk * 2048, kAtom, 1024), id_y, kk > 0);
+                tc_commit(bar_accfull(a));
+                tc_commit(bar_mempty(a));
+                tc_commit(bar_empty(s));
+            }
+        }
+    } else {
+        // ================= epilogue / math warps (128 threads) =================
+        const int e = tid - kEpi0;
+        const int quad = warp & 3;           // TMEM lane quadrant of this warp
+        const int row = quad * 32 + lane;    // tree node owned in TMEM-based work
+        uint64_t* rows = (uint64_t*)(sm + S::ROWS);
+        int* jmp = (int*)(sm + S::JMP);
+        float* sbuf = (float*)(sm + S::SBUF);
+        float* dts = (float*)(sm + S::DTS);
+        float* lam = (float*)(sm + S::LAM);
+        float* cj = (float*)(sm + S::CJ);
+        float* ei = (float*)(sm + S::EI);
+        float* e0 = (float*)(sm + S::E0);
+        int* mode = (int*)(sm + S::MODE);
+        int rounds = 0;
+        while ((1 << rounds) < T) ++rounds;
+
+        // ---- ancestor mask rows by pointer jumping ----
+        uint64_t myrow = 0;
+        int myj = -1;
+        if (e < T) {
+            myrow = 1ull << e;
+            myj = sp[e];
+            rows[e] = myrow;
+            jmp[e] = myj;
+        }
+        named_bar(1, 128);
+        for (int r = 0; r < rounds; ++r) {
+            uint64_t orow = 0;
+            int oj = -1;
+            if (e < T && myj >= 0) { orow = rows[myj]; oj = jmp[r * 64 + myj]; }
+            named_bar(1, 128);
+            if (e < T) {
+                myrow |= orow;
+                myj = oj;
+                rows[e] = myrow;
+                jmp[(r + 1) * 64 + e] = myj;
+            }
+            named_bar(1, 128);
+        }
+        // ---- per-head tree segsum Λ = L·(dt A_h), pointer jumping ----
+        for (int k = e; k < nh * T; k += 128) {
+            int hh = k / T, i = k % T;
+            float d = prm.dt[((size_t)b * T + i) * H + hbeg + hh];
+            dts[hh * 64 + i] = d;
+            sbuf[hh * 64 + i] = d * prm.A[hbeg + hh];
+        }
+        named_bar(1, 128);
+        float* scur = sbuf;
+        float* snext = sbuf + kHPC * 64;
+        for (int r = 0; r < rounds; ++r) {
+            for (int k = e; k < nh * T; k += 128) {
+                int hh = k / T, i = k % T;
+                int j = jmp[r * 64 + i];
+                snext[hh * 64 + i] = scur[hh * 64 + i] + (j >= 0 ? scur[hh * 64 + j] : 0.f);
+            }
+            named_bar(1, 128);
+            float* t = scur; scur = snext; snext = t;
+        }
+        for (int k = e; k < nh * T; k += 128) lam[(k / T) * 64 + k % T] = scur[(k / T) * 64 + k % T];
+        named_bar(1, 128);
+        if (e < nh) {
+            float mn = 0.f;
+            for (int i = 0; i < T; ++i) mn = fminf(mn, lam[e * 64 + i]);
+            mode[e] = (mn >= -120.f) ? 1 : 0;   // 1: factorised decay
+            sbuf[e] = 0.5f * mn;                  // ref (scratch: scur no longer needed)
+        }
+        named_bar(1, 128);
+        for (int k = e; k < nh * T; k += 128) {
+            int hh = k / T, i = k % T;
+            float l = lam[hh * 64 + i], ref = sbuf[hh];
+            bool f = mode[hh] != 0;
+            cj[hh * 64 + i] = f ? __expf(ref - l) * dts[hh * 64 + i] : dts[hh * 64 + i];
+            ei[hh * 64 + i] = f ? __expf(l - ref) : 1.f;
+            e0[hh * 64 + i] = __expf(l);
+        }
+        // ---- C (bf16, TMA) -> tf32 operand tile; zero the padded x rows ----
+        mbar_wait(BAR_TREE, 0);
+        {
+            const int i = e & 63, half = e >> 6;      // two threads per row
+            if (i < T) {
+                constexpr int kChunks = NS / 8;        // 16-byte bf16 chunks per row
+                for (int c = half * (kChunks / 2); c < (half + 1) * (kChunks / 2); ++c) {
+                    const int a = c >> 3, cc = c & 7;  // bf16 atom / chunk
+                    uint4 v = *reinterpret_cast<const uint4*>(sm + S::CB + a * kAtom + swz(i, cc));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    float f[8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        f[2 * q] = __uint_as_float(w[q] << 16);
+                        f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                    }
+                    // 8 fp32 = 2 tf32 chunks: column 8c..8c+7 -> tf32 atom (8c)/32, chunk ((8c)%32)/4
+                    const int col = 8 * c, ta = col >> 5, tc0 = (col & 31) >> 2;
+                    *reinterpret_cast<float4*>(sm + S::CT + ta * kAtom + swz(i, tc0)) =
+                        make_float4(f[0], f[1], f[2], f[3]);
+                    *reinterpret_cast<float4*>(sm + S::CT + ta * kAtom + swz(i, tc0 + 1)) =
+                        make_float4(f[4], f[5], f[6], f[7]);
+                }
+            }
+            for (int k = e; k < kStages * (Tp16 - T) * 8; k += 128) {
+                const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
+                *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        fence_proxy_async();
+        mbar_arrive(BAR_CTF);
+        named_bar(1, 128);
+
+        // ---- G row (TMEM lanes 0..T-1) -> registers ----
+        mbar_wait(BAR_G, 0);
+        tc_fence_after();
+        const bool own = (quad < 2) && (row < T);
+        float gr[64];
+        uint64_t mybits = 0;
+        if (quad < 2) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + 16 * c, gr + 16 * c);
+            if (row < T) mybits = rows[row];
+        }
+
+        // masked weights of head k into M'[k & 1] (row-owner threads only)
+        auto build_m = [&](int k) {
+            const int a = k & 1;
+            mbar_wait(bar_mempty(a), ((k >> 1) & 1) ^ 1);
+            if (own) {
+                const float* c = cj + k * 64;
+                const bool f = mode[k] != 0;
+                const float li = lam[k * 64 + row];
+                unsigned char* mrow = sm + S::MB + a * kAtom;
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    float w[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int j = 8 * ch + q;
+                        float v;
+                        if (f) v = c[j] * gr[j];
+                        else v = __expf(fminf(li - lam[k * 64 + j], 0.f)) * c[j] * gr[j];
+                        w[q] = ((mybits >> j) & 1ull) ? v : 0.f;
+                    }
+                    *reinterpret_cast<uint4*>(mrow + swz(row, ch)) =
+                        make_uint4(pack_bf16(w[0], w[1]), pack_bf16(w[2], w[3]), pack_bf16(w[4], w[5]),
+                                   pack_bf16(w[6], w[7]));
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_mfull(a));
+        };
+
+        build_m(0);
+        for (int k = 0; k < nh; ++k) {
+            if (k + 1 < nh) build_m(k + 1);
+            const int s = k % kStages, a = k & 1;
+            const int h = hbeg + k;
+            mbar_wait(bar_accfull(a), (k >> 1) & 1);
+            tc_fence_after();
+            if (e == 0) bulk_wait_read1();
+            named_bar(1, 128);
+            if (quad < 2) {
+                const float Dh = prm.D ? prm.D[h] : 0.f;
+                const float s0 = own ? e0[k * 64 + row] : 0.f, s1 = own ? ei[k * 64 + row] : 0.f;
+                const unsigned char* xr = sm + S::X + s * S::XS;
+                unsigned char* yr = sm + S::YS + a * kAtom;
+                const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + kAccCol0 + 128 * a;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float v0[16], v1[16];
+                    if (prm.has_h0) tmem_ld16(tl + 16 * c, v0);
+                    else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) v0[q] = 0.f;
+                    }
+                    tmem_ld16(tl + 64 + 16 * c, v1);
+                    if (own) {
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            const int ch = 2 * c + half;
+                            uint4 xv = *reinterpret_cast<const uint4*>(xr + swz(row, ch));
+                            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+                            uint32_t o[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
+                                const int p = 8 * half + 2 * q;
+                                const float ya = fmaf(s0, v0[p], fmaf(s1, v1[p], Dh * xa));
+                                const float yb = fmaf(s0, v0[p + 1], fmaf(s1, v1[p + 1], Dh * xb));
+                                o[q] = pack_bf16(ya, yb);
+                            }
+                            *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_accempty(a));
+            named_bar(1, 128);
+            if (e == 0) {
+                tma_store_2d(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T);
+                bulk_commit();
+                mbar_arrive(bar_empty(s));
+            }
+        }
+        if (e == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+}  // namespace tc
+}  // namespace stree
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace
+
+extern "C" int stree_tc_supports(const stree_dims* d) {
+    if (!d) return 0;
+    if (d->io_dtype != STREE_BF16) return 0;
+    if (d->head_dim != stree::tc::kP) return 0;
+    if (d->d_state != 64 && d->d_state != 128) return 0;
+    if (d->n_nodes < 1 || d->n_nodes > stree::tc::kT) return 0;
+    if (d->n_groups < 1 || d->n_heads % d->n_groups) return 0;
+    return 1;
+}
+
+extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                    const void* Bm, const void* Cm, const float* D, const float* h0,
+                                    const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s) {
+    using namespace stree::tc;
+    if (!stree_tc_supports(d)) return (int)cudaErrorNotSupported;
+    const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
+    CUtensorMap mc, mb, mx, mh, my;
+    const uint64_t BT = (uint64_t)B * T;
+    bool ok = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
+              make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
+              make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, T) &&
+              make_map(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, T);
+    if (h0)
+        ok = ok && make_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h0, (uint64_t)N, (uint64_t)B * H * P,
+                            (uint64_t)N * 4, 32, 64);
+    else
+        mh = mx;  // unused
+    if (!ok) return (int)cudaErrorInvalidValue;
+    // work split: one tree per CTA, heads of one group in chunks, ~1 wave over the SMs
+    const int hpg = H / G;
+    int target = (num_sms() + B - 1) / B;          // CTAs per tree
+    int cpg = (target + G - 1) / G;                 // chunks per group
+    if (cpg < 1) cpg = 1;
+    int hpc = (hpg + cpg - 1) / cpg;
+    if (hpc > kHPC) hpc = kHPC;
+    cpg = (hpg + hpc - 1) / hpc;
+    stree::tc::Params prm{B, T, H, G, cpg, hpc, dt, A, D, parent, (__nv_bfloat16*)y, dev_status, h0 != nullptr};
+    dim3 grid(B * G * cpg);
+    cudaError_t e;
+    if (N == 128) {
+        size_t smem = Smem<128>::TOTAL + 1024;
+        e = cudaFuncSetAttribute(scan_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        scan_tc_kernel<128><<<grid, kThreads, smem, s>>>(mc, mb, mx, mh, my, prm);
+    } else {
+        size_t smem = Smem<64>::TOTAL + 1024;
+        e = cudaFuncSetAttribute(scan_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        scan_tc_kernel<64><<<grid, kThreads, smem, s>>>(mc, mb, mx, mh, my, prm);
+    }
+    return (int)cudaGetLastError();
 }
