@@ -18,8 +18,9 @@
 // 192 threads, warp-specialised:
 //   warp 0      TMA producer: C, B once; then per head h0_h (4 boxes) + x_h, NSTAGE-deep ring
 //   warp 1      tcgen05.mma issuer (one elected thread) + TMEM allocator
-//   warps 2-5   tree / segsum prologue, C -> tf32 conversion, masked-weight build,
-//               TMEM -> register epilogue, TMA store of y
+//   warps 2-5   tree / segsum prologue, C -> tf32 conversion; then warps 2,3 build the
+//               masked weights of head k+1 while warps 4,5 (TMEM lanes 0..63) run the
+//               TMEM -> register epilogue of head k and the TMA store of y
 // Rows are the tree nodes (M = 128 with rows >= T ignored; every MMA row is
 // independent so the unused rows may read arbitrary shared memory).
 //
@@ -34,20 +35,19 @@ namespace tc {
 
 constexpr int kT = 64;          // max nodes per tree served
 constexpr int kP = 64;          // head dim
-constexpr int kStages = 3;      // h0/x ring depth
+constexpr int kStages = 4;      // h0/x ring depth
 constexpr int kHPC = 12;        // max heads per CTA
 constexpr int kThreads = 192;
 constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
 constexpr uint32_t kTmemCols = 512;
-constexpr int kAccCol0 = 128;   // acc a: Y0 at 128 + 128a, Y' at 128 + 128a + 64
+constexpr int kCCol = 64;       // C as tf32 (A operand of Y0) in TMEM columns [64, 64 + N)
+constexpr int kAccCol0 = 256;   // acc a: Y0 at 256 + 128a, Y' at 256 + 128a + 64
 
 template <int NS>
 struct Smem {
-    static constexpr int kCtAtoms = NS / 32;              // tf32 C: 32 fp32 per 128B row chunk
     static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
-    static constexpr int CT = 0;                          // C as tf32 (A of Y0)
-    static constexpr int U = CT + kCtAtoms * kAtom;       // union: {C bf16, B bf16} then {M'[2], ystage[2]}
+    static constexpr int U = 0;                           // union: {C bf16, B bf16} then {M'[2], ystage[2]}
     static constexpr int CB = U;
     static constexpr int BB = U + kCbAtoms * kAtom;
     static constexpr int MB = U;                          // M'[a] at MB + a*kAtom
@@ -61,15 +61,14 @@ struct Smem {
     // misc (4-byte words unless noted)
     static constexpr int PAR = MISC;                      // int[64]
     static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
-    static constexpr int JMP = ROWS + 64 * 8;             // int[7][64]
-    static constexpr int SBUF = JMP + 7 * 64 * 4;         // float[2][kHPC][64]
-    static constexpr int DTS = SBUF + 2 * kHPC * 64 * 4;  // float[kHPC][64]
-    static constexpr int LAM = DTS + kHPC * 64 * 4;       // float[kHPC][64]
+    static constexpr int LAM = ROWS + 64 * 8;             // float[kHPC][64]
     static constexpr int CJ = LAM + kHPC * 64 * 4;        // float[kHPC][64]
     static constexpr int EI = CJ + kHPC * 64 * 4;         // float[kHPC][64]
     static constexpr int E0 = EI + kHPC * 64 * 4;         // float[kHPC][64]
     static constexpr int MODE = E0 + kHPC * 64 * 4;       // int[kHPC]
-    static constexpr int BAR = (MODE + kHPC * 4 + 7) & ~7;
+    static constexpr int AS = MODE + kHPC * 4;            // float[kHPC]  A_h
+    static constexpr int DS = AS + kHPC * 4;              // float[kHPC]  D_h
+    static constexpr int BAR = (DS + kHPC * 4 + 7) & ~7;
     // barriers (u64): tree, ctf32, gdone, full[3], empty[3], mfull[2], mempty[2], accfull[2], accempty[2]
     static constexpr int NBAR = 3 + 2 * kStages + 8;
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -142,6 +141,26 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+// D[tmem] (+)= A[tmem] · B[smem desc]ᵀ  (A in tensor memory: M lanes x K columns of 32 bit)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // 32 lanes x 32 bit, 16 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     uint32_t r[16];
@@ -154,6 +173,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// 32 lanes x 32 bit, 32 consecutive columns per thread; caller issues tmem_wait() before use
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (sm_100 encoding: version 1, layout 2).
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -180,7 +212,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct Params {
+    unsigned long long* trace;  // optional per-CTA phase timestamps (debug)
     int B, T, H, G, cpg, hpc;  // cpg = head chunks per group, hpc = heads per chunk
     const float* dt;
     const float* A;
@@ -198,8 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tm_y, const Params prm) {
     using S = Smem<NS>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
+    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 64 : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = gtimer();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int T = prm.T, H = prm.H;
     const int b = blockIdx.x / (prm.G * prm.cpg);
@@ -211,6 +252,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (nh <= 0) return;
     int* sp = (int*)(sm + S::PAR);
 
+    // ---- per-CTA inputs issued first so their latency overlaps the setup ----
+    // epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane and lane+32
+    constexpr int kHPW = kHPC / 4;            // heads per epilogue warp
+    float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
+    if (tid >= kEpi0) {
+        const int ew = (tid - kEpi0) >> 5;
+#pragma unroll
+        for (int q = 0; q < kHPW; ++q) {
+            const int hh = ew + 4 * q;
+            const bool hv = hh < nh;
+            a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
+            d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
+            }
+        }
+    }
     // ---- tree validation (all threads; PAPER.md:90 precondition) ----
     int bad = 0;
     for (int i = tid; i < T; i += kThreads) {
@@ -248,10 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(bar_empty(s), 2);
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_mfull(a), 4);
+            mbar_init(bar_mfull(a), 2);
             mbar_init(bar_mempty(a), 1);
             mbar_init(bar_accfull(a), 1);
-            mbar_init(bar_accempty(a), 4);
+            mbar_init(bar_accempty(a), 2);
         }
         fence_barrier_init();
     }
@@ -308,15 +368,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages, a = k & 1;
                 mbar_wait(bar_full(s), (k / kStages) & 1);
+                if (trace && k < 12) trace[30 + k] = gtimer();
                 mbar_wait(bar_accempty(a), ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d0 = tmem + kAccCol0 + 128 * a;
                 if (prm.has_h0) {
-                    // Y0 = C·h0_hᵀ, kind::tf32, K = NS in steps of 8 (32 B)
+                    // Y0 = C·h0_hᵀ, kind::tf32, A = C from TMEM, K = NS in steps of 8 (32 B / 8 columns)
                     for (int kk = 0; kk < NS / 8; ++kk) {
                         uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-                        mma_tf32(d0, sdesc(sb + S::CT + off, 16, 1024), sdesc(sb + S::H0 + s * S::H0S + off, 16, 1024),
-                                 id_y0, kk > 0);
+                        mma_tf32_ts(d0, tmem + kCCol + 8 * kk, sdesc(sb + S::H0 + s * S::H0S + off, 16, 1024), id_y0,
+                                    kk > 0);
                     }
                 }
                 mbar_wait(bar_mfull(a), (k >> 1) & 1);
@@ -336,210 +397,254 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;           // TMEM lane quadrant of this warp
         const int row = quad * 32 + lane;    // tree node owned in TMEM-based work
         uint64_t* rows = (uint64_t*)(sm + S::ROWS);
-        int* jmp = (int*)(sm + S::JMP);
-        float* sbuf = (float*)(sm + S::SBUF);
-        float* dts = (float*)(sm + S::DTS);
         float* lam = (float*)(sm + S::LAM);
         float* cj = (float*)(sm + S::CJ);
         float* ei = (float*)(sm + S::EI);
         float* e0 = (float*)(sm + S::E0);
         int* mode = (int*)(sm + S::MODE);
-        int rounds = 0;
-        while ((1 << rounds) < T) ++rounds;
-
-        // ---- ancestor mask rows by pointer jumping ----
-        uint64_t myrow = 0;
-        int myj = -1;
-        if (e < T) {
-            myrow = 1ull << e;
-            myj = sp[e];
-            rows[e] = myrow;
-            jmp[e] = myj;
-        }
-        named_bar(1, 128);
-        for (int r = 0; r < rounds; ++r) {
-            uint64_t orow = 0;
-            int oj = -1;
-            if (e < T && myj >= 0) { orow = rows[myj]; oj = jmp[r * 64 + myj]; }
-            named_bar(1, 128);
-            if (e < T) {
-                myrow |= orow;
-                myj = oj;
-                rows[e] = myrow;
-                jmp[(r + 1) * 64 + e] = myj;
-            }
-            named_bar(1, 128);
-        }
-        // ---- per-head tree segsum Λ = L·(dt A_h), pointer jumping ----
-        for (int k = e; k < nh * T; k += 128) {
-            int hh = k / T, i = k % T;
-            float d = prm.dt[((size_t)b * T + i) * H + hbeg + hh];
-            dts[hh * 64 + i] = d;
-            sbuf[hh * 64 + i] = d * prm.A[hbeg + hh];
-        }
-        named_bar(1, 128);
-        float* scur = sbuf;
-        float* snext = sbuf + kHPC * 64;
-        for (int r = 0; r < rounds; ++r) {
-            for (int k = e; k < nh * T; k += 128) {
-                int hh = k / T, i = k % T;
-                int j = jmp[r * 64 + i];
-                snext[hh * 64 + i] = scur[hh * 64 + i] + (j >= 0 ? scur[hh * 64 + j] : 0.f);
-            }
-            named_bar(1, 128);
-            float* t = scur; scur = snext; snext = t;
-        }
-        for (int k = e; k < nh * T; k += 128) lam[(k / T) * 64 + k % T] = scur[(k / T) * 64 + k % T];
-        named_bar(1, 128);
-        if (e < nh) {
-            float mn = 0.f;
-            for (int i = 0; i < T; ++i) mn = fminf(mn, lam[e * 64 + i]);
-            mode[e] = (mn >= -120.f) ? 1 : 0;   // 1: factorised decay
-            sbuf[e] = 0.5f * mn;                  // ref (scratch: scur no longer needed)
-        }
-        named_bar(1, 128);
-        for (int k = e; k < nh * T; k += 128) {
-            int hh = k / T, i = k % T;
-            float l = lam[hh * 64 + i], ref = sbuf[hh];
-            bool f = mode[hh] != 0;
-            cj[hh * 64 + i] = f ? __expf(ref - l) * dts[hh * 64 + i] : dts[hh * 64 + i];
-            ei[hh * 64 + i] = f ? __expf(l - ref) : 1.f;
-            e0[hh * 64 + i] = __expf(l);
-        }
         // ---- C (bf16, TMA) -> tf32 operand tile; zero the padded x rows ----
+        if (trace && e == 0) trace[1] = gtimer();
         mbar_wait(BAR_TREE, 0);
-        {
-            const int i = e & 63, half = e >> 6;      // two threads per row
-            if (i < T) {
-                constexpr int kChunks = NS / 8;        // 16-byte bf16 chunks per row
-                for (int c = half * (kChunks / 2); c < (half + 1) * (kChunks / 2); ++c) {
-                    const int a = c >> 3, cc = c & 7;  // bf16 atom / chunk
-                    uint4 v = *reinterpret_cast<const uint4*>(sm + S::CB + a * kAtom + swz(i, cc));
+        if (trace && e == 0) trace[2] = gtimer();
+        if (quad < 2) {
+            // C row (bf16, swizzled TMA tile) -> fp32 -> TMEM lane = row, columns [kCCol, kCCol + NS)
+            const int i = row;
+#pragma unroll
+            for (int c32 = 0; c32 < NS / 32; ++c32) {
+                uint32_t f[32];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int c = 4 * c32 + cc, a = c >> 3;   // 16-byte bf16 chunk index along the row
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (i < T) v = *reinterpret_cast<const uint4*>(sm + S::CB + a * kAtom + swz(i, c & 7));
                     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                    float f[8];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        f[2 * q] = __uint_as_float(w[q] << 16);
-                        f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                        f[8 * cc + 2 * q] = w[q] << 16;
+                        f[8 * cc + 2 * q + 1] = w[q] & 0xFFFF0000u;
                     }
-                    // 8 fp32 = 2 tf32 chunks: column 8c..8c+7 -> tf32 atom (8c)/32, chunk ((8c)%32)/4
-                    const int col = 8 * c, ta = col >> 5, tc0 = (col & 31) >> 2;
-                    *reinterpret_cast<float4*>(sm + S::CT + ta * kAtom + swz(i, tc0)) =
-                        make_float4(f[0], f[1], f[2], f[3]);
-                    *reinterpret_cast<float4*>(sm + S::CT + ta * kAtom + swz(i, tc0 + 1)) =
-                        make_float4(f[4], f[5], f[6], f[7]);
                 }
+                tmem_st32(tmem + ((uint32_t)(quad * 32) << 16) + kCCol + 32 * c32, f);
             }
-            for (int k = e; k < kStages * (Tp16 - T) * 8; k += 128) {
+            tmem_st_wait();
+            tc_fence_before();
+        } else {
+            for (int k = e; k < kStages * (Tp16 - T) * 8; k += 64) {
                 const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
                 *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
             }
         }
         fence_proxy_async();
         mbar_arrive(BAR_CTF);
-        named_bar(1, 128);
+        if (trace && e == 0) trace[46] = gtimer();
 
-        // ---- G row (TMEM lanes 0..T-1) -> registers ----
-        mbar_wait(BAR_G, 0);
-        tc_fence_after();
-        const bool own = (quad < 2) && (row < T);
-        float gr[64];
-        uint64_t mybits = 0;
-        if (quad < 2) {
+        int rounds = 0;
+        while ((1 << rounds) < T) ++rounds;
+        const int ew = warp - 2;
+        // ---- ancestor rows L[i] and tree segsum Λ = L·(dt A_h) by pointer jumping in registers
+        //      (PAPER.md:63-66, 86-90): lane holds nodes lane and lane+32; after round r a node's
+        //      row holds its ancestors at distance < 2^r and jp is its 2^r-th ancestor ----
+        uint64_t rw[2];
+        int jp[2];
+        float lm[kHPW][2];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + 16 * c, gr + 16 * c);
-            if (row < T) mybits = rows[row];
+        for (int hf = 0; hf < 2; ++hf) {
+            const int i = lane + 32 * hf;
+            rw[hf] = (i < T) ? (1ull << i) : 0ull;
+            jp[hf] = (i < T) ? sp[i] : -1;
+#pragma unroll
+            for (int q = 0; q < kHPW; ++q) lm[q][hf] = dtr[q][hf] * a_h[q];
         }
-
-        // masked weights of head k into M'[k & 1] (row-owner threads only)
-        auto build_m = [&](int k) {
-            const int a = k & 1;
-            mbar_wait(bar_mempty(a), ((k >> 1) & 1) ^ 1);
-            if (own) {
-                const float* c = cj + k * 64;
-                const bool f = mode[k] != 0;
-                const float li = lam[k * 64 + row];
-                unsigned char* mrow = sm + S::MB + a * kAtom;
+        for (int r = 0; r < rounds; ++r) {
+            uint64_t nrw[2];
+            int njp[2];
+            float nlm[kHPW][2];
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    float w[8];
+            for (int hf = 0; hf < 2; ++hf) {
+                const int j = jp[hf];
+                const int sl = (j >= 0) ? (j & 31) : lane;
+                const bool hi = j >= 32;
+                const uint64_t r0 = __shfl_sync(0xffffffffu, rw[0], sl), r1 = __shfl_sync(0xffffffffu, rw[1], sl);
+                const int j0 = __shfl_sync(0xffffffffu, jp[0], sl), j1 = __shfl_sync(0xffffffffu, jp[1], sl);
+                nrw[hf] = rw[hf] | ((j >= 0) ? (hi ? r1 : r0) : 0ull);
+                njp[hf] = (j >= 0) ? (hi ? j1 : j0) : -1;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int j = 8 * ch + q;
-                        float v;
-                        if (f) v = c[j] * gr[j];
-                        else v = __expf(fminf(li - lam[k * 64 + j], 0.f)) * c[j] * gr[j];
-                        w[q] = ((mybits >> j) & 1ull) ? v : 0.f;
-                    }
-                    *reinterpret_cast<uint4*>(mrow + swz(row, ch)) =
-                        make_uint4(pack_bf16(w[0], w[1]), pack_bf16(w[2], w[3]), pack_bf16(w[4], w[5]),
-                                   pack_bf16(w[6], w[7]));
+                for (int q = 0; q < kHPW; ++q) {
+                    const float v0 = __shfl_sync(0xffffffffu, lm[q][0], sl), v1 = __shfl_sync(0xffffffffu, lm[q][1], sl);
+                    nlm[q][hf] = lm[q][hf] + ((j >= 0) ? (hi ? v1 : v0) : 0.f);
                 }
             }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_mfull(a));
-        };
-
-        build_m(0);
-        for (int k = 0; k < nh; ++k) {
-            if (k + 1 < nh) build_m(k + 1);
-            const int s = k % kStages, a = k & 1;
-            const int h = hbeg + k;
-            mbar_wait(bar_accfull(a), (k >> 1) & 1);
-            tc_fence_after();
-            if (e == 0) bulk_wait_read1();
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                rw[hf] = nrw[hf];
+                jp[hf] = njp[hf];
+#pragma unroll
+                for (int q = 0; q < kHPW; ++q) lm[q][hf] = nlm[q][hf];
+            }
+        }
+        if (ew == 0) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf)
+                if (lane + 32 * hf < T) rows[lane + 32 * hf] = rw[hf];
+        }
+        // ---- per-head decay mode and coefficients (warp-local) ----
+#pragma unroll
+        for (int q = 0; q < kHPW; ++q) {
+            const int hh = ew + 4 * q;
+            if (hh < nh) {   // warp-uniform
+                float mn = fminf(lm[q][0], lm[q][1]);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                const bool f = mn >= -120.f;      // factorised decay (e^{Λi-ref} e^{ref-Λj}, ref = min/2)
+                const float ref = 0.5f * mn;
+                if (lane == 0) {
+                    mode[hh] = f ? 1 : 0;
+                    ((float*)(sm + S::DS))[hh] = d_h[q];
+                }
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int i = lane + 32 * hf;
+                    if (i < T) {
+                        const float l = lm[q][hf];
+                        lam[hh * 64 + i] = l;
+                        cj[hh * 64 + i] = f ? __expf(ref - l) * dtr[q][hf] : dtr[q][hf];
+                        ei[hh * 64 + i] = f ? __expf(l - ref) : 1.f;
+                        e0[hh * 64 + i] = __expf(l);
+                    }
+                }
+            }
+        }
+        named_bar(1, 128);
+        if (trace && e == 0) trace[50] = gtimer();
+        // ---- G rows: TMEM (lanes 0..T-1, quadrants 0/1) -> smem (rotated, conflict-free) -> the
+        //      builder warps 2,3, which then build the masked weights while warps 4,5 run the
+        //      TMEM epilogue of the previous head ----
+        mbar_wait(BAR_G, 0);
+        tc_fence_after();
+        if (trace && e == 0) trace[51] = gtimer();
+        float* gs = (float*)(sm + S::YS);      // 64 x 64 fp32; the y staging area is idle until head 0's output
+        if (quad < 2) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float g16[16];
+                tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + 16 * c, g16);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) gs[row * 64 + ((16 * c + q + row) & 63)] = g16[q];
+            }
+        }
+        named_bar(1, 128);
+        const bool builder = (warp == 2 || warp == 3);
+        if (trace && e == 0) trace[3] = gtimer();
+        if (builder) {
+            const int brow = (warp - 2) * 32 + lane;
+            const bool bown = brow < T;
+            float gr[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) gr[j] = gs[brow * 64 + ((j + brow) & 63)];
+            const uint64_t mybits = bown ? rows[brow] : 0ull;
+            named_bar(1, 128);   // G staging consumed before the y staging area is reused
+            for (int k = 0; k < nh; ++k) {
+                // masked weights of head k into M'[k & 1]:  M'_ij = L_ij G_ij c_j  (factorised)
+                //                                        or  L_ij e^{Λi-Λj} dt_j G_ij (direct)
+                const int a = k & 1;
+                mbar_wait(bar_mempty(a), ((k >> 1) & 1) ^ 1);
+                if (bown) {
+                    const float* c = cj + k * 64;
+                    const bool f = mode[k] != 0;
+                    const float li = lam[k * 64 + brow];
+                    unsigned char* mrow = sm + S::MB + a * kAtom;
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch) {
+                        float w[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int j = 8 * ch + q;
+                            float v;
+                            if (f) v = c[j] * gr[j];
+                            else v = __expf(fminf(li - lam[k * 64 + j], 0.f)) * c[j] * gr[j];
+                            w[q] = ((mybits >> j) & 1ull) ? v : 0.f;
+                        }
+                        *reinterpret_cast<uint4*>(mrow + swz(brow, ch)) =
+                            make_uint4(pack_bf16(w[0], w[1]), pack_bf16(w[2], w[3]), pack_bf16(w[4], w[5]),
+                                       pack_bf16(w[6], w[7]));
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_mfull(a));
+            }
+        } else {
+            // ---- TMEM epilogue (warps 4,5 = TMEM lanes 0..63 = tree nodes) ----
             named_bar(1, 128);
-            if (quad < 2) {
-                const float Dh = prm.D ? prm.D[h] : 0.f;
+            const bool own = row < T;
+            const bool leader = (warp == 4 && lane == 0);
+            for (int k = 0; k < nh; ++k) {
+                const int s = k % kStages, a = k & 1;
+                const int h = hbeg + k;
+                mbar_wait(bar_accfull(a), (k >> 1) & 1);
+                tc_fence_after();
+                if (trace && leader && k < 12) trace[4 + 2 * k] = gtimer();
+                if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
+                named_bar(2, 64);
+                if (trace && leader && k < 6) trace[52 + 2 * k] = gtimer();
+                const float Dh = ((const float*)(sm + S::DS))[k];
                 const float s0 = own ? e0[k * 64 + row] : 0.f, s1 = own ? ei[k * 64 + row] : 0.f;
                 const unsigned char* xr = sm + S::X + s * S::XS;
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + kAccCol0 + 128 * a;
+                uint32_t v0[2][32], v1[2][32];
+                if (prm.has_h0) tmem_ld32(tl, v0[0]);
+                tmem_ld32(tl + 64, v1[0]);
+                tmem_wait();
+                if (prm.has_h0) tmem_ld32(tl + 32, v0[1]);
+                tmem_ld32(tl + 96, v1[1]);          // in flight while chunk 0 is computed
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float v0[16], v1[16];
-                    if (prm.has_h0) tmem_ld16(tl + 16 * c, v0);
-                    else {
+                for (int c = 0; c < 2; ++c) {
+                    if (c == 1) tmem_wait();
+                    if (!prm.has_h0) {
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) v0[q] = 0.f;
+                        for (int q = 0; q < 32; ++q) v0[c][q] = 0u;
                     }
-                    tmem_ld16(tl + 64 + 16 * c, v1);
                     if (own) {
 #pragma unroll
-                        for (int half = 0; half < 2; ++half) {
-                            const int ch = 2 * c + half;
-                            uint4 xv = *reinterpret_cast<const uint4*>(xr + swz(row, ch));
+                        for (int qc = 0; qc < 4; ++qc) {
+                            const int ch = 4 * c + qc;
+                            const uint4 xv = *reinterpret_cast<const uint4*>(xr + swz(row, ch));
                             const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
                             uint32_t o[4];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
-                                const int p = 8 * half + 2 * q;
-                                const float ya = fmaf(s0, v0[p], fmaf(s1, v1[p], Dh * xa));
-                                const float yb = fmaf(s0, v0[p + 1], fmaf(s1, v1[p + 1], Dh * xb));
+                                const int p = 8 * qc + 2 * q;
+                                const float ya =
+                                    fmaf(s0, __uint_as_float(v0[c][p]), fmaf(s1, __uint_as_float(v1[c][p]), Dh * xa));
+                                const float yb = fmaf(s0, __uint_as_float(v0[c][p + 1]),
+                                                      fmaf(s1, __uint_as_float(v1[c][p + 1]), Dh * xb));
                                 o[q] = pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
                         }
                     }
                 }
+                if (trace && leader && k < 6) trace[53 + 2 * k] = gtimer();
+                tc_fence_before();
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_accempty(a));
+                named_bar(2, 64);
+                if (leader) {
+                    tma_store_2d(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T);
+                    bulk_commit();
+                    mbar_arrive(bar_empty(s));
+                    if (trace && k < 12) trace[5 + 2 * k] = gtimer();
+                }
             }
-            tc_fence_before();
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_accempty(a));
-            named_bar(1, 128);
-            if (e == 0) {
-                tma_store_2d(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T);
-                bulk_commit();
-                mbar_arrive(bar_empty(s));
-            }
+            if (leader) bulk_wait_all();
         }
-        if (e == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
+    if (trace && tid == 0) trace[45] = gtimer();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -583,6 +688,8 @@ bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+unsigned long long* g_trace = nullptr;
+
 int num_sms() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -594,6 +701,9 @@ int num_sms() {
 }
 
 }  // namespace
+
+// Debug hook (not part of the ABI): per-CTA globaltimer phase stamps, 64 u64 per CTA.
+extern "C" void stree_debug_tc_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
 
 extern "C" int stree_tc_supports(const stree_dims* d) {
     if (!d) return 0;
@@ -625,13 +735,14 @@ extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const fl
     if (!ok) return (int)cudaErrorInvalidValue;
     // work split: one tree per CTA, heads of one group in chunks, ~1 wave over the SMs
     const int hpg = H / G;
-    int target = (num_sms() + B - 1) / B;          // CTAs per tree
-    int cpg = (target + G - 1) / G;                 // chunks per group
+    int cpg = num_sms() / (B * G);                  // head chunks per group: at most one wave of CTAs
     if (cpg < 1) cpg = 1;
+    if (cpg > hpg) cpg = hpg;
     int hpc = (hpg + cpg - 1) / cpg;
     if (hpc > kHPC) hpc = kHPC;
     cpg = (hpg + hpc - 1) / hpc;
-    stree::tc::Params prm{B, T, H, G, cpg, hpc, dt, A, D, parent, (__nv_bfloat16*)y, dev_status, h0 != nullptr};
+    stree::tc::Params prm{g_trace, B, T, H, G, cpg, hpc, dt, A, D, parent, (__nv_bfloat16*)y, dev_status,
+                          h0 != nullptr};
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (N == 128) {

@@ -1,0 +1,138 @@
+// TMA streaming probe: achievable HBM read bandwidth for the state-block access
+// patterns the scan kernel can use (standalone; not part of the library).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tma_probe tools/tma_probe.cu
+//   ./tma_probe
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c)); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t b, uint32_t n) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t ph) {
+    asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}" ::"r"(b), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+                 "l"((uint64_t)m), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+                 "l"((uint64_t)m), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void bulk1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"((uint64_t)src), "r"(bytes), "r"(bar) : "memory");
+}
+
+constexpr int kUnit = 32768;   // bytes per "head" (one 64 x 128 fp32 state block)
+
+template <int MODE, int STAGES>
+__global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap m2, const __grid_constant__ CUtensorMap m3,
+                                                const __grid_constant__ CUtensorMap mc, const float* base, int units_per_cta,
+                                                unsigned long long* sink) {
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) unsigned long long bars[16];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(su32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int u0 = blockIdx.x * units_per_cta;
+        for (int k = 0; k < units_per_cta + STAGES; ++k) {
+            if (k >= STAGES) {   // consume unit k - STAGES
+                const int s = (k - STAGES) % STAGES;
+                mbar_wait(su32(&bars[s]), ((k - STAGES) / STAGES) & 1);
+            }
+            if (k < units_per_cta) {
+                const int s = k % STAGES, u = u0 + k;
+                const uint32_t dst = su32(sm + s * kUnit), bar = su32(&bars[s]);
+                mbar_expect_tx(bar, kUnit);
+                if (MODE == 0) {        // 4 boxes [64 rows][32 fp32], SW128 (current scan kernel)
+                    for (int a = 0; a < 4; ++a) tma2d(dst + a * 8192, &m2, bar, 32 * a, u * 64);
+                } else if (MODE == 1) { // one 3D box {32, 64, 4} = the same 4 K-atoms
+                    tma3d(dst, &m3, bar, 0, u * 64, 0);
+                } else if (MODE == 2) { // contiguous [256 rows][32 fp32] box
+                    tma2d(dst, &mc, bar, 0, u * 256);
+                } else {                // 1D bulk copy of the contiguous 32 KB
+                    bulk1d(dst, (const char*)base + (size_t)u * kUnit, kUnit, bar);
+                }
+            }
+        }
+        sink[blockIdx.x] = bars[0];
+    }
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    EncFn enc = (EncFn)fp;
+    const int ctas = 144, per = 36;                   // 36 units of 32 KB per CTA
+    const size_t units = (size_t)ctas * per, bytes = units * kUnit;
+    float* buf;
+    cudaMalloc(&buf, bytes * 2);
+    cudaMemset(buf, 0, bytes * 2);
+    unsigned long long* sink;
+    cudaMalloc(&sink, 4096 * 8);
+    CUtensorMap m2, m3, mc;
+    {
+        cuuint64_t d[2] = {128, units * 64}, st[1] = {512};
+        cuuint32_t box[2] = {32, 64}, es[2] = {1, 1};
+        enc(&m2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, buf, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    {
+        cuuint64_t d[3] = {32, units * 64, 4}, st[2] = {512, 128};
+        cuuint32_t box[3] = {32, 64, 4}, es[3] = {1, 1, 1};
+        CUresult r = enc(&m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, buf, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) printf("3d map encode failed %d\n", (int)r);
+    }
+    {
+        cuuint64_t d[2] = {32, units * 256}, st[1] = {128};
+        cuuint32_t box[2] = {32, 256}, es[2] = {1, 1};
+        enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, buf, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    auto run = [&](auto kern, int stages, const char* name) {
+        size_t smem = (size_t)stages * kUnit + 1024;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best = 1e9;
+        for (int it = 0; it < 6; ++it) {
+            // flush L2 by touching the second half
+            cudaMemsetAsync((char*)buf + bytes, it, bytes);
+            cudaEventRecord(e0);
+            kern<<<ctas, 128, smem>>>(m2, m3, mc, buf, per, sink);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it) best = ms < best ? ms : best;
+        }
+        printf("%-28s stages=%d  %8.2f us  %7.1f GB/s\n", name, stages, best * 1e3, bytes / (best * 1e-3) / 1e9);
+        cudaError_t err = cudaGetLastError();
+        if (err) printf("  error %s\n", cudaGetErrorString(err));
+    };
+    run(probe<0, 4>, 4, "4x2D [64][32] SW128");
+    run(probe<0, 6>, 6, "4x2D [64][32] SW128");
+    run(probe<1, 4>, 4, "1x3D {32,64,4} SW128");
+    run(probe<1, 6>, 6, "1x3D {32,64,4} SW128");
+    run(probe<2, 4>, 4, "1x2D [256][32] contiguous");
+    run(probe<3, 4>, 4, "1D bulk 32KB");
+    run(probe<3, 6>, 6, "1D bulk 32KB");
+    return 0;
+}
