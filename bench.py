@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p-match", type=float, default=0.9)
+    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
+                    help="N>1: batch = each rank verifies its own trees (no collective, weak scaling); "
+                         "heads = ranks split the heads of the same trees + NCCL all-gather of y (strong)")
     return ap.parse_args()
 
 
@@ -244,15 +247,22 @@ def run_stree(args):
     binding.stree_set_scan_impl({"auto": 0, "simt": 1, "tc": 2}[args.scan_impl])
     L = args.layers
     # every rank verifies its own batch of trees (weak scaling; no data-path collective)
+    from paper_2505_14969_b200 import dist as sdist
     base = inputs.config_problem(args.config)
     d = base.dims
     par_np = base.parent
-    if world > 1:
+    heads_mode = world > 1 and args.shard == "heads"
+    h_lo, h_hi = sdist.shard_heads(d.n_heads, d.n_groups, world, rank) if heads_mode else (0, d.n_heads)
+    if world > 1 and not heads_mode:
         rng = np.random.default_rng(inputs.BASE_SEED + 1000 + rank)
         from gen import trees as _t
         par_np = np.stack([_t.random_recursive(d.n_nodes, 4, rng) for _ in range(d.batch)]) \
             if args.config == "c4" else par_np
-    tok, vt = inputs.make_accept_inputs(par_np, seed=inputs.BASE_SEED + 77 + rank, p_match=args.p_match)
+    if heads_mode:
+        import dataclasses
+        d = dataclasses.replace(d, n_heads=h_hi - h_lo, n_groups=max(1, d.n_groups * (h_hi - h_lo) // d.n_heads))
+    seed_rank = 0 if heads_mode else rank
+    tok, vt = inputs.make_accept_inputs(par_np, seed=inputs.BASE_SEED + 77 + seed_rank, p_match=args.p_match)
 
     # per-layer inputs: distinct buffers (values generated on device to keep setup fast;
     # layer 0 is the seeded host problem, the others are seeded device randoms of the same recipe)
@@ -260,6 +270,7 @@ def run_stree(args):
     g.manual_seed(inputs.BASE_SEED + 10 * rank)
     layers = []
     t0 = api.upload(inputs.make_problem(d, par_np, seed=inputs.BASE_SEED + 3 + 100 * rank), device=dev)
+    ygath = None
     io_t = t0["x"].dtype
     for li in range(L):
         if li == 0:
@@ -299,6 +310,8 @@ def run_stree(args):
         for t in layers:
             binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"],
                                     status, dims=dims)
+            if heads_mode:   # the layer needs the full y: all-gather the head shards over NVLink (NCCL)
+                t["y_full"] = sdist.gather_heads(t["y"])
 
     def ph_accept():
         binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
@@ -316,10 +329,15 @@ def run_stree(args):
     torch.cuda.synchronize()
     graphs = []
     for f in phases:
-        gr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gr, stream=stream):
-            f()
-        graphs.append(gr)
+        try:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                f()
+            graphs.append(gr)
+        except Exception as exc:   # e.g. a collective that cannot be captured: replay eagerly
+            if rank == 0:
+                print(f"[bench] graph capture failed ({exc}); running phase eagerly", file=sys.stderr)
+            graphs.append(f)
     torch.cuda.synchronize()
     assert status.item() == 0, f"device status {status.item()}"
     plen_host = plen.cpu().numpy()
@@ -328,7 +346,10 @@ def run_stree(args):
         for i, gr in enumerate(graphs):
             if evs is not None:
                 evs[i].record(stream)
-            gr.replay()
+            if callable(gr):
+                gr()
+            else:
+                gr.replay()
         if evs is not None:
             evs[len(graphs)].record(stream)
 
@@ -356,7 +377,7 @@ def run_stree(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms_per_step = total_ms / K
-    nodes_per_step = d.batch * d.n_nodes * L * world
+    nodes_per_step = d.batch * d.n_nodes * L * (1 if heads_mode else world)
     value = nodes_per_step / (ms_per_step * 1e-3)
     ph_mean = phase_ms.mean(0)
     scan_us = ph_mean[1] * 1e3 / L
@@ -387,10 +408,13 @@ def run_stree(args):
         e2e = run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if heads_mode else "weak",
+            "vs_baseline": None,
             "dtype": d.io_dtype, "data": "synthetic", "config": workload_desc(args.config, base, L),
             "gpu_launches": (2 * L + 2) * K, "roofline": roofline, "e2e": e2e,
-            "clocks": sampler.summary(), "parallelism": f"batch-replicas x{world}" if world > 1 else "single"}
+            "clocks": sampler.summary(),
+            "parallelism": (f"heads x{world} (+NCCL all-gather of y)" if heads_mode else
+                            f"batch-replicas x{world}") if world > 1 else "single"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(base, tok, vt)
     if rank == 0:

@@ -1,195 +1,416 @@
 // K4 stree_commit — activation replay of the accepted path (PAPER.md:113,
 // Alg. 1 l.123):  h_new = e^{Λ_k} h0 + Σ_{s∈path} e^{Λ_k-Λ_s} dt_s x_s B_sᵀ.
 //
-// HBM-bound streaming kernel (intensity ≈ r/4 FLOP/B): one CTA per (tree, head)
-// state block (P x N fp32, 32 KB at P=64, N=128), 256 threads.  Every thread
-// issues its 16-byte state loads at kernel entry — before the dependent
-// path_len -> path -> dt chain of the prologue — so the state stream overlaps
-// the prologue latency; the rank-r update uses the path rows of x and B staged in
-// shared memory; results are written with streaming stores.
+// HBM-bound streaming (intensity ≈ r/4 FLOP/B).  Main kernel: one CTA per
+// (tree, chunk of heads), ≈ one wave over the SMs, 288 threads:
+//   warp 0      producer: 1-D bulk copies (cp.async.bulk) of the chunk's contiguous
+//               P x N fp32 state blocks into a ring of shared-memory slots
+//   warps 1-8   once per CTA: path validation, per-head path-cumsum of log-decays
+//               and coefficients, staging of the path rows of x (pre-scaled) and B;
+//               then per state block: 16-byte shared loads -> decay·h + Σ_m u_m B_mᵀ
+//               -> streaming 16-byte global stores (the slot is released as soon as
+//               every warp has read it)
+// The state stream starts at kernel entry and never waits for the dependent
+// path prologue.  Accepted paths longer than kRMax (and shapes the ring cannot
+// hold) use the simple per-(tree, head) kernel below.
 #include "stree_common.cuh"
 
 namespace stree {
 
-constexpr int kCommitThreads = 256;
-constexpr int kCommitVec = 8;        // float4 per thread held in registers (P*N <= 8192 fp32)
-constexpr int kCommitChunk = 16;     // path nodes staged per smem round
+constexpr int kRMax = 16;            // path nodes staged by the ring kernel
+constexpr int kCHPC = 16;            // max heads per CTA
+constexpr int kCThreads = 288;       // 1 producer warp + 8 compute warps
+constexpr int kCompute = 256;
+constexpr int kRingBytes = 128 * 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void c_mbar_init(uint32_t b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c));
+}
+__device__ __forceinline__ void c_mbar_arrive(uint32_t b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void c_mbar_expect_tx(uint32_t b, uint32_t n) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n) : "memory");
+}
+__device__ __forceinline__ void c_mbar_wait(uint32_t b, uint32_t ph) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(b),
+        "r"(ph)
+        : "memory");
+}
+__device__ __forceinline__ void c_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+struct CommitParams {
+    int B, T, H, P, N, G, cpg, hpc, slots;
+    const void* x;
+    const float* dt;
+    const float* A;
+    const void* Bm;
+    const float* h0;
+    const int32_t* parent;
+    const int32_t* path;
+    const int32_t* path_len;
+    float* h_new;
+    int32_t* dev_status;
+    unsigned long long* trace;   // debug: per-CTA globaltimer stamps (64 per CTA)
+};
+
+__device__ __forceinline__ unsigned long long c_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <typename IO>
-__global__ void __launch_bounds__(kCommitThreads) commit_kernel(int T, int H, int P, int N, int G,
-                                                                const IO* __restrict__ x, const float* __restrict__ dt,
-                                                                const float* __restrict__ A,
-                                                                const IO* __restrict__ Bm, const float* h0,
-                                                                const int32_t* __restrict__ parent,
-                                                                const int32_t* __restrict__ path,
-                                                                const int32_t* __restrict__ path_len, float* h_new,
-                                                                int32_t* dev_status) {
-    extern __shared__ float smem[];
-    const int h = blockIdx.x, b = blockIdx.y;
-    const int g = h / (H / G);
+__global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitParams prm) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int H = prm.H, T = prm.T, P = prm.P, N = prm.N;
+    const int b = blockIdx.x / (prm.G * prm.cpg);
+    const int rem = blockIdx.x % (prm.G * prm.cpg);
+    const int g = rem / prm.cpg, chunk = rem % prm.cpg;
+    const int hpg = H / prm.G, hbeg = g * hpg + chunk * prm.hpc;
+    const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
+    if (nh <= 0) return;
+    const int blk = P * N;                              // floats per state block
+    const uint32_t blk_bytes = (uint32_t)blk * 4;
+    // shared layout: ring | u[nh][kRMax][P] (long paths: coef[kCHPC][kMaxNodes]) | Bs[kRMax][N] |
+    //                decay[kCHPC] | path[kMaxNodes] | r | barriers
+    float* ring = (float*)csm;
+    float* u = (float*)(csm + (size_t)prm.slots * blk_bytes);
+    float* coefl = u;
+    float* Bs = u + kCHPC * kRMax * P;
+    float* decay = Bs + kRMax * N;                      // [kCHPC]
+    int* spath = (int*)(decay + kCHPC);                 // [kMaxNodes]
+    int* sr = spath + kMaxNodes;                        // [1]
+    unsigned long long* bars = (unsigned long long*)(((uintptr_t)(sr + 1) + 7) & ~(uintptr_t)7);
+    const uint32_t bar0 = su32(bars);
+    auto bar_full = [&](int s) { return bar0 + 8 * s; };
+    auto bar_empty = [&](int s) { return bar0 + 8 * (prm.slots + s); };
+    const size_t base = ((size_t)b * H + hbeg) * (size_t)blk;
+    unsigned long long* tr = prm.trace ? prm.trace + (size_t)blockIdx.x * 64 : nullptr;
+    if (tr && tid == 0) tr[0] = c_gtimer();
+
+    if (tid == 0) {
+        for (int s = 0; s < prm.slots; ++s) {
+            c_mbar_init(bar_full(s), 1);
+            c_mbar_init(bar_empty(s), kCompute / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ================= producer =================
+        if (lane == 0 && prm.h0) {
+            for (int k = 0; k < nh; ++k) {
+                const int s = k % prm.slots;
+                c_mbar_wait(bar_empty(s), ((k / prm.slots) & 1) ^ 1);
+                c_mbar_expect_tx(bar_full(s), blk_bytes);
+                c_bulk_load(su32(ring + (size_t)s * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(s));
+            }
+        }
+        return;
+    }
+    // ================= compute warps =================
+    const int ct = tid - 32;                            // 0..255
+    const IO* x = (const IO*)prm.x;
+    const IO* Bm = (const IO*)prm.Bm;
+    // ---- path validation (warp 1) ----
+    if (warp == 1) {
+        const int r = prm.path_len[b];
+        int ok = (r >= 1 && r <= T);
+        if (ok) {
+            for (int m = lane; m < r; m += 32) {
+                const int v = prm.path[(size_t)b * T + m];
+                spath[m] = v;
+                bool good = (v >= 0 && v < T);
+                if (m == 0) good = good && v == 0;
+                else {
+                    const int pu = prm.path[(size_t)b * T + m - 1];
+                    good = good && v > pu;
+                    if (prm.parent && good) good = prm.parent[(size_t)b * T + v] == pu;
+                }
+                if (!good) ok = 0;
+            }
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) {
+            sr[0] = ok ? r : 0;
+            if (!ok && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+        }
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (tr && tid == 32) tr[1] = c_gtimer();
+    const int r = sr[0];                                // > 0 valid, 0 invalid (state unchanged)
+    const bool staged = r <= kRMax;
+    // ---- per-head path coefficients (one warp per head): lam_m = Σ_{q<=m} dt A_h,
+    //      c_m = e^{lam_{r-1}-lam_m} dt_m, decay = e^{lam_{r-1}}  (PAPER.md:86-90 on the path) ----
+    if (r > 0) {
+        for (int hh = warp - 1; hh < nh; hh += 8) {
+            const int h = hbeg + hh;
+            const float Ah = prm.A[h];
+            float carry = 0.f;
+            float* cl = coefl + hh * kMaxNodes;          // long paths: lam then c in smem
+            float cst = 0.f, dst0 = 0.f;
+            for (int m0 = 0; m0 < r; m0 += 32) {
+                const int m = m0 + lane;
+                float d = 0.f, a = 0.f;
+                if (m < r) {
+                    d = prm.dt[((size_t)b * T + spath[m]) * H + h];
+                    a = d * Ah;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xffffffffu, a, o);
+                    if (lane >= o) a += t;
+                }
+                a += carry;
+                if (staged) { cst = a; dst0 = d; }
+                else if (m < r) cl[m] = a;
+                carry = __shfl_sync(0xffffffffu, a, 31);
+            }
+            const float last = staged ? __shfl_sync(0xffffffffu, cst, r - 1) : carry;
+            if (lane == 0) decay[hh] = expf(last);
+            if (staged) {
+                const float c = expf(last - cst) * dst0;
+                for (int m = 0; m < r; ++m) {       // u[hh][m][p] = c_m x[b, s_m, h, p]
+                    const float cm = __shfl_sync(0xffffffffu, c, m);
+                    const IO* xr = x + (((size_t)b * T + spath[m]) * H + h) * P;
+                    for (int p = lane; p < P; p += 32) u[(hh * kRMax + m) * P + p] = cm * to_f32(xr[p]);
+                }
+            } else {
+                __syncwarp();
+                for (int m = lane; m < r; m += 32)
+                    cl[m] = expf(last - cl[m]) * prm.dt[((size_t)b * T + spath[m]) * H + h];
+            }
+        }
+        if (staged)
+            for (int k = ct; k < r * N; k += kCompute) {
+                const int m = k / N, n = k % N;
+                Bs[m * N + n] = to_f32(Bm[(((size_t)b * T + spath[m]) * prm.G + g) * N + n]);
+            }
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (tr && tid == 32) tr[2] = c_gtimer();
+    // ---- stream the state blocks ----
+    const int nvec = blk / 4;
+    const int n0 = (4 * ct) % N, p0 = (4 * ct) / N, pstep = (4 * kCompute) / N;   // N divides 1024 (host-checked)
+    for (int k = 0; k < nh; ++k) {
+        const int s = k % prm.slots;
+        float* dst = prm.h_new + base + (size_t)k * blk;
+        float4 v[8];
+        if (prm.h0) {
+            c_mbar_wait(bar_full(s), (k / prm.slots) & 1);
+            if (tr && tid == 32 && k < 16) tr[4 + 2 * k] = c_gtimer();
+            const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * blk);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int e = ct + q * kCompute;
+                v[q] = e < nvec ? src[e] : make_float4(0, 0, 0, 0);
+            }
+            __syncwarp();
+            if (lane == 0) c_mbar_arrive(bar_empty(s));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = make_float4(0, 0, 0, 0);
+        }
+        if (r == 0) {                                                // invalid path: state unchanged
+            if (prm.h0 != prm.h_new) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = ct + q * kCompute;
+                    if (e < nvec) __stcs(reinterpret_cast<float4*>(dst) + e, v[q]);
+                }
+            }
+            continue;
+        }
+        const float dk = decay[k];
+        const int h = hbeg + k;
+        // thread ct owns float4 columns n0 = (4 ct) mod N of rows p0 + q (1024/N), q = 0..7: the same n for
+        // every q, so one B load per path node feeds 8 independent accumulator chains
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = make_float4(dk * v[q].x, dk * v[q].y, dk * v[q].z, dk * v[q].w);
+        if (staged) {
+            const float* uk = u + k * kRMax * P;
+            for (int m = 0; m < r; ++m) {
+                const float4 bb = *reinterpret_cast<const float4*>(&Bs[m * N + n0]);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (ct + q * kCompute >= nvec) break;
+                    const float um = uk[m * P + p0 + q * pstep];
+                    v[q].x = fmaf(um, bb.x, v[q].x); v[q].y = fmaf(um, bb.y, v[q].y);
+                    v[q].z = fmaf(um, bb.z, v[q].z); v[q].w = fmaf(um, bb.w, v[q].w);
+                }
+            }
+        } else {   // long accepted path: operands straight from L2
+            const float* cl = coefl + k * kMaxNodes;
+            for (int m = 0; m < r; ++m) {
+                const int sm_ = spath[m];
+                const IO* br = Bm + (((size_t)b * T + sm_) * prm.G + g) * N + n0;
+                const float4 bb = make_float4(to_f32(br[0]), to_f32(br[1]), to_f32(br[2]), to_f32(br[3]));
+                const IO* xr = x + (((size_t)b * T + sm_) * H + h) * P;
+                const float cm = cl[m];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (ct + q * kCompute >= nvec) break;
+                    const float um = cm * to_f32(xr[p0 + q * pstep]);
+                    v[q].x = fmaf(um, bb.x, v[q].x); v[q].y = fmaf(um, bb.y, v[q].y);
+                    v[q].z = fmaf(um, bb.z, v[q].z); v[q].w = fmaf(um, bb.w, v[q].w);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = ct + q * kCompute;
+            if (e < nvec) __stcs(reinterpret_cast<float4*>(dst) + e, v[q]);
+        }
+        if (tr && tid == 32 && k < 16) tr[5 + 2 * k] = c_gtimer();
+    }
+    if (tr && tid == 32) tr[3] = c_gtimer();
+}
+
+// Simple per-(tree, head) kernel: long paths (r > kRMax) and shapes the ring kernel does not take.
+template <typename IO>
+__global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, int N, int G, const IO* __restrict__ x,
+                                                           const float* __restrict__ dt, const float* __restrict__ A,
+                                                           const IO* __restrict__ Bm, const float* h0,
+                                                           const int32_t* __restrict__ parent,
+                                                           const int32_t* __restrict__ path,
+                                                           const int32_t* __restrict__ path_len, float* h_new,
+                                                           int32_t* dev_status) {
     __shared__ int s_path[kMaxNodes];
     __shared__ float s_coef[kMaxNodes];
     __shared__ float s_decay;
-    __shared__ int s_ok;
-    const int tid = threadIdx.x;
-    const size_t off = ((size_t)b * H + h) * (size_t)P * N;
-    const float* src = h0 ? h0 + off : nullptr;
-    float* dst = h_new + off;
-    const int total = P * N;
-    const bool vec = (N % 4 == 0) && (total <= kCommitThreads * kCommitVec * 4);
-    const int nvec = total / 4;
-
-    // ---- 1. state loads first (independent of the path) ----
-    float4 acc[kCommitVec];
-    if (vec) {
-#pragma unroll
-        for (int q = 0; q < kCommitVec; ++q) {
-            const int e = tid + q * kCommitThreads;
-            acc[q] = (e < nvec && src) ? __ldcs(reinterpret_cast<const float4*>(src) + e) : make_float4(0, 0, 0, 0);
-        }
-    }
-    // ---- 2. path validation + coefficients (warp 0) ----
+    __shared__ int s_r;
+    const int h = blockIdx.x, b = blockIdx.y, g = h / (H / G), tid = threadIdx.x;
+    const int r0 = path_len[b];
     if (tid < 32) {
-        const int r = path_len[b];
-        int ok = (r >= 1 && r <= T);
+        int ok = (r0 >= 1 && r0 <= T);
         if (ok) {
-            for (int m = tid; m < r; m += 32) {
+            for (int m = tid; m < r0; m += 32) {
                 const int v = path[(size_t)b * T + m];
                 s_path[m] = v;
                 bool good = (v >= 0 && v < T);
                 if (m == 0) good = good && v == 0;
                 else {
-                    const int u = path[(size_t)b * T + m - 1];
-                    good = good && v > u;
-                    if (parent && good) good = parent[(size_t)b * T + v] == u;
+                    const int pu = path[(size_t)b * T + m - 1];
+                    good = good && v > pu;
+                    if (parent && good) good = parent[(size_t)b * T + v] == pu;
                 }
                 if (!good) ok = 0;
             }
         }
         ok = __all_sync(0xffffffffu, ok);
         if (ok) {
-            // path-cumsum of log-decays lam_m = Σ_{q<=m} dt_q A_h (PAPER.md:86-90 on the path);
-            // c_m = e^{lam_{r-1} - lam_m} dt_m,  decay = e^{lam_{r-1}}
             const float Ah = A[h];
             float carry = 0.f;
-            for (int base = 0; base < r; base += 32) {
+            for (int base = 0; base < r0; base += 32) {
                 const int m = base + tid;
-                float a = (m < r) ? dt[((size_t)b * T + s_path[m]) * H + h] * Ah : 0.f;
+                float a = (m < r0) ? dt[((size_t)b * T + s_path[m]) * H + h] * Ah : 0.f;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float t = __shfl_up_sync(0xffffffffu, a, o);
                     if (tid >= o) a += t;
                 }
                 a += carry;
-                if (m < r) s_coef[m] = a;
+                if (m < r0) s_coef[m] = a;
                 carry = __shfl_sync(0xffffffffu, a, 31);
             }
             __syncwarp();
-            for (int m = tid; m < r; m += 32)
+            for (int m = tid; m < r0; m += 32)
                 s_coef[m] = expf(carry - s_coef[m]) * dt[((size_t)b * T + s_path[m]) * H + h];
             if (tid == 0) s_decay = expf(carry);
         }
-        if (tid == 0) s_ok = ok ? r : 0;
+        if (tid == 0) s_r = ok ? r0 : 0;
     }
     __syncthreads();
-    const int r = s_ok;
-    if (r == 0) {
-        if (tid == 0 && h == 0) report(dev_status, STREE_DEV_BAD_PATH);
-        if (src != dst) {
-            if (vec) {
-#pragma unroll
-                for (int q = 0; q < kCommitVec; ++q) {
-                    const int e = tid + q * kCommitThreads;
-                    if (e < nvec) __stcs(reinterpret_cast<float4*>(dst) + e, acc[q]);
-                }
-            } else {
-                for (int k = tid; k < total; k += kCommitThreads) dst[k] = src ? src[k] : 0.f;
-            }
-        }
-        return;
-    }
-    const float decay = s_decay;
-    float* s_u = smem;                           // [chunk][P]  c_m * x_m[p]
-    float* s_B = smem + kCommitChunk * P;        // [chunk][N]
-    if (vec) {
-#pragma unroll
-        for (int q = 0; q < kCommitVec; ++q)
-            acc[q] = make_float4(decay * acc[q].x, decay * acc[q].y, decay * acc[q].z, decay * acc[q].w);
-        for (int m0 = 0; m0 < r; m0 += kCommitChunk) {
-            const int mc = min(kCommitChunk, r - m0);
-            if (m0) __syncthreads();
-            for (int k = tid; k < mc * P; k += kCommitThreads) {
-                const int m = k / P, p = k % P;
-                s_u[m * P + p] = s_coef[m0 + m] * to_f32(x[(((size_t)b * T + s_path[m0 + m]) * H + h) * P + p]);
-            }
-            for (int k = tid; k < mc * N; k += kCommitThreads) {
-                const int m = k / N, n = k % N;
-                s_B[m * N + n] = to_f32(Bm[(((size_t)b * T + s_path[m0 + m]) * G + g) * N + n]);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < kCommitVec; ++q) {
-                const int e = tid + q * kCommitThreads;
-                if (e < nvec) {
-                    const int p = (e * 4) / N, n = (e * 4) % N;
-                    float4 a = acc[q];
-                    for (int m = 0; m < mc; ++m) {
-                        const float u = s_u[m * P + p];
-                        const float4 bb = *reinterpret_cast<const float4*>(&s_B[m * N + n]);
-                        a.x = fmaf(u, bb.x, a.x); a.y = fmaf(u, bb.y, a.y);
-                        a.z = fmaf(u, bb.z, a.z); a.w = fmaf(u, bb.w, a.w);
-                    }
-                    acc[q] = a;
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kCommitVec; ++q) {
-            const int e = tid + q * kCommitThreads;
-            if (e < nvec) __stcs(reinterpret_cast<float4*>(dst) + e, acc[q]);
-        }
-    } else {
-        // generic fallback (N % 4 != 0 or a state block larger than 32 K fp32)
-        for (int e = tid; e < total; e += kCommitThreads) {
-            const int p = e / N, n = e % N;
-            float a = decay * (src ? src[e] : 0.f);
-            for (int m = 0; m < r; ++m) {
+    const size_t off = ((size_t)b * H + h) * (size_t)P * N;
+    const float* src = h0 ? h0 + off : nullptr;
+    float* dst = h_new + off;
+    if (s_r == 0 && tid == 0) report(dev_status, STREE_DEV_BAD_PATH);
+    for (int e = tid; e < P * N; e += 256) {
+        const int p = e / N, n = e % N;
+        float a = src ? src[e] : 0.f;
+        if (s_r) {
+            a *= s_decay;
+            for (int m = 0; m < s_r; ++m) {
                 const int s = s_path[m];
                 a = fmaf(s_coef[m] * to_f32(x[(((size_t)b * T + s) * H + h) * P + p]),
                          to_f32(Bm[(((size_t)b * T + s) * G + g) * N + n]), a);
             }
-            dst[e] = a;
         }
+        dst[e] = a;
     }
 }
 
 }  // namespace stree
 
+namespace {
+
+unsigned long long* g_commit_trace = nullptr;
+
+int commit_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <typename IO>
+int launch(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm, const float* h0,
+           const int32_t* parent, const int32_t* path, const int32_t* path_len, float* h_new, int32_t* dev_status,
+           cudaStream_t s) {
+    const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
+    const size_t blk_bytes = (size_t)P * N * 4;
+    const bool ring_ok = (N % 4 == 0) && (1024 % N == 0) && (P * N <= 8 * stree::kCompute * 4) &&
+                         (blk_bytes % 16 == 0) &&
+                         (blk_bytes * 2 <= (size_t)stree::kRingBytes);
+    if (!ring_ok) {
+        stree::commit_block_kernel<IO><<<dim3(H, B), 256, 0, s>>>(T, H, P, N, G, (const IO*)x, dt, A, (const IO*)Bm,
+                                                                  h0, parent, path, path_len, h_new, dev_status);
+        return (int)cudaGetLastError();
+    }
+    const int hpg = H / G;
+    int cpg = commit_sms() / (B * G);
+    if (cpg < 1) cpg = 1;
+    if (cpg > hpg) cpg = hpg;
+    int hpc = (hpg + cpg - 1) / cpg;
+    if (hpc > stree::kCHPC) hpc = stree::kCHPC;
+    cpg = (hpg + hpc - 1) / hpc;
+    int slots = (int)(stree::kRingBytes / blk_bytes);
+    if (slots > 8) slots = 8;
+    stree::CommitParams prm{B, T, H, P, N, G, cpg, hpc, slots, x, dt, A, Bm, h0, parent, path, path_len,
+                            h_new, dev_status, g_commit_trace};
+    size_t ustage = (size_t)stree::kCHPC * stree::kRMax * P * 4;
+    const size_t lcoef = (size_t)stree::kCHPC * stree::kMaxNodes * 4;
+    if (ustage < lcoef) ustage = lcoef;
+    const size_t smem = (size_t)slots * blk_bytes + ustage + (size_t)stree::kRMax * N * 4 + stree::kCHPC * 4 +
+                        (stree::kMaxNodes + 1) * 4 + 16 + (size_t)2 * slots * 8 + 64;
+    auto k = stree::commit_ring_kernel<IO>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    k<<<B * G * cpg, stree::kCThreads, smem, s>>>(prm);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" void stree_debug_commit_trace(unsigned long long* dev_buf) { g_commit_trace = dev_buf; }
+
 extern "C" int stree_launch_commit(const stree_dims* d, const void* x, const float* dt, const float* A,
                                    const void* Bm, const float* h0, const int32_t* parent,
                                    const int32_t* path, const int32_t* path_len, float* h_new,
                                    int32_t* dev_status, cudaStream_t s) {
-    const int P = d->head_dim, N = d->d_state;
-    dim3 grid(d->n_heads, d->batch);
-    size_t smem = (size_t)stree::kCommitChunk * (P + N) * sizeof(float);
-    if (smem > 200 * 1024) return (int)cudaErrorInvalidValue;
-    cudaError_t e;
-    if (d->io_dtype == STREE_BF16) {
-        auto k = stree::commit_kernel<__nv_bfloat16>;
-        if (smem > 48 * 1024 && (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          (int)smem)) != cudaSuccess)
-            return (int)e;
-        k<<<grid, stree::kCommitThreads, smem, s>>>(d->n_nodes, d->n_heads, P, N, d->n_groups,
-                                                     (const __nv_bfloat16*)x, dt, A, (const __nv_bfloat16*)Bm, h0,
-                                                     parent, path, path_len, h_new, dev_status);
-    } else {
-        auto k = stree::commit_kernel<float>;
-        if (smem > 48 * 1024 && (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          (int)smem)) != cudaSuccess)
-            return (int)e;
-        k<<<grid, stree::kCommitThreads, smem, s>>>(d->n_nodes, d->n_heads, P, N, d->n_groups, (const float*)x, dt,
-                                                     A, (const float*)Bm, h0, parent, path, path_len, h_new,
-                                                     dev_status);
-    }
-    return (int)cudaGetLastError();
+    if (d->io_dtype == STREE_BF16)
+        return launch<__nv_bfloat16>(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s);
+    return launch<float>(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s);
 }

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
                                                      int32_t* __restrict__ path,
                                                      int32_t* __restrict__ path_len,
                                                      int32_t* __restrict__ bonus, int32_t* dev_status) {
-    __shared__ int s_par[4][kMaxNodes], s_tok[4][kMaxNodes];
+    __shared__ int s_par[4][kMaxNodes], s_tok[4][kMaxNodes], s_vt[4][kMaxNodes];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * 4 + warp;
     if (b >= B) return;
@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
         int p = par[i];
         s_par[warp][i] = p;
         s_tok[warp][i] = tokens[(size_t)b * T + i];
+        s_vt[warp][i] = vtok[(size_t)b * T + i];
         if (i == 0) { if (p != -1) bad = 1; }
         else if (p < 0 || p >= i) bad = bad ? bad : 2;
         path[(size_t)b * T + i] = -1;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
         return;
     }
     __syncwarp();
-    const int32_t* vt = vtok + (size_t)b * T;
+    const int* vt = s_vt[warp];
     int cur = 0, len = 1;
     if (lane == 0) path[(size_t)b * T] = 0;
     for (;;) {

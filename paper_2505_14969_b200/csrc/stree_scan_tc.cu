@@ -336,6 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(sb + S::CB + a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
                 tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
             }
+            // the tree operands (and the epilogue's small loads) go first: the state stream starts
+            // once they have landed, so they do not queue behind ~kStages x 40 KB per SM of bulk data
+            mbar_wait(BAR_TREE, 0);
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
                 mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);

@@ -69,6 +69,23 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     }
 }
 
+// plain vectorised LDG streaming read (reference for the read-only ceiling)
+__global__ void __launch_bounds__(256) ldg_read(const float4* __restrict__ p, size_t n, unsigned long long* sink) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        float4 a = __ldcs(p + i), b = __ldcs(p + i + stride), c = __ldcs(p + i + 2 * stride), d = __ldcs(p + i + 3 * stride);
+        acc.x += a.x + b.x + c.x + d.x;
+    }
+    for (; i < n; i += stride) acc.x += __ldcs(p + i).x;
+    if (acc.x == 12345.f) sink[0] = 1;
+}
+__global__ void __launch_bounds__(256) ldg_copy(const float4* __restrict__ p, float4* __restrict__ q, size_t n) {
+    size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) __stcs(q + i, __ldcs(p + i));
+}
+
 typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -78,7 +95,7 @@ int main() {
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
     EncFn enc = (EncFn)fp;
-    const int ctas = 144, per = 36;                   // 36 units of 32 KB per CTA
+    const int ctas = 144, per = 108;                   // 36 units of 32 KB per CTA
     const size_t units = (size_t)ctas * per, bytes = units * kUnit;
     float* buf;
     cudaMalloc(&buf, bytes * 2);
@@ -127,6 +144,39 @@ int main() {
         cudaError_t err = cudaGetLastError();
         if (err) printf("  error %s\n", cudaGetErrorString(err));
     };
+    {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        size_t n = bytes / 16;
+        for (int g : {148 * 4, 148 * 8, 148 * 16}) {
+            float best = 1e9;
+            for (int it = 0; it < 6; ++it) {
+                cudaMemsetAsync((char*)buf + bytes, it, bytes);
+                cudaEventRecord(e0);
+                ldg_read<<<g, 256>>>((const float4*)buf, n, sink);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (it) best = ms < best ? ms : best;
+            }
+            printf("LDG.128 stream read grid=%5d      %8.2f us  %7.1f GB/s\n", g, best * 1e3, bytes / (best * 1e-3) / 1e9);
+        }
+        for (int g : {148 * 8}) {
+            float best = 1e9;
+            for (int it = 0; it < 6; ++it) {
+                cudaEventRecord(e0);
+                ldg_copy<<<g, 256>>>((const float4*)buf, (float4*)((char*)buf + bytes), n);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (it) best = ms < best ? ms : best;
+            }
+            printf("LDG/STG copy grid=%5d (r+w bytes) %8.2f us  %7.1f GB/s\n", g, best * 1e3, 2 * bytes / (best * 1e-3) / 1e9);
+        }
+    }
     run(probe<0, 4>, 4, "4x2D [64][32] SW128");
     run(probe<0, 6>, 6, "4x2D [64][32] SW128");
     run(probe<1, 4>, 4, "1x3D {32,64,4} SW128");
