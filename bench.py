@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=64)
     ap.add_argument("--scan-impl", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-early-state", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p-match", type=float, default=0.9)
     ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
@@ -245,6 +246,10 @@ def run_stree(args):
     from paper_2505_14969_b200 import api, binding
 
     binding.stree_set_scan_impl({"auto": 0, "simt": 1, "tc": 2}[args.scan_impl])
+    # PDL between consecutive kernels; in this step the kernel preceding a scan / commit of layer l never
+    # writes layer l's state, so the state stream may start before the dependency wait (EARLY_STATE)
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL |
+                                   (0 if args.no_early_state else binding.STREE_LAUNCH_EARLY_STATE))
     L = args.layers
     # every rank verifies its own batch of trees (weak scaling; no data-path collective)
     from paper_2505_14969_b200 import dist as sdist

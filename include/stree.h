@@ -148,6 +148,19 @@ const char* stree_status_string(stree_status s);
 /* Select the scan kernel for subsequent stree_tree_scan calls (process-wide). */
 stree_status stree_set_scan_impl(stree_scan_impl impl);
 
+/*
+ * Launch options (process-wide, default STREE_LAUNCH_PDL).
+ *  STREE_LAUNCH_PDL          launch with programmatic dependent launch: each kernel lets the next
+ *                            grid in the stream be scheduled early and waits (griddepcontrol.wait)
+ *                            before its first access to argument memory.  Always safe.
+ *  STREE_LAUNCH_EARLY_STATE  promise: the state h0 passed to stree_tree_scan / stree_commit is not
+ *                            written by the kernel immediately preceding the call in its stream
+ *                            (true in a decode loop: the state was committed an iteration earlier).
+ *                            The kernels then start streaming h0 before that wait.
+ */
+enum { STREE_LAUNCH_PDL = 1, STREE_LAUNCH_EARLY_STATE = 2 };
+stree_status stree_set_launch_flags(uint32_t flags);
+
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
 

@@ -52,6 +52,7 @@ def lib():
             "stree_accept": [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp],
             "stree_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
             "stree_set_scan_impl": [ctypes.c_int],
+            "stree_set_launch_flags": [ctypes.c_uint32],
             "stree_scan_kernel_for": [vp],
         }
         for name, args in sig.items():
@@ -66,8 +67,10 @@ def lib():
     return _lib
 
 
+STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE = 1, 2
+
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
-                    "stree_status_string", "stree_set_scan_impl", "stree_scan_kernel_for", "stree_version")
+                    "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version")
 
 
 def status_string(s: int) -> str:
@@ -143,6 +146,10 @@ def stree_commit(x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status=Non
 
 def stree_set_scan_impl(impl: int):
     _check("stree_set_scan_impl", lib().stree_set_scan_impl(int(impl)))
+
+
+def stree_set_launch_flags(flags: int):
+    _check("stree_set_launch_flags", lib().stree_set_launch_flags(int(flags)))
 
 
 def stree_scan_kernel_for(dims: stree_dims) -> int:

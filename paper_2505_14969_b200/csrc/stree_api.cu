@@ -23,6 +23,7 @@ extern "C" int stree_tc_supports(const stree_dims*);
 namespace {
 
 std::atomic<int> g_scan_impl{STREE_SCAN_AUTO};
+std::atomic<uint32_t> g_launch_flags{STREE_LAUNCH_PDL};
 
 bool sync_check_enabled() {
     static int v = [] {
@@ -61,6 +62,14 @@ stree_status check_dims(const stree_dims* d) {
 extern "C" {
 
 const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
+
+uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed); }
+
+stree_status stree_set_launch_flags(uint32_t flags) {
+    if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE)) return STREE_ERR_UNSUPPORTED;
+    g_launch_flags.store(flags);
+    return STREE_OK;
+}
 
 const char* stree_status_string(stree_status s) {
     switch (s) {

@@ -58,6 +58,7 @@ struct CommitParams {
     float* h_new;
     int32_t* dev_status;
     unsigned long long* trace;   // debug: per-CTA globaltimer stamps (64 per CTA)
+    int early_state;             // STREE_LAUNCH_EARLY_STATE: stream h0 before the PDL wait
 };
 
 __device__ __forceinline__ unsigned long long c_gtimer() {
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     const size_t base = ((size_t)b * H + hbeg) * (size_t)blk;
     unsigned long long* tr = prm.trace ? prm.trace + (size_t)blockIdx.x * 64 : nullptr;
     if (tr && tid == 0) tr[0] = c_gtimer();
+    pdl_trigger();
 
     if (tid == 0) {
         for (int s = 0; s < prm.slots; ++s) {
@@ -108,7 +110,14 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     if (warp == 0) {
         // ================= producer =================
         if (lane == 0 && prm.h0) {
-            for (int k = 0; k < nh; ++k) {
+            int k = 0;
+            if (prm.early_state)   // the state is not written by the preceding kernel: stream it now
+                for (; k < nh && k < prm.slots; ++k) {
+                    c_mbar_expect_tx(bar_full(k), blk_bytes);
+                    c_bulk_load(su32(ring + (size_t)k * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(k));
+                }
+            pdl_wait();
+            for (; k < nh; ++k) {
                 const int s = k % prm.slots;
                 c_mbar_wait(bar_empty(s), ((k / prm.slots) & 1) ^ 1);
                 c_mbar_expect_tx(bar_full(s), blk_bytes);
@@ -118,6 +127,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
         return;
     }
     // ================= compute warps =================
+    pdl_wait();
     const int ct = tid - 32;                            // 0..255
     const IO* x = (const IO*)prm.x;
     const IO* Bm = (const IO*)prm.Bm;
@@ -289,6 +299,8 @@ __global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, 
     __shared__ float s_decay;
     __shared__ int s_r;
     const int h = blockIdx.x, b = blockIdx.y, g = h / (H / G), tid = threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
     const int r0 = path_len[b];
     if (tid < 32) {
         int ok = (r0 >= 1 && r0 <= T);
@@ -375,9 +387,9 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
                          (blk_bytes % 16 == 0) &&
                          (blk_bytes * 2 <= (size_t)stree::kRingBytes);
     if (!ring_ok) {
-        stree::commit_block_kernel<IO><<<dim3(H, B), 256, 0, s>>>(T, H, P, N, G, (const IO*)x, dt, A, (const IO*)Bm,
-                                                                  h0, parent, path, path_len, h_new, dev_status);
-        return (int)cudaGetLastError();
+        return (int)stree::launch_k(stree::commit_block_kernel<IO>, dim3(H, B), dim3(256), 0, s, T, H, P, N, G,
+                                    (const IO*)x, dt, A, (const IO*)Bm, h0, parent, path, path_len, h_new,
+                                    dev_status);
     }
     const int hpg = H / G;
     int cpg = commit_sms() / (B * G);
@@ -389,7 +401,8 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
     int slots = (int)(stree::kRingBytes / blk_bytes);
     if (slots > 8) slots = 8;
     stree::CommitParams prm{B, T, H, P, N, G, cpg, hpc, slots, x, dt, A, Bm, h0, parent, path, path_len,
-                            h_new, dev_status, g_commit_trace};
+                            h_new, dev_status, g_commit_trace,
+                            (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0};
     size_t ustage = (size_t)stree::kCHPC * stree::kRMax * P * 4;
     const size_t lcoef = (size_t)stree::kCHPC * stree::kMaxNodes * 4;
     if (ustage < lcoef) ustage = lcoef;
@@ -398,8 +411,7 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
     auto k = stree::commit_ring_kernel<IO>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    k<<<B * G * cpg, stree::kCThreads, smem, s>>>(prm);
-    return (int)cudaGetLastError();
+    return (int)stree::launch_k(k, dim3(B * G * cpg), dim3(stree::kCThreads), smem, s, prm);
 }
 
 }  // namespace

@@ -4,12 +4,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/stree.h"
 
 namespace stree {
 
 constexpr int kMaxNodes = STREE_MAX_NODES;          // T <= 256
 constexpr int kMaxWords = (kMaxNodes + 31) / 32;    // mask words per row
+
+// ---- Programmatic dependent launch (PDL) ----
+// Every kernel calls pdl_trigger() at entry (the next grid in the stream may be scheduled as SMs free
+// up) and pdl_wait() before its first global read or write of call arguments; setup that touches
+// no argument memory (barrier init, TMEM alloc, descriptor prefetch) runs before the wait.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void report(int32_t* dev_status, int code) {
     if (dev_status) atomicCAS(dev_status, 0, code);
@@ -80,4 +89,26 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* rows, int W, int i, int
     return (rows[i * W + (j >> 5)] >> (j & 31)) & 1u;
 }
 
+}  // namespace stree
+
+// launch options (stree_set_launch_flags), read by every launcher
+extern "C" uint32_t stree_launch_flags_get();
+
+namespace stree {
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute when PDL is enabled
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (stree_launch_flags_get() & STREE_LAUNCH_PDL) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 }  // namespace stree

@@ -17,6 +17,8 @@ __global__ void __launch_bounds__(256) build_mask_kernel(const int32_t* __restri
     __shared__ int sp[kMaxNodes], jmp[kMaxNodes], jmp2[kMaxNodes];
     __shared__ uint32_t rows[kMaxNodes * kMaxWords], rows2[kMaxNodes * kMaxWords];
     const int b = blockIdx.x, W = (T + 31) >> 5;
+    pdl_trigger();
+    pdl_wait();
     for (int i = threadIdx.x; i < T; i += blockDim.x) sp[i] = parent[(size_t)b * T + i];
     __syncthreads();
     int code = build_tree_rows(sp, T, W, rows, rows2, jmp, jmp2);
@@ -41,6 +43,8 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
                                                      int32_t* __restrict__ bonus, int32_t* dev_status) {
     __shared__ int s_par[4][kMaxNodes], s_tok[4][kMaxNodes], s_vt[4][kMaxNodes];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_trigger();
+    pdl_wait();
     const int b = blockIdx.x * 4 + warp;
     if (b >= B) return;
     const int32_t* par = parent + (size_t)b * T;
@@ -92,14 +96,13 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
 
 extern "C" int stree_launch_build_mask(const int32_t* parent, int B, int T, uint32_t* mask,
                                        int32_t* depth, int32_t* dev_status, cudaStream_t s) {
-    stree::build_mask_kernel<<<B, 256, 0, s>>>(parent, T, mask, depth, dev_status);
-    return (int)cudaGetLastError();
+    return (int)stree::launch_k(stree::build_mask_kernel, dim3(B), dim3(256), 0, s, parent, T, mask, depth,
+                                dev_status);
 }
 
 extern "C" int stree_launch_accept(const int32_t* tokens, const int32_t* parent, const int32_t* vtok,
                                    int B, int T, int32_t* path, int32_t* path_len, int32_t* bonus,
                                    int32_t* dev_status, cudaStream_t s) {
-    stree::accept_kernel<<<(B + 3) / 4, 128, 0, s>>>(tokens, parent, vtok, B, T, path, path_len, bonus,
-                                                     dev_status);
-    return (int)cudaGetLastError();
+    return (int)stree::launch_k(stree::accept_kernel, dim3((B + 3) / 4), dim3(128), 0, s, tokens, parent, vtok, B, T,
+                                path, path_len, bonus, dev_status);
 }

@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
     const int W = L.W, mp = L.mpitch;
     const int h = blockIdx.x, b = blockIdx.y, g = h / (H / G);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    pdl_trigger();
+    pdl_wait();
 
     for (int i = tid; i < T; i += 256) sp[i] = parent[(size_t)b * T + i];
     __syncthreads();
@@ -190,15 +192,18 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
         auto k = stree::scan_simt_kernel<__nv_bfloat16>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        k<<<grid, 256, smem, s>>>(T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
-                                  (const __nv_bfloat16*)x, dt, A, (const __nv_bfloat16*)Bm,
-                                  (const __nv_bfloat16*)Cm, D, h0, parent, (__nv_bfloat16*)y, dev_status);
+        e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
+                            (const __nv_bfloat16*)x, dt, A, (const __nv_bfloat16*)Bm, (const __nv_bfloat16*)Cm, D, h0,
+                            parent, (__nv_bfloat16*)y, dev_status);
+        if (e != cudaSuccess) return (int)e;
     } else {
         auto k = stree::scan_simt_kernel<float>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        k<<<grid, 256, smem, s>>>(T, d->n_heads, d->head_dim, d->d_state, d->n_groups, (const float*)x, dt, A,
-                                  (const float*)Bm, (const float*)Cm, D, h0, parent, (float*)y, dev_status);
+        e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
+                            (const float*)x, dt, A, (const float*)Bm, (const float*)Cm, D, h0, parent, (float*)y,
+                            dev_status);
+        if (e != cudaSuccess) return (int)e;
     }
     return (int)cudaGetLastError();
 }

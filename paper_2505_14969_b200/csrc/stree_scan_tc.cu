@@ -68,7 +68,8 @@ struct Smem {
     static constexpr int MODE = E0 + kHPC * 64 * 4;       // int[kHPC]
     static constexpr int AS = MODE + kHPC * 4;            // float[kHPC]  A_h
     static constexpr int DS = AS + kHPC * 4;              // float[kHPC]  D_h
-    static constexpr int BAR = (DS + kHPC * 4 + 7) & ~7;
+    static constexpr int BADF = DS + kHPC * 4;            // int
+    static constexpr int BAR = (BADF + 4 + 7) & ~7;
     // barriers (u64): tree, ctf32, gdone, full[3], empty[3], mfull[2], mempty[2], accfull[2], accempty[2]
     static constexpr int NBAR = 3 + 2 * kStages + 8;
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -88,6 +89,10 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// adds to the barrier's expected transaction bytes without arriving
+__device__ __forceinline__ void mbar_add_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -228,6 +233,7 @@ struct Params {
     __nv_bfloat16* y;
     int32_t* dev_status;
     int has_h0;
+    int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
 };
 
 template <int NS>
@@ -251,43 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
     if (nh <= 0) return;
     int* sp = (int*)(sm + S::PAR);
-
-    // ---- per-CTA inputs issued first so their latency overlaps the setup ----
-    // epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane and lane+32
-    constexpr int kHPW = kHPC / 4;            // heads per epilogue warp
-    float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
-    if (tid >= kEpi0) {
-        const int ew = (tid - kEpi0) >> 5;
-#pragma unroll
-        for (int q = 0; q < kHPW; ++q) {
-            const int hh = ew + 4 * q;
-            const bool hv = hh < nh;
-            a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
-            d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int i = lane + 32 * hf;
-                dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
-            }
-        }
-    }
-    // ---- tree validation (all threads; PAPER.md:90 precondition) ----
-    int bad = 0;
-    for (int i = tid; i < T; i += kThreads) {
-        int p = prm.parent[(size_t)b * T + i];
-        sp[i] = p;
-        if (i == 0) { if (p != -1) bad = 1; }
-        else if (p < 0 || p >= i) bad = 2;
-    }
-    const int any1 = __syncthreads_or(bad == 1), any2 = __syncthreads_or(bad == 2);
-    if (any1 | any2) {
-        if (tid == 0 && chunk == 0 && g == 0) report(prm.dev_status, any1 ? 1 : 2);
-        for (int k = tid; k < T * nh * kP; k += kThreads) {
-            int i = k / (nh * kP), hh = (k / kP) % nh, p = k % kP;
-            prm.y[(((size_t)b * T + i) * H + hbeg + hh) * kP + p] = __float2bfloat16_rn(0.f);
-        }
-        return;
-    }
+    pdl_trigger();
 
     const uint32_t bar0 = sb + S::BAR;
     const uint32_t BAR_TREE = bar0, BAR_CTF = bar0 + 8, BAR_G = bar0 + 16;
@@ -299,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto bar_accempty = [&](int a) { return bar0 + 24 + 16 * kStages + 48 + 8 * a; };
     uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
 
+    // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
     if (tid == 0) {
         mbar_init(BAR_TREE, 1);
         mbar_init(BAR_CTF, 128);
@@ -323,6 +294,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    const int n_early = (prm.early_state && prm.has_h0) ? min(nh, kStages) : 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
+        // the state of the first heads is streamed before the dependency wait (caller's promise)
+        for (int k = 0; k < n_early; ++k) {
+            mbar_add_tx(bar_full(k), S::H0S);
+            for (int a = 0; a < NS / 32; ++a)
+                tma_load_2d(sb + S::H0 + k * S::H0S + a * kAtom, &tm_h0, bar_full(k), 32 * a,
+                            ((b * H) + hbeg + k) * kP);
+        }
+    }
+    pdl_wait();
+
+    // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
+    //      The producer issues the tree operands right after the wait; tree validation runs in the
+    //      epilogue warps (an invalid tree yields y = 0), so nothing waits on it ----
+    constexpr int kHPW = kHPC / 4;            // heads per epilogue warp
+    float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
+    int* sbad = (int*)(sm + S::BADF);
+    if (tid >= kEpi0) {
+        const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
+        if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
+#pragma unroll
+        for (int q = 0; q < kHPW; ++q) {
+            const int hh = ew + 4 * q;
+            const bool hv = hh < nh;
+            a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
+            d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
+            }
+        }
+        if (e == 0) *sbad = 0;
+        named_bar(1, 128);
+        if (e < T) {   // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i
+            const int p = sp[e];
+            const int code = (e == 0) ? (p != -1 ? 1 : 0) : ((p < 0 || p >= e) ? 2 : 0);
+            if (code) atomicMax(sbad, code == 1 ? 2 : 1);   // root error takes precedence
+        }
+        named_bar(1, 128);
+        if (*sbad) {
+            // invalid tree: make the pointer chains harmless; the output stage writes zeros
+            if (e < T) sp[e] = (e == 0) ? -1 : 0;
+            if (e == 0 && chunk == 0 && g == 0) report(prm.dev_status, *sbad == 2 ? 1 : 2);
+        }
+        named_bar(1, 128);
+    }
     const uint32_t tmem = *tmem_slot;
     const int Tp16 = (T + 15) & ~15;
     const int xbytes = T * 128;
@@ -330,24 +350,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ================= TMA producer =================
         if (lane == 0) {
-            tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
             mbar_expect_tx(BAR_TREE, 2 * S::kCbAtoms * xbytes);
             for (int a = 0; a < S::kCbAtoms; ++a) {
                 tma_load_2d(sb + S::CB + a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
                 tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
             }
-            // the tree operands (and the epilogue's small loads) go first: the state stream starts
-            // once they have landed, so they do not queue behind ~kStages x 40 KB per SM of bulk data
+            // the bulk state stream starts once the tree operands have landed: issued together, the
+            // ~kStages x 40 KB per CTA would queue the small critical-path loads behind it
             mbar_wait(BAR_TREE, 0);
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
-                mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
                 const int h = hbeg + k;
-                mbar_expect_tx(bar_full(s), (prm.has_h0 ? S::H0S : 0) + xbytes);
-                if (prm.has_h0)
-                    for (int a = 0; a < NS / 32; ++a)
-                        tma_load_2d(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
-                                    ((b * H) + h) * kP);
+                if (k < n_early) {   // state already in flight: add x and arrive
+                    mbar_expect_tx(bar_full(s), xbytes);
+                } else {
+                    mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
+                    mbar_expect_tx(bar_full(s), (prm.has_h0 ? S::H0S : 0) + xbytes);
+                    if (prm.has_h0)
+                        for (int a = 0; a < NS / 32; ++a)
+                            tma_load_2d(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
+                                        ((b * H) + h) * kP);
+                }
                 tma_load_2d(sb + S::X + s * S::XS, &tm_x, bar_full(s), h * kP, b * T);
             }
         }
@@ -590,8 +613,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
                 named_bar(2, 64);
                 if (trace && leader && k < 6) trace[52 + 2 * k] = gtimer();
-                const float Dh = ((const float*)(sm + S::DS))[k];
-                const float s0 = own ? e0[k * 64 + row] : 0.f, s1 = own ? ei[k * 64 + row] : 0.f;
+                const bool zero_out = *sbad != 0;
+                const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[k];
+                const float s0 = (own && !zero_out) ? e0[k * 64 + row] : 0.f;
+                const float s1 = (own && !zero_out) ? ei[k * 64 + row] : 0.f;
                 const unsigned char* xr = sm + S::X + s * S::XS;
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + kAccCol0 + 128 * a;
@@ -623,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     fmaf(s0, __uint_as_float(v0[c][p]), fmaf(s1, __uint_as_float(v1[c][p]), Dh * xa));
                                 const float yb = fmaf(s0, __uint_as_float(v0[c][p + 1]),
                                                       fmaf(s1, __uint_as_float(v1[c][p + 1]), Dh * xb));
-                                o[q] = pack_bf16(ya, yb);
+                                o[q] = zero_out ? 0u : pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
                         }
@@ -745,19 +770,21 @@ extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const fl
     if (hpc > kHPC) hpc = kHPC;
     cpg = (hpg + hpc - 1) / hpc;
     stree::tc::Params prm{g_trace, B, T, H, G, cpg, hpc, dt, A, D, parent, (__nv_bfloat16*)y, dev_status,
-                          h0 != nullptr};
+                          h0 != nullptr, (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0};
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (N == 128) {
         size_t smem = Smem<128>::TOTAL + 1024;
         e = cudaFuncSetAttribute(scan_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        scan_tc_kernel<128><<<grid, kThreads, smem, s>>>(mc, mb, mx, mh, my, prm);
+        e = stree::launch_k(scan_tc_kernel<128>, grid, dim3(kThreads), smem, s, mc, mb, mx, mh, my, prm);
+        if (e != cudaSuccess) return (int)e;
     } else {
         size_t smem = Smem<64>::TOTAL + 1024;
         e = cudaFuncSetAttribute(scan_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        scan_tc_kernel<64><<<grid, kThreads, smem, s>>>(mc, mb, mx, mh, my, prm);
+        e = stree::launch_k(scan_tc_kernel<64>, grid, dim3(kThreads), smem, s, mc, mb, mx, mh, my, prm);
+        if (e != cudaSuccess) return (int)e;
     }
     return (int)cudaGetLastError();
 }

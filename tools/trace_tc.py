@@ -16,17 +16,32 @@ from paper_2505_14969_b200 import api, binding  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
+ap.add_argument("--flags", type=int, default=0)
 args = ap.parse_args()
+binding.stree_set_launch_flags(args.flags)
 prob = inputs.config_problem(args.config)
-t = api.upload(prob)
+layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BASE_SEED + 50 + i)) for i in range(8)]
+t = layers[-1]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
 buf = torch.zeros((1024, 64), dtype=torch.int64, device="cuda")
+ys = [torch.empty_like(l["x"]) for l in layers]
 for _ in range(3):
-    api.tree_scan(t)
+    for l, y in zip(layers, ys):
+        api.tree_scan(l, y=y)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    for l, y in zip(layers, ys):
+        api.tree_scan(l, y=y)
+e1.record()
+torch.cuda.synchronize()
+print(f"eager back-to-back over 8 layers: {e0.elapsed_time(e1) / 40 * 1e3:.2f} us per scan")
+for l, y in zip(layers[:-1], ys):
+    api.tree_scan(l, y=y)
 L.stree_debug_tc_trace(ctypes.c_void_p(buf.data_ptr()))
-api.tree_scan(t)
+api.tree_scan(t, y=ys[-1])
 torch.cuda.synchronize()
 L.stree_debug_tc_trace(None)
 tr = buf.cpu().numpy().astype(np.int64)
