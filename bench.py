@@ -3,9 +3,12 @@
 "tree-verify nodes/s per SSM layer (1/2/4/8 B200); % of roofline").
 
 One STEP = one verify iteration of an L-layer Mamba-2 stack over one batch of
-synthetic drafted trees, i.e. one pass through every §8(a) row:
-    stree_build_mask (once)  ->  L x stree_tree_scan  ->  stree_accept (once)
-    ->  L x stree_commit (in place, the committed state is the next step's h0)
+synthetic drafted trees, i.e. one pass through every §8(a) row, in Alg. 1's
+order (PAPER.md:121-125: ActivationReplay, TreeScan, FirstRejected):
+    stree_build_mask (once) -> L x stree_replay_scan (commit of the previous
+    step's accepted path into the layer state + scan of the tree) -> stree_accept
+With --no-fuse the commit runs as separate kernels after accept:
+    stree_build_mask -> L x stree_tree_scan -> stree_accept -> L x stree_commit
 Workload (default) = BASELINE configs[3] / SURVEY c4 per GPU: 16 random
 recursive trees x 64 nodes, Mamba-2 2.7B layer shape (H=80, P=64, N=128, G=1),
 bf16 x/B/C/y, fp32 dt/A/D/state, L = 64 distinct layers (every layer has its
@@ -51,6 +54,8 @@ def parse():
     ap.add_argument("--scan-impl", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-early-state", action="store_true")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="separate commit kernels instead of the fused replay+scan (stree_replay_scan)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--p-match", type=float, default=0.9)
     ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
@@ -69,7 +74,7 @@ def dist_env():
 def workload_desc(cfg, prob, L):
     d = prob.dims
     return {"workload": f"{cfg}: Mamba-2 2.7B-shaped SSM layer stack, tree verify "
-                        f"(mask + {L} x scan + accept + {L} x commit)" if cfg != "c2" else
+                        f"(mask, scan + commit of {L} layers, accept)" if cfg != "c2" else
             f"{cfg}: Mamba-2 130M-shaped layer stack, tree verify",
             "trees_per_gpu": d.batch, "nodes_per_tree": d.n_nodes, "heads": d.n_heads, "head_dim": d.head_dim,
             "d_state": d.d_state, "n_groups": d.n_groups, "layers": L, "io_dtype": d.io_dtype,
@@ -321,15 +326,27 @@ def run_stree(args):
     def ph_accept():
         binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
 
+    def ph_replay_scan():
+        # commit of the previous step's accepted path (cache = this layer's x, dt, B of that step)
+        # fused with the scan of the current tree, state updated in place
+        for t in layers:
+            binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
+                                      t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status, dims_prev=dims,
+                                      dims=dims)
+
     def ph_commit():
         for t in layers:
             binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"], status,
                                  dims=dims)
 
-    phases = [ph_mask, ph_scan, ph_accept, ph_commit]
+    fused = not args.no_fuse and not heads_mode
+    phases = [ph_mask, ph_replay_scan, ph_accept] if fused else [ph_mask, ph_scan, ph_accept, ph_commit]
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        for f in phases:      # eager warm-up (loads modules, sets smem attributes)
+        ph_mask()
+        ph_scan()
+        ph_accept()        # a valid accepted path exists before the first replay
+        for f in phases:   # eager warm-up (loads modules, sets smem attributes)
             f()
     torch.cuda.synchronize()
     graphs = []
@@ -385,38 +402,48 @@ def run_stree(args):
     nodes_per_step = d.batch * d.n_nodes * L * (1 if heads_mode else world)
     value = nodes_per_step / (ms_per_step * 1e-3)
     ph_mean = phase_ms.mean(0)
-    scan_us = ph_mean[1] * 1e3 / L
-    commit_us = ph_mean[3] * 1e3 / L
     hbm_peak, bf16_peak, peak_src = load_peaks()
     sb = scan_bytes(d)
     cb = commit_bytes(d, plen_host)
-    scan_gbs = sb / (scan_us * 1e-6) / 1e9
-    commit_gbs = cb / (commit_us * 1e-6) / 1e9
-    dominant = "stree_tree_scan" if scan_us >= commit_us else "stree_commit"
-    dom_gbs, dom_bytes = (scan_gbs, sb) if dominant == "stree_tree_scan" else (commit_gbs, cb)
     traffic = load_traffic(args.config) or {}
+    kernels = {"stree_build_mask": {"us": ph_mean[0] * 1e3}, "stree_accept": {"us": ph_mean[2] * 1e3}}
+    if fused:
+        # fused bytes: the scan's bytes + the committed state written back + the previous path's rows
+        fb = sb + cb - d.batch * d.n_heads * d.head_dim * d.d_state * 4
+        fu_us = ph_mean[1] * 1e3 / L
+        fu_gbs = fb / (fu_us * 1e-6) / 1e9
+        kernels["stree_replay_scan"] = {"us": fu_us, "bytes": fb, "GB/s": fu_gbs, "frac": fu_gbs / hbm_peak,
+                                        "impl": {1: "simt+commit", 2: "tcgen05 fused"}.get(kernel),
+                                        "mean_path_len": float(plen_host.mean())}
+        dominant, dom_gbs, dom_bytes = "stree_replay_scan", fu_gbs, fb
+    else:
+        scan_us = ph_mean[1] * 1e3 / L
+        commit_us = ph_mean[3] * 1e3 / L
+        scan_gbs = sb / (scan_us * 1e-6) / 1e9
+        commit_gbs = cb / (commit_us * 1e-6) / 1e9
+        kernels["stree_tree_scan"] = {"us": scan_us, "bytes": sb, "GB/s": scan_gbs, "frac": scan_gbs / hbm_peak,
+                                      "impl": {1: "simt", 2: "tcgen05"}.get(kernel)}
+        kernels["stree_commit"] = {"us": commit_us, "bytes": cb, "GB/s": commit_gbs, "frac": commit_gbs / hbm_peak,
+                                   "mean_path_len": float(plen_host.mean())}
+        dominant = "stree_tree_scan" if scan_us >= commit_us else "stree_commit"
+        dom_gbs, dom_bytes = (scan_gbs, sb) if dominant == "stree_tree_scan" else (commit_gbs, cb)
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": dom_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": dom_gbs / hbm_peak, "traffic": traffic.get(dominant), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": dom_bytes,
-                "kernels": {"stree_tree_scan": {"us": scan_us, "bytes": sb, "GB/s": scan_gbs,
-                                                "frac": scan_gbs / hbm_peak,
-                                                "impl": {1: "simt", 2: "tcgen05"}.get(kernel)},
-                            "stree_commit": {"us": commit_us, "bytes": cb, "GB/s": commit_gbs,
-                                             "frac": commit_gbs / hbm_peak, "mean_path_len":
-                                                 float(plen_host.mean())},
-                            "stree_build_mask": {"us": ph_mean[0] * 1e3},
-                            "stree_accept": {"us": ph_mean[2] * 1e3}}}
+                "algorithmic_bytes_per_launch": dom_bytes, "kernels": kernels}
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L)
+        e2e = run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L,
+                      fused)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if heads_mode else "weak",
             "vs_baseline": None,
             "dtype": d.io_dtype, "data": "synthetic", "config": workload_desc(args.config, base, L),
-            "gpu_launches": (2 * L + 2) * K, "roofline": roofline, "e2e": e2e,
+            "gpu_launches": ((L + 2) if fused else (2 * L + 2)) * K, "roofline": roofline, "e2e": e2e,
+            "step": "mask + L x replay_scan (fused commit+scan) + accept" if fused else
+                    "mask + L x scan + accept + L x commit",
             "clocks": sampler.summary(),
             "parallelism": (f"heads x{world} (+NCCL all-gather of y)" if heads_mode else
                             f"batch-replicas x{world}") if world > 1 else "single"}
@@ -429,7 +456,7 @@ def run_stree(args):
     return 0
 
 
-def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L):
+def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L, fused):
     """Same step through the public API, inputs copied from pinned host memory
     every step (x, dt, B, C of every layer + tree + tokens) and the acceptance
     result (path, path_len, bonus) read back."""
@@ -459,12 +486,18 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
             for t, hh in zip(layers, host):
                 for k, v in hh.items():
                     t[k].copy_(v, non_blocking=True)
-                binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent,
-                                        t["y"], status, dims=dims)
+                if fused:
+                    binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
+                                              t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status,
+                                              dims_prev=dims, dims=dims)
+                else:
+                    binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent,
+                                            t["y"], status, dims=dims)
             binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
-            for t in layers:
-                binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"],
-                                     status, dims=dims)
+            if not fused:
+                for t in layers:
+                    binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"],
+                                         status, dims=dims)
             for o, s in zip(out, (path, plen, bonus)):
                 o.copy_(s, non_blocking=True)
         stream.synchronize()

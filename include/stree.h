@@ -142,6 +142,30 @@ stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, c
                           const int32_t* path, const int32_t* path_len, float* h_new,
                           int32_t* dev_status, void* stream);
 
+/*
+ * stree_replay_scan — fused activation replay + tree scan (Alg. 1 l.123-124 in order:
+ * ActivationReplay then TreeScan).  Equivalent to
+ *   stree_commit(d_prev, x_prev, dt_prev, A, Bm_prev, h, parent_prev, path, path_len, h)   (in place)
+ *   stree_tree_scan(d, x, dt, A, Bm, Cm, D, h, parent, y)
+ * but every state block is read from HBM once and written once: the replay is applied to the
+ * block on chip and the updated block is both the scan's carry-in and the committed state.
+ *   d_prev                 dims of the previous (cached) tree; must match d except n_nodes
+ *   x_prev, dt_prev, Bm_prev, parent_prev, path, path_len
+ *                          the previous iteration's cache and acceptance (as for stree_commit;
+ *                          parent_prev may be NULL)
+ *   h      [B][H][P][N] f32, in/out: on entry the state the previous tree was scanned from,
+ *                          on exit the committed state (h after the accepted path)
+ *   x, dt, A, Bm, Cm, D, parent, y   the new tree, as for stree_tree_scan
+ * Invalid previous path for tree b: dev_status <- 3 and h[b] is left unchanged (the scan uses it).
+ * Invalid new tree: dev_status <- 1/2 and y[b] = 0 (the replay is still applied).
+ */
+stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                               const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                               const int32_t* path_len, const stree_dims* d, const void* x,
+                               const float* dt, const float* A, const void* Bm, const void* Cm,
+                               const float* D, float* h, const int32_t* parent, void* y,
+                               int32_t* dev_status, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 const char* stree_status_string(stree_status s);
 

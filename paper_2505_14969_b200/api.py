@@ -62,3 +62,13 @@ def commit(t: dict, path, path_len, h_new=None, dev_status=None, use_parent=True
     _b.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], t["parent"] if use_parent else None, path,
                     path_len, h_new, dev_status)
     return h_new
+
+
+def replay_scan(prev: dict, path, path_len, t: dict, h, dev_status=None, y=None, use_parent=True):
+    """Fused commit of the previous tree (cache `prev`, accepted `path`) into the state `h` (in place)
+    and scan of the new tree `t` from the committed state; returns y."""
+    if y is None:
+        y = torch.empty_like(t["x"])
+    _b.stree_replay_scan(prev["x"], prev["dt"], prev["Bm"], prev["parent"] if use_parent else None, path, path_len,
+                         t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t.get("D"), h, t["parent"], y, dev_status)
+    return y

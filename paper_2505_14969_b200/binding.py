@@ -53,6 +53,7 @@ def lib():
             "stree_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
             "stree_set_scan_impl": [ctypes.c_int],
             "stree_set_launch_flags": [ctypes.c_uint32],
+            "stree_replay_scan": [vp] * 19,
             "stree_scan_kernel_for": [vp],
         }
         for name, args in sig.items():
@@ -70,7 +71,8 @@ def lib():
 STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE = 1, 2
 
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
-                    "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version")
+                    "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",
+                    "stree_replay_scan")
 
 
 def status_string(s: int) -> str:
@@ -142,6 +144,16 @@ def stree_commit(x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status=Non
     _check("stree_commit", lib().stree_commit(ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(h0),
                                               _ptr(parent), _ptr(path), _ptr(path_len), _ptr(h_new),
                                               _ptr(dev_status), _stream(stream)))
+
+
+def stree_replay_scan(x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, x, dt, A, Bm, Cm, D, h, parent, y,
+                      dev_status=None, stream=None, dims_prev=None, dims=None):
+    dp = dims_prev if dims_prev is not None else make_dims(x_prev, Bm_prev)
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_replay_scan", lib().stree_replay_scan(
+        ctypes.byref(dp), _ptr(x_prev), _ptr(dt_prev), _ptr(Bm_prev), _ptr(parent_prev), _ptr(path),
+        _ptr(path_len), ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h),
+        _ptr(parent), _ptr(y), _ptr(dev_status), _stream(stream)))
 
 
 def stree_set_scan_impl(impl: int):

@@ -19,6 +19,10 @@ extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*
                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
                                     cudaStream_t);
 extern "C" int stree_tc_supports(const stree_dims*);
+extern "C" int stree_launch_replay_scan_tc(const stree_dims*, const void*, const float*, const void*, const int32_t*,
+                                           const int32_t*, const int32_t*, const stree_dims*, const void*,
+                                           const float*, const float*, const void*, const void*, const float*, float*,
+                                           const int32_t*, void*, int32_t*, cudaStream_t);
 
 namespace {
 
@@ -154,6 +158,39 @@ stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, c
     }
     cudaStream_t s = (cudaStream_t)stream;
     return finish(stree_launch_commit(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s),
+                  dev_status, s);
+}
+
+stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                               const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                               const int32_t* path_len, const stree_dims* d, const void* x, const float* dt,
+                               const float* A, const void* Bm, const void* Cm, const float* D, float* h,
+                               const int32_t* parent, void* y, int32_t* dev_status, void* stream) {
+    stree_status st = check_dims(d);
+    if (st != STREE_OK) return st;
+    if ((st = check_dims(d_prev)) != STREE_OK) return st;
+    if (d_prev->batch != d->batch || d_prev->n_heads != d->n_heads || d_prev->head_dim != d->head_dim ||
+        d_prev->d_state != d->d_state || d_prev->n_groups != d->n_groups || d_prev->io_dtype != d->io_dtype)
+        return STREE_ERR_SHAPE;
+    if (d->batch == 0) return STREE_OK;
+    if (!h) return STREE_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool fused = d->n_nodes > 0 && d_prev->n_nodes > 0 && stree_scan_kernel_for(d) == 2;
+    if (!fused) {   // two launches: commit (in place), then scan from the committed state
+        if (d_prev->n_nodes > 0) {
+            st = stree_commit(d_prev, x_prev, dt_prev, A, Bm_prev, h, parent_prev, path, path_len, h, dev_status,
+                              stream);
+            if (st != STREE_OK) return st;
+        }
+        return stree_tree_scan(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, stream);
+    }
+    if (!x_prev || !dt_prev || !Bm_prev || !path || !path_len || !x || !dt || !A || !Bm || !Cm || !parent || !y)
+        return STREE_ERR_NULL;
+    const void* ptrs[] = {x_prev, dt_prev, Bm_prev, x, dt, A, Bm, Cm, D, h, parent, y};
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return STREE_ERR_ALIGN;
+    return finish(stree_launch_replay_scan_tc(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt,
+                                              A, Bm, Cm, D, h, parent, y, dev_status, s),
                   dev_status, s);
 }
 

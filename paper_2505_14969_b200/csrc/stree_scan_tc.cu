@@ -35,17 +35,19 @@ namespace tc {
 
 constexpr int kT = 64;          // max nodes per tree served
 constexpr int kP = 64;          // head dim
-constexpr int kStages = 4;      // h0/x ring depth
 constexpr int kHPC = 12;        // max heads per CTA
-constexpr int kThreads = 192;
+constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
+constexpr int kThreadsReplay = 320;   // + warps 6-9 replay updaters
+constexpr int kRStage = 16;           // previous-path nodes staged on chip by the replay
 constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
 constexpr uint32_t kTmemCols = 512;
 constexpr int kCCol = 64;       // C as tf32 (A operand of Y0) in TMEM columns [64, 64 + N)
 constexpr int kAccCol0 = 256;   // acc a: Y0 at 256 + 128a, Y' at 256 + 128a + 64
 
-template <int NS>
+template <int NS, bool R>
 struct Smem {
+    static constexpr int kSt = R ? 3 : 4;                 // h0/x ring depth
     static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
     static constexpr int U = 0;                           // union: {C bf16, B bf16} then {M'[2], ystage[2]}
     static constexpr int CB = U;
@@ -55,9 +57,9 @@ struct Smem {
     static constexpr int UBYTES = (2 * kCbAtoms * kAtom > 4 * kAtom) ? 2 * kCbAtoms * kAtom : 4 * kAtom;
     static constexpr int H0 = U + UBYTES;                 // h0 stages
     static constexpr int H0S = kP * NS * 4;               // bytes per stage
-    static constexpr int X = H0 + kStages * H0S;          // x stages
+    static constexpr int X = H0 + kSt * H0S;              // x stages
     static constexpr int XS = kAtom;
-    static constexpr int MISC = X + kStages * XS;
+    static constexpr int MISC = X + kSt * XS;
     // misc (4-byte words unless noted)
     static constexpr int PAR = MISC;                      // int[64]
     static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
@@ -69,9 +71,16 @@ struct Smem {
     static constexpr int AS = MODE + kHPC * 4;            // float[kHPC]  A_h
     static constexpr int DS = AS + kHPC * 4;              // float[kHPC]  D_h
     static constexpr int BADF = DS + kHPC * 4;            // int
-    static constexpr int BAR = (BADF + 4 + 7) & ~7;
-    // barriers (u64): tree, ctf32, gdone, full[3], empty[3], mfull[2], mempty[2], accfull[2], accempty[2]
-    static constexpr int NBAR = 3 + 2 * kStages + 8;
+    // replay (fused commit of the previous tree)
+    static constexpr int RPATH = BADF + 16;               // int[kMaxNodes]   previous accepted path
+    static constexpr int RINFO = RPATH + (R ? kMaxNodes * 4 : 0);   // int[4]: r (0 = invalid / nothing)
+    static constexpr int RCOEF = RINFO + 16;              // float[kHPC][kMaxNodes] c_{h,m}
+    static constexpr int RDEC = RCOEF + (R ? kHPC * kMaxNodes * 4 : 0);   // float[kHPC] decay
+    static constexpr int XPREV = RDEC + (R ? kHPC * 4 : 0);               // bf16 [kHPC][kRStage][64]
+    static constexpr int BPREV = XPREV + (R ? kHPC * kRStage * kP * 2 : 0);   // float[kRStage][NS]
+    static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
+    // barriers (u64): tree, ctf32, gdone, full[S], empty[S], mfull[2], mempty[2], accfull[2], accempty[2], upd[S]
+    static constexpr int NBAR = 3 + 2 * kSt + 8 + (R ? kSt : 0);
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
 };
@@ -234,14 +243,171 @@ struct Params {
     int32_t* dev_status;
     int has_h0;
     int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
+    // replay (fused commit of the previous tree), kReplay only
+    int Tp;
+    const __nv_bfloat16* x_prev;
+    const float* dt_prev;
+    const __nv_bfloat16* b_prev;
+    const int32_t* parent_prev;
+    const int32_t* path;
+    const int32_t* path_len;
 };
 
-template <int NS>
-__global__ void __launch_bounds__(kThreads, 1)
+// ---------------------------------------------------------------------------
+// Replay updaters (fused mode, warps 6-9): activation replay of the previous tree's accepted path
+// (Alg. 1 l.123) applied on chip to each TMA-staged state tile before the scan uses it:
+//   h <- e^{lam_{r-1}} h + Σ_m c_m x_prev[s_m] B_prev[s_m]ᵀ,  c_m = e^{lam_{r-1} - lam_m} dt_prev[s_m],
+//   lam_m = Σ_{q<=m} dt_prev[s_q] A_h   (the path-cumsum of log-decays, PAPER.md:86-90 on the path).
+// The updated tile is the carry-in of the scan (bar_upd) and is TMA-stored as the committed state.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+template <int NS, bool R>
+__device__ __forceinline__ void replay_updater(const Params& prm, unsigned char* sm, uint32_t sb,
+                                               const CUtensorMap* tm_h, int b, int g, int chunk, int hbeg, int nh,
+                                               uint32_t bar0) {
+    using S = Smem<NS, R>;
+    constexpr int kSt = S::kSt;
+    auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };
+    auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };
+    auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kSt + 64 + 8 * s; };
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int u = tid - kThreadsScan;     // 0..127
+    const int uw = warp - 6;              // 0..3
+    const int H = prm.H, Tp = prm.Tp, G = prm.G;
+    int* rpath = (int*)(sm + S::RPATH);
+    int* rinfo = (int*)(sm + S::RINFO);
+    float* rcoef = (float*)(sm + S::RCOEF);
+    float* rdec = (float*)(sm + S::RDEC);
+    __nv_bfloat16* xprev = (__nv_bfloat16*)(sm + S::XPREV);
+    float* bprev = (float*)(sm + S::BPREV);
+    // ---- previous path: validation (root-anchored, increasing, parent-linked) ----
+    if (uw == 0) {
+        const int r = prm.path_len[b];
+        int ok = (r >= 1 && r <= Tp);
+        if (ok) {
+            for (int m = lane; m < r; m += 32) {
+                const int v = prm.path[(size_t)b * Tp + m];
+                rpath[m] = v;
+                bool good = (v >= 0 && v < Tp);
+                if (m == 0) good = good && v == 0;
+                else {
+                    const int pu = prm.path[(size_t)b * Tp + m - 1];
+                    good = good && v > pu;
+                    if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
+                }
+                if (!good) ok = 0;
+            }
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) {
+            rinfo[0] = ok ? r : 0;
+            if (!ok && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+        }
+    }
+    named_bar(3, 128);
+    const int r = rinfo[0];
+    const int rs = min(r, kRStage);
+    if (r > 0) {
+        for (int hh = uw; hh < nh; hh += 4) {   // one warp per head
+            const int h = hbeg + hh;
+            const float Ah = prm.A[h];
+            float* cl = rcoef + hh * kMaxNodes;
+            float carry = 0.f;
+            for (int m0 = 0; m0 < r; m0 += 32) {
+                const int m = m0 + lane;
+                float a = (m < r) ? prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h] * Ah : 0.f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xffffffffu, a, o);
+                    if (lane >= o) a += t;
+                }
+                a += carry;
+                if (m < r) cl[m] = a;
+                carry = __shfl_sync(0xffffffffu, a, 31);
+            }
+            __syncwarp();
+            for (int m = lane; m < r; m += 32)
+                cl[m] = expf(carry - cl[m]) * prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h];
+            if (lane == 0) rdec[hh] = expf(carry);
+            for (int m = 0; m < rs; ++m) {   // x_prev rows of the staged path nodes (64 bf16 = 32 words)
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(prm.x_prev + (((size_t)b * Tp + rpath[m]) * H + h) * kP);
+                reinterpret_cast<uint32_t*>(xprev + (hh * kRStage + m) * kP)[lane] = src[lane];
+            }
+        }
+        for (int k = u; k < rs * NS; k += 128) {
+            const int m = k / NS, n = k % NS;
+            bprev[m * NS + n] = __bfloat162float(prm.b_prev[(((size_t)b * Tp + rpath[m]) * G + g) * NS + n]);
+        }
+    }
+    named_bar(3, 128);
+    // ---- per head: replay the state tile in place (swizzle-128B K-major layout of the TMA boxes) ----
+    const int pc = u & 7;   // 16-byte chunk within the 128-byte row; a warp covers 4 rows x 8 chunks
+    for (int k = 0; k < nh; ++k) {
+        const int s = k % kSt;
+        mbar_wait(bar_full(s), (k / kSt) & 1);
+        if (r > 0) {
+            const float dk = rdec[k];
+            const float* cl = rcoef + k * kMaxNodes;
+            unsigned char* tile = sm + S::H0 + s * S::H0S;
+#pragma unroll 1
+            for (int i = 0; i < 4; ++i) {
+                const int p = (u >> 3) + 16 * i;
+                const int cg = pc;               // logical chunk (swz() places it): columns 4 cg .. 4 cg + 3
+                float um[kRStage];
+#pragma unroll
+                for (int m = 0; m < kRStage; ++m)
+                    um[m] = (m < rs) ? cl[m] * __bfloat162float(xprev[(k * kRStage + m) * kP + p]) : 0.f;
+#pragma unroll
+                for (int a = 0; a < NS / 32; ++a) {
+                    float4* hp = reinterpret_cast<float4*>(tile + a * kAtom + swz(p, pc));
+                    float4 hv = *hp;
+                    hv.x *= dk; hv.y *= dk; hv.z *= dk; hv.w *= dk;
+                    const int n0 = 32 * a + 4 * cg;
+#pragma unroll
+                    for (int m = 0; m < kRStage; ++m) {
+                        if (m < rs) {
+                            const float4 bb = *reinterpret_cast<const float4*>(&bprev[m * NS + n0]);
+                            hv.x = fmaf(um[m], bb.x, hv.x); hv.y = fmaf(um[m], bb.y, hv.y);
+                            hv.z = fmaf(um[m], bb.z, hv.z); hv.w = fmaf(um[m], bb.w, hv.w);
+                        }
+                    }
+                    for (int m = kRStage; m < r; ++m) {   // long accepted paths: operands from L2
+                        const int sm_ = rpath[m];
+                        const float uu =
+                            cl[m] * __bfloat162float(prm.x_prev[(((size_t)b * Tp + sm_) * H + hbeg + k) * kP + p]);
+                        const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + n0;
+                        hv.x = fmaf(uu, __bfloat162float(br[0]), hv.x); hv.y = fmaf(uu, __bfloat162float(br[1]), hv.y);
+                        hv.z = fmaf(uu, __bfloat162float(br[2]), hv.z); hv.w = fmaf(uu, __bfloat162float(br[3]), hv.w);
+                    }
+                    *hp = hv;
+                }
+            }
+        }
+        fence_proxy_async();
+        named_bar(3, 128);
+        if (u == 0) {
+            mbar_arrive(bar_upd(s));
+            if (r > 0) {   // committed state back to HBM (in place)
+                for (int a = 0; a < NS / 32; ++a)
+                    tma_store_2d(tm_h, sb + S::H0 + s * S::H0S + a * kAtom, 32 * a, ((b * H) + hbeg + k) * kP);
+                bulk_commit();
+                bulk_wait_read0();   // the stage may be recycled only after the store has read it
+            }
+            mbar_arrive(bar_empty(s));
+        }
+    }
+    if (u == 0) bulk_wait_all();
+}
+
+template <int NS, bool kReplay>
+__global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
                    const __grid_constant__ CUtensorMap tm_y, const Params prm) {
-    using S = Smem<NS>;
+    using S = Smem<NS, kReplay>;
+    constexpr int kStages = S::kSt;
+    constexpr int kThreads = kReplay ? kThreadsReplay : kThreadsScan;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
@@ -267,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto bar_mempty = [&](int a) { return bar0 + 24 + 16 * kStages + 16 + 8 * a; };
     auto bar_accfull = [&](int a) { return bar0 + 24 + 16 * kStages + 32 + 8 * a; };
     auto bar_accempty = [&](int a) { return bar0 + 24 + 16 * kStages + 48 + 8 * a; };
+    auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kStages + 64 + 8 * s; };   // replay: stage s updated
     uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
 
     // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
@@ -276,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(BAR_G, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full(s), 1);
-            mbar_init(bar_empty(s), 2);
+            mbar_init(bar_empty(s), kReplay ? 3 : 2);   // MMA, epilogue (x), [replay store]
+            if (kReplay) mbar_init(bar_upd(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_mfull(a), 2);
@@ -313,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kHPW = kHPC / 4;            // heads per epilogue warp
     float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
     int* sbad = (int*)(sm + S::BADF);
-    if (tid >= kEpi0) {
+    if (tid >= kEpi0 && tid < kEpi0 + 128) {
         const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
         if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
 #pragma unroll
@@ -394,6 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages, a = k & 1;
                 mbar_wait(bar_full(s), (k / kStages) & 1);
+                if (kReplay) mbar_wait(bar_upd(s), (k / kStages) & 1);   // state tile replayed on chip
                 if (trace && k < 12) trace[30 + k] = gtimer();
                 mbar_wait(bar_accempty(a), ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -417,6 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_commit(bar_empty(s));
             }
         }
+    } else if (kReplay && warp >= 6) {
+        replay_updater<NS, kReplay>(prm, sm, sb, &tm_h0, b, g, chunk, hbeg, nh, bar0);
     } else {
         // ================= epilogue / math warps (128 threads) =================
         const int e = tid - kEpi0;
@@ -743,9 +914,23 @@ extern "C" int stree_tc_supports(const stree_dims* d) {
     return 1;
 }
 
-extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const float* dt, const float* A,
-                                    const void* Bm, const void* Cm, const float* D, const float* h0,
-                                    const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s) {
+namespace {
+
+template <int NS, bool R>
+cudaError_t launch_tc_inst(dim3 grid, size_t smem, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb,
+                           const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& my,
+                           const stree::tc::Params& prm) {
+    using namespace stree::tc;
+    auto k = scan_tc_kernel<NS, R>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return stree::launch_k(k, grid, dim3(R ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, prm);
+}
+
+// shared by the scan-only and the fused replay+scan launches
+int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm, const void* Cm,
+              const float* D, const float* h0, const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s,
+              bool replay, const stree::tc::Params* rp) {
     using namespace stree::tc;
     if (!stree_tc_supports(d)) return (int)cudaErrorNotSupported;
     const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
@@ -769,22 +954,47 @@ extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const fl
     int hpc = (hpg + cpg - 1) / cpg;
     if (hpc > kHPC) hpc = kHPC;
     cpg = (hpg + hpc - 1) / hpc;
-    stree::tc::Params prm{g_trace, B, T, H, G, cpg, hpc, dt, A, D, parent, (__nv_bfloat16*)y, dev_status,
-                          h0 != nullptr, (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0};
+    stree::tc::Params prm{};
+    if (rp) prm = *rp;
+    prm.trace = g_trace;
+    prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc;
+    prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
+    prm.has_h0 = h0 != nullptr;
+    prm.early_state = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
-    if (N == 128) {
-        size_t smem = Smem<128>::TOTAL + 1024;
-        e = cudaFuncSetAttribute(scan_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        e = stree::launch_k(scan_tc_kernel<128>, grid, dim3(kThreads), smem, s, mc, mb, mx, mh, my, prm);
-        if (e != cudaSuccess) return (int)e;
-    } else {
-        size_t smem = Smem<64>::TOTAL + 1024;
-        e = cudaFuncSetAttribute(scan_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        e = stree::launch_k(scan_tc_kernel<64>, grid, dim3(kThreads), smem, s, mc, mb, mx, mh, my, prm);
-        if (e != cudaSuccess) return (int)e;
-    }
+    if (N == 128)
+        e = replay ? launch_tc_inst<128, true>(grid, Smem<128, true>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm)
+                   : launch_tc_inst<128, false>(grid, Smem<128, false>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm);
+    else
+        e = replay ? launch_tc_inst<64, true>(grid, Smem<64, true>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm)
+                   : launch_tc_inst<64, false>(grid, Smem<64, false>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm);
+    if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" int stree_launch_scan_tc(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                    const void* Bm, const void* Cm, const float* D, const float* h0,
+                                    const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s) {
+    return launch_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s, false, nullptr);
+}
+
+// fused replay + scan; h is read (pre-commit state) and written (committed state) in place
+extern "C" int stree_launch_replay_scan_tc(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                           const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                                           const int32_t* path_len, const stree_dims* d, const void* x,
+                                           const float* dt, const float* A, const void* Bm, const void* Cm,
+                                           const float* D, float* h, const int32_t* parent, void* y,
+                                           int32_t* dev_status, cudaStream_t s) {
+    stree::tc::Params rp{};
+    rp.Tp = d_prev->n_nodes;
+    rp.x_prev = (const __nv_bfloat16*)x_prev;
+    rp.dt_prev = dt_prev;
+    rp.b_prev = (const __nv_bfloat16*)Bm_prev;
+    rp.parent_prev = parent_prev;
+    rp.path = path;
+    rp.path_len = path_len;
+    return launch_tc(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, s, true, &rp);
 }

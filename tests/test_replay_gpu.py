@@ -1,0 +1,130 @@
+"""GPU parity of the fused replay + scan call (stree_replay_scan, §8(f) NEXT #1):
+result == oracle.commit(previous tree, accepted path, h) followed by
+oracle.tree_scan(new tree, h0 = committed state)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import inputs, trees
+from tests.helpers import TOL_BF16, TOL_F32, assert_h_close, assert_y_close
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2505_14969_b200 import api, binding
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    binding.lib()
+    yield
+
+
+def make_pair(B, Tp, T, H, P, N, G, io, seed, prev_kind="recursive", p_match=0.9):
+    rng = np.random.default_rng(seed)
+    if prev_kind == "chain":
+        pp = np.stack([trees.chain(Tp)] * B)
+    else:
+        pp = np.stack([trees.random_recursive(Tp, 3, rng) for _ in range(B)])
+    pn = np.stack([trees.random_recursive(T, 4, rng) for _ in range(B)])
+    prev = inputs.make_problem(inputs.Dims(B, Tp, H, P, N, G, io), pp, seed=seed)
+    new = inputs.make_problem(inputs.Dims(B, T, H, P, N, G, io), pn, seed=seed + 1)
+    new.A, new.D, new.h0 = prev.A, prev.D, prev.h0   # same layer, same state
+    if prev_kind == "chain":
+        tok = np.tile(np.arange(100, 100 + Tp, dtype=np.int32), (B, 1))
+        vt = np.roll(tok, -1, axis=1)
+    else:
+        tok, vt = inputs.make_accept_inputs(pp, seed=seed + 2, p_match=p_match)
+    path, plen, _, _ = oracle.accept(tok, pp, vt)
+    return prev, new, path, plen
+
+
+def run_fused(prev, new, path, plen, use_parent=True):
+    tp = api.upload(prev)
+    tn = api.upload(new)
+    h = tp["h0"].clone()
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y = api.replay_scan(tp, torch.from_numpy(path).cuda(), torch.from_numpy(plen).cuda(), tn, h, dev_status=st,
+                        use_parent=use_parent)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy(), h.cpu().numpy(), int(st.item())
+
+
+def oracle_pair(prev, new, path, plen):
+    hk, hst = oracle.commit_problem(prev, path, plen)
+    y, yst = oracle.tree_scan(new.io_as_f32("x"), new.dt, new.A, new.io_as_f32("Bm"), new.io_as_f32("Cm"), new.D,
+                              hk, new.parent, n_groups=new.dims.n_groups)
+    return y, hk, hst, yst
+
+
+@pytest.mark.parametrize("shape", [(16, 64, 64, 80, 64, 128, 1), (1, 64, 64, 80, 64, 128, 1),
+                                   (3, 40, 24, 16, 64, 64, 1), (4, 32, 50, 24, 64, 128, 2),
+                                   (2, 13, 64, 12, 64, 128, 1)])
+def test_replay_scan_matches_oracle(shape):
+    B, Tp, T, H, P, N, G = shape
+    prev, new, path, plen = make_pair(B, Tp, T, H, P, N, G, "bf16", seed=Tp * 7 + T)
+    d = binding.stree_dims(B, T, H, P, N, G, 1)
+    assert binding.stree_scan_kernel_for(d) == 2      # the fused tcgen05 kernel serves this shape
+    y, h, st = run_fused(prev, new, path, plen)
+    yr, hr, hst, yst = oracle_pair(prev, new, path, plen)
+    assert st == 0 and not hst.any() and not yst.any()
+    assert_h_close(h, hr, TOL_F32)
+    assert_y_close(y, yr, TOL_BF16)
+
+
+def test_replay_long_paths_use_l2_path():
+    """Accepted paths longer than the 16 staged nodes (full chains)."""
+    prev, new, path, plen = make_pair(2, 64, 64, 8, 64, 128, 1, "bf16", seed=5, prev_kind="chain")
+    assert (plen == 64).all()
+    y, h, st = run_fused(prev, new, path, plen, use_parent=False)
+    yr, hr, _, _ = oracle_pair(prev, new, path, plen)
+    assert_h_close(h, hr, TOL_F32)
+    assert_y_close(y, yr, TOL_BF16)
+
+
+def test_replay_invalid_path_keeps_state():
+    prev, new, path, plen = make_pair(3, 32, 32, 8, 64, 128, 1, "bf16", seed=9)
+    path = path.copy()
+    path[1, 0] = 3            # not root-anchored
+    y, h, st = run_fused(prev, new, path, plen)
+    assert st == 3
+    hr, hst = oracle.commit_problem(prev, path, plen)
+    assert list(hst) == [0, 3, 0]
+    assert np.array_equal(h[1], prev.h0[1])
+    assert_h_close(h, hr, TOL_F32)
+    yr, _ = oracle.tree_scan(new.io_as_f32("x"), new.dt, new.A, new.io_as_f32("Bm"), new.io_as_f32("Cm"), new.D,
+                             hr, new.parent)
+    assert_y_close(y, yr, TOL_BF16)
+
+
+def test_replay_invalid_new_tree_zero_y_state_committed():
+    prev, new, path, plen = make_pair(3, 32, 32, 8, 64, 128, 1, "bf16", seed=11)
+    new.parent = new.parent.copy()
+    new.parent[2, 5] = 30
+    y, h, st = run_fused(prev, new, path, plen)
+    assert st == 2 and not y[2].any()
+    yr, hr, _, _ = oracle_pair(prev, new, path, plen)
+    assert_h_close(h, hr, TOL_F32)
+    assert_y_close(y[:2], yr[:2], TOL_BF16)
+
+
+def test_replay_fp32_falls_back_to_two_launches():
+    prev, new, path, plen = make_pair(2, 24, 24, 4, 64, 128, 1, "f32", seed=13)
+    y, h, st = run_fused(prev, new, path, plen)
+    yr, hr, _, _ = oracle_pair(prev, new, path, plen)
+    assert_h_close(h, hr, TOL_F32)
+    assert_y_close(y, yr, TOL_F32)
+
+
+def test_replay_equals_separate_commit_then_scan():
+    prev, new, path, plen = make_pair(16, 64, 64, 80, 64, 128, 1, "bf16", seed=21)
+    yf, hf, _ = run_fused(prev, new, path, plen)
+    tp, tn = api.upload(prev), api.upload(new)
+    hs = api.commit(tp, torch.from_numpy(path).cuda(), torch.from_numpy(plen).cuda())
+    tn["h0"] = hs
+    ys = api.tree_scan(tn).float().cpu().numpy()
+    assert_h_close(hf, hs.cpu().numpy(), 1e-5)
+    assert_y_close(yf, ys, 1e-2)
