@@ -341,61 +341,87 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         }
     }
     named_bar(3, 128);
-    // ---- per head: replay the state tile in place (swizzle-128B K-major layout of the TMA boxes) ----
-    const int pc = u & 7;   // 16-byte chunk within the 128-byte row; a warp covers 4 rows x 8 chunks
+    // ---- per head: replay the state tile in place (swizzle-128B K-major layout of the TMA boxes).
+    //      Thread u owns logical chunk pc (columns 4 pc .. 4 pc + 3 of every atom) of rows
+    //      (u >> 3) + 16 i: its 16 chunks stay in registers while the path is applied. ----
+    const int pc = u & 7;
+    constexpr int kAt = NS / 32;
+    int pending = -1;   // stage whose state store has been issued but not yet released
+    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
         mbar_wait(bar_full(s), (k / kSt) & 1);
+        if (trace && u == 0 && k < 12) trace[64 + 3 * k] = gtimer();
         if (r > 0) {
             const float dk = rdec[k];
             const float* cl = rcoef + k * kMaxNodes;
             unsigned char* tile = sm + S::H0 + s * S::H0S;
-#pragma unroll 1
-            for (int i = 0; i < 4; ++i) {
-                const int p = (u >> 3) + 16 * i;
-                const int cg = pc;               // logical chunk (swz() places it): columns 4 cg .. 4 cg + 3
-                float um[kRStage];
+            float4 hv[4][kAt];
 #pragma unroll
-                for (int m = 0; m < kRStage; ++m)
-                    um[m] = (m < rs) ? cl[m] * __bfloat162float(xprev[(k * kRStage + m) * kP + p]) : 0.f;
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int a = 0; a < NS / 32; ++a) {
-                    float4* hp = reinterpret_cast<float4*>(tile + a * kAtom + swz(p, pc));
-                    float4 hv = *hp;
-                    hv.x *= dk; hv.y *= dk; hv.z *= dk; hv.w *= dk;
-                    const int n0 = 32 * a + 4 * cg;
-#pragma unroll
-                    for (int m = 0; m < kRStage; ++m) {
-                        if (m < rs) {
-                            const float4 bb = *reinterpret_cast<const float4*>(&bprev[m * NS + n0]);
-                            hv.x = fmaf(um[m], bb.x, hv.x); hv.y = fmaf(um[m], bb.y, hv.y);
-                            hv.z = fmaf(um[m], bb.z, hv.z); hv.w = fmaf(um[m], bb.w, hv.w);
-                        }
-                    }
-                    for (int m = kRStage; m < r; ++m) {   // long accepted paths: operands from L2
-                        const int sm_ = rpath[m];
-                        const float uu =
-                            cl[m] * __bfloat162float(prm.x_prev[(((size_t)b * Tp + sm_) * H + hbeg + k) * kP + p]);
-                        const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + n0;
-                        hv.x = fmaf(uu, __bfloat162float(br[0]), hv.x); hv.y = fmaf(uu, __bfloat162float(br[1]), hv.y);
-                        hv.z = fmaf(uu, __bfloat162float(br[2]), hv.z); hv.w = fmaf(uu, __bfloat162float(br[3]), hv.w);
-                    }
-                    *hp = hv;
+                for (int a = 0; a < kAt; ++a) {
+                    float4 v = *reinterpret_cast<const float4*>(tile + a * kAtom + swz((u >> 3) + 16 * i, pc));
+                    hv[i][a] = make_float4(dk * v.x, dk * v.y, dk * v.z, dk * v.w);
                 }
+            for (int m = 0; m < r; ++m) {
+                const bool st_ = m < kRStage;
+                float4 bb[kAt];
+                float uu[4];
+                if (st_) {
+#pragma unroll
+                    for (int a = 0; a < kAt; ++a) bb[a] = *reinterpret_cast<const float4*>(&bprev[m * NS + 32 * a + 4 * pc]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        uu[i] = cl[m] * __bfloat162float(xprev[(k * kRStage + m) * kP + (u >> 3) + 16 * i]);
+                } else {   // long accepted paths: operands from L2
+                    const int sm_ = rpath[m];
+                    const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + 4 * pc;
+#pragma unroll
+                    for (int a = 0; a < kAt; ++a)
+                        bb[a] = make_float4(__bfloat162float(br[32 * a]), __bfloat162float(br[32 * a + 1]),
+                                            __bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
+                    const __nv_bfloat16* xr = prm.x_prev + (((size_t)b * Tp + sm_) * H + hbeg + k) * kP;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) uu[i] = cl[m] * __bfloat162float(xr[(u >> 3) + 16 * i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int a = 0; a < kAt; ++a) {
+                        hv[i][a].x = fmaf(uu[i], bb[a].x, hv[i][a].x); hv[i][a].y = fmaf(uu[i], bb[a].y, hv[i][a].y);
+                        hv[i][a].z = fmaf(uu[i], bb[a].z, hv[i][a].z); hv[i][a].w = fmaf(uu[i], bb[a].w, hv[i][a].w);
+                    }
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int a = 0; a < kAt; ++a)
+                    *reinterpret_cast<float4*>(tile + a * kAtom + swz((u >> 3) + 16 * i, pc)) = hv[i][a];
         }
         fence_proxy_async();
         named_bar(3, 128);
+        if (trace && u == 0 && k < 12) trace[65 + 3 * k] = gtimer();
         if (u == 0) {
             mbar_arrive(bar_upd(s));
             if (r > 0) {   // committed state back to HBM (in place)
                 for (int a = 0; a < NS / 32; ++a)
                     tma_store_2d(tm_h, sb + S::H0 + s * S::H0S + a * kAtom, 32 * a, ((b * H) + hbeg + k) * kP);
                 bulk_commit();
-                bulk_wait_read0();   // the stage may be recycled only after the store has read it
+                if (pending >= 0) {   // the previous head's store has read its tile: release that stage
+                    bulk_wait_read1();
+                    mbar_arrive(bar_empty(pending));
+                }
+                pending = s;
+                if (trace && k < 12) trace[66 + 3 * k] = gtimer();
+            } else {
+                mbar_arrive(bar_empty(s));
             }
-            mbar_arrive(bar_empty(s));
         }
+    }
+    if (u == 0 && pending >= 0) {
+        bulk_wait_read0();
+        mbar_arrive(bar_empty(pending));
     }
     if (u == 0) bulk_wait_all();
 }
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
-    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 64 : nullptr;
+    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
     if (trace && threadIdx.x == 0) trace[0] = gtimer();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int T = prm.T, H = prm.H;

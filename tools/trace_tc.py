@@ -24,7 +24,7 @@ layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BAS
 t = layers[-1]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
-buf = torch.zeros((1024, 64), dtype=torch.int64, device="cuda")
+buf = torch.zeros((1024, 128), dtype=torch.int64, device="cuda")
 ys = [torch.empty_like(l["x"]) for l in layers]
 for _ in range(3):
     for l, y in zip(layers, ys):
