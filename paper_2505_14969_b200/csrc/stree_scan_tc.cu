@@ -79,8 +79,9 @@ struct Smem {
     static constexpr int XPREV = RDEC + (R ? kHPC * 4 : 0);               // bf16 [kHPC][kRStage][64]
     static constexpr int BPREV = XPREV + (R ? kHPC * kRStage * kP * 2 : 0);   // float[kRStage][NS]
     static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
-    // barriers (u64): tree, ctf32, gdone, full[S], empty[S], mfull[2], mempty[2], accfull[2], accempty[2], upd[S]
-    static constexpr int NBAR = 3 + 2 * kSt + 8 + (R ? kSt : 0);
+    // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[2], accempty[2],
+    //                 upd[S], xfull[S], xempty[S]
+    static constexpr int NBAR = 3 + 2 * kSt + 8 + 3 * kSt;
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
 };
@@ -129,6 +130,26 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src,
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(m)),
                  "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+// L2 evict-first policy for data streamed exactly once (state, x, y): dirty lines are written back
+// while this kernel runs instead of being evicted by the next kernel's reads
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_ef(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
+                                               uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_ef(const CUtensorMap* m, uint32_t src, int c0, int c1, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(c0), "r"(c1), "l"(pol)
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -268,8 +289,8 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
                                                uint32_t bar0) {
     using S = Smem<NS, R>;
     constexpr int kSt = S::kSt;
-    auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };
-    auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };
+    auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };            // state tile landed
+    auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };  // state tile free
     auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kSt + 64 + 8 * s; };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int u = tid - kThreadsScan;     // 0..127
@@ -346,7 +367,6 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     //      (u >> 3) + 16 i: its 16 chunks stay in registers while the path is applied. ----
     const int pc = u & 7;
     constexpr int kAt = NS / 32;
-    int pending = -1;   // stage whose state store has been issued but not yet released
     unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
@@ -404,24 +424,16 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         if (trace && u == 0 && k < 12) trace[65 + 3 * k] = gtimer();
         if (u == 0) {
             mbar_arrive(bar_upd(s));
-            if (r > 0) {   // committed state back to HBM (in place)
+            if (r > 0) {   // committed state back to HBM (in place); the tile is free once the store read it
+                const uint64_t pol = policy_evict_first();
                 for (int a = 0; a < NS / 32; ++a)
-                    tma_store_2d(tm_h, sb + S::H0 + s * S::H0S + a * kAtom, 32 * a, ((b * H) + hbeg + k) * kP);
+                    tma_store_2d_ef(tm_h, sb + S::H0 + s * S::H0S + a * kAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
                 bulk_commit();
-                if (pending >= 0) {   // the previous head's store has read its tile: release that stage
-                    bulk_wait_read1();
-                    mbar_arrive(bar_empty(pending));
-                }
-                pending = s;
+                bulk_wait_read0();
                 if (trace && k < 12) trace[66 + 3 * k] = gtimer();
-            } else {
-                mbar_arrive(bar_empty(s));
             }
+            mbar_arrive(bar_empty(s));
         }
-    }
-    if (u == 0 && pending >= 0) {
-        bulk_wait_read0();
-        mbar_arrive(bar_empty(pending));
     }
     if (u == 0) bulk_wait_all();
 }
@@ -460,6 +472,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     auto bar_accfull = [&](int a) { return bar0 + 24 + 16 * kStages + 32 + 8 * a; };
     auto bar_accempty = [&](int a) { return bar0 + 24 + 16 * kStages + 48 + 8 * a; };
     auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kStages + 64 + 8 * s; };   // replay: stage s updated
+    auto bar_xfull = [&](int s) { return bar0 + 24 + 24 * kStages + 64 + 8 * s; };  // x tile landed
+    auto bar_xempty = [&](int s) { return bar0 + 24 + 32 * kStages + 64 + 8 * s; }; // x tile free
     uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
 
     // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
@@ -469,8 +483,10 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         mbar_init(BAR_G, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full(s), 1);
-            mbar_init(bar_empty(s), kReplay ? 3 : 2);   // MMA, epilogue (x), [replay store]
-            if (kReplay) mbar_init(bar_upd(s), 1);
+            mbar_init(bar_empty(s), kReplay ? 2 : 1);   // state tile: MMA (Y0) [+ replay store read]
+            mbar_init(bar_upd(s), 1);
+            mbar_init(bar_xfull(s), 1);
+            mbar_init(bar_xempty(s), 2);                  // x tile: MMA (Y') + epilogue (D x)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_mfull(a), 2);
@@ -488,7 +504,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const int n_early = (prm.early_state && prm.has_h0) ? min(nh, kStages) : 0;
+    const int n_early = (prm.early_state && prm.has_h0) ? 1 : 0;
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
         // the state of the first heads is streamed before the dependency wait (caller's promise)
@@ -544,6 +560,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     if (warp == 0) {
         // ================= TMA producer =================
         if (lane == 0) {
+            const uint64_t pol_ef = policy_evict_first();
             mbar_expect_tx(BAR_TREE, 2 * S::kCbAtoms * xbytes);
             for (int a = 0; a < S::kCbAtoms; ++a) {
                 tma_load_2d(sb + S::CB + a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
@@ -555,17 +572,22 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
                 const int h = hbeg + k;
-                if (k < n_early) {   // state already in flight: add x and arrive
-                    mbar_expect_tx(bar_full(s), xbytes);
+                if (k < n_early) {   // state already in flight: arrive
+                    mbar_expect_tx(bar_full(s), 0);
                 } else {
                     mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
-                    mbar_expect_tx(bar_full(s), (prm.has_h0 ? S::H0S : 0) + xbytes);
+                    mbar_expect_tx(bar_full(s), prm.has_h0 ? S::H0S : 0);
                     if (prm.has_h0)
                         for (int a = 0; a < NS / 32; ++a)
-                            tma_load_2d(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
-                                        ((b * H) + h) * kP);
+                            tma_load_2d_ef(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
+                                           ((b * H) + h) * kP, pol_ef);
                 }
-                tma_load_2d(sb + S::X + s * S::XS, &tm_x, bar_full(s), h * kP, b * T);
+                mbar_wait(bar_xempty(s), ((k / kStages) & 1) ^ 1);
+                mbar_expect_tx(bar_xfull(s), xbytes);
+                tma_load_2d_ef(sb + S::X + s * S::XS, &tm_x, bar_xfull(s), h * kP, b * T, pol_ef);
+                // ramp: the rest of the ring is requested only once head 0 has landed, so every CTA's
+                // first tile is near the front of the DRAM queue instead of behind other CTAs' later stages
+                if (k == 0) mbar_wait(bar_full(0), 0);
             }
         }
     } else if (warp == 1) {
@@ -601,6 +623,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                                     kk > 0);
                     }
                 }
+                tc_commit(bar_empty(s));                  // state tile no longer needed by the tensor core
+                mbar_wait(bar_xfull(s), (k / kStages) & 1);
                 mbar_wait(bar_mfull(a), (k >> 1) & 1);
                 tc_fence_after();
                 // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j)
@@ -609,7 +633,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             sdesc(sb + S::X + s * S::XS + kk * 2048, kAtom, 1024), id_y, kk > 0);
                 tc_commit(bar_accfull(a));
                 tc_commit(bar_mempty(a));
-                tc_commit(bar_empty(s));
+                tc_commit(bar_xempty(s));
             }
         }
     } else if (kReplay && warp >= 6) {
@@ -858,9 +882,9 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 if (lane == 0) mbar_arrive(bar_accempty(a));
                 named_bar(2, 64);
                 if (leader) {
-                    tma_store_2d(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T);
+                    tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
                     bulk_commit();
-                    mbar_arrive(bar_empty(s));
+                    mbar_arrive(bar_xempty(s));
                     if (trace && k < 12) trace[5 + 2 * k] = gtimer();
                 }
             }

@@ -1,0 +1,66 @@
+"""Summarise the ncu outputs of tools/profile_round.sh (run where ncu -i works)."""
+import csv
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[hi]
+    per = defaultdict(lambda: defaultdict(list))
+    for r in rows[hi + 1:]:
+        d = dict(zip(hdr, r))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        per[name][d["Metric Name"]].append(float(d["Metric Value"].replace(",", "")))
+    return per
+
+
+print("== launch list (ncu, cold-cache, serialised): per-kernel mean over launches ==")
+per = launches(os.path.join(out, "launches.csv"))
+tot = sum(sum(m["gpu__time_duration.sum"]) for m in per.values())
+traffic = {}
+for k, m in sorted(per.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
+    t = m["gpu__time_duration.sum"]
+    rd = sum(m["dram__bytes_read.sum"]) / len(t)
+    wr = sum(m["dram__bytes_write.sum"]) / len(t)
+    print(f"{k[:60]:60s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  share={sum(t) / tot * 100:5.1f}%  "
+          f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB")
+    traffic[k] = rd + wr
+
+
+def details(rep, names):
+    try:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    except Exception as e:  # noqa: BLE001
+        return str(e)
+    rows = list(csv.reader(txt.splitlines()))
+    if not rows:
+        return "(no data)"
+    hdr = rows[0]
+    res = []
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") in names:
+            res.append(f"  {d.get('ID', '')} {d['Metric Name']:45s} {d['Metric Value']} {d.get('Metric Unit', '')}")
+    return "\n".join(res)
+
+
+names = {"Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Registers Per Thread",
+         "Dynamic Shared Memory Per Block", "Grid Size", "Block Size", "L2 Hit Rate", "Achieved Active Warps Per SM",
+         "Issued Warp Per Scheduler", "No Eligible"}
+for rep in ("prof_fused", "prof_commit"):
+    p = os.path.join(out, rep + ".ncu-rep")
+    if os.path.exists(p):
+        print(f"== ncu --set full: {rep} ==")
+        print(details(p, names))
+        raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv", "--metrics",
+                              "dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tc.sum"],
+                             capture_output=True, text=True).stdout
+        print(raw[-2000:])
+json.dump({"c4": traffic}, open(os.path.join(out, "traffic.json"), "w"), indent=1)

@@ -18,6 +18,7 @@ ap.add_argument("--config", default="c4")
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--scan-impl", default="auto")
+ap.add_argument("--fused", action="store_true")
 args = ap.parse_args()
 binding.stree_set_scan_impl({"auto": 0, "simt": 1, "tc": 2}[args.scan_impl])
 prob = inputs.config_problem(args.config)
@@ -25,11 +26,16 @@ layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BAS
           for li in range(args.layers)]
 tok, vt = inputs.make_accept_inputs(prob.parent, seed=5, p_match=0.9)
 tok, vt = torch.from_numpy(tok).cuda(), torch.from_numpy(vt).cuda()
+path, plen, bonus = api.accept(tok, layers[0]["parent"], vt)
 for it in range(args.iters):
     mask, depth = api.build_mask(layers[0]["parent"])
-    ys = [api.tree_scan(t) for t in layers]
+    if args.fused:   # replay of the previous acceptance fused with the scan (state in place)
+        ys = [api.replay_scan(t, path, plen, t, t["h0"]) for t in layers]
+    else:
+        ys = [api.tree_scan(t) for t in layers]
     path, plen, bonus = api.accept(tok, layers[0]["parent"], vt)
-    for t in layers:
-        api.commit(t, path, plen, h_new=t["h0"])
+    if not args.fused:
+        for t in layers:
+            api.commit(t, path, plen, h_new=t["h0"])
 torch.cuda.synchronize()
 print("ok")

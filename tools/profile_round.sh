@@ -1,0 +1,17 @@
+#!/bin/bash
+# Run under gpurun: ncu evidence for the bench's kernels.
+#   1. launch list (per-launch device time, cold-cache/serialised) of the bench command itself
+#   2. one --set full capture of the dominant kernel (fused replay+scan) and of the scan / commit kernels
+#   3. summaries -> gpurun_out/profile_summary.txt, gpurun_out/traffic.json
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 \
+    --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --layers 8 --no-e2e --no-cpu-baseline \
+    > $OUT/ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:scan_tc_kernel -s 12 -c 2 \
+    -o $OUT/prof_fused python tools/prof_kernels.py --fused > $OUT/ncu_fused.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:commit_ring -s 4 -c 1 \
+    -o $OUT/prof_commit python tools/prof_kernels.py > $OUT/ncu_commit.log 2>&1
+python tools/ncu_summary.py $OUT > $OUT/profile_summary.txt 2>&1
+cat $OUT/profile_summary.txt
