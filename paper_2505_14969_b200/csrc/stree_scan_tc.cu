@@ -38,7 +38,7 @@ constexpr int kP = 64;          // head dim
 constexpr int kHPC = 12;        // max heads per CTA
 constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
 constexpr int kThreadsReplay = 320;   // + warps 6-9 replay updaters
-constexpr int kRStage = 16;           // previous-path nodes staged on chip by the replay
+constexpr int kRStage = 8;            // previous-path nodes staged on chip by the replay
 constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
 constexpr uint32_t kTmemCols = 512;
@@ -47,19 +47,20 @@ constexpr int kAccCol0 = 256;   // acc a: Y0 at 256 + 128a, Y' at 256 + 128a + 6
 
 template <int NS, bool R>
 struct Smem {
-    static constexpr int kSt = R ? 3 : 4;                 // h0/x ring depth
+    static constexpr int kSt = R ? 3 : 4;                 // state (h0) ring depth
+    static constexpr int kStX = R ? 3 : 4;                // x ring depth
     static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
     static constexpr int U = 0;                           // union: {C bf16, B bf16} then {M'[2], ystage[2]}
-    static constexpr int CB = U;
-    static constexpr int BB = U + kCbAtoms * kAtom;
+    static constexpr int CB = U;                          // C bf16: atom a at CB + 2a*kAtom, copy at +kAtom
+    static constexpr int BB = U + 2 * kCbAtoms * kAtom;
     static constexpr int MB = U;                          // M'[a] at MB + a*kAtom
     static constexpr int YS = U + 2 * kAtom;              // ystage[a] at YS + a*kAtom
-    static constexpr int UBYTES = (2 * kCbAtoms * kAtom > 4 * kAtom) ? 2 * kCbAtoms * kAtom : 4 * kAtom;
+    static constexpr int UBYTES = (3 * kCbAtoms * kAtom > 4 * kAtom) ? 3 * kCbAtoms * kAtom : 4 * kAtom;
     static constexpr int H0 = U + UBYTES;                 // h0 stages
     static constexpr int H0S = kP * NS * 4;               // bytes per stage
     static constexpr int X = H0 + kSt * H0S;              // x stages
     static constexpr int XS = kAtom;
-    static constexpr int MISC = X + kSt * XS;
+    static constexpr int MISC = X + kStX * XS;
     // misc (4-byte words unless noted)
     static constexpr int PAR = MISC;                      // int[64]
     static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
@@ -74,16 +75,18 @@ struct Smem {
     // replay (fused commit of the previous tree)
     static constexpr int RPATH = BADF + 16;               // int[kMaxNodes]   previous accepted path
     static constexpr int RINFO = RPATH + (R ? kMaxNodes * 4 : 0);   // int[4]: r (0 = invalid / nothing)
-    static constexpr int RCOEF = RINFO + 16;              // float[kHPC][kMaxNodes] c_{h,m}
-    static constexpr int RDEC = RCOEF + (R ? kHPC * kMaxNodes * 4 : 0);   // float[kHPC] decay
+    static constexpr int RCOEF = RINFO + 16;              // float[kHPC][kRStage] c_{h,m} of the staged nodes
+    static constexpr int RLAM = RCOEF + (R ? kHPC * kRStage * 4 : 0);     // float[kHPC][2]: lam_{r-1}, lam_{kRStage-1}
+    static constexpr int RDEC = RLAM + (R ? kHPC * 8 : 0);                // float[kHPC] decay
     static constexpr int XPREV = RDEC + (R ? kHPC * 4 : 0);               // bf16 [kHPC][kRStage][64]
     static constexpr int BPREV = XPREV + (R ? kHPC * kRStage * kP * 2 : 0);   // float[kRStage][NS]
     static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
     // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[2], accempty[2],
-    //                 upd[S], xfull[S], xempty[S]
+    //                 upd[S], xfull[S], xempty[S]   (xfull/xempty use the first kStX)
     static constexpr int NBAR = 3 + 2 * kSt + 8 + 3 * kSt;
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
+    static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
 };
 
 // ---------------------------------------------------------------------------
@@ -299,6 +302,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     int* rpath = (int*)(sm + S::RPATH);
     int* rinfo = (int*)(sm + S::RINFO);
     float* rcoef = (float*)(sm + S::RCOEF);
+    float* rlam = (float*)(sm + S::RLAM);
     float* rdec = (float*)(sm + S::RDEC);
     __nv_bfloat16* xprev = (__nv_bfloat16*)(sm + S::XPREV);
     float* bprev = (float*)(sm + S::BPREV);
@@ -333,24 +337,31 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         for (int hh = uw; hh < nh; hh += 4) {   // one warp per head
             const int h = hbeg + hh;
             const float Ah = prm.A[h];
-            float* cl = rcoef + hh * kMaxNodes;
-            float carry = 0.f;
+            float* cl = rcoef + hh * kRStage;
+            float carry = 0.f, lam_st = 0.f, d_st = 0.f, a_st = 0.f;
             for (int m0 = 0; m0 < r; m0 += 32) {
                 const int m = m0 + lane;
-                float a = (m < r) ? prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h] * Ah : 0.f;
+                const float d = (m < r) ? prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h] : 0.f;
+                float a = d * Ah;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float t = __shfl_up_sync(0xffffffffu, a, o);
                     if (lane >= o) a += t;
                 }
                 a += carry;
-                if (m < r) cl[m] = a;
+                if (m0 == 0) { a_st = a; d_st = d; }
+                if (m == kRStage - 1) lam_st = a;
                 carry = __shfl_sync(0xffffffffu, a, 31);
             }
-            __syncwarp();
-            for (int m = lane; m < r; m += 32)
-                cl[m] = expf(carry - cl[m]) * prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h];
-            if (lane == 0) rdec[hh] = expf(carry);
+            // r <= 32 keeps lam_{r-1} in lane r-1 of the first chunk; longer paths carry it
+            const float last = (r <= 32) ? __shfl_sync(0xffffffffu, a_st, r - 1) : carry;
+            const float lst = __shfl_sync(0xffffffffu, lam_st, kRStage - 1);
+            if (lane < kRStage && lane < r) cl[lane] = expf(last - a_st) * d_st;
+            if (lane == 0) {
+                rdec[hh] = expf(last);
+                rlam[2 * hh] = last;
+                rlam[2 * hh + 1] = lst;
+            }
             for (int m = 0; m < rs; ++m) {   // x_prev rows of the staged path nodes (64 bf16 = 32 words)
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(prm.x_prev + (((size_t)b * Tp + rpath[m]) * H + h) * kP);
                 reinterpret_cast<uint32_t*>(xprev + (hh * kRStage + m) * kP)[lane] = src[lane];
@@ -374,7 +385,9 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         if (trace && u == 0 && k < 12) trace[64 + 3 * k] = gtimer();
         if (r > 0) {
             const float dk = rdec[k];
-            const float* cl = rcoef + k * kMaxNodes;
+            const float* cl = rcoef + k * kRStage;
+            const float Ak = prm.A[hbeg + k], last = rlam[2 * k];
+            float lam_run = rlam[2 * k + 1];   // long paths: lam_m accumulated from the last staged node
             unsigned char* tile = sm + S::H0 + s * S::H0S;
             float4 hv[4][kAt];
 #pragma unroll
@@ -394,8 +407,11 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         uu[i] = cl[m] * __bfloat162float(xprev[(k * kRStage + m) * kP + (u >> 3) + 16 * i]);
-                } else {   // long accepted paths: operands from L2
+                } else {   // long accepted paths: operands and coefficients from L2 / on the fly
                     const int sm_ = rpath[m];
+                    const float dm = prm.dt_prev[((size_t)b * Tp + sm_) * H + hbeg + k];
+                    lam_run += dm * Ak;
+                    const float cm = expf(last - lam_run) * dm;
                     const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + 4 * pc;
 #pragma unroll
                     for (int a = 0; a < kAt; ++a)
@@ -403,7 +419,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
                                             __bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
                     const __nv_bfloat16* xr = prm.x_prev + (((size_t)b * Tp + sm_) * H + hbeg + k) * kP;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) uu[i] = cl[m] * __bfloat162float(xr[(u >> 3) + 16 * i]);
+                    for (int i = 0; i < 4; ++i) uu[i] = cm * __bfloat162float(xr[(u >> 3) + 16 * i]);
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -561,9 +577,10 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         // ================= TMA producer =================
         if (lane == 0) {
             const uint64_t pol_ef = policy_evict_first();
-            mbar_expect_tx(BAR_TREE, 2 * S::kCbAtoms * xbytes);
+            mbar_expect_tx(BAR_TREE, 3 * S::kCbAtoms * xbytes);
             for (int a = 0; a < S::kCbAtoms; ++a) {
-                tma_load_2d(sb + S::CB + a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
+                tma_load_2d(sb + S::CB + 2 * a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
+                tma_load_2d(sb + S::CB + (2 * a + 1) * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
                 tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
             }
             // the bulk state stream starts once the tree operands have landed: issued together, the
@@ -582,9 +599,10 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             tma_load_2d_ef(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
                                            ((b * H) + h) * kP, pol_ef);
                 }
-                mbar_wait(bar_xempty(s), ((k / kStages) & 1) ^ 1);
-                mbar_expect_tx(bar_xfull(s), xbytes);
-                tma_load_2d_ef(sb + S::X + s * S::XS, &tm_x, bar_xfull(s), h * kP, b * T, pol_ef);
+                const int sx = k % S::kStX;
+                mbar_wait(bar_xempty(sx), ((k / S::kStX) & 1) ^ 1);
+                mbar_expect_tx(bar_xfull(sx), xbytes);
+                tma_load_2d_ef(sb + S::X + sx * S::XS, &tm_x, bar_xfull(sx), h * kP, b * T, pol_ef);
                 // ramp: the rest of the ring is requested only once head 0 has landed, so every CTA's
                 // first tile is near the front of the DRAM queue instead of behind other CTAs' later stages
                 if (k == 0) mbar_wait(bar_full(0), 0);
@@ -597,10 +615,12 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             tc_fence_after();
             // G = C·Bᵀ (once per tree), kind::f16 bf16, M=128, N=Tp16, K=NS
             const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
+            // rows 64..127 of A are a copy of C, so G lands in TMEM lanes 0..63 and again in 64..127
+#pragma unroll 1
             for (int kk = 0; kk < NS / 16; ++kk) {
-                uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-                mma_f16(tmem + 0, sdesc(sb + S::CB + off, 16, 1024), sdesc(sb + S::BB + off, 16, 1024), id_g,
-                        kk > 0);
+                const uint32_t off = (kk & 3) * 32;
+                mma_f16(tmem + 0, sdesc(sb + S::CB + (kk >> 2) * 2 * kAtom + off, 16, 1024),
+                        sdesc(sb + S::BB + (kk >> 2) * kAtom + off, 16, 1024), id_g, kk > 0);
             }
             tc_commit(BAR_G);
             mbar_wait(BAR_CTF, 0);
@@ -614,9 +634,11 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 if (trace && k < 12) trace[30 + k] = gtimer();
                 mbar_wait(bar_accempty(a), ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
+                if (trace && k < 9) trace[118 + k] = gtimer();
                 const uint32_t d0 = tmem + kAccCol0 + 128 * a;
                 if (prm.has_h0) {
                     // Y0 = C·h0_hᵀ, kind::tf32, A = C from TMEM, K = NS in steps of 8 (32 B / 8 columns)
+#pragma unroll 1
                     for (int kk = 0; kk < NS / 8; ++kk) {
                         uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
                         mma_tf32_ts(d0, tmem + kCCol + 8 * kk, sdesc(sb + S::H0 + s * S::H0S + off, 16, 1024), id_y0,
@@ -624,16 +646,20 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     }
                 }
                 tc_commit(bar_empty(s));                  // state tile no longer needed by the tensor core
-                mbar_wait(bar_xfull(s), (k / kStages) & 1);
+                if (trace && k < 9) trace[100 + k] = gtimer();
+                const int sx = k % S::kStX;
+                mbar_wait(bar_xfull(sx), (k / S::kStX) & 1);
                 mbar_wait(bar_mfull(a), (k >> 1) & 1);
+                if (trace && k < 9) trace[109 + k] = gtimer();
                 tc_fence_after();
                 // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j)
+#pragma unroll 1
                 for (int kk = 0; kk < Tp16 / 16; ++kk)
                     mma_f16(d0 + 64, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
-                            sdesc(sb + S::X + s * S::XS + kk * 2048, kAtom, 1024), id_y, kk > 0);
+                            sdesc(sb + S::X + sx * S::XS + kk * 2048, kAtom, 1024), id_y, kk > 0);
                 tc_commit(bar_accfull(a));
                 tc_commit(bar_mempty(a));
-                tc_commit(bar_xempty(s));
+                tc_commit(bar_xempty(sx));
             }
         }
     } else if (kReplay && warp >= 6) {
@@ -663,7 +689,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 for (int cc = 0; cc < 4; ++cc) {
                     const int c = 4 * c32 + cc, a = c >> 3;   // 16-byte bf16 chunk index along the row
                     uint4 v = make_uint4(0, 0, 0, 0);
-                    if (i < T) v = *reinterpret_cast<const uint4*>(sm + S::CB + a * kAtom + swz(i, c & 7));
+                    if (i < T) v = *reinterpret_cast<const uint4*>(sm + S::CB + 2 * a * kAtom + swz(i, c & 7));
                     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -676,7 +702,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             tmem_st_wait();
             tc_fence_before();
         } else {
-            for (int k = e; k < kStages * (Tp16 - T) * 8; k += 64) {
+            for (int k = e; k < S::kStX * (Tp16 - T) * 8; k += 64) {
                 const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
                 *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
             }
@@ -702,6 +728,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
 #pragma unroll
             for (int q = 0; q < kHPW; ++q) lm[q][hf] = dtr[q][hf] * a_h[q];
         }
+#pragma unroll 1
         for (int r = 0; r < rounds; ++r) {
             uint64_t nrw[2];
             int njp[2];
@@ -763,66 +790,56 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         }
         named_bar(1, 128);
         if (trace && e == 0) trace[50] = gtimer();
-        // ---- G rows: TMEM (lanes 0..T-1, quadrants 0/1) -> smem (rotated, conflict-free) -> the
-        //      builder warps 2,3, which then build the masked weights while warps 4,5 run the
-        //      TMEM epilogue of the previous head ----
+        // ---- builder warps 2,3 (TMEM lanes 64..127 hold a copy of G) build the masked weights of head
+        //      k+1 while warps 4,5 (TMEM lanes 0..63) run the epilogue of head k ----
         mbar_wait(BAR_G, 0);
         tc_fence_after();
         if (trace && e == 0) trace[51] = gtimer();
-        float* gs = (float*)(sm + S::YS);      // 64 x 64 fp32; the y staging area is idle until head 0's output
-        if (quad < 2) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float g16[16];
-                tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + 16 * c, g16);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) gs[row * 64 + ((16 * c + q + row) & 63)] = g16[q];
-            }
-        }
-        named_bar(1, 128);
         const bool builder = (warp == 2 || warp == 3);
         if (trace && e == 0) trace[3] = gtimer();
         if (builder) {
             const int brow = (warp - 2) * 32 + lane;
             const bool bown = brow < T;
-            float gr[64];
-#pragma unroll
-            for (int j = 0; j < 64; ++j) gr[j] = gs[brow * 64 + ((j + brow) & 63)];
             const uint64_t mybits = bown ? rows[brow] : 0ull;
-            named_bar(1, 128);   // G staging consumed before the y staging area is reused
+            const uint32_t gl = tmem + ((uint32_t)(quad * 32) << 16);   // G row brow, columns 0..63
+#pragma unroll 1
             for (int k = 0; k < nh; ++k) {
                 // masked weights of head k into M'[k & 1]:  M'_ij = L_ij G_ij c_j  (factorised)
                 //                                        or  L_ij e^{Λi-Λj} dt_j G_ij (direct)
                 const int a = k & 1;
                 mbar_wait(bar_mempty(a), ((k >> 1) & 1) ^ 1);
-                if (bown) {
-                    const float* c = cj + k * 64;
-                    const bool f = mode[k] != 0;
-                    const float li = lam[k * 64 + brow];
-                    unsigned char* mrow = sm + S::MB + a * kAtom;
+                const float* c = cj + k * 64;
+                const float* lk = lam + k * 64;
+                const bool f = mode[k] != 0;
+                const float li = bown ? lk[brow] : 0.f;
+                unsigned char* mrow = sm + S::MB + a * kAtom;
+#pragma unroll 1
+                for (int c16 = 0; c16 < Tp16 / 16; ++c16) {
+                    float g16[16];
+                    tmem_ld16(gl + 16 * c16, g16);
+                    uint32_t o[8];
 #pragma unroll
-                    for (int ch = 0; ch < 8; ++ch) {
-                        float w[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const int j = 8 * ch + q;
-                            float v;
-                            if (f) v = c[j] * gr[j];
-                            else v = __expf(fminf(li - lam[k * 64 + j], 0.f)) * c[j] * gr[j];
-                            w[q] = ((mybits >> j) & 1ull) ? v : 0.f;
+                    for (int q = 0; q < 16; q += 2) {
+                        const int j = 16 * c16 + q;
+                        float v0 = c[j] * g16[q], v1 = c[j + 1] * g16[q + 1];
+                        if (!f) {
+                            v0 *= __expf(fminf(li - lk[j], 0.f));
+                            v1 *= __expf(fminf(li - lk[j + 1], 0.f));
                         }
-                        *reinterpret_cast<uint4*>(mrow + swz(brow, ch)) =
-                            make_uint4(pack_bf16(w[0], w[1]), pack_bf16(w[2], w[3]), pack_bf16(w[4], w[5]),
-                                       pack_bf16(w[6], w[7]));
+                        o[q >> 1] = pack_bf16(((mybits >> j) & 1ull) ? v0 : 0.f, ((mybits >> (j + 1)) & 1ull) ? v1 : 0.f);
+                    }
+                    if (bown) {
+                        *reinterpret_cast<uint4*>(mrow + swz(brow, 2 * c16)) = make_uint4(o[0], o[1], o[2], o[3]);
+                        *reinterpret_cast<uint4*>(mrow + swz(brow, 2 * c16 + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
                     }
                 }
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_mfull(a));
+                if (trace && warp == 2 && lane == 0 && k < 9) trace[91 + k] = gtimer();
             }
         } else {
             // ---- TMEM epilogue (warps 4,5 = TMEM lanes 0..63 = tree nodes) ----
-            named_bar(1, 128);
             const bool own = row < T;
             const bool leader = (warp == 4 && lane == 0);
             for (int k = 0; k < nh; ++k) {
@@ -838,7 +855,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[k];
                 const float s0 = (own && !zero_out) ? e0[k * 64 + row] : 0.f;
                 const float s1 = (own && !zero_out) ? ei[k * 64 + row] : 0.f;
-                const unsigned char* xr = sm + S::X + s * S::XS;
+                const int sx = k % S::kStX;
+                const unsigned char* xr = sm + S::X + sx * S::XS;
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + kAccCol0 + 128 * a;
                 uint32_t v0[2][32], v1[2][32];
@@ -884,7 +902,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 if (leader) {
                     tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
                     bulk_commit();
-                    mbar_arrive(bar_xempty(s));
+                    mbar_arrive(bar_xempty(sx));
                     if (trace && k < 12) trace[5 + 2 * k] = gtimer();
                 }
             }

@@ -9,7 +9,7 @@ mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 \
     --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --layers 8 --no-e2e --no-cpu-baseline \
     > $OUT/ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:scan_tc_kernel -s 12 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:scan_tc_kernel -s 4 -c 2 \
     -o $OUT/prof_fused python tools/prof_kernels.py --fused > $OUT/ncu_fused.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:commit_ring -s 4 -c 1 \
     -o $OUT/prof_commit python tools/prof_kernels.py > $OUT/ncu_commit.log 2>&1

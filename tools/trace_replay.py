@@ -15,6 +15,8 @@ prob = inputs.config_problem("c4")
 layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BASE_SEED + 50 + i)) for i in range(8)]
 tok, vt = inputs.make_accept_inputs(prob.parent, seed=5, p_match=0.9)
 path, plen, _ = api.accept(torch.from_numpy(tok).cuda(), layers[0]["parent"], torch.from_numpy(vt).cuda())
+if os.environ.get("NOREPLAY"):   # path_len = 0: replay disabled (state unchanged, no state store)
+    plen.zero_()
 ys = [torch.empty_like(l["x"]) for l in layers]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
@@ -39,6 +41,13 @@ torch.cuda.synchronize()
 print(f"eager back-to-back over 8 layers: {e0.elapsed_time(e1) / 40 * 1e3:.2f} us per replay_scan")
 for l, y in zip(layers[:-1], ys):
     run(l, y)
+if os.environ.get("ISOLATED"):   # flush L2 and drain before the traced launch
+    junk = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    if os.environ.get("ISOLATED") == "clean":   # read-only sweep: L2 ends up clean
+        for _ in range(3):
+            float(junk.sum())
+    torch.cuda.synchronize()
 L.stree_debug_tc_trace(ctypes.c_void_p(buf.data_ptr()))
 run(layers[-1], ys[-1])
 torch.cuda.synchronize()
@@ -48,7 +57,7 @@ n = int((tr[:, 0] > 0).sum())
 tr = tr[:n]
 t0 = tr[:, 0].min()
 rel = np.where(tr > 0, tr - t0, -1) / 1000.0
-names = {0: "start", 3: "G ready", 50: "coefs done", 51: "BAR_G"}
+names = {0: "start", 1: "epi start", 2: "C landed", 3: "G ready", 46: "ctf32", 50: "coefs done", 51: "BAR_G"}
 for k in range(9):
     names[4 + 2 * k] = f"acc{k}"
     names[5 + 2 * k] = f"out{k}"
@@ -56,6 +65,11 @@ for k in range(9):
     names[64 + 3 * k] = f"upd_full{k}"
     names[65 + 3 * k] = f"upd_done{k}"
     names[66 + 3 * k] = f"upd_store{k}"
+for k in range(9):
+    names[100 + k] = f"mma_y0issued{k}"
+    names[109 + k] = f"mma_x+m_ready{k}"
+    names[118 + k] = f"mma_accempty{k}"
+    names[91 + k] = f"built_m{k}"
 for c in sorted(names):
     v = rel[:, c]
     v = v[v >= 0]
