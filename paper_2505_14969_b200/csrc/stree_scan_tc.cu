@@ -6,13 +6,14 @@
 //     G   = C·Bᵀ                 (T x T, K = N)    kind::f16   bf16 x bf16 -> fp32 TMEM   (once per tree)
 //     Y0  = C·h0_hᵀ              (T x P, K = N)    kind::tf32  fp32 state  -> fp32 TMEM   (per head; dominant stream)
 //     Y'  = (L∘G∘c_h)·X_h        (T x P, K = T)    kind::f16   bf16 masked weights x bf16 x   (per head)
-// and an epilogue y = e^{Λ_i} Y0 + e'_i Y' + D x (fp32) -> bf16 -> TMA store.
+// and an epilogue y = e^{Λ_i} (Y0 + Y') + D x (fp32) -> bf16 -> TMA store.
 // Λ = L·(dt A_h) is the tree segsum (Eq. a_tree) built by pointer
 // jumping over the ancestor chains; the decay mask is applied before any exp
-// (SURVEY R4).  The decay factorises, e^{Λ_i-Λ_j} = e^{Λ_i-ref}·e^{ref-Λ_j},
-// whenever min Λ >= -120 (ref = min Λ / 2 keeps both factors inside e^{±60});
-// the masked weights then need no per-element exp.  Heads with deeper decay use
-// the direct per-element e^{Λ_i-Λ_j}.
+// (SURVEY R4).  The decay factorises, e^{Λ_i-Λ_j} = e^{Λ_i}·e^{-Λ_j}, whenever
+// min Λ >= -64 (both factors inside fp32 range with e^{64} of headroom): then
+// c_j = e^{-Λ_j} dt_j, Y' accumulates onto Y0 in the same TMEM columns and the
+// epilogue applies the single row factor e^{Λ_i}.  Heads with deeper decay use
+// the direct per-element e^{Λ_i-Λ_j} with Y' in separate TMEM columns.
 //
 // One CTA = one tree and a range of heads of one group (grid = B x G x chunks),
 // 192 threads, warp-specialised:
@@ -35,7 +36,7 @@ namespace tc {
 
 constexpr int kT = 64;          // max nodes per tree served
 constexpr int kP = 64;          // head dim
-constexpr int kHPC = 12;        // max heads per CTA
+constexpr int kHPC = 10;        // max heads per CTA
 constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
 constexpr int kThreadsReplay = 320;   // + warps 6-9 replay updaters
 constexpr int kRStage = 8;            // previous-path nodes staged on chip by the replay
@@ -43,11 +44,13 @@ constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
 constexpr uint32_t kTmemCols = 512;
 constexpr int kCCol = 64;       // C as tf32 (A operand of Y0) in TMEM columns [64, 64 + N)
-constexpr int kAccCol0 = 256;   // acc a: Y0 at 256 + 128a, Y' at 256 + 128a + 64
+constexpr int kAccCol0 = 192;   // accumulator a (of kAcc): columns [192 + 64a, 256 + 64a)
+constexpr int kAcc = 4;
+constexpr int kDirCol = 448;    // Y' of direct-decay heads (rare): columns [448, 512)
 
 template <int NS, bool R>
 struct Smem {
-    static constexpr int kSt = R ? 3 : 4;                 // state (h0) ring depth
+    static constexpr int kSt = 4;                         // state (h0) ring depth: 2 pairs of head slots
     static constexpr int kStX = R ? 3 : 4;                // x ring depth
     static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
     static constexpr int U = 0;                           // union: {C bf16, B bf16} then {M'[2], ystage[2]}
@@ -58,6 +61,10 @@ struct Smem {
     static constexpr int UBYTES = (3 * kCbAtoms * kAtom > 4 * kAtom) ? 3 * kCbAtoms * kAtom : 4 * kAtom;
     static constexpr int H0 = U + UBYTES;                 // h0 stages
     static constexpr int H0S = kP * NS * 4;               // bytes per stage
+    // the two head slots of a pair interleave by atom, so the pair is one 128-row K-major operand
+    // (Y0 of both heads in one N = 128 MMA): atom a of slot s at slot(s) + a * kSlotAtom
+    static constexpr int kSlotAtom = 2 * kAtom;
+    __device__ static constexpr int slot(int s) { return H0 + (s >> 1) * 2 * H0S + (s & 1) * kAtom; }
     static constexpr int X = H0 + kSt * H0S;              // x stages
     static constexpr int XS = kAtom;
     static constexpr int MISC = X + kStX * XS;
@@ -66,8 +73,7 @@ struct Smem {
     static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
     static constexpr int LAM = ROWS + 64 * 8;             // float[kHPC][64]
     static constexpr int CJ = LAM + kHPC * 64 * 4;        // float[kHPC][64]
-    static constexpr int EI = CJ + kHPC * 64 * 4;         // float[kHPC][64]
-    static constexpr int E0 = EI + kHPC * 64 * 4;         // float[kHPC][64]
+    static constexpr int E0 = CJ + kHPC * 64 * 4;         // float[kHPC][64]
     static constexpr int MODE = E0 + kHPC * 64 * 4;       // int[kHPC]
     static constexpr int AS = MODE + kHPC * 4;            // float[kHPC]  A_h
     static constexpr int DS = AS + kHPC * 4;              // float[kHPC]  D_h
@@ -81,9 +87,11 @@ struct Smem {
     static constexpr int XPREV = RDEC + (R ? kHPC * 4 : 0);               // bf16 [kHPC][kRStage][64]
     static constexpr int BPREV = XPREV + (R ? kHPC * kRStage * kP * 2 : 0);   // float[kRStage][NS]
     static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
-    // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[2], accempty[2],
-    //                 upd[S], xfull[S], xempty[S]   (xfull/xempty use the first kStX)
-    static constexpr int NBAR = 3 + 2 * kSt + 8 + 3 * kSt;
+    // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[kAcc],
+    //                 accempty[kAcc], dirempty, upd[S], xfull[S], xempty[S]   (xfull/xempty use the first kStX)
+    static constexpr int NBAR = 3 + 2 * kSt + 4 + 2 * kAcc + 1 + 3 * kSt;
+    static constexpr int BAR2 = 24 + 16 * kSt;                       // byte offset of mfull[0]
+    static constexpr int BAR3 = BAR2 + 8 * (4 + 2 * kAcc + 1);       // byte offset of upd[0]
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
     static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
@@ -294,7 +302,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     constexpr int kSt = S::kSt;
     auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };            // state tile landed
     auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };  // state tile free
-    auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kSt + 64 + 8 * s; };
+    auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int u = tid - kThreadsScan;     // 0..127
     const int uw = warp - 6;              // 0..3
@@ -306,70 +314,100 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     float* rdec = (float*)(sm + S::RDEC);
     __nv_bfloat16* xprev = (__nv_bfloat16*)(sm + S::XPREV);
     float* bprev = (float*)(sm + S::BPREV);
-    // ---- previous path: validation (root-anchored, increasing, parent-linked) ----
-    if (uw == 0) {
-        const int r = prm.path_len[b];
-        int ok = (r >= 1 && r <= Tp);
-        if (ok) {
-            for (int m = lane; m < r; m += 32) {
-                const int v = prm.path[(size_t)b * Tp + m];
-                rpath[m] = v;
-                bool good = (v >= 0 && v < Tp);
-                if (m == 0) good = good && v == 0;
-                else {
-                    const int pu = prm.path[(size_t)b * Tp + m - 1];
-                    good = good && v > pu;
-                    if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
-                }
-                if (!good) ok = 0;
+    // ---- previous accepted path.  Two rounds of DRAM latency: the path itself, then everything that
+    //      depends only on it (validation, dt_prev, x_prev rows, B_prev rows), issued together ----
+    const int r_raw = prm.path_len[b];
+    for (int m = u; m < Tp; m += 128) rpath[m] = prm.path[(size_t)b * Tp + m];
+    named_bar(3, 128);
+    const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
+    const int rs = min(rr, kRStage);
+    auto node = [&](int m) {   // path node clamped into the tree: loads stay in bounds before validation
+        const int v = rpath[m];
+        return (v >= 0 && v < Tp) ? v : 0;
+    };
+    constexpr int kQ = (kHPC + 3) / 4;    // heads per updater warp: uw, uw + 4, uw + 8
+    float dv[kQ][2];
+    uint32_t xv[kQ][kRStage];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const int hh = uw + 4 * q;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int m = lane + 32 * c;
+            dv[q][c] = (hh < nh && m < rr) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] : 0.f;
+        }
+#pragma unroll
+        for (int m = 0; m < kRStage; ++m)
+            xv[q][m] = (hh < nh && m < rs)
+                           ? reinterpret_cast<const uint32_t*>(prm.x_prev + (((size_t)b * Tp + node(m)) * H + hbeg + hh) * kP)[lane]
+                           : 0u;
+    }
+    for (int k = u; k < rs * NS; k += 128) {
+        const int m = k / NS, n = k % NS;
+        bprev[m * NS + n] = __bfloat162float(prm.b_prev[(((size_t)b * Tp + node(m)) * G + g) * NS + n]);
+    }
+    if (uw == 0) {   // root-anchored, increasing, parent-linked (PAPER.md:90 on the accepted path)
+        int ok = rr > 0;
+        for (int m = lane; m < rr; m += 32) {
+            const int v = rpath[m];
+            bool good = (v >= 0 && v < Tp);
+            if (m == 0) good = good && v == 0;
+            else {
+                const int pu = rpath[m - 1];
+                good = good && v > pu;
+                if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
             }
+            if (!good) ok = 0;
         }
         ok = __all_sync(0xffffffffu, ok);
         if (lane == 0) {
-            rinfo[0] = ok ? r : 0;
+            rinfo[0] = ok ? rr : 0;
             if (!ok && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
         }
     }
     named_bar(3, 128);
     const int r = rinfo[0];
-    const int rs = min(r, kRStage);
     if (r > 0) {
-        for (int hh = uw; hh < nh; hh += 4) {   // one warp per head
-            const int h = hbeg + hh;
-            const float Ah = prm.A[h];
-            float* cl = rcoef + hh * kRStage;
-            float carry = 0.f, lam_st = 0.f, d_st = 0.f, a_st = 0.f;
-            for (int m0 = 0; m0 < r; m0 += 32) {
-                const int m = m0 + lane;
-                const float d = (m < r) ? prm.dt_prev[((size_t)b * Tp + rpath[m]) * H + h] : 0.f;
-                float a = d * Ah;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float t = __shfl_up_sync(0xffffffffu, a, o);
-                    if (lane >= o) a += t;
-                }
-                a += carry;
-                if (m0 == 0) { a_st = a; d_st = d; }
-                if (m == kRStage - 1) lam_st = a;
-                carry = __shfl_sync(0xffffffffu, a, 31);
+        for (int q = 0; q < kQ; ++q) {
+            const int hh = uw + 4 * q;
+            if (hh >= nh) continue;   // warp-uniform
+            const float Ah = prm.A[hbeg + hh];
+            // lam_m = Σ_{q<=m} dt_prev[s_q] A_h: inclusive warp scans over m = lane and lane + 32
+            float a0 = dv[q][0] * Ah, a1 = dv[q][1] * Ah;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
+                if (lane >= o) { a0 += t0; a1 += t1; }
             }
-            // r <= 32 keeps lam_{r-1} in lane r-1 of the first chunk; longer paths carry it
-            const float last = (r <= 32) ? __shfl_sync(0xffffffffu, a_st, r - 1) : carry;
-            const float lst = __shfl_sync(0xffffffffu, lam_st, kRStage - 1);
-            if (lane < kRStage && lane < r) cl[lane] = expf(last - a_st) * d_st;
+            a1 += __shfl_sync(0xffffffffu, a0, 31);
+            float last;
+            if (r <= 32) last = __shfl_sync(0xffffffffu, a0, r - 1);
+            else if (r <= 64) last = __shfl_sync(0xffffffffu, a1, r - 33);
+            else {   // paths beyond 64 nodes: the remaining chunks from global memory
+                float carry = __shfl_sync(0xffffffffu, a1, 31);
+                for (int m0 = 64; m0 < r; m0 += 32) {
+                    const int m = m0 + lane;
+                    float a = (m < r) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] * Ah : 0.f;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const float t = __shfl_up_sync(0xffffffffu, a, o);
+                        if (lane >= o) a += t;
+                    }
+                    carry += __shfl_sync(0xffffffffu, a, 31);
+                }
+                last = carry;
+            }
+            const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
+            if (lane < rs) rcoef[hh * kRStage + lane] = expf(last - a0) * dv[q][0];
             if (lane == 0) {
                 rdec[hh] = expf(last);
                 rlam[2 * hh] = last;
                 rlam[2 * hh + 1] = lst;
             }
-            for (int m = 0; m < rs; ++m) {   // x_prev rows of the staged path nodes (64 bf16 = 32 words)
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(prm.x_prev + (((size_t)b * Tp + rpath[m]) * H + h) * kP);
-                reinterpret_cast<uint32_t*>(xprev + (hh * kRStage + m) * kP)[lane] = src[lane];
-            }
-        }
-        for (int k = u; k < rs * NS; k += 128) {
-            const int m = k / NS, n = k % NS;
-            bprev[m * NS + n] = __bfloat162float(prm.b_prev[(((size_t)b * Tp + rpath[m]) * G + g) * NS + n]);
+#pragma unroll
+            for (int m = 0; m < kRStage; ++m)
+                if (m < rs) reinterpret_cast<uint32_t*>(xprev + (hh * kRStage + m) * kP)[lane] = xv[q][m];
         }
     }
     named_bar(3, 128);
@@ -388,13 +426,13 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
             const float* cl = rcoef + k * kRStage;
             const float Ak = prm.A[hbeg + k], last = rlam[2 * k];
             float lam_run = rlam[2 * k + 1];   // long paths: lam_m accumulated from the last staged node
-            unsigned char* tile = sm + S::H0 + s * S::H0S;
+            unsigned char* tile = sm + S::slot(s);
             float4 hv[4][kAt];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int a = 0; a < kAt; ++a) {
-                    float4 v = *reinterpret_cast<const float4*>(tile + a * kAtom + swz((u >> 3) + 16 * i, pc));
+                    float4 v = *reinterpret_cast<const float4*>(tile + a * S::kSlotAtom + swz((u >> 3) + 16 * i, pc));
                     hv[i][a] = make_float4(dk * v.x, dk * v.y, dk * v.z, dk * v.w);
                 }
             for (int m = 0; m < r; ++m) {
@@ -433,25 +471,38 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int a = 0; a < kAt; ++a)
-                    *reinterpret_cast<float4*>(tile + a * kAtom + swz((u >> 3) + 16 * i, pc)) = hv[i][a];
+                    *reinterpret_cast<float4*>(tile + a * S::kSlotAtom + swz((u >> 3) + 16 * i, pc)) = hv[i][a];
         }
         fence_proxy_async();
         named_bar(3, 128);
         if (trace && u == 0 && k < 12) trace[65 + 3 * k] = gtimer();
         if (u == 0) {
             mbar_arrive(bar_upd(s));
-            if (r > 0) {   // committed state back to HBM (in place); the tile is free once the store read it
+            if (r > 0) {
+                // committed state back to HBM (in place).  The slot is free once the store has read it:
+                // released one head later (wait for all but the newest store group) so the updater never
+                // stalls on the store
                 const uint64_t pol = policy_evict_first();
                 for (int a = 0; a < NS / 32; ++a)
-                    tma_store_2d_ef(tm_h, sb + S::H0 + s * S::H0S + a * kAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
+                    tma_store_2d_ef(tm_h, sb + S::slot(s) + a * S::kSlotAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
                 bulk_commit();
-                bulk_wait_read0();
+                if (k > 0) {
+                    bulk_wait_read1();
+                    mbar_arrive(bar_empty((k - 1) % kSt));
+                }
                 if (trace && k < 12) trace[66 + 3 * k] = gtimer();
+            } else {
+                mbar_arrive(bar_empty(s));
             }
-            mbar_arrive(bar_empty(s));
         }
     }
-    if (u == 0) bulk_wait_all();
+    if (u == 0) {
+        if (r > 0 && nh > 0) {
+            bulk_wait_read0();
+            mbar_arrive(bar_empty((nh - 1) % kSt));
+        }
+        bulk_wait_all();
+    }
 }
 
 template <int NS, bool kReplay>
@@ -461,7 +512,6 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                    const __grid_constant__ CUtensorMap tm_y, const Params prm) {
     using S = Smem<NS, kReplay>;
     constexpr int kStages = S::kSt;
-    constexpr int kThreads = kReplay ? kThreadsReplay : kThreadsScan;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
@@ -483,13 +533,14 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     const uint32_t BAR_TREE = bar0, BAR_CTF = bar0 + 8, BAR_G = bar0 + 16;
     auto bar_full = [&](int s) { return bar0 + 24 + 8 * s; };
     auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kStages + 8 * s; };
-    auto bar_mfull = [&](int a) { return bar0 + 24 + 16 * kStages + 8 * a; };
-    auto bar_mempty = [&](int a) { return bar0 + 24 + 16 * kStages + 16 + 8 * a; };
-    auto bar_accfull = [&](int a) { return bar0 + 24 + 16 * kStages + 32 + 8 * a; };
-    auto bar_accempty = [&](int a) { return bar0 + 24 + 16 * kStages + 48 + 8 * a; };
-    auto bar_upd = [&](int s) { return bar0 + 24 + 16 * kStages + 64 + 8 * s; };   // replay: stage s updated
-    auto bar_xfull = [&](int s) { return bar0 + 24 + 24 * kStages + 64 + 8 * s; };  // x tile landed
-    auto bar_xempty = [&](int s) { return bar0 + 24 + 32 * kStages + 64 + 8 * s; }; // x tile free
+    auto bar_mfull = [&](int a) { return bar0 + S::BAR2 + 8 * a; };
+    auto bar_mempty = [&](int a) { return bar0 + S::BAR2 + 16 + 8 * a; };
+    auto bar_accfull = [&](int a) { return bar0 + S::BAR2 + 32 + 8 * a; };
+    auto bar_accempty = [&](int a) { return bar0 + S::BAR2 + 32 + 8 * kAcc + 8 * a; };
+    const uint32_t BAR_DIRE = bar0 + S::BAR2 + 32 + 16 * kAcc;                       // direct Y' read
+    auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };                    // replay: stage s updated
+    auto bar_xfull = [&](int s) { return bar0 + S::BAR3 + 8 * kStages + 8 * s; };    // x tile landed
+    auto bar_xempty = [&](int s) { return bar0 + S::BAR3 + 16 * kStages + 8 * s; };  // x tile free
     uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
 
     // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
@@ -507,9 +558,12 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_mfull(a), 2);
             mbar_init(bar_mempty(a), 1);
+        }
+        for (int a = 0; a < kAcc; ++a) {
             mbar_init(bar_accfull(a), 1);
             mbar_init(bar_accempty(a), 2);
         }
+        mbar_init(BAR_DIRE, 2);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -527,7 +581,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         for (int k = 0; k < n_early; ++k) {
             mbar_add_tx(bar_full(k), S::H0S);
             for (int a = 0; a < NS / 32; ++a)
-                tma_load_2d(sb + S::H0 + k * S::H0S + a * kAtom, &tm_h0, bar_full(k), 32 * a,
+                tma_load_2d(sb + S::slot(k) + a * S::kSlotAtom, &tm_h0, bar_full(k), 32 * a,
                             ((b * H) + hbeg + k) * kP);
         }
     }
@@ -536,7 +590,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
     //      The producer issues the tree operands right after the wait; tree validation runs in the
     //      epilogue warps (an invalid tree yields y = 0), so nothing waits on it ----
-    constexpr int kHPW = kHPC / 4;            // heads per epilogue warp
+    constexpr int kHPW = (kHPC + 3) / 4;      // heads per epilogue warp
     float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
     int* sbad = (int*)(sm + S::BADF);
     if (tid >= kEpi0 && tid < kEpi0 + 128) {
@@ -596,7 +650,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     mbar_expect_tx(bar_full(s), prm.has_h0 ? S::H0S : 0);
                     if (prm.has_h0)
                         for (int a = 0; a < NS / 32; ++a)
-                            tma_load_2d_ef(sb + S::H0 + s * S::H0S + a * kAtom, &tm_h0, bar_full(s), 32 * a,
+                            tma_load_2d_ef(sb + S::slot(s) + a * S::kSlotAtom, &tm_h0, bar_full(s), 32 * a,
                                            ((b * H) + h) * kP, pol_ef);
                 }
                 const int sx = k % S::kStX;
@@ -604,8 +658,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 mbar_expect_tx(bar_xfull(sx), xbytes);
                 tma_load_2d_ef(sb + S::X + sx * S::XS, &tm_x, bar_xfull(sx), h * kP, b * T, pol_ef);
                 // ramp: the rest of the ring is requested only once head 0 has landed, so every CTA's
-                // first tile is near the front of the DRAM queue instead of behind other CTAs' later stages
-                if (k == 0) mbar_wait(bar_full(0), 0);
+                // first pair is near the front of the DRAM queue instead of behind other CTAs' later stages
+                if (k == 1 || nh == 1) mbar_wait(bar_full(0), 0);
             }
         }
     } else if (warp == 1) {
@@ -627,39 +681,62 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             tc_fence_after();
             const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
             const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
-            for (int k = 0; k < nh; ++k) {
-                const int s = k % kStages, a = k & 1;
-                mbar_wait(bar_full(s), (k / kStages) & 1);
-                if (kReplay) mbar_wait(bar_upd(s), (k / kStages) & 1);   // state tile replayed on chip
+            const int* mode = (const int*)(sm + S::MODE);
+            int ndir = 0;
+            const unsigned long long dbg = trace ? trace[127] : 0ull;   // debug: 1 skip Y0, 2 skip Y'
+            const uint32_t id_y02 = idesc(kFmtTF32, 0, 128, 2 * kP);
+            for (int k = 0; k < nh; k += 2) {
+                // heads k, k+1 (slots s, s+1 of one pair, accumulators ac, ac+1 adjacent in TMEM)
+                const int s = k % kStages, ac = k % kAcc;
+                const int nq = (k + 1 < nh) ? 2 : 1;
+                for (int q = 0; q < nq; ++q) {
+                    mbar_wait(bar_full(s + q), ((k + q) / kStages) & 1);
+                    if (kReplay) mbar_wait(bar_upd(s + q), ((k + q) / kStages) & 1);   // replayed on chip
+                }
                 if (trace && k < 12) trace[30 + k] = gtimer();
-                mbar_wait(bar_accempty(a), ((k >> 1) & 1) ^ 1);
+                for (int q = 0; q < nq; ++q) mbar_wait(bar_accempty(ac + q), (((k + q) / kAcc) & 1) ^ 1);
                 tc_fence_after();
                 if (trace && k < 9) trace[118 + k] = gtimer();
-                const uint32_t d0 = tmem + kAccCol0 + 128 * a;
-                if (prm.has_h0) {
-                    // Y0 = C·h0_hᵀ, kind::tf32, A = C from TMEM, K = NS in steps of 8 (32 B / 8 columns)
+                const uint32_t d0 = tmem + kAccCol0 + 64 * ac;
+                if (prm.has_h0 && !(dbg & 1)) {
+                    // Y0 = C·h0ᵀ of both heads in one N = 2 x 64 MMA chain, kind::tf32, A = C from TMEM,
+                    // K = NS in steps of 8 (32 B / 8 columns)
 #pragma unroll 1
                     for (int kk = 0; kk < NS / 8; ++kk) {
-                        uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-                        mma_tf32_ts(d0, tmem + kCCol + 8 * kk, sdesc(sb + S::H0 + s * S::H0S + off, 16, 1024), id_y0,
-                                    kk > 0);
+                        const uint32_t off = (kk >> 2) * S::kSlotAtom + (kk & 3) * 32;
+                        mma_tf32_ts(d0, tmem + kCCol + 8 * kk, sdesc(sb + S::slot(s) + off, 16, 1024),
+                                    nq == 2 ? id_y02 : id_y0, kk > 0);
                     }
                 }
-                tc_commit(bar_empty(s));                  // state tile no longer needed by the tensor core
+                for (int q = 0; q < nq; ++q) tc_commit(bar_empty(s + q));   // state tiles no longer needed
                 if (trace && k < 9) trace[100 + k] = gtimer();
-                const int sx = k % S::kStX;
-                mbar_wait(bar_xfull(sx), (k / S::kStX) & 1);
-                mbar_wait(bar_mfull(a), (k >> 1) & 1);
-                if (trace && k < 9) trace[109 + k] = gtimer();
-                tc_fence_after();
-                // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j)
+                for (int q = 0; q < nq; ++q) {
+                    const int kq = k + q, a = kq & 1;
+                    const int sx = kq % S::kStX;
+                    mbar_wait(bar_xfull(sx), (kq / S::kStX) & 1);
+                    mbar_wait(bar_mfull(a), (kq >> 1) & 1);
+                    if (trace && kq < 9) trace[109 + kq] = gtimer();
+                    tc_fence_after();
+                    // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j).  Factorised
+                    // decay: accumulated onto Y0 (M' carries e^{-Λ_j}, the epilogue e^{Λ_i}); direct decay:
+                    // into the separate columns kDirCol, once the epilogue has read the previous direct head's
+                    const bool fac = mode[kq] != 0;
+                    uint32_t dy = d0 + 64 * q, acc0 = prm.has_h0 ? 1u : 0u;
+                    if (!fac) {
+                        mbar_wait(BAR_DIRE, (ndir & 1) ^ 1);
+                        tc_fence_after();
+                        ++ndir;
+                        dy = tmem + kDirCol;
+                        acc0 = 0;
+                    }
 #pragma unroll 1
-                for (int kk = 0; kk < Tp16 / 16; ++kk)
-                    mma_f16(d0 + 64, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
-                            sdesc(sb + S::X + sx * S::XS + kk * 2048, kAtom, 1024), id_y, kk > 0);
-                tc_commit(bar_accfull(a));
-                tc_commit(bar_mempty(a));
-                tc_commit(bar_xempty(sx));
+                    for (int kk = 0; kk < ((dbg & 2) ? 0 : Tp16 / 16); ++kk)
+                        mma_f16(dy, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
+                                sdesc(sb + S::X + sx * S::XS + kk * 2048, kAtom, 1024), id_y, (kk > 0) | acc0);
+                    tc_commit(bar_accfull(ac + q));
+                    tc_commit(bar_mempty(a));
+                    tc_commit(bar_xempty(sx));
+                }
             }
         }
     } else if (kReplay && warp >= 6) {
@@ -672,7 +749,6 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         uint64_t* rows = (uint64_t*)(sm + S::ROWS);
         float* lam = (float*)(sm + S::LAM);
         float* cj = (float*)(sm + S::CJ);
-        float* ei = (float*)(sm + S::EI);
         float* e0 = (float*)(sm + S::E0);
         int* mode = (int*)(sm + S::MODE);
         // ---- C (bf16, TMA) -> tf32 operand tile; zero the padded x rows ----
@@ -769,8 +845,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 float mn = fminf(lm[q][0], lm[q][1]);
 #pragma unroll
                 for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                const bool f = mn >= -120.f;      // factorised decay (e^{Λi-ref} e^{ref-Λj}, ref = min/2)
-                const float ref = 0.5f * mn;
+                const bool f = mn >= -64.f;       // factorised decay e^{Λi-Λj} = e^{Λi}·e^{-Λj}
                 if (lane == 0) {
                     mode[hh] = f ? 1 : 0;
                     ((float*)(sm + S::DS))[hh] = d_h[q];
@@ -781,8 +856,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     if (i < T) {
                         const float l = lm[q][hf];
                         lam[hh * 64 + i] = l;
-                        cj[hh * 64 + i] = f ? __expf(ref - l) * dtr[q][hf] : dtr[q][hf];
-                        ei[hh * 64 + i] = f ? __expf(l - ref) : 1.f;
+                        cj[hh * 64 + i] = f ? __expf(-l) * dtr[q][hf] : dtr[q][hf];
                         e0[hh * 64 + i] = __expf(l);
                     }
                 }
@@ -843,9 +917,9 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             const bool own = row < T;
             const bool leader = (warp == 4 && lane == 0);
             for (int k = 0; k < nh; ++k) {
-                const int s = k % kStages, a = k & 1;
+                const int a = k & 1, ac = k % kAcc;
                 const int h = hbeg + k;
-                mbar_wait(bar_accfull(a), (k >> 1) & 1);
+                mbar_wait(bar_accfull(ac), (k / kAcc) & 1);
                 tc_fence_after();
                 if (trace && leader && k < 12) trace[4 + 2 * k] = gtimer();
                 if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
@@ -853,24 +927,30 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 if (trace && leader && k < 6) trace[52 + 2 * k] = gtimer();
                 const bool zero_out = *sbad != 0;
                 const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[k];
+                const bool fac = mode[k] != 0;
+                const bool has0 = prm.has_h0 || fac;    // accumulator written (Y0 and / or Y')
                 const float s0 = (own && !zero_out) ? e0[k * 64 + row] : 0.f;
-                const float s1 = (own && !zero_out) ? ei[k * 64 + row] : 0.f;
                 const int sx = k % S::kStX;
                 const unsigned char* xr = sm + S::X + sx * S::XS;
                 unsigned char* yr = sm + S::YS + a * kAtom;
-                const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + kAccCol0 + 128 * a;
+                const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
+                const uint32_t tl = tq + kAccCol0 + 64 * ac;
                 uint32_t v0[2][32], v1[2][32];
-                if (prm.has_h0) tmem_ld32(tl, v0[0]);
-                tmem_ld32(tl + 64, v1[0]);
+                if (has0) tmem_ld32(tl, v0[0]);
+                if (!fac) tmem_ld32(tq + kDirCol, v1[0]);
                 tmem_wait();
-                if (prm.has_h0) tmem_ld32(tl + 32, v0[1]);
-                tmem_ld32(tl + 96, v1[1]);          // in flight while chunk 0 is computed
+                if (has0) tmem_ld32(tl + 32, v0[1]);
+                if (!fac) tmem_ld32(tq + kDirCol + 32, v1[1]);   // in flight while chunk 0 is computed
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     if (c == 1) tmem_wait();
-                    if (!prm.has_h0) {
+                    if (!has0) {
 #pragma unroll
                         for (int q = 0; q < 32; ++q) v0[c][q] = 0u;
+                    }
+                    if (fac) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) v1[c][q] = 0u;
                     }
                     if (own) {
 #pragma unroll
@@ -883,10 +963,9 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             for (int q = 0; q < 4; ++q) {
                                 const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
                                 const int p = 8 * qc + 2 * q;
-                                const float ya =
-                                    fmaf(s0, __uint_as_float(v0[c][p]), fmaf(s1, __uint_as_float(v1[c][p]), Dh * xa));
-                                const float yb = fmaf(s0, __uint_as_float(v0[c][p + 1]),
-                                                      fmaf(s1, __uint_as_float(v1[c][p + 1]), Dh * xb));
+                                const float ya = fmaf(s0, __uint_as_float(v0[c][p]), fmaf(Dh, xa, __uint_as_float(v1[c][p])));
+                                const float yb =
+                                    fmaf(s0, __uint_as_float(v0[c][p + 1]), fmaf(Dh, xb, __uint_as_float(v1[c][p + 1])));
                                 o[q] = zero_out ? 0u : pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
@@ -897,7 +976,10 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 tc_fence_before();
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_accempty(a));
+                if (lane == 0) {
+                    mbar_arrive(bar_accempty(ac));
+                    if (!fac) mbar_arrive(BAR_DIRE);
+                }
                 named_bar(2, 64);
                 if (leader) {
                     tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());

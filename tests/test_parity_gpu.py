@@ -345,6 +345,34 @@ def test_tc_forced_stress(variant):
     assert_y_close(y, ref, TOL_BF16)
 
 
+@pytest.mark.parametrize("with_h0", [True, False])
+def test_tc_mixed_decay_modes(with_h0):
+    """Heads of one CTA alternate between the factorised decay (Y' accumulated onto Y0) and the
+    direct per-element decay (Y' in its own TMEM columns): A_h spans 1..16 over a chain, so
+    min Λ crosses the -64 switch within the head range."""
+    d = inputs.Dims(16, 64, 48, 64, 128, 1, "bf16")      # 16 trees: several heads per CTA
+    par = np.stack([trees.chain(64) if i % 2 == 0 else trees.heap_kary(64, 2) for i in range(16)])
+    prob = inputs.make_problem(d, par, seed=77, dt_range=(0.05, 0.2), A_range=(1.0, 24.0))
+    lam_min = (prob.dt[0] * prob.A[None, :]).sum(axis=0)
+    assert (lam_min < -64).any() and (lam_min > -64).any()
+    if not with_h0:
+        binding.stree_set_scan_impl(binding.STREE_SCAN_TC)
+        try:
+            t = api.upload(prob)
+            y = torch.empty_like(t["x"])
+            binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], None, t["parent"], y)
+            torch.cuda.synchronize()
+        finally:
+            binding.stree_set_scan_impl(binding.STREE_SCAN_AUTO)
+        ref, _ = oracle.tree_scan(prob.io_as_f32("x"), prob.dt, prob.A, prob.io_as_f32("Bm"),
+                                  prob.io_as_f32("Cm"), prob.D, None, prob.parent)
+        assert_y_close(y_of(y), ref, TOL_BF16)
+        return
+    y, ref, st, _ = scan_both(prob, binding.STREE_SCAN_TC)
+    assert st == 0
+    assert_y_close(y, ref, TOL_BF16)
+
+
 def test_tc_null_h0_D_and_invalid_tree():
     prob = inputs.config_problem("c2")
     t = api.upload(prob)

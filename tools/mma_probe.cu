@@ -19,7 +19,7 @@ __host__ __device__ constexpr uint32_t idesc(uint32_t fmt, int M, int N) {
     return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int MODE, int N>   // 0: tf32 TS, 1: tf32 SS, 2: f16 SS
+template <int MODE, int N, int M = 128>   // 0: tf32 TS, 1: tf32 SS, 2: f16 SS
 __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint32_t tslot;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, unsigned long long* o
     if (threadIdx.x == 0) {
         const uint32_t base = su32(sm);
         const uint32_t fmt = MODE == 2 ? 1 : 2;
-        const uint32_t id = idesc(fmt, 128, N);
+        const uint32_t id = idesc(fmt, M, N);
         unsigned long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             const uint64_t bd = sdesc(base + 32768 + (it & 3) * 32, 16, 1024);
@@ -89,6 +89,10 @@ int main() {
     run(probe<1, 64>, "tf32 SS M128 N64 K8", 2.0 * 128 * 64 * 8);
     run(probe<0, 128>, "tf32 TS M128 N128 K8", 2.0 * 128 * 128 * 8);
     run(probe<1, 128>, "tf32 SS M128 N128 K8", 2.0 * 128 * 128 * 8);
+    run(probe<1, 64, 64>, "tf32 SS M64 N64 K8", 2.0 * 64 * 64 * 8);
+    run(probe<1, 128, 64>, "tf32 SS M64 N128 K8", 2.0 * 64 * 128 * 8);
+    run(probe<1, 256, 128>, "tf32 SS M128 N256 K8", 2.0 * 128 * 256 * 8);
+    run(probe<0, 256, 128>, "tf32 TS M128 N256 K8", 2.0 * 128 * 256 * 8);
     run(probe<2, 64>, "f16 SS M128 N64 K16", 2.0 * 128 * 64 * 16);
     run(probe<2, 128>, "f16 SS M128 N128 K16", 2.0 * 128 * 128 * 16);
     return 0;

@@ -48,6 +48,7 @@ if os.environ.get("ISOLATED"):   # flush L2 and drain before the traced launch
         for _ in range(3):
             float(junk.sum())
     torch.cuda.synchronize()
+buf[:, 127] = int(os.environ.get("DBG", "0"))   # kernel debug knobs (1: skip Y0 MMAs, 2: skip Y' MMAs)
 L.stree_debug_tc_trace(ctypes.c_void_p(buf.data_ptr()))
 run(layers[-1], ys[-1])
 torch.cuda.synchronize()
