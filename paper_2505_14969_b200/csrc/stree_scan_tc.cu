@@ -38,7 +38,7 @@ constexpr int kT = 64;          // max nodes per tree served
 constexpr int kP = 64;          // head dim
 constexpr int kHPC = 10;        // max heads per CTA
 constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
-constexpr int kThreadsReplay = 320;   // + warps 6-9 replay updaters
+constexpr int kThreadsReplay = 352;   // + warps 6-9 replay updaters, warp 10 committed-state stores
 constexpr int kRStage = 8;            // previous-path nodes staged on chip by the replay
 constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
@@ -51,7 +51,9 @@ constexpr int kDirCol = 448;    // Y' of direct-decay heads (rare): columns [448
 template <int NS, bool R>
 struct Smem {
     static constexpr int kSt = 4;                         // state (h0) ring depth: 2 pairs of head slots
-    static constexpr int kStX = R ? 3 : 4;                // x ring depth
+    static constexpr int kStX0 = R ? 3 : 4;               // x slots in the X region
+    static constexpr int kXB = NS >= 128 ? 2 : 0;         // + x slots in the B tile region, free after G = C·Bᵀ
+    static constexpr int kStX = kStX0 + kXB;              // x ring depth
     static constexpr int kCbAtoms = NS / 64;              // bf16 C / B: 64 bf16 per 128B
     static constexpr int U = 0;                           // union: {C bf16, B bf16} then {M'[2], ystage[2]}
     static constexpr int CB = U;                          // C bf16: atom a at CB + 2a*kAtom, copy at +kAtom
@@ -67,7 +69,8 @@ struct Smem {
     __device__ static constexpr int slot(int s) { return H0 + (s >> 1) * 2 * H0S + (s & 1) * kAtom; }
     static constexpr int X = H0 + kSt * H0S;              // x stages
     static constexpr int XS = kAtom;
-    static constexpr int MISC = X + kStX * XS;
+    static constexpr int MISC = X + kStX0 * XS;
+    __device__ static constexpr int xslot(int s) { return s < kStX0 ? X + s * XS : BB + (s - kStX0) * XS; }
     // misc (4-byte words unless noted)
     static constexpr int PAR = MISC;                      // int[64]
     static constexpr int ROWS = PAR + 64 * 4;             // u64[64]
@@ -88,8 +91,8 @@ struct Smem {
     static constexpr int BPREV = XPREV + (R ? kHPC * kRStage * kP * 2 : 0);   // float[kRStage][NS]
     static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
     // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[kAcc],
-    //                 accempty[kAcc], dirempty, upd[S], xfull[S], xempty[S]   (xfull/xempty use the first kStX)
-    static constexpr int NBAR = 3 + 2 * kSt + 4 + 2 * kAcc + 1 + 3 * kSt;
+    //                 accempty[kAcc], dirempty, upd[S], xfull[kStX]
+    static constexpr int NBAR = 3 + 2 * kSt + 4 + 2 * kAcc + 1 + kSt + kStX;
     static constexpr int BAR2 = 24 + 16 * kSt;                       // byte offset of mfull[0]
     static constexpr int BAR3 = BAR2 + 8 * (4 + 2 * kAcc + 1);       // byte offset of upd[0]
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -421,7 +424,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         const int s = k % kSt;
         mbar_wait(bar_full(s), (k / kSt) & 1);
         if (trace && u == 0 && k < 12) trace[64 + 3 * k] = gtimer();
-        if (r > 0) {
+        if (r > 0 && !(trace && (trace[127] & 4))) {   // debug knob 4: skip the tile update
             const float dk = rdec[k];
             const float* cl = rcoef + k * kRStage;
             const float Ak = prm.A[hbeg + k], last = rlam[2 * k];
@@ -476,33 +479,36 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         fence_proxy_async();
         named_bar(3, 128);
         if (trace && u == 0 && k < 12) trace[65 + 3 * k] = gtimer();
-        if (u == 0) {
-            mbar_arrive(bar_upd(s));
-            if (r > 0) {
-                // committed state back to HBM (in place).  The slot is free once the store has read it:
-                // released one head later (wait for all but the newest store group) so the updater never
-                // stalls on the store
-                const uint64_t pol = policy_evict_first();
-                for (int a = 0; a < NS / 32; ++a)
-                    tma_store_2d_ef(tm_h, sb + S::slot(s) + a * S::kSlotAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
-                bulk_commit();
-                if (k > 0) {
-                    bulk_wait_read1();
-                    mbar_arrive(bar_empty((k - 1) % kSt));
-                }
-                if (trace && k < 12) trace[66 + 3 * k] = gtimer();
-            } else {
-                mbar_arrive(bar_empty(s));
-            }
-        }
+        if (u == 0) mbar_arrive(bar_upd(s));   // to the MMA issuer (Y0) and the state storer
     }
-    if (u == 0) {
-        if (r > 0 && nh > 0) {
+}
+
+// Warp 10 (one thread): the committed state back to HBM, in place, once a slot has been replayed; the
+// slot is released (with the MMA issuer's Y0 commit) when the store has read it.  Kept off the updater
+// warps so they never stall on the store.
+template <int NS, bool R>
+__device__ __forceinline__ void state_storer(const Params& prm, unsigned char* sm, uint32_t sb, const CUtensorMap* tm_h,
+                                             int b, int hbeg, int nh, uint32_t bar0) {
+    using S = Smem<NS, R>;
+    constexpr int kSt = S::kSt;
+    auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };
+    auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };
+    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
+    const uint64_t pol = policy_evict_first();
+    const int H = prm.H;
+    for (int k = 0; k < nh; ++k) {
+        const int s = k % kSt;
+        mbar_wait(bar_upd(s), (k / kSt) & 1);
+        if (((const int*)(sm + S::RINFO))[0] > 0) {   // path length, published before the first bar_upd
+            for (int a = 0; a < NS / 32; ++a)
+                tma_store_2d_ef(tm_h, sb + S::slot(s) + a * S::kSlotAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
+            bulk_commit();
             bulk_wait_read0();
-            mbar_arrive(bar_empty((nh - 1) % kSt));
+            if (trace && k < 12) trace[66 + 3 * k] = gtimer();
         }
-        bulk_wait_all();
+        mbar_arrive(bar_empty(s));
     }
+    bulk_wait_all();
 }
 
 template <int NS, bool kReplay>
@@ -540,7 +546,6 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     const uint32_t BAR_DIRE = bar0 + S::BAR2 + 32 + 16 * kAcc;                       // direct Y' read
     auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };                    // replay: stage s updated
     auto bar_xfull = [&](int s) { return bar0 + S::BAR3 + 8 * kStages + 8 * s; };    // x tile landed
-    auto bar_xempty = [&](int s) { return bar0 + S::BAR3 + 16 * kStages + 8 * s; };  // x tile free
     uint32_t* tmem_slot = (uint32_t*)(sm + S::TMEMP);
 
     // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
@@ -552,8 +557,6 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             mbar_init(bar_full(s), 1);
             mbar_init(bar_empty(s), kReplay ? 2 : 1);   // state tile: MMA (Y0) [+ replay store read]
             mbar_init(bar_upd(s), 1);
-            mbar_init(bar_xfull(s), 1);
-            mbar_init(bar_xempty(s), 2);                  // x tile: MMA (Y') + epilogue (D x)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_mfull(a), 2);
@@ -564,6 +567,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             mbar_init(bar_accempty(a), 2);
         }
         mbar_init(BAR_DIRE, 2);
+        for (int s = 0; s < S::kStX; ++s) mbar_init(bar_xfull(s), 1);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const int n_early = (prm.early_state && prm.has_h0) ? 1 : 0;
+    const int n_early = (prm.early_state && prm.has_h0) ? min(kStages, nh) : 0;   // whole state ring
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
         // the state of the first heads is streamed before the dependency wait (caller's promise)
@@ -639,7 +643,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             }
             // the bulk state stream starts once the tree operands have landed: issued together, the
             // ~kStages x 40 KB per CTA would queue the small critical-path loads behind it
-            mbar_wait(BAR_TREE, 0);
+            const unsigned long long pdbg = trace ? trace[127] : 0ull;   // debug knob 8: no ramp
+            if (!(pdbg & 8)) mbar_wait(BAR_TREE, 0);
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
                 const int h = hbeg + k;
@@ -653,13 +658,13 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             tma_load_2d_ef(sb + S::slot(s) + a * S::kSlotAtom, &tm_h0, bar_full(s), 32 * a,
                                            ((b * H) + h) * kP, pol_ef);
                 }
-                const int sx = k % S::kStX;
-                mbar_wait(bar_xempty(sx), ((k / S::kStX) & 1) ^ 1);
-                mbar_expect_tx(bar_xfull(sx), xbytes);
-                tma_load_2d_ef(sb + S::X + sx * S::XS, &tm_x, bar_xfull(sx), h * kP, b * T, pol_ef);
+                if (k < S::kStX0) {   // first x tiles; later ones are requested by the epilogue that frees the slot
+                    mbar_expect_tx(bar_xfull(k), xbytes);
+                    tma_load_2d_ef(sb + S::xslot(k), &tm_x, bar_xfull(k), h * kP, b * T, pol_ef);
+                }
                 // ramp: the rest of the ring is requested only once head 0 has landed, so every CTA's
                 // first pair is near the front of the DRAM queue instead of behind other CTAs' later stages
-                if (k == 1 || nh == 1) mbar_wait(bar_full(0), 0);
+                if ((k == 1 || nh == 1) && !(pdbg & 8)) mbar_wait(bar_full(0), 0);
             }
         }
     } else if (warp == 1) {
@@ -685,10 +690,11 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             int ndir = 0;
             const unsigned long long dbg = trace ? trace[127] : 0ull;   // debug: 1 skip Y0, 2 skip Y'
             const uint32_t id_y02 = idesc(kFmtTF32, 0, 128, 2 * kP);
-            for (int k = 0; k < nh; k += 2) {
+            const bool pairs = !(dbg & 16);   // debug knob 16: one head per Y0 chain
+            for (int k = 0; k < nh; k += (pairs ? 2 : 1)) {
                 // heads k, k+1 (slots s, s+1 of one pair, accumulators ac, ac+1 adjacent in TMEM)
                 const int s = k % kStages, ac = k % kAcc;
-                const int nq = (k + 1 < nh) ? 2 : 1;
+                const int nq = (pairs && k + 1 < nh) ? 2 : 1;
                 for (int q = 0; q < nq; ++q) {
                     mbar_wait(bar_full(s + q), ((k + q) / kStages) & 1);
                     if (kReplay) mbar_wait(bar_upd(s + q), ((k + q) / kStages) & 1);   // replayed on chip
@@ -732,13 +738,14 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
 #pragma unroll 1
                     for (int kk = 0; kk < ((dbg & 2) ? 0 : Tp16 / 16); ++kk)
                         mma_f16(dy, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
-                                sdesc(sb + S::X + sx * S::XS + kk * 2048, kAtom, 1024), id_y, (kk > 0) | acc0);
+                                sdesc(sb + S::xslot(sx) + kk * 2048, kAtom, 1024), id_y, (kk > 0) | acc0);
                     tc_commit(bar_accfull(ac + q));
                     tc_commit(bar_mempty(a));
-                    tc_commit(bar_xempty(sx));
                 }
             }
         }
+    } else if (kReplay && warp == 10) {
+        if (lane == 0) state_storer<NS, kReplay>(prm, sm, sb, &tm_h0, b, hbeg, nh, bar0);
     } else if (kReplay && warp >= 6) {
         replay_updater<NS, kReplay>(prm, sm, sb, &tm_h0, b, g, chunk, hbeg, nh, bar0);
     } else {
@@ -778,7 +785,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             tmem_st_wait();
             tc_fence_before();
         } else {
-            for (int k = e; k < S::kStX * (Tp16 - T) * 8; k += 64) {
+            for (int k = e; k < S::kStX0 * (Tp16 - T) * 8; k += 64) {
                 const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
                 *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
             }
@@ -916,6 +923,22 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             // ---- TMEM epilogue (warps 4,5 = TMEM lanes 0..63 = tree nodes) ----
             const bool own = row < T;
             const bool leader = (warp == 4 && lane == 0);
+            if (S::kXB > 0 && nh > S::kStX0) {
+                // G is done, so the B tile region holds the last x slots: zero their padded rows, then
+                // request their first tiles
+                const int e2 = tid - kEpi0 - 64;   // 0..63
+                for (int q = e2; q < S::kXB * (Tp16 - T) * 8; q += 64) {
+                    const int sx = S::kStX0 + q / ((Tp16 - T) * 8), rr = T + (q / 8) % (Tp16 - T), c = q & 7;
+                    *reinterpret_cast<uint4*>(sm + S::xslot(sx) + swz(rr, c)) = make_uint4(0, 0, 0, 0);
+                }
+                fence_proxy_async();
+                named_bar(2, 64);
+                if (leader)
+                    for (int k = S::kStX0; k < S::kStX && k < nh; ++k) {
+                        mbar_expect_tx(bar_xfull(k), xbytes);
+                        tma_load_2d_ef(sb + S::xslot(k), &tm_x, bar_xfull(k), (hbeg + k) * kP, b * T, policy_evict_first());
+                    }
+            }
             for (int k = 0; k < nh; ++k) {
                 const int a = k & 1, ac = k % kAcc;
                 const int h = hbeg + k;
@@ -931,7 +954,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 const bool has0 = prm.has_h0 || fac;    // accumulator written (Y0 and / or Y')
                 const float s0 = (own && !zero_out) ? e0[k * 64 + row] : 0.f;
                 const int sx = k % S::kStX;
-                const unsigned char* xr = sm + S::X + sx * S::XS;
+                const unsigned char* xr = sm + S::xslot(sx);
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
                 const uint32_t tl = tq + kAccCol0 + 64 * ac;
@@ -984,7 +1007,13 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 if (leader) {
                     tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
                     bulk_commit();
-                    mbar_arrive(bar_xempty(sx));
+                    // x slot free (Y' read it before accfull, the epilogue above): refill it with head k + kStX,
+                    // so the x stream never waits in the state producer's queue
+                    if (k + S::kStX < nh) {
+                        mbar_expect_tx(bar_xfull(sx), xbytes);
+                        tma_load_2d_ef(sb + S::xslot(sx), &tm_x, bar_xfull(sx), (h + S::kStX) * kP, b * T,
+                                       policy_evict_first());
+                    }
                     if (trace && k < 12) trace[5 + 2 * k] = gtimer();
                 }
             }

@@ -322,7 +322,7 @@ def test_tc_kernel_selected_for_mamba2_shapes():
 
 @pytest.mark.parametrize("shape", [(1, 64, 80, 64, 128, 1), (16, 64, 80, 64, 128, 1), (3, 1, 5, 64, 128, 1),
                                    (2, 13, 7, 64, 64, 1), (4, 50, 24, 64, 128, 2), (2, 33, 30, 64, 64, 3),
-                                   (5, 17, 40, 64, 128, 1)])
+                                   (5, 17, 40, 64, 128, 1), (16, 50, 80, 64, 128, 1), (12, 37, 96, 64, 128, 1)])
 def test_tc_forced_shapes(shape):
     B, T, H, P, N, G = shape
     rng = np.random.default_rng(B * 1000 + T)

@@ -62,7 +62,7 @@ def oracle_pair(prev, new, path, plen):
 
 @pytest.mark.parametrize("shape", [(16, 64, 64, 80, 64, 128, 1), (1, 64, 64, 80, 64, 128, 1),
                                    (3, 40, 24, 16, 64, 64, 1), (4, 32, 50, 24, 64, 128, 2),
-                                   (2, 13, 64, 12, 64, 128, 1)])
+                                   (2, 13, 64, 12, 64, 128, 1), (16, 64, 50, 80, 64, 128, 1), (12, 30, 37, 96, 64, 128, 1)])
 def test_replay_scan_matches_oracle(shape):
     B, Tp, T, H, P, N, G = shape
     prev, new, path, plen = make_pair(B, Tp, T, H, P, N, G, "bf16", seed=Tp * 7 + T)

@@ -53,6 +53,49 @@ __global__ void __launch_bounds__(32, 1) rmw(float* h, char* x, char* y, int uni
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// same traffic with x / y in the tree-scan layout: per unit (b, h) 64 rows of 128 B strided by H*P*2 bytes
+// (x[B][T][H][P] bf16), issued by one warp (lane i: rows i, i + 32)
+template <int STAGES, bool CONTIG = false>
+__global__ void __launch_bounds__(32, 1) rmw_strided(float* h, char* x, char* y, int units, int H) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) unsigned long long bars[8];
+    const int u0 = blockIdx.x * units;
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(su32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncwarp();
+    const uint32_t SZ = 40960;
+    auto xrow = [&](int unit, int t) {   // unit = b * H + h
+        const int b = unit / H, hh = unit % H;
+        if (CONTIG) return (size_t)unit * 8192 + t * 128;
+        return ((size_t)(b * 64 + t) * H + hh) * 128;
+    };
+    for (int k = 0; k < units + STAGES; ++k) {
+        if (k >= STAGES) {
+            const int j = k - STAGES, s = j % STAGES;
+            mwait(su32(&bars[s]), (j / STAGES) & 1);
+            if (lane == 0) st(h + (size_t)(u0 + j) * 8192, su32(sm + s * SZ), 32768);
+            for (int t = lane; t < 64; t += 32) st(y + xrow(u0 + j, t), su32(sm + s * SZ + 32768 + t * 128), 128);
+            asm volatile("cp.async.bulk.commit_group;");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+        }
+        if (k < units) {
+            const int s = k % STAGES;
+            const uint32_t bar = su32(&bars[s]);
+            if (lane == 0) {
+                expect_tx(bar, SZ);
+                ld(su32(sm + s * SZ), h + (size_t)(u0 + k) * 8192, 32768, bar);
+            }
+            __syncwarp();
+            for (int t = lane; t < 64; t += 32) ld(su32(sm + s * SZ + 32768 + t * 128), x + xrow(u0 + k, t), 128, bar);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     const int ctas = 144, units = 9, layers = 8;
     const size_t nunit = (size_t)ctas * units;
@@ -89,5 +132,26 @@ int main() {
     run(rmw<3, false>, 3, "load 40KB/unit only", 40960);
     run(rmw<3, true>, 3, "load 40KB + store 40KB (in place)", 81920);
     run(rmw<5, true>, 5, "load 40KB + store 40KB (in place)", 81920);
+    auto run2 = [&](auto k, int stages, const char* name) {
+        size_t smem = (size_t)stages * 40960;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        for (int w = 0; w < 2; ++w)
+            for (int l = 0; l < layers; ++l) k<<<ctas, 32, smem>>>(h[l], x[l], y[l], units, 81);
+        cudaEventRecord(e0);
+        const int reps = 5;
+        for (int r = 0; r < reps; ++r)
+            for (int l = 0; l < layers; ++l) k<<<ctas, 32, smem>>>(h[l], x[l], y[l], units, 81);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double us = ms * 1e3 / (reps * layers);
+        printf("%-34s stages=%d %8.2f us/launch  %7.1f GB/s\n", name, stages, us, nunit * 81920.0 / (us * 1e-6) / 1e9);
+        cudaError_t err = cudaGetLastError();
+        if (err) printf("  error %s\n", cudaGetErrorString(err));
+    };
+    run2(rmw_strided<3>, 3, "x/y strided 128B rows, state in place");
+    run2(rmw_strided<5>, 5, "x/y strided 128B rows, state in place");
+    run2(rmw_strided<3, true>, 3, "x/y 64 x 128B ops, contiguous");
     return 0;
 }
