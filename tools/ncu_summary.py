@@ -21,7 +21,22 @@ def launches(path):
     return per
 
 
-print("== launch list (ncu, cold-cache, serialised): per-kernel mean over launches ==")
+API = {"scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "stree_replay_scan",
+       "scan_tc_kernel<128, 0>": "stree_tree_scan", "scan_tc_kernel<64, 0>": "stree_tree_scan",
+       "commit_ring_kernel": "stree_commit", "commit_block_kernel": "stree_commit",
+       "build_mask_kernel": "stree_build_mask", "accept_kernel": "stree_accept"}
+
+
+def api_name(k):
+    for pre, v in API.items():
+        if k.split("::")[-1].startswith(pre) or pre in k:
+            return v
+    if "scan_simt" in k:
+        return "stree_tree_scan"
+    return k
+
+
+print("== launch list (ncu --cache-control none, serialised): per-kernel mean over launches ==")
 per = launches(os.path.join(out, "launches.csv"))
 tot = sum(sum(m["gpu__time_duration.sum"]) for m in per.values())
 traffic = {}
@@ -31,7 +46,7 @@ for k, m in sorted(per.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.su
     wr = sum(m["dram__bytes_write.sum"]) / len(t)
     print(f"{k[:60]:60s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  share={sum(t) / tot * 100:5.1f}%  "
           f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB")
-    traffic[k] = rd + wr
+    traffic.setdefault(api_name(k), rd + wr)
 
 
 def details(rep, names):
@@ -54,7 +69,8 @@ def details(rep, names):
 names = {"Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Registers Per Thread",
          "Dynamic Shared Memory Per Block", "Grid Size", "Block Size", "L2 Hit Rate", "Achieved Active Warps Per SM",
          "Issued Warp Per Scheduler", "No Eligible"}
-for rep in ("prof_fused", "prof_commit"):
+full = {}
+for rep in ("prof_fused", "prof_scan", "prof_commit"):
     p = os.path.join(out, rep + ".ncu-rep")
     if os.path.exists(p):
         print(f"== ncu --set full: {rep} ==")
@@ -63,4 +79,23 @@ for rep in ("prof_fused", "prof_commit"):
                               "dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tc.sum"],
                              capture_output=True, text=True).stdout
         print(raw[-2000:])
-json.dump({"c4": traffic}, open(os.path.join(out, "traffic.json"), "w"), indent=1)
+        # per-launch DRAM bytes of the --set full capture (first captured launch)
+        rows = list(csv.reader(raw.splitlines()))
+        if len(rows) > 2:
+            hdr = rows[0]
+            d = dict(zip(hdr, rows[2]))
+            try:
+                unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                tot = sum(float(d[m].replace(",", "")) * unit.get(dict(zip(hdr, rows[1]))[m], 1)
+                          for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                full[api_name(d.get("Kernel Name", rep))] = tot
+            except (KeyError, ValueError):
+                pass
+# traffic = DRAM read + write per launch from the launch list (steady state, caches not flushed: the
+# write-back of a launch's dirty lines lands in the following launches, so the mean is the per-launch
+# traffic).  A --set full capture replays the kernel ~40 times: with flushed caches its writes stay in
+# L2 (under-counted), without flushing its replays hit L2 -- kept for reference only.
+print("traffic per launch (bytes, launch list):", json.dumps(traffic))
+print("--set full capture DRAM bytes (replayed, reference only):", json.dumps(full))
+json.dump({"c4": traffic, "source": "ncu launch list of bench.py, --cache-control none, mean read+write per launch"},
+          open(os.path.join(out, "traffic.json"), "w"), indent=1)

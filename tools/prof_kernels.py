@@ -15,7 +15,7 @@ from paper_2505_14969_b200 import api, binding  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
-ap.add_argument("--layers", type=int, default=4)
+ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--scan-impl", default="auto")
 ap.add_argument("--fused", action="store_true")
