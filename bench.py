@@ -254,7 +254,8 @@ def run_stree(args):
     # PDL between consecutive kernels; in this step the kernel preceding a scan / commit of layer l never
     # writes layer l's state, so the state stream may start before the dependency wait (EARLY_STATE)
     binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL |
-                                   (0 if args.no_early_state else binding.STREE_LAUNCH_EARLY_STATE))
+                                   (0 if args.no_early_state else
+                                    binding.STREE_LAUNCH_EARLY_STATE | binding.STREE_LAUNCH_EARLY_REPLAY))
     L = args.layers
     # every rank verifies its own batch of trees (weak scaling; no data-path collective)
     from paper_2505_14969_b200 import dist as sdist

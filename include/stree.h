@@ -181,8 +181,14 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *                            written by the kernel immediately preceding the call in its stream
  *                            (true in a decode loop: the state was committed an iteration earlier).
  *                            The kernels then start streaming h0 before that wait.
+ *  STREE_LAUNCH_EARLY_REPLAY promise: the previous tree's operands of stree_replay_scan (path,
+ *                            path_len, x_prev, dt_prev, Bm_prev, parent_prev) are not written by the
+ *                            kernel immediately preceding the call (true in a decode loop: they are
+ *                            the previous iteration's inputs and acceptance).  The replay prologue
+ *                            (path validation, coefficients, staging) then runs before that wait;
+ *                            every global write still follows it.
  */
-enum { STREE_LAUNCH_PDL = 1, STREE_LAUNCH_EARLY_STATE = 2 };
+enum { STREE_LAUNCH_PDL = 1, STREE_LAUNCH_EARLY_STATE = 2, STREE_LAUNCH_EARLY_REPLAY = 4 };
 stree_status stree_set_launch_flags(uint32_t flags);
 
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */

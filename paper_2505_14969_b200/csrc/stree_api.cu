@@ -70,7 +70,8 @@ const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
 uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed); }
 
 stree_status stree_set_launch_flags(uint32_t flags) {
-    if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE)) return STREE_ERR_UNSUPPORTED;
+    if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE | STREE_LAUNCH_EARLY_REPLAY))
+        return STREE_ERR_UNSUPPORTED;
     g_launch_flags.store(flags);
     return STREE_OK;
 }

@@ -278,6 +278,7 @@ struct Params {
     int32_t* dev_status;
     int has_h0;
     int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
+    int early_replay;  // STREE_LAUNCH_EARLY_REPLAY: the replay prologue may run before the PDL wait
     // replay (fused commit of the previous tree), kReplay only
     int Tp;
     const __nv_bfloat16* x_prev;
@@ -365,10 +366,12 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         ok = __all_sync(0xffffffffu, ok);
         if (lane == 0) {
             rinfo[0] = ok ? rr : 0;
-            if (!ok && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+            rinfo[1] = ok ? 0 : 1;
         }
     }
     named_bar(3, 128);
+    if (prm.early_replay) pdl_wait();   // global writes (status, committed state) follow the dependency
+    if (u == 0 && rinfo[1] && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
     const int r = rinfo[0];
     if (r > 0) {
 #pragma unroll
@@ -496,6 +499,7 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
     unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
     const uint64_t pol = policy_evict_first();
     const int H = prm.H;
+    if (prm.early_replay) pdl_wait();   // stores follow the dependency wait
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
         mbar_wait(bar_upd(s), (k / kSt) & 1);
@@ -589,7 +593,9 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             ((b * H) + hbeg + k) * kP);
         }
     }
-    pdl_wait();
+    // replay warps with the EARLY_REPLAY promise wait inside their own code (after the prologue's
+    // loads of the previous tree's operands, before any global write)
+    if (!(kReplay && warp >= 6 && prm.early_replay)) pdl_wait();
 
     // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
     //      The producer issues the tree operands right after the wait; tree validation runs in the
@@ -1140,6 +1146,7 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.has_h0 = h0 != nullptr;
     prm.early_state = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
+    prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (N == 128)

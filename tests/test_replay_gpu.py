@@ -75,6 +75,24 @@ def test_replay_scan_matches_oracle(shape):
     assert_y_close(y, yr, TOL_BF16)
 
 
+@pytest.mark.parametrize("flags", [0, 7])
+def test_replay_launch_flags(flags):
+    """PDL off, and PDL with the EARLY_STATE + EARLY_REPLAY promises (state ring and replay prologue
+    ahead of the dependency wait): same result, including an invalid path's status."""
+    prev, new, path, plen = make_pair(16, 64, 64, 80, 64, 128, 1, "bf16", seed=31)
+    path = path.copy()
+    path[3, 0] = 2
+    binding.stree_set_launch_flags(flags)
+    try:
+        y, h, st = run_fused(prev, new, path, plen)
+    finally:
+        binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
+    yr, hr, hst, _ = oracle_pair(prev, new, path, plen)
+    assert st == 3 and hst[3] == 3
+    assert_h_close(h, hr, TOL_F32)
+    assert_y_close(y, yr, TOL_BF16)
+
+
 def test_replay_long_paths_use_l2_path():
     """Accepted paths longer than the 16 staged nodes (full chains)."""
     prev, new, path, plen = make_pair(2, 64, 64, 8, 64, 128, 1, "bf16", seed=5, prev_kind="chain")
