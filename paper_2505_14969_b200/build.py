@@ -40,6 +40,10 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+    # STREE_TRACE=1: compile the kernels' timeline instrumentation in (tools/trace_*.py); off by default
+    if os.environ.get("STREE_TRACE") == "1":
+        extra = (*extra, "-DSTREE_TRACE")
+        force = True
     if not force and up_to_date():
         return LIB
     objs = []

@@ -39,6 +39,12 @@ constexpr int kP = 64;          // head dim
 constexpr int kHPC = 10;        // max heads per CTA
 constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
 constexpr int kThreadsReplay = 352;   // + warps 6-9 replay updaters, warp 10 committed-state stores
+constexpr int kTraceWords = 256;   // debug trace: u64 stamps per CTA (stree_debug_tc_trace)
+#ifdef STREE_TRACE
+constexpr bool kTrace = true;      // timeline instrumentation compiled in (STREE_TRACE=1 builds, tools/trace_*.py)
+#else
+constexpr bool kTrace = false;     // production: no instrumentation code in the kernels (instruction-cache footprint)
+#endif
 constexpr int kRStage = 8;            // previous-path nodes staged on chip by the replay
 constexpr int kEpi0 = 64;       // first epilogue thread
 constexpr int kAtom = 8192;     // one 64-row x 128-byte swizzle-128B tile
@@ -92,7 +98,7 @@ struct Smem {
     static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
     // barriers (u64): tree, ctf32, gdone, hfull[S], hempty[S], mfull[2], mempty[2], accfull[kAcc],
     //                 accempty[kAcc], dirempty, upd[S], xfull[kStX]
-    static constexpr int NBAR = 3 + 2 * kSt + 4 + 2 * kAcc + 1 + kSt + kStX;
+    static constexpr int NBAR = 3 + 2 * kSt + 4 + 2 * kAcc + 1 + kSt + kStX + 1;   // + debug
     static constexpr int BAR2 = 24 + 16 * kSt;                       // byte offset of mfull[0]
     static constexpr int BAR3 = BAR2 + 8 * (4 + 2 * kAcc + 1);       // byte offset of upd[0]
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -188,6 +194,29 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uin
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// Warp-converged issue: the whole warp runs the issuer code (operands stay warp-uniform, no per-MMA
+// waterfall), one elected lane issues the instruction.  tcgen05.commit must come from the same lane:
+// elect.sync picks the lowest active lane, so with the full warp converged it is always lane 0.
+__device__ __forceinline__ void mma_f16_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_w(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
         : "memory");
 }
 // D[tmem] (+)= A[tmem] · B[smem desc]ᵀ  (A in tensor memory: M lanes x K columns of 32 bit)
@@ -321,6 +350,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     // ---- previous accepted path.  Two rounds of DRAM latency: the path itself, then everything that
     //      depends only on it (validation, dt_prev, x_prev rows, B_prev rows), issued together ----
     const int r_raw = prm.path_len[b];
+#pragma unroll 1
     for (int m = u; m < Tp; m += 128) rpath[m] = prm.path[(size_t)b * Tp + m];
     named_bar(3, 128);
     const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
@@ -332,25 +362,28 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     constexpr int kQ = (kHPC + 3) / 4;    // heads per updater warp: uw, uw + 4, uw + 8
     float dv[kQ][2];
     uint32_t xv[kQ][kRStage];
+    // row offsets of the path nodes: dt_prev / x_prev rows (b, node) of the previous tree
+    const size_t row0 = ((size_t)b * Tp + node(lane)) * H + hbeg, row1 = ((size_t)b * Tp + node(lane + 32)) * H + hbeg;
+    size_t rowm[kRStage];
+#pragma unroll
+    for (int m = 0; m < kRStage; ++m) rowm[m] = ((size_t)b * Tp + node(m)) * H + hbeg;
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
         const int hh = uw + 4 * q;
+        const bool hv = hh < nh;
+        dv[q][0] = (hv && lane < rr) ? prm.dt_prev[row0 + hh] : 0.f;
+        dv[q][1] = (hv && lane + 32 < rr) ? prm.dt_prev[row1 + hh] : 0.f;
+        const uint32_t* xp = reinterpret_cast<const uint32_t*>(prm.x_prev) + lane;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int m = lane + 32 * c;
-            dv[q][c] = (hh < nh && m < rr) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] : 0.f;
-        }
-#pragma unroll
-        for (int m = 0; m < kRStage; ++m)
-            xv[q][m] = (hh < nh && m < rs)
-                           ? reinterpret_cast<const uint32_t*>(prm.x_prev + (((size_t)b * Tp + node(m)) * H + hbeg + hh) * kP)[lane]
-                           : 0u;
+        for (int m = 0; m < kRStage; ++m) xv[q][m] = (hv && m < rs) ? xp[(rowm[m] + hh) * (kP / 2)] : 0u;
     }
+#pragma unroll 1
     for (int k = u; k < rs * NS; k += 128) {
         const int m = k / NS, n = k % NS;
         bprev[m * NS + n] = __bfloat162float(prm.b_prev[(((size_t)b * Tp + node(m)) * G + g) * NS + n]);
     }
-    if (uw == 0) {   // root-anchored, increasing, parent-linked (PAPER.md:90 on the accepted path)
+    {   // root-anchored, increasing, parent-linked (PAPER.md:90 on the accepted path); every updater
+        // warp runs the same check (no warp-divergent branch around the vote)
         int ok = rr > 0;
         for (int m = lane; m < rr; m += 32) {
             const int v = rpath[m];
@@ -364,7 +397,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
             if (!good) ok = 0;
         }
         ok = __all_sync(0xffffffffu, ok);
-        if (lane == 0) {
+        if (u == 0) {
             rinfo[0] = ok ? rr : 0;
             rinfo[1] = ok ? 0 : 1;
         }
@@ -372,39 +405,41 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     named_bar(3, 128);
     if (prm.early_replay) pdl_wait();   // global writes (status, committed state) follow the dependency
     if (u == 0 && rinfo[1] && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
-    const int r = rinfo[0];
-    if (r > 0) {
+    // r is read back from shared memory and broadcast, so every branch on it is provably warp-uniform
+    // (no collective fix-up code around the shuffles below)
+    const int r = __shfl_sync(0xffffffffu, rinfo[0], 0);
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-            const int hh = uw + 4 * q;
-            if (hh >= nh) continue;   // warp-uniform
-            const float Ah = prm.A[hbeg + hh];
-            // lam_m = Σ_{q<=m} dt_prev[s_q] A_h: inclusive warp scans over m = lane and lane + 32
-            float a0 = dv[q][0] * Ah, a1 = dv[q][1] * Ah;
+    for (int q = 0; q < kQ; ++q) {
+        const int hh = uw + 4 * q;
+        const bool hv = hh < nh && r > 0;
+        const float Ah = hv ? prm.A[hbeg + hh] : 0.f;
+        // lam_m = Σ_{q<=m} dt_prev[s_q] A_h: inclusive warp scans over m = lane and lane + 32
+        float a0 = dv[q][0] * Ah, a1 = dv[q][1] * Ah;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
-                if (lane >= o) { a0 += t0; a1 += t1; }
-            }
-            a1 += __shfl_sync(0xffffffffu, a0, 31);
-            float last;
-            if (r <= 32) last = __shfl_sync(0xffffffffu, a0, r - 1);
-            else if (r <= 64) last = __shfl_sync(0xffffffffu, a1, r - 33);
-            else {   // paths beyond 64 nodes: the remaining chunks from global memory
-                float carry = __shfl_sync(0xffffffffu, a1, 31);
-                for (int m0 = 64; m0 < r; m0 += 32) {
-                    const int m = m0 + lane;
-                    float a = (m < r) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] * Ah : 0.f;
+        for (int o = 1; o < 32; o <<= 1) {
+            const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
+            if (lane >= o) { a0 += t0; a1 += t1; }
+        }
+        a1 += __shfl_sync(0xffffffffu, a0, 31);
+        const float l32 = __shfl_sync(0xffffffffu, a0, (r - 1) & 31), l64 = __shfl_sync(0xffffffffu, a1, (r - 33) & 31);
+        float last = r <= 32 ? l32 : l64;
+        if (r > 64) {   // paths beyond 64 nodes: the remaining chunks from global memory
+            float carry = __shfl_sync(0xffffffffu, a1, 31);
+#pragma unroll 1
+            for (int m0 = 64; m0 < r; m0 += 32) {
+                const int m = m0 + lane;
+                float a = (hv && m < r) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] * Ah : 0.f;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const float t = __shfl_up_sync(0xffffffffu, a, o);
-                        if (lane >= o) a += t;
-                    }
-                    carry += __shfl_sync(0xffffffffu, a, 31);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xffffffffu, a, o);
+                    if (lane >= o) a += t;
                 }
-                last = carry;
+                carry += __shfl_sync(0xffffffffu, a, 31);
             }
-            const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
+            last = carry;
+        }
+        const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
+        if (hv) {
             if (lane < rs) rcoef[hh * kRStage + lane] = expf(last - a0) * dv[q][0];
             if (lane == 0) {
                 rdec[hh] = expf(last);
@@ -422,7 +457,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     //      (u >> 3) + 16 i: its 16 chunks stay in registers while the path is applied. ----
     const int pc = u & 7;
     constexpr int kAt = NS / 32;
-    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
+    unsigned long long* trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
         mbar_wait(bar_full(s), (k / kSt) & 1);
@@ -441,6 +476,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
                     float4 v = *reinterpret_cast<const float4*>(tile + a * S::kSlotAtom + swz((u >> 3) + 16 * i, pc));
                     hv[i][a] = make_float4(dk * v.x, dk * v.y, dk * v.z, dk * v.w);
                 }
+#pragma unroll 1
             for (int m = 0; m < r; ++m) {
                 const bool st_ = m < kRStage;
                 float4 bb[kAt];
@@ -496,7 +532,7 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
     constexpr int kSt = S::kSt;
     auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };
     auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };
-    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
+    unsigned long long* trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
     const uint64_t pol = policy_evict_first();
     const int H = prm.H;
     if (prm.early_replay) pdl_wait();   // stores follow the dependency wait
@@ -525,9 +561,11 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
-    unsigned long long* trace = prm.trace ? prm.trace + (size_t)blockIdx.x * 128 : nullptr;
+    unsigned long long* trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
     if (trace && threadIdx.x == 0) trace[0] = gtimer();
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // warp index and TMEM base broadcast from lane 0: provably warp-uniform for ptxas, so descriptor and
+    // address arithmetic stays on the uniform datapath (no per-instruction waterfall around tcgen05/TMA)
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
     const int T = prm.T, H = prm.H;
     const int b = blockIdx.x / (prm.G * prm.cpg);
     const int rem = blockIdx.x % (prm.G * prm.cpg);
@@ -571,6 +609,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             mbar_init(bar_accempty(a), 2);
         }
         mbar_init(BAR_DIRE, 2);
+        if (kTrace) mbar_init(bar0 + (S::NBAR - 1) * 8, 1);
         for (int s = 0; s < S::kStX; ++s) mbar_init(bar_xfull(s), 1);
         fence_barrier_init();
     }
@@ -633,7 +672,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         }
         named_bar(1, 128);
     }
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
     const int Tp16 = (T + 15) & ~15;
     const int xbytes = T * 128;
 
@@ -658,6 +697,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     mbar_expect_tx(bar_full(s), 0);
                 } else {
                     mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
+                    if (trace && k < 32) trace[128 + k] = gtimer();   // state load k issued (slot released)
                     mbar_expect_tx(bar_full(s), prm.has_h0 ? S::H0S : 0);
                     if (prm.has_h0)
                         for (int a = 0; a < NS / 32; ++a)
@@ -674,8 +714,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             }
         }
     } else if (warp == 1) {
-        // ================= MMA issuer =================
-        if (lane == 0) {
+        // ================= MMA issuer (whole warp converged, elected lane issues) =================
+        {
             mbar_wait(BAR_TREE, 0);
             tc_fence_after();
             // G = C·Bᵀ (once per tree), kind::f16 bf16, M=128, N=Tp16, K=NS
@@ -684,10 +724,10 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
 #pragma unroll 1
             for (int kk = 0; kk < NS / 16; ++kk) {
                 const uint32_t off = (kk & 3) * 32;
-                mma_f16(tmem + 0, sdesc(sb + S::CB + (kk >> 2) * 2 * kAtom + off, 16, 1024),
+                mma_f16_w(tmem + 0, sdesc(sb + S::CB + (kk >> 2) * 2 * kAtom + off, 16, 1024),
                         sdesc(sb + S::BB + (kk >> 2) * kAtom + off, 16, 1024), id_g, kk > 0);
             }
-            tc_commit(BAR_G);
+            tc_commit_w(BAR_G);
             mbar_wait(BAR_CTF, 0);
             tc_fence_after();
             const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
@@ -705,29 +745,35 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     mbar_wait(bar_full(s + q), ((k + q) / kStages) & 1);
                     if (kReplay) mbar_wait(bar_upd(s + q), ((k + q) / kStages) & 1);   // replayed on chip
                 }
-                if (trace && k < 12) trace[30 + k] = gtimer();
+                if (trace && lane == 0 && k < 12) trace[30 + k] = gtimer();
                 for (int q = 0; q < nq; ++q) mbar_wait(bar_accempty(ac + q), (((k + q) / kAcc) & 1) ^ 1);
                 tc_fence_after();
-                if (trace && k < 9) trace[118 + k] = gtimer();
+                if (trace && lane == 0 && k < 9) trace[118 + k] = gtimer();
                 const uint32_t d0 = tmem + kAccCol0 + 64 * ac;
                 if (prm.has_h0 && !(dbg & 1)) {
                     // Y0 = C·h0ᵀ of both heads in one N = 2 x 64 MMA chain, kind::tf32, A = C from TMEM,
                     // K = NS in steps of 8 (32 B / 8 columns)
-#pragma unroll 1
-                    for (int kk = 0; kk < NS / 8; ++kk) {
-                        const uint32_t off = (kk >> 2) * S::kSlotAtom + (kk & 3) * 32;
-                        mma_tf32_ts(d0, tmem + kCCol + 8 * kk, sdesc(sb + S::slot(s) + off, 16, 1024),
-                                    nq == 2 ? id_y02 : id_y0, kk > 0);
-                    }
+                    // one base descriptor, per-step offsets are compile-time (address field is addr >> 4)
+                    const uint64_t bd = sdesc(sb + S::slot(s), 16, 1024);
+                    const uint32_t idy0 = nq == 2 ? id_y02 : id_y0;
+#pragma unroll
+                    for (int kk = 0; kk < NS / 8; ++kk)
+                        mma_tf32_ts_w(d0, tmem + kCCol + 8 * kk,
+                                    bd + (uint64_t)(((kk >> 2) * S::kSlotAtom + (kk & 3) * 32) >> 4), idy0, kk > 0);
                 }
-                for (int q = 0; q < nq; ++q) tc_commit(bar_empty(s + q));   // state tiles no longer needed
-                if (trace && k < 9) trace[100 + k] = gtimer();
+                for (int q = 0; q < nq; ++q) tc_commit_w(bar_empty(s + q));   // state tiles no longer needed
+                if (trace && lane == 0 && k < 9) trace[100 + k] = gtimer();
+                if (trace && (dbg & 128) && k < 9) {   // debug knob 128: wait for Y0 to complete (timing)
+                    tc_commit_w(bar0 + (S::NBAR - 1) * 8);
+                    mbar_wait(bar0 + (S::NBAR - 1) * 8, (k >> 1) & 1);
+                    if (lane == 0) trace[180 + k] = gtimer();
+                }
                 for (int q = 0; q < nq; ++q) {
                     const int kq = k + q, a = kq & 1;
                     const int sx = kq % S::kStX;
                     mbar_wait(bar_xfull(sx), (kq / S::kStX) & 1);
                     mbar_wait(bar_mfull(a), (kq >> 1) & 1);
-                    if (trace && kq < 9) trace[109 + kq] = gtimer();
+                    if (trace && lane == 0 && kq < 9) trace[109 + kq] = gtimer();
                     tc_fence_after();
                     // Y' = M'·X_h, kind::f16, A K-major (masked weights), B MN-major (x rows j).  Factorised
                     // decay: accumulated onto Y0 (M' carries e^{-Λ_j}, the epilogue e^{Λ_i}); direct decay:
@@ -741,12 +787,20 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                         dy = tmem + kDirCol;
                         acc0 = 0;
                     }
-#pragma unroll 1
-                    for (int kk = 0; kk < ((dbg & 2) ? 0 : Tp16 / 16); ++kk)
-                        mma_f16(dy, sdesc(sb + S::MB + a * kAtom + kk * 32, 16, 1024),
-                                sdesc(sb + S::xslot(sx) + kk * 2048, kAtom, 1024), id_y, (kk > 0) | acc0);
-                    tc_commit(bar_accfull(ac + q));
-                    tc_commit(bar_mempty(a));
+                    const uint64_t ad = sdesc(sb + S::MB + a * kAtom, 16, 1024);
+                    const uint64_t xd = sdesc(sb + S::xslot(sx), kAtom, 1024);
+                    const int nk = (dbg & 2) ? 0 : Tp16 / 16;
+#pragma unroll
+                    for (int kk = 0; kk < kT / 16; ++kk)
+                        if (kk < nk)
+                            mma_f16_w(dy, ad + (uint64_t)(kk * 2), xd + (uint64_t)(kk * 128), id_y, (kk > 0) | acc0);
+                    if (trace && (dbg & 256) && kq < 9) {   // debug knob 256: wait for Y' to complete (timing)
+                        tc_commit_w(bar0 + (S::NBAR - 1) * 8);
+                        mbar_wait(bar0 + (S::NBAR - 1) * 8, kq & 1);
+                        if (lane == 0) trace[190 + kq] = gtimer();
+                    }
+                    tc_commit_w(bar_accfull(ac + q));
+                    tc_commit_w(bar_mempty(a));
                 }
             }
         }
@@ -791,6 +845,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             tmem_st_wait();
             tc_fence_before();
         } else {
+#pragma unroll 1
             for (int k = e; k < S::kStX0 * (Tp16 - T) * 8; k += 64) {
                 const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
                 *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
@@ -933,6 +988,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                 // G is done, so the B tile region holds the last x slots: zero their padded rows, then
                 // request their first tiles
                 const int e2 = tid - kEpi0 - 64;   // 0..63
+#pragma unroll 1
                 for (int q = e2; q < S::kXB * (Tp16 - T) * 8; q += 64) {
                     const int sx = S::kStX0 + q / ((Tp16 - T) * 8), rr = T + (q / 8) % (Tp16 - T), c = q & 7;
                     *reinterpret_cast<uint4*>(sm + S::xslot(sx) + swz(rr, c)) = make_uint4(0, 0, 0, 0);
@@ -945,41 +1001,50 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                         tma_load_2d_ef(sb + S::xslot(k), &tm_x, bar_xfull(k), (hbeg + k) * kP, b * T, policy_evict_first());
                     }
             }
-            for (int k = 0; k < nh; ++k) {
-                const int a = k & 1, ac = k % kAcc;
-                const int h = hbeg + k;
-                mbar_wait(bar_accfull(ac), (k / kAcc) & 1);
-                tc_fence_after();
-                if (trace && leader && k < 12) trace[4 + 2 * k] = gtimer();
-                if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
+            // k = -1 is a dry pass while the first accumulator is still far away: it runs the epilogue code
+            // once on garbage (TMEM columns of accumulator kAcc-1, x slot 0, y staging 1; nothing is stored
+            // or signalled), so head 0 does not pay the instruction-cache misses of its first execution
+            const int kfirst = (trace && (trace[127] & 32)) ? 0 : -1;   // debug knob 32: no dry pass
+            for (int k = kfirst; k < nh; ++k) {
+                const bool dry = k < 0;
+                const int kd = dry ? 0 : k;
+                const int a = dry ? 1 : (k & 1), ac = dry ? kAcc - 1 : k % kAcc;
+                const int h = hbeg + kd;
+                if (!dry) {
+                    mbar_wait(bar_accfull(ac), (k / kAcc) & 1);
+                    tc_fence_after();
+                    if (trace && leader && k < 12) trace[4 + 2 * k] = gtimer();
+                    if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
+                }
+                if (trace && leader && dry) trace[170] = gtimer();
                 named_bar(2, 64);
-                if (trace && leader && k < 6) trace[52 + 2 * k] = gtimer();
+                if (trace && leader && !dry && k < 6) trace[52 + 2 * k] = gtimer();
                 const bool zero_out = *sbad != 0;
-                const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[k];
-                const bool fac = mode[k] != 0;
+                const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[kd];
+                const bool fac = mode[kd] != 0;
                 const bool has0 = prm.has_h0 || fac;    // accumulator written (Y0 and / or Y')
-                const float s0 = (own && !zero_out) ? e0[k * 64 + row] : 0.f;
-                const int sx = k % S::kStX;
+                const float s0 = (own && !zero_out) ? e0[kd * 64 + row] : 0.f;
+                const int sx = kd % S::kStX;
                 const unsigned char* xr = sm + S::xslot(sx);
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
                 const uint32_t tl = tq + kAccCol0 + 64 * ac;
-                uint32_t v0[2][32], v1[2][32];
-                if (has0) tmem_ld32(tl, v0[0]);
-                if (!fac) tmem_ld32(tq + kDirCol, v1[0]);
-                tmem_wait();
-                if (has0) tmem_ld32(tl + 32, v0[1]);
-                if (!fac) tmem_ld32(tq + kDirCol + 32, v1[1]);   // in flight while chunk 0 is computed
-#pragma unroll
+                // two 32-column chunks in a rolled loop (half the code of an unrolled pair: the first pass
+                // through this code is instruction-fetch bound)
+#pragma unroll 1
                 for (int c = 0; c < 2; ++c) {
-                    if (c == 1) tmem_wait();
+                    uint32_t v0[32], v1[32];
+                    if (has0) tmem_ld32(tl + 32 * c, v0);
+                    if (!fac) tmem_ld32(tq + kDirCol + 32 * c, v1);
+                    tmem_wait();
+                    if (trace && leader && !dry && k < 6 && c == 0) trace[160 + k] = gtimer();
                     if (!has0) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) v0[c][q] = 0u;
+                        for (int q = 0; q < 32; ++q) v0[q] = 0u;
                     }
                     if (fac) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) v1[c][q] = 0u;
+                        for (int q = 0; q < 32; ++q) v1[q] = 0u;
                     }
                     if (own) {
 #pragma unroll
@@ -992,16 +1057,17 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             for (int q = 0; q < 4; ++q) {
                                 const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
                                 const int p = 8 * qc + 2 * q;
-                                const float ya = fmaf(s0, __uint_as_float(v0[c][p]), fmaf(Dh, xa, __uint_as_float(v1[c][p])));
-                                const float yb =
-                                    fmaf(s0, __uint_as_float(v0[c][p + 1]), fmaf(Dh, xb, __uint_as_float(v1[c][p + 1])));
+                                const float ya = fmaf(s0, __uint_as_float(v0[p]), fmaf(Dh, xa, __uint_as_float(v1[p])));
+                                const float yb = fmaf(s0, __uint_as_float(v0[p + 1]), fmaf(Dh, xb, __uint_as_float(v1[p + 1])));
                                 o[q] = zero_out ? 0u : pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
                         }
                     }
                 }
-                if (trace && leader && k < 6) trace[53 + 2 * k] = gtimer();
+                if (trace && leader && !dry && k < 6) trace[53 + 2 * k] = gtimer();
+                if (trace && leader && dry) trace[171] = gtimer();
+                if (dry) continue;
                 tc_fence_before();
                 fence_proxy_async();
                 __syncwarp();

@@ -20,7 +20,7 @@ if os.environ.get("NOREPLAY"):   # path_len = 0: replay disabled (state unchange
 ys = [torch.empty_like(l["x"]) for l in layers]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
-buf = torch.zeros((1024, 128), dtype=torch.int64, device="cuda")
+buf = torch.zeros((1024, 256), dtype=torch.int64, device="cuda")
 
 
 def run(l, y):
@@ -71,8 +71,33 @@ for k in range(9):
     names[109 + k] = f"mma_x+m_ready{k}"
     names[118 + k] = f"mma_accempty{k}"
     names[91 + k] = f"built_m{k}"
+for k in range(16):
+    names[128 + k] = f"state_issue{k}"
+for k in range(6):
+    names[52 + 2 * k] = f"epi_bar{k}"
+    names[53 + 2 * k] = f"epi_comp{k}"
+    names[160 + k] = f"epi_tmem{k}"
+names[170] = "epi_dry_start"
+for k in range(9):
+    names[180 + k] = f"y0_done{k}"
+    names[190 + k] = f"yp_done{k}"
+names[171] = "epi_dry_end"
 for c in sorted(names):
     v = rel[:, c]
     v = v[v >= 0]
     if len(v):
         print(f"{names[c]:>12s}: min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
+# per-CTA state-slot cycle: latency = landed (updater sees it) - issued; hold = released (next issue into
+# the slot) - landed
+lat, hold = [], []
+for row in tr:
+    for k in range(4, 9):
+        iss, land = row[128 + k], row[64 + 3 * k]
+        land_prev = row[64 + 3 * (k - 4)]
+        if iss > 0 and land > 0:
+            lat.append((land - iss) / 1000.0)
+        if iss > 0 and land_prev > 0:
+            hold.append((iss - land_prev) / 1000.0)
+if lat:
+    print(f"state load latency (issue->landed, k>=4): med {np.median(lat):.2f} us  p90 {np.percentile(lat, 90):.2f}")
+    print(f"state slot hold (landed->reissued):       med {np.median(hold):.2f} us  p90 {np.percentile(hold, 90):.2f}")
