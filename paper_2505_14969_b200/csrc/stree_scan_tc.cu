@@ -440,9 +440,9 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         }
         const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
         if (hv) {
-            if (lane < rs) rcoef[hh * kRStage + lane] = expf(last - a0) * dv[q][0];
+            if (lane < rs) rcoef[hh * kRStage + lane] = __expf(last - a0) * dv[q][0];
             if (lane == 0) {
-                rdec[hh] = expf(last);
+                rdec[hh] = __expf(last);
                 rlam[2 * hh] = last;
                 rlam[2 * hh + 1] = lst;
             }
@@ -491,7 +491,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
                     const int sm_ = rpath[m];
                     const float dm = prm.dt_prev[((size_t)b * Tp + sm_) * H + hbeg + k];
                     lam_run += dm * Ak;
-                    const float cm = expf(last - lam_run) * dm;
+                    const float cm = __expf(last - lam_run) * dm;
                     const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + 4 * pc;
 #pragma unroll
                     for (int a = 0; a < kAt; ++a)
@@ -540,6 +540,7 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
         const int s = k % kSt;
         mbar_wait(bar_upd(s), (k / kSt) & 1);
         if (((const int*)(sm + S::RINFO))[0] > 0) {   // path length, published before the first bar_upd
+#pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
                 tma_store_2d_ef(tm_h, sb + S::slot(s) + a * S::kSlotAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
             bulk_commit();
@@ -627,6 +628,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         // the state of the first heads is streamed before the dependency wait (caller's promise)
         for (int k = 0; k < n_early; ++k) {
             mbar_add_tx(bar_full(k), S::H0S);
+#pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
                 tma_load_2d(sb + S::slot(k) + a * S::kSlotAtom, &tm_h0, bar_full(k), 32 * a,
                             ((b * H) + hbeg + k) * kP);
@@ -681,6 +683,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         if (lane == 0) {
             const uint64_t pol_ef = policy_evict_first();
             mbar_expect_tx(BAR_TREE, 3 * S::kCbAtoms * xbytes);
+#pragma unroll 1
             for (int a = 0; a < S::kCbAtoms; ++a) {
                 tma_load_2d(sb + S::CB + 2 * a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
                 tma_load_2d(sb + S::CB + (2 * a + 1) * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
@@ -700,6 +703,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     if (trace && k < 32) trace[128 + k] = gtimer();   // state load k issued (slot released)
                     mbar_expect_tx(bar_full(s), prm.has_h0 ? S::H0S : 0);
                     if (prm.has_h0)
+#pragma unroll 1
                         for (int a = 0; a < NS / 32; ++a)
                             tma_load_2d_ef(sb + S::slot(s) + a * S::kSlotAtom, &tm_h0, bar_full(s), 32 * a,
                                            ((b * H) + h) * kP, pol_ef);
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                     // one base descriptor, per-step offsets are compile-time (address field is addr >> 4)
                     const uint64_t bd = sdesc(sb + S::slot(s), 16, 1024);
                     const uint32_t idy0 = nq == 2 ? id_y02 : id_y0;
-#pragma unroll
+#pragma unroll 2
                     for (int kk = 0; kk < NS / 8; ++kk)
                         mma_tf32_ts_w(d0, tmem + kCCol + 8 * kk,
                                     bd + (uint64_t)(((kk >> 2) * S::kSlotAtom + (kk & 3) * 32) >> 4), idy0, kk > 0);
