@@ -425,6 +425,8 @@ def run_stree(args):
         kernels["stree_tree_scan"] = {"us": scan_us, "bytes": sb, "GB/s": scan_gbs, "frac": scan_gbs / hbm_peak,
                                       "impl": {1: "simt", 2: "tcgen05"}.get(kernel)}
         kernels["stree_commit"] = {"us": commit_us, "bytes": cb, "GB/s": commit_gbs, "frac": commit_gbs / hbm_peak,
+                                   "impl": {1: "ring (CUDA cores)", 2: "TMA pipeline"}.get(
+                                       binding.stree_commit_kernel_for(dims, True)),
                                    "mean_path_len": float(plen_host.mean())}
         dominant = "stree_tree_scan" if scan_us >= commit_us else "stree_commit"
         dom_gbs, dom_bytes = (scan_gbs, sb) if dominant == "stree_tree_scan" else (commit_gbs, cb)

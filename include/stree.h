@@ -69,11 +69,13 @@ typedef struct {
     stree_dtype io_dtype; /* dtype of x, B, C and y */
 } stree_dims;
 
-/* Scan kernel selection (stree_set_scan_impl). */
+/* Kernel family selection for stree_tree_scan and stree_commit (stree_set_scan_impl). */
 typedef enum {
-    STREE_SCAN_AUTO = 0,  /* tcgen05 kernel when supported (bf16 io, P==64, N in {64,128}, T<=128), else SIMT */
-    STREE_SCAN_SIMT = 1,  /* generic FP32-FMA kernel (any shape; the fp32 1e-4 path) */
-    STREE_SCAN_TC = 2     /* force the tcgen05 kernel; STREE_ERR_UNSUPPORTED if the shape is not served */
+    STREE_SCAN_AUTO = 0,  /* TMA / tcgen05 pipeline kernels when supported, else the CUDA-core kernels.
+                             scan: bf16 io, P == 64, N in {64,128}, T <= 64;
+                             commit: bf16 io, P == 64, N in {64,128}, T <= 256, h0 given */
+    STREE_SCAN_SIMT = 1,  /* CUDA-core kernels (FP32-FMA scan, ring commit; any shape; the fp32 1e-4 path) */
+    STREE_SCAN_TC = 2     /* force the pipeline kernels; STREE_ERR_UNSUPPORTED if the shape is not served */
 } stree_scan_impl;
 
 /*
@@ -193,6 +195,10 @@ stree_status stree_set_launch_flags(uint32_t flags);
 
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
+
+/* Which kernel stree_commit would launch (has_h0: h0 != NULL): 1 = CUDA-core ring / block kernel,
+ * 2 = the TMA pipeline kernel (replay warps of the tcgen05 scan kernel), 0 = invalid. */
+int32_t stree_commit_kernel_for(const stree_dims* d, int32_t has_h0);
 
 /* Library version string. */
 const char* stree_version(void);

@@ -55,6 +55,7 @@ def lib():
             "stree_set_launch_flags": [ctypes.c_uint32],
             "stree_replay_scan": [vp] * 19,
             "stree_scan_kernel_for": [vp],
+            "stree_commit_kernel_for": [vp, i32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -72,7 +73,7 @@ STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY = 1, 2, 4
 
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
                     "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",
-                    "stree_replay_scan")
+                    "stree_replay_scan", "stree_commit_kernel_for")
 
 
 def status_string(s: int) -> str:
@@ -166,3 +167,7 @@ def stree_set_launch_flags(flags: int):
 
 def stree_scan_kernel_for(dims: stree_dims) -> int:
     return lib().stree_scan_kernel_for(ctypes.byref(dims))
+
+
+def stree_commit_kernel_for(dims: stree_dims, has_h0: bool = True) -> int:
+    return lib().stree_commit_kernel_for(ctypes.byref(dims), int(bool(has_h0)))

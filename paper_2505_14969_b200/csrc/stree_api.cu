@@ -19,6 +19,10 @@ extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*
                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
                                     cudaStream_t);
 extern "C" int stree_tc_supports(const stree_dims*);
+extern "C" int stree_tc_commit_supports(const stree_dims*);
+extern "C" int stree_launch_commit_tc(const stree_dims*, const void*, const float*, const float*, const void*,
+                                      const float*, const int32_t*, const int32_t*, const int32_t*, float*, int32_t*,
+                                      cudaStream_t);
 extern "C" int stree_launch_replay_scan_tc(const stree_dims*, const void*, const float*, const void*, const int32_t*,
                                            const int32_t*, const int32_t*, const stree_dims*, const void*,
                                            const float*, const float*, const void*, const void*, const float*, float*,
@@ -96,6 +100,14 @@ stree_status stree_set_scan_impl(stree_scan_impl impl) {
     return STREE_OK;
 }
 
+int32_t stree_commit_kernel_for(const stree_dims* d, int32_t has_h0) {
+    if (check_dims(d) != STREE_OK) return 0;
+    int impl = g_scan_impl.load();
+    if (impl == STREE_SCAN_SIMT) return 1;
+    if (has_h0 && stree_tc_commit_supports(d)) return 2;
+    return impl == STREE_SCAN_TC ? 0 : 1;
+}
+
 int32_t stree_scan_kernel_for(const stree_dims* d) {
     if (check_dims(d) != STREE_OK) return 0;
     int impl = g_scan_impl.load();
@@ -158,6 +170,13 @@ stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, c
         if (a < b + bytes && b < a + bytes) return STREE_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    const int which = stree_commit_kernel_for(d, h0 != nullptr);
+    if (which == 0) return STREE_ERR_UNSUPPORTED;
+    if (which == 2) {
+        if (!aligned16(x) || !aligned16(Bm) || !aligned16(dt)) return STREE_ERR_ALIGN;
+        return finish(stree_launch_commit_tc(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s),
+                      dev_status, s);
+    }
     return finish(stree_launch_commit(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, s),
                   dev_status, s);
 }

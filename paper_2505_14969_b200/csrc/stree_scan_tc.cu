@@ -308,6 +308,7 @@ struct Params {
     int has_h0;
     int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
     int early_replay;  // STREE_LAUNCH_EARLY_REPLAY: the replay prologue may run before the PDL wait
+    int store_always;  // commit into a distinct h_new: store the state even when the path is invalid
     // replay (fused commit of the previous tree), kReplay only
     int Tp;
     const __nv_bfloat16* x_prev;
@@ -539,7 +540,7 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
         mbar_wait(bar_upd(s), (k / kSt) & 1);
-        if (((const int*)(sm + S::RINFO))[0] > 0) {   // path length, published before the first bar_upd
+        if (((const int*)(sm + S::RINFO))[0] > 0 || prm.store_always) {   // path length, published before bar_upd
 #pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
                 tma_store_2d_ef(tm_h, sb + S::slot(s) + a * S::kSlotAtom, 32 * a, ((b * H) + hbeg + k) * kP, pol);
@@ -552,11 +553,14 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
     bulk_wait_all();
 }
 
-template <int NS, bool kReplay>
-__global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
+// MODE 0: tree scan; 1: replay of the previous tree's accepted path fused with the scan (in place);
+// 2: replay only (stree_commit): warps 0 (state producer), 6-9 (replay) and 10 (stores to tm_y = h_new)
+template <int NS, int MODE>
+__global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
                    const __grid_constant__ CUtensorMap tm_y, const Params prm) {
+    constexpr bool kReplay = MODE >= 1, kScan = MODE <= 1;
     using S = Smem<NS, kReplay>;
     constexpr int kStages = S::kSt;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         mbar_init(BAR_G, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full(s), 1);
-            mbar_init(bar_empty(s), kReplay ? 2 : 1);   // state tile: MMA (Y0) [+ replay store read]
+            mbar_init(bar_empty(s), (kReplay && kScan) ? 2 : 1);   // state tile: MMA (Y0) and / or the store read
             mbar_init(bar_upd(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         for (int s = 0; s < S::kStX; ++s) mbar_init(bar_xfull(s), 1);
         fence_barrier_init();
     }
-    if (warp == 1) {
+    if (kScan && warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     constexpr int kHPW = (kHPC + 3) / 4;      // heads per epilogue warp
     float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
     int* sbad = (int*)(sm + S::BADF);
-    if (tid >= kEpi0 && tid < kEpi0 + 128) {
+    if (kScan && tid >= kEpi0 && tid < kEpi0 + 128) {
         const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
         if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
 #pragma unroll
@@ -674,7 +678,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         }
         named_bar(1, 128);
     }
-    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t tmem = kScan ? __shfl_sync(0xffffffffu, *tmem_slot, 0) : 0u;
     const int Tp16 = (T + 15) & ~15;
     const int xbytes = T * 128;
 
@@ -682,17 +686,19 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
         // ================= TMA producer =================
         if (lane == 0) {
             const uint64_t pol_ef = policy_evict_first();
-            mbar_expect_tx(BAR_TREE, 3 * S::kCbAtoms * xbytes);
-#pragma unroll 1
-            for (int a = 0; a < S::kCbAtoms; ++a) {
-                tma_load_2d(sb + S::CB + 2 * a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
-                tma_load_2d(sb + S::CB + (2 * a + 1) * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
-                tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
-            }
-            // the bulk state stream starts once the tree operands have landed: issued together, the
-            // ~kStages x 40 KB per CTA would queue the small critical-path loads behind it
             const unsigned long long pdbg = trace ? trace[127] : 0ull;   // debug knob 8: no ramp
-            if (!(pdbg & 8)) mbar_wait(BAR_TREE, 0);
+            if (kScan) {
+                mbar_expect_tx(BAR_TREE, 3 * S::kCbAtoms * xbytes);
+#pragma unroll 1
+                for (int a = 0; a < S::kCbAtoms; ++a) {
+                    tma_load_2d(sb + S::CB + 2 * a * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
+                    tma_load_2d(sb + S::CB + (2 * a + 1) * kAtom, &tm_c, BAR_TREE, g * NS + 64 * a, b * T);
+                    tma_load_2d(sb + S::BB + a * kAtom, &tm_b, BAR_TREE, g * NS + 64 * a, b * T);
+                }
+                // the bulk state stream starts once the tree operands have landed: issued together, the
+                // ~kStages x 40 KB per CTA would queue the small critical-path loads behind it
+                if (!(pdbg & 8)) mbar_wait(BAR_TREE, 0);
+            }
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
                 const int h = hbeg + k;
@@ -708,15 +714,17 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
                             tma_load_2d_ef(sb + S::slot(s) + a * S::kSlotAtom, &tm_h0, bar_full(s), 32 * a,
                                            ((b * H) + h) * kP, pol_ef);
                 }
-                if (k < S::kStX0) {   // first x tiles; later ones are requested by the epilogue that frees the slot
+                if (kScan && k < S::kStX0) {   // first x tiles; later ones are requested by the epilogue that frees the slot
                     mbar_expect_tx(bar_xfull(k), xbytes);
                     tma_load_2d_ef(sb + S::xslot(k), &tm_x, bar_xfull(k), h * kP, b * T, pol_ef);
                 }
                 // ramp: the rest of the ring is requested only once head 0 has landed, so every CTA's
                 // first pair is near the front of the DRAM queue instead of behind other CTAs' later stages
-                if ((k == 1 || nh == 1) && !(pdbg & 8)) mbar_wait(bar_full(0), 0);
+                if (kScan && (k == 1 || nh == 1) && !(pdbg & 8)) mbar_wait(bar_full(0), 0);
             }
         }
+    } else if (!kScan && warp <= 5) {
+        // commit only: no tensor-core work, these warps idle
     } else if (warp == 1) {
         // ================= MMA issuer (whole warp converged, elected lane issues) =================
         {
@@ -809,7 +817,8 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
             }
         }
     } else if (kReplay && warp == 10) {
-        if (lane == 0) state_storer<NS, kReplay>(prm, sm, sb, &tm_h0, b, hbeg, nh, bar0);
+        // fused: committed state in place (tm_h0); commit only: into h_new (tm_y)
+        if (lane == 0) state_storer<NS, kReplay>(prm, sm, sb, kScan ? &tm_h0 : &tm_y, b, hbeg, nh, bar0);
     } else if (kReplay && warp >= 6) {
         replay_updater<NS, kReplay>(prm, sm, sb, &tm_h0, b, g, chunk, hbeg, nh, bar0);
     } else {
@@ -1099,7 +1108,7 @@ __global__ void __launch_bounds__(kReplay ? kThreadsReplay : kThreadsScan, 1)
     tc_fence_before();
     __syncthreads();
     if (trace && tid == 0) trace[45] = gtimer();
-    if (warp == 1) {
+    if (kScan && warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
@@ -1171,15 +1180,29 @@ extern "C" int stree_tc_supports(const stree_dims* d) {
 
 namespace {
 
-template <int NS, bool R>
-cudaError_t launch_tc_inst(dim3 grid, size_t smem, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb,
+template <int NS, int MODE>
+cudaError_t launch_tc_inst(dim3 grid, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb,
                            const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& my,
                            const stree::tc::Params& prm) {
     using namespace stree::tc;
-    auto k = scan_tc_kernel<NS, R>;
+    auto k = scan_tc_kernel<NS, MODE>;
+    const size_t smem = Smem<NS, (MODE >= 1)>::TOTAL + 1024;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return stree::launch_k(k, grid, dim3(R ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, prm);
+    return stree::launch_k(k, grid, dim3(MODE ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, prm);
+}
+
+// work split: one tree per CTA, heads of one group in chunks, ~1 wave over the SMs
+void split_heads(int B, int H, int G, int* cpg_out, int* hpc_out) {
+    using namespace stree::tc;
+    const int hpg = H / G;
+    int cpg = num_sms() / (B * G);                  // head chunks per group: at most one wave of CTAs
+    if (cpg < 1) cpg = 1;
+    if (cpg > hpg) cpg = hpg;
+    int hpc = (hpg + cpg - 1) / cpg;
+    if (hpc > kHPC) hpc = kHPC;
+    *cpg_out = (hpg + hpc - 1) / hpc;
+    *hpc_out = hpc;
 }
 
 // shared by the scan-only and the fused replay+scan launches
@@ -1201,14 +1224,8 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     else
         mh = mx;  // unused
     if (!ok) return (int)cudaErrorInvalidValue;
-    // work split: one tree per CTA, heads of one group in chunks, ~1 wave over the SMs
-    const int hpg = H / G;
-    int cpg = num_sms() / (B * G);                  // head chunks per group: at most one wave of CTAs
-    if (cpg < 1) cpg = 1;
-    if (cpg > hpg) cpg = hpg;
-    int hpc = (hpg + cpg - 1) / cpg;
-    if (hpc > kHPC) hpc = kHPC;
-    cpg = (hpg + hpc - 1) / hpc;
+    int cpg, hpc;
+    split_heads(B, H, G, &cpg, &hpc);
     stree::tc::Params prm{};
     if (rp) prm = *rp;
     prm.trace = g_trace;
@@ -1220,11 +1237,11 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (N == 128)
-        e = replay ? launch_tc_inst<128, true>(grid, Smem<128, true>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm)
-                   : launch_tc_inst<128, false>(grid, Smem<128, false>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm);
+        e = replay ? launch_tc_inst<128, 1>(grid, s, mc, mb, mx, mh, my, prm)
+                   : launch_tc_inst<128, 0>(grid, s, mc, mb, mx, mh, my, prm);
     else
-        e = replay ? launch_tc_inst<64, true>(grid, Smem<64, true>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm)
-                   : launch_tc_inst<64, false>(grid, Smem<64, false>::TOTAL + 1024, s, mc, mb, mx, mh, my, prm);
+        e = replay ? launch_tc_inst<64, 1>(grid, s, mc, mb, mx, mh, my, prm)
+                   : launch_tc_inst<64, 0>(grid, s, mc, mb, mx, mh, my, prm);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
@@ -1253,4 +1270,50 @@ extern "C" int stree_launch_replay_scan_tc(const stree_dims* d_prev, const void*
     rp.path = path;
     rp.path_len = path_len;
     return launch_tc(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, s, true, &rp);
+}
+
+// stree_commit on the same pipeline (MODE 2): bf16 activations, P = 64, N in {64, 128}, any T <= 256,
+// h0 given.  h_new may alias h0 (in place) or be a distinct buffer.
+extern "C" int stree_tc_commit_supports(const stree_dims* d) {
+    if (!d) return 0;
+    if (d->io_dtype != STREE_BF16 || d->head_dim != stree::tc::kP) return 0;
+    if (d->d_state != 64 && d->d_state != 128) return 0;
+    if (d->n_nodes < 1 || d->n_nodes > stree::kMaxNodes) return 0;
+    if (d->n_groups < 1 || d->n_heads % d->n_groups) return 0;
+    return 1;
+}
+
+extern "C" int stree_launch_commit_tc(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                      const void* Bm, const float* h0, const int32_t* parent, const int32_t* path,
+                                      const int32_t* path_len, float* h_new, int32_t* dev_status, cudaStream_t s) {
+    using namespace stree::tc;
+    if (!stree_tc_commit_supports(d) || !h0) return (int)cudaErrorNotSupported;
+    const int B = d->batch, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
+    CUtensorMap mh, mo;
+    bool ok = make_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h0, (uint64_t)N, (uint64_t)B * H * P, (uint64_t)N * 4, 32, 64) &&
+              make_map(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h_new, (uint64_t)N, (uint64_t)B * H * P, (uint64_t)N * 4, 32,
+                       64);
+    if (!ok) return (int)cudaErrorInvalidValue;
+    int cpg, hpc;
+    split_heads(B, H, G, &cpg, &hpc);
+    Params prm{};
+    prm.trace = g_trace;
+    prm.B = B; prm.T = d->n_nodes; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc;
+    prm.A = A; prm.dev_status = dev_status;
+    prm.has_h0 = 1;
+    prm.early_state = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
+    prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
+    prm.store_always = h_new != h0;
+    prm.Tp = d->n_nodes;
+    prm.x_prev = (const __nv_bfloat16*)x;
+    prm.dt_prev = dt;
+    prm.b_prev = (const __nv_bfloat16*)Bm;
+    prm.parent_prev = parent;
+    prm.path = path;
+    prm.path_len = path_len;
+    dim3 grid(B * G * cpg);
+    cudaError_t e = N == 128 ? launch_tc_inst<128, 2>(grid, s, mh, mh, mh, mh, mo, prm)
+                             : launch_tc_inst<64, 2>(grid, s, mh, mh, mh, mh, mo, prm);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
 }

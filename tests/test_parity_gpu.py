@@ -267,6 +267,39 @@ def test_commit_inplace_long_chain_and_no_parent():
     assert_h_close(h.cpu().numpy(), ref, TOL_F32)
 
 
+@pytest.mark.parametrize("shape", [(16, 64, 80, 64, 128, 1), (3, 37, 24, 64, 64, 2), (2, 200, 12, 64, 128, 3),
+                                   (1, 1, 3, 64, 128, 1)])
+def test_commit_pipeline_kernel(shape):
+    """stree_commit on the TMA pipeline (replay warps of the tcgen05 kernel): oracle parity, equality with
+    the CUDA-core ring kernel, distinct and in-place outputs."""
+    B, T, H, P, N, G = shape
+    rng = np.random.default_rng(T * 13 + H)
+    par = np.stack([trees.random_recursive(T, 4, rng) for _ in range(B)])
+    prob = inputs.make_problem(inputs.Dims(B, T, H, P, N, G, "bf16"), par, seed=T + N)
+    tok, vt = inputs.make_accept_inputs(par, seed=T + 1, p_match=0.9)
+    rp, rl, _, _ = oracle.accept(tok, par, vt)
+    d = binding.stree_dims(B, T, H, P, N, G, 1)
+    assert binding.stree_commit_kernel_for(d, True) == 2
+    assert binding.stree_commit_kernel_for(d, False) == 1
+    t = api.upload(prob)
+    path, plen = torch.from_numpy(rp).cuda(), torch.from_numpy(rl).cuda()
+    st = dev_status()
+    hn = api.commit(t, path, plen, dev_status=st)
+    ref, rst = oracle.commit_problem(prob, rp, rl)
+    assert st.item() == 0 and not rst.any()
+    assert_h_close(hn.cpu().numpy(), ref, TOL_F32)
+    binding.stree_set_scan_impl(binding.STREE_SCAN_SIMT)
+    try:
+        hs = api.commit(t, path, plen)
+    finally:
+        binding.stree_set_scan_impl(binding.STREE_SCAN_AUTO)
+    assert_h_close(hn.cpu().numpy(), hs.cpu().numpy(), 1e-5)
+    h = t["h0"].clone()
+    t2 = dict(t, h0=h)
+    api.commit(t2, path, plen, h_new=h)
+    assert torch.equal(h, hn)
+
+
 def test_commit_invalid_paths():
     prob = inputs.config_problem("c2")
     T = prob.dims.n_nodes
