@@ -37,8 +37,9 @@ namespace tc {
 constexpr int kT = 64;          // max nodes per tree served
 constexpr int kP = 64;          // head dim
 constexpr int kHPC = 10;        // max heads per CTA
-constexpr int kThreadsScan = 192;     // warps 0 TMA, 1 MMA, 2-3 builders, 4-5 epilogue
-constexpr int kThreadsReplay = 352;   // + warps 6-9 replay updaters, warp 10 committed-state stores
+constexpr int kThreadsScan = 320;     // warps 0 TMA, 1 MMA, 2-3 + 6-7 builders, 4-5 + 8-9 epilogue
+constexpr int kThreadsReplay = 352;   // warps 0-5 as the scan's first six, 6-9 replay updaters, 10 state stores
+constexpr int kUpd0 = 192;            // first replay-updater thread (warp 6)
 constexpr int kTraceWords = 256;   // debug trace: u64 stamps per CTA (stree_debug_tc_trace)
 #ifdef STREE_TRACE
 constexpr bool kTrace = true;      // timeline instrumentation compiled in (STREE_TRACE=1 builds, tools/trace_*.py)
@@ -338,7 +339,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };  // state tile free
     auto bar_upd = [&](int s) { return bar0 + S::BAR3 + 8 * s; };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = tid - kThreadsScan;     // 0..127
+    const int u = tid - kUpd0;            // 0..127
     const int uw = warp - 6;              // 0..3
     const int H = prm.H, Tp = prm.Tp, G = prm.G;
     int* rpath = (int*)(sm + S::RPATH);
@@ -561,6 +562,12 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
                    const __grid_constant__ CUtensorMap tm_y, const Params prm) {
     constexpr bool kReplay = MODE >= 1, kScan = MODE <= 1;
+    // scan only: 8 math warps, two per TMEM lane quadrant, each pair splitting the columns of its rows
+    // (builders: j halves of M'; epilogue: p halves of y).  With replay: 4 (warps 6-10 replay / store).
+    constexpr bool kSplit = !kReplay;
+    constexpr int kMathW = kSplit ? 8 : 4;
+    constexpr int kMath = 32 * kMathW;   // math threads (warps 2 .. 2 + kMathW)
+    constexpr int kEpiT = kMath / 2;     // epilogue threads
     using S = Smem<NS, kReplay>;
     constexpr int kStages = S::kSt;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     // ---- setup that touches no argument memory (overlaps the previous grid under PDL) ----
     if (tid == 0) {
         mbar_init(BAR_TREE, 1);
-        mbar_init(BAR_CTF, 128);
+        mbar_init(BAR_CTF, kMath);
         mbar_init(BAR_G, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full(s), 1);
@@ -606,14 +613,14 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             mbar_init(bar_upd(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_mfull(a), 2);
+            mbar_init(bar_mfull(a), kMathW / 2);
             mbar_init(bar_mempty(a), 1);
         }
         for (int a = 0; a < kAcc; ++a) {
             mbar_init(bar_accfull(a), 1);
-            mbar_init(bar_accempty(a), 2);
+            mbar_init(bar_accempty(a), kMathW / 2);
         }
-        mbar_init(BAR_DIRE, 2);
+        mbar_init(BAR_DIRE, kMathW / 2);
         if (kTrace) mbar_init(bar0 + (S::NBAR - 1) * 8, 1);
         for (int s = 0; s < S::kStX; ++s) mbar_init(bar_xfull(s), 1);
         fence_barrier_init();
@@ -645,15 +652,15 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
     //      The producer issues the tree operands right after the wait; tree validation runs in the
     //      epilogue warps (an invalid tree yields y = 0), so nothing waits on it ----
-    constexpr int kHPW = (kHPC + 3) / 4;      // heads per epilogue warp
+    constexpr int kHPW = (kHPC + kMathW - 1) / kMathW;   // heads per math warp
     float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
     int* sbad = (int*)(sm + S::BADF);
-    if (kScan && tid >= kEpi0 && tid < kEpi0 + 128) {
+    if (kScan && tid >= kEpi0 && tid < kEpi0 + kMath) {
         const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
         if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
 #pragma unroll
         for (int q = 0; q < kHPW; ++q) {
-            const int hh = ew + 4 * q;
+            const int hh = ew + kMathW * q;
             const bool hv = hh < nh;
             a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
             d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
@@ -664,19 +671,19 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             }
         }
         if (e == 0) *sbad = 0;
-        named_bar(1, 128);
+        named_bar(1, kMath);
         if (e < T) {   // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i
             const int p = sp[e];
             const int code = (e == 0) ? (p != -1 ? 1 : 0) : ((p < 0 || p >= e) ? 2 : 0);
             if (code) atomicMax(sbad, code == 1 ? 2 : 1);   // root error takes precedence
         }
-        named_bar(1, 128);
+        named_bar(1, kMath);
         if (*sbad) {
             // invalid tree: make the pointer chains harmless; the output stage writes zeros
             if (e < T) sp[e] = (e == 0) ? -1 : 0;
             if (e == 0 && chunk == 0 && g == 0) report(prm.dev_status, *sbad == 2 ? 1 : 2);
         }
-        named_bar(1, 128);
+        named_bar(1, kMath);
     }
     const uint32_t tmem = kScan ? __shfl_sync(0xffffffffu, *tmem_slot, 0) : 0u;
     const int Tp16 = (T + 15) & ~15;
@@ -822,10 +829,11 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     } else if (kReplay && warp >= 6) {
         replay_updater<NS, kReplay>(prm, sm, sb, &tm_h0, b, g, chunk, hbeg, nh, bar0);
     } else {
-        // ================= epilogue / math warps (128 threads) =================
+        // ================= epilogue / math warps (kMath threads) =================
         const int e = tid - kEpi0;
         const int quad = warp & 3;           // TMEM lane quadrant of this warp
         const int row = quad * 32 + lane;    // tree node owned in TMEM-based work
+        const int half = kSplit ? ((warp - 2) >> 2) : 0;   // column half of a split warp pair
         uint64_t* rows = (uint64_t*)(sm + S::ROWS);
         float* lam = (float*)(sm + S::LAM);
         float* cj = (float*)(sm + S::CJ);
@@ -838,8 +846,10 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
         if (quad < 2) {
             // C row (bf16, swizzled TMA tile) -> fp32 -> TMEM lane = row, columns [kCCol, kCCol + NS)
             const int i = row;
+            constexpr int kC32 = NS / 32 / (kSplit ? 2 : 1);
 #pragma unroll
-            for (int c32 = 0; c32 < NS / 32; ++c32) {
+            for (int cq = 0; cq < kC32; ++cq) {
+                const int c32 = half * kC32 + cq;
                 uint32_t f[32];
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
@@ -858,8 +868,9 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             tmem_st_wait();
             tc_fence_before();
         } else {
+            const int zi = (quad - 2) * 32 + lane + half * 64;   // 0 .. kMath/2 - 1
 #pragma unroll 1
-            for (int k = e; k < S::kStX0 * (Tp16 - T) * 8; k += 64) {
+            for (int k = zi; k < S::kStX0 * (Tp16 - T) * 8; k += kMath / 2) {
                 const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
                 *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
             }
@@ -921,7 +932,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
         // ---- per-head decay mode and coefficients (warp-local) ----
 #pragma unroll
         for (int q = 0; q < kHPW; ++q) {
-            const int hh = ew + 4 * q;
+            const int hh = ew + kMathW * q;
             if (hh < nh) {   // warp-uniform
                 float mn = fminf(lm[q][0], lm[q][1]);
 #pragma unroll
@@ -943,17 +954,17 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                 }
             }
         }
-        named_bar(1, 128);
+        named_bar(1, kMath);
         if (trace && e == 0) trace[50] = gtimer();
         // ---- builder warps 2,3 (TMEM lanes 64..127 hold a copy of G) build the masked weights of head
         //      k+1 while warps 4,5 (TMEM lanes 0..63) run the epilogue of head k ----
         mbar_wait(BAR_G, 0);
         tc_fence_after();
         if (trace && e == 0) trace[51] = gtimer();
-        const bool builder = (warp == 2 || warp == 3);
+        const bool builder = quad >= 2;
         if (trace && e == 0) trace[3] = gtimer();
         if (builder) {
-            const int brow = (warp - 2) * 32 + lane;
+            const int brow = (quad - 2) * 32 + lane;
             const bool bown = brow < T;
             const uint64_t mybits = bown ? rows[brow] : 0ull;
             const uint32_t gl = tmem + ((uint32_t)(quad * 32) << 16);   // G row brow, columns 0..63
@@ -968,8 +979,10 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                 const bool f = mode[k] != 0;
                 const float li = bown ? lk[brow] : 0.f;
                 unsigned char* mrow = sm + S::MB + a * kAtom;
+                // split builders: half 0 takes columns j < 32, half 1 the rest
+                const int c16b = kSplit ? 2 * half : 0, c16e = kSplit ? min(Tp16 / 16, 2 * half + 2) : Tp16 / 16;
 #pragma unroll 1
-                for (int c16 = 0; c16 < Tp16 / 16; ++c16) {
+                for (int c16 = c16b; c16 < c16e; ++c16) {
                     float g16[16];
                     tmem_ld16(gl + 16 * c16, g16);
                     uint32_t o[8];
@@ -1000,14 +1013,14 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             if (S::kXB > 0 && nh > S::kStX0) {
                 // G is done, so the B tile region holds the last x slots: zero their padded rows, then
                 // request their first tiles
-                const int e2 = tid - kEpi0 - 64;   // 0..63
+                const int e2 = quad * 32 + lane + half * 64;   // 0 .. kEpiT - 1
 #pragma unroll 1
-                for (int q = e2; q < S::kXB * (Tp16 - T) * 8; q += 64) {
+                for (int q = e2; q < S::kXB * (Tp16 - T) * 8; q += kEpiT) {
                     const int sx = S::kStX0 + q / ((Tp16 - T) * 8), rr = T + (q / 8) % (Tp16 - T), c = q & 7;
                     *reinterpret_cast<uint4*>(sm + S::xslot(sx) + swz(rr, c)) = make_uint4(0, 0, 0, 0);
                 }
                 fence_proxy_async();
-                named_bar(2, 64);
+                named_bar(2, kEpiT);
                 if (leader)
                     for (int k = S::kStX0; k < S::kStX && k < nh; ++k) {
                         mbar_expect_tx(bar_xfull(k), xbytes);
@@ -1030,7 +1043,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                     if (leader) bulk_wait_read1();      // y staging [a] free (store of head k-2 has read it)
                 }
                 if (trace && leader && dry) trace[170] = gtimer();
-                named_bar(2, 64);
+                named_bar(2, kEpiT);
                 if (trace && leader && !dry && k < 6) trace[52 + 2 * k] = gtimer();
                 const bool zero_out = *sbad != 0;
                 const float Dh = zero_out ? 0.f : ((const float*)(sm + S::DS))[kd];
@@ -1042,22 +1055,27 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                 unsigned char* yr = sm + S::YS + a * kAtom;
                 const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
                 const uint32_t tl = tq + kAccCol0 + 64 * ac;
-                // two 32-column chunks in a rolled loop (half the code of an unrolled pair: the first pass
-                // through this code is instruction-fetch bound)
-#pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t v0[32], v1[32];
-                    if (has0) tmem_ld32(tl + 32 * c, v0);
-                    if (!fac) tmem_ld32(tq + kDirCol + 32 * c, v1);
-                    tmem_wait();
-                    if (trace && leader && !dry && k < 6 && c == 0) trace[160 + k] = gtimer();
+                // the warp's 32-column chunks (both, or its half when split) requested up front, then computed
+                constexpr int kNC = kSplit ? 1 : 2;
+                const int cb = kSplit ? half : 0;
+                uint32_t v0[kNC][32], v1[kNC][32];
+#pragma unroll
+                for (int cc = 0; cc < kNC; ++cc) {
+                    if (has0) tmem_ld32(tl + 32 * (cb + cc), v0[cc]);
+                    if (!fac) tmem_ld32(tq + kDirCol + 32 * (cb + cc), v1[cc]);
+                }
+                tmem_wait();
+                if (trace && leader && !dry && k < 6) trace[160 + k] = gtimer();
+#pragma unroll
+                for (int cc = 0; cc < kNC; ++cc) {
+                    const int c = cb + cc;
                     if (!has0) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) v0[q] = 0u;
+                        for (int q = 0; q < 32; ++q) v0[cc][q] = 0u;
                     }
                     if (fac) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) v1[q] = 0u;
+                        for (int q = 0; q < 32; ++q) v1[cc][q] = 0u;
                     }
                     if (own) {
 #pragma unroll
@@ -1070,8 +1088,9 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                             for (int q = 0; q < 4; ++q) {
                                 const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
                                 const int p = 8 * qc + 2 * q;
-                                const float ya = fmaf(s0, __uint_as_float(v0[p]), fmaf(Dh, xa, __uint_as_float(v1[p])));
-                                const float yb = fmaf(s0, __uint_as_float(v0[p + 1]), fmaf(Dh, xb, __uint_as_float(v1[p + 1])));
+                                const float ya = fmaf(s0, __uint_as_float(v0[cc][p]), fmaf(Dh, xa, __uint_as_float(v1[cc][p])));
+                                const float yb =
+                                    fmaf(s0, __uint_as_float(v0[cc][p + 1]), fmaf(Dh, xb, __uint_as_float(v1[cc][p + 1])));
                                 o[q] = zero_out ? 0u : pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
@@ -1088,7 +1107,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                     mbar_arrive(bar_accempty(ac));
                     if (!fac) mbar_arrive(BAR_DIRE);
                 }
-                named_bar(2, 64);
+                named_bar(2, kEpiT);
                 if (leader) {
                     tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
                     bulk_commit();

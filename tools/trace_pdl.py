@@ -18,7 +18,7 @@ layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BAS
 ys = [torch.empty_like(l["x"]) for l in layers]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
-bufs = [torch.zeros((1024, 128), dtype=torch.int64, device="cuda") for _ in range(4)]
+bufs = [torch.zeros((1024, 256), dtype=torch.int64, device="cuda") for _ in range(4)]
 for _ in range(2):
     for l, y in zip(layers, ys):
         api.tree_scan(l, y=y)

@@ -24,7 +24,7 @@ layers = [api.upload(inputs.make_problem(prob.dims, prob.parent, seed=inputs.BAS
 t = layers[-1]
 L = binding.lib()
 L.stree_debug_tc_trace.argtypes = [ctypes.c_void_p]
-buf = torch.zeros((1024, 128), dtype=torch.int64, device="cuda")
+buf = torch.zeros((1024, 256), dtype=torch.int64, device="cuda")
 ys = [torch.empty_like(l["x"]) for l in layers]
 for _ in range(3):
     for l, y in zip(layers, ys):
@@ -55,6 +55,15 @@ for k in range(12):
     names[4 + 2 * k] = f"acc{k}"
     names[5 + 2 * k] = f"out{k}"
     names[30 + k] = f"mma_full{k}"
+for k in range(16):
+    names[128 + k] = f"state_issue{k}"
+for k in range(9):
+    names[100 + k] = f"mma_y0issued{k}"
+    names[109 + k] = f"mma_x+m_ready{k}"
+    names[118 + k] = f"mma_accempty{k}"
+    names[91 + k] = f"built_m{k}"
+names[170] = "epi_dry_start"
+names[171] = "epi_dry_end"
 for k in range(6):
     names[52 + 2 * k] = f"epi_go{k}"
     names[53 + 2 * k] = f"epi_done{k}"
