@@ -479,16 +479,28 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
         (hp.numel() + htok.numel() + hvt.numel()) * 4
     d2h = sum(o.numel() * 4 for o in out)
 
+    # host->device copies run on their own stream, layer by layer, so layer l's kernel overlaps the copy
+    # of layer l+1 (PCIe bound: the step time is ~ the copy time of the whole step's inputs)
+    cstream = torch.cuda.Stream(device=dev)
+    evs = [torch.cuda.Event() for _ in range(len(layers) + 1)]
+
     def step():
-        with torch.cuda.stream(stream):
+        cstream.wait_stream(stream)   # previous step's kernels are done with the buffers
+        with torch.cuda.stream(cstream):
             parent.copy_(hp, non_blocking=True)
             tok_d.copy_(htok, non_blocking=True)
             vt_d.copy_(hvt, non_blocking=True)
-            binding.stree_build_mask(parent, torch.empty((d.batch, d.n_nodes, (d.n_nodes + 31) // 32),
-                                                         dtype=torch.int32, device=dev), None, status)
-            for t, hh in zip(layers, host):
+            evs[-1].record(cstream)
+            for t, hh, ev in zip(layers, host, evs):
                 for k, v in hh.items():
                     t[k].copy_(v, non_blocking=True)
+                ev.record(cstream)
+        with torch.cuda.stream(stream):
+            stream.wait_event(evs[-1])
+            binding.stree_build_mask(parent, torch.empty((d.batch, d.n_nodes, (d.n_nodes + 31) // 32),
+                                                         dtype=torch.int32, device=dev), None, status)
+            for t, ev in zip(layers, evs):
+                stream.wait_event(ev)
                 if fused:
                     binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
                                               t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status,
