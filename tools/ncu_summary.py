@@ -23,6 +23,7 @@ def launches(path):
 
 API = {"scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "stree_replay_scan",
        "scan_tc_kernel<128, 0>": "stree_tree_scan", "scan_tc_kernel<64, 0>": "stree_tree_scan",
+       "scan_tc_kernel<128, 2>": "stree_commit", "scan_tc_kernel<64, 2>": "stree_commit",
        "commit_ring_kernel": "stree_commit", "commit_block_kernel": "stree_commit",
        "build_mask_kernel": "stree_build_mask", "accept_kernel": "stree_accept"}
 
@@ -36,10 +37,22 @@ def api_name(k):
     return k
 
 
+traffic = {}
+nf = os.path.join(out, "launches_nofuse.csv")
+if os.path.exists(nf):
+    print("== launch list, unfused order (bench.py --no-fuse) ==")
+    pn = launches(nf)
+    tn = sum(sum(m["gpu__time_duration.sum"]) for m in pn.values())
+    for k, m in sorted(pn.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
+        t = m["gpu__time_duration.sum"]
+        rd = sum(m["dram__bytes_read.sum"]) / len(t)
+        wr = sum(m["dram__bytes_write.sum"]) / len(t)
+        print(f"{k[:60]:60s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  share={sum(t) / tn * 100:5.1f}%  "
+              f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB")
+        traffic.setdefault(api_name(k), rd + wr)
 print("== launch list (ncu --cache-control none, serialised): per-kernel mean over launches ==")
 per = launches(os.path.join(out, "launches.csv"))
 tot = sum(sum(m["gpu__time_duration.sum"]) for m in per.values())
-traffic = {}
 for k, m in sorted(per.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
     t = m["gpu__time_duration.sum"]
     rd = sum(m["dram__bytes_read.sum"]) / len(t)

@@ -11,11 +11,16 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --cache-control none -k regex:'scan_tc|scan_simt|commit_|build_mask|accept_' -c 400 \
     --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
     > $OUT/ncu_launches.log 2>&1
+# the unfused order too (scan-only and commit-only kernels)
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --cache-control none -k regex:'scan_tc|scan_simt|commit_|build_mask|accept_' -c 400 \
+    --csv --log-file $OUT/launches_nofuse.csv python bench.py --steps 2 --warmup 1 --no-fuse --no-e2e \
+    --no-cpu-baseline > $OUT/ncu_launches_nofuse.log 2>&1
 ncu --set full --clock-control none --cache-control none --import-source on -k regex:scan_tc_kernel -s 8 -c 2 \
     -o $OUT/prof_fused python tools/prof_kernels.py --fused > $OUT/ncu_fused.log 2>&1
-ncu --set full --clock-control none --cache-control none --import-source on -k regex:scan_tc_kernel -s 8 -c 1 \
-    -o $OUT/prof_scan python tools/prof_kernels.py > $OUT/ncu_scan.log 2>&1
-ncu --set full --clock-control none --cache-control none --import-source on -k regex:commit_ring -s 8 -c 1 \
-    -o $OUT/prof_commit python tools/prof_kernels.py > $OUT/ncu_commit.log 2>&1
+ncu --set full --clock-control none --cache-control none --import-source on --kernel-name-base demangled \
+    -k regex:'scan_tc_kernel.*\)0>' -s 8 -c 1 -o $OUT/prof_scan python tools/prof_kernels.py > $OUT/ncu_scan.log 2>&1
+ncu --set full --clock-control none --cache-control none --import-source on --kernel-name-base demangled \
+    -k regex:'scan_tc_kernel.*\)2>' -s 8 -c 1 -o $OUT/prof_commit python tools/prof_kernels.py > $OUT/ncu_commit.log 2>&1
 python tools/ncu_summary.py $OUT > $OUT/profile_summary.txt 2>&1
 cat $OUT/profile_summary.txt
