@@ -47,8 +47,10 @@ def _load():
         lib.oracle_accept.argtypes = [P, P, P, i, i, P, P, P, P]
         lib.oracle_commit.argtypes = [i, i, i, i, i, i, P, P, P, P, P, P, P, P, P, P]
         lib.oracle_num_threads.argtypes = []
+        lib.oracle_tree_conv.argtypes = [i, i, i, i, P, P, P, P, P, i, P, P]
+        lib.oracle_conv_commit.argtypes = [i, i, i, i, P, P, P, P, P, P, P]
         for f in (lib.oracle_build_mask, lib.oracle_tree_scan, lib.oracle_accept,
-                  lib.oracle_commit, lib.oracle_num_threads):
+                  lib.oracle_commit, lib.oracle_num_threads, lib.oracle_tree_conv, lib.oracle_conv_commit):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -135,3 +137,34 @@ def scan_problem(prob):
 def commit_problem(prob, path, path_len, use_parent=True):
     return commit(prob.io_as_f32("x"), prob.dt, prob.A, prob.io_as_f32("Bm"), prob.h0, path, path_len,
                   parent=prob.parent if use_parent else None, n_groups=prob.dims.n_groups)
+
+
+def tree_conv(u, weight, bias, state, parent, act=True):
+    """Tree-causal depthwise conv1d (stree_oracle.c, reading R-conv).
+    u [B][T][C], weight [C][W], bias [C] or None, state [B][W-1][C] or None, parent [B][T]
+    -> (out fp64 [B][T][C], status [B])."""
+    u, weight = _f64(u), _f64(weight)
+    bias = None if bias is None else _f64(bias)
+    state = None if state is None else _f64(state)
+    parent = _i32(parent)
+    B, T, C = u.shape
+    W = weight.shape[1]
+    out = np.zeros((B, T, C), np.float64)
+    st = np.zeros(B, np.int32)
+    _load().oracle_tree_conv(B, T, C, W, _p(u), _p(weight), _p(bias), _p(state), _p(parent), int(bool(act)),
+                             _p(out), _p(st))
+    return out, st
+
+
+def conv_commit(u, state, path, path_len, W, parent=None):
+    """Conv-state commit: last W-1 inputs of state ++ u[path] -> (state_new fp64 [B][W-1][C], status [B])."""
+    u = _f64(u)
+    state = None if state is None else _f64(state)
+    path, path_len = _i32(path), _i32(path_len)
+    parent = None if parent is None else _i32(parent)
+    B, T, C = u.shape
+    out = np.zeros((B, W - 1, C), np.float64)
+    st = np.zeros(B, np.int32)
+    _load().oracle_conv_commit(B, T, C, W, _p(u), _p(state), _p(parent), _p(path), _p(path_len), _p(out), _p(st))
+    return out, st
+

@@ -21,6 +21,10 @@
  *   commit: activation replay (Alg. 1): re-run the same
  *           recurrence along the accepted path from h0; h_new = state after the
  *           last accepted node.
+ *   conv:   tree-causal depthwise conv1d (the paper is silent,
+ *           DESIGN.md reading R-conv): Mamba-2's causal conv of width W applied along
+ *           every root-to-node path, the committed conv state prepended; conv commit
+ *           keeps the last W-1 inputs of (state ++ accepted path).
  *
  * Everything is double precision; bf16 inputs are widened exactly by the
  * Python wrapper.  Parallelism: OpenMP over independent (tree, head) pairs
@@ -217,3 +221,78 @@ int oracle_commit(int B, int T, int H, int P, int N, int G,
     }
     return 0;
 }
+
+/*
+ * Tree-causal depthwise conv1d (reading R-conv).  For node i with
+ * root-to-i path s_i (time order) and the committed conv state (the last W-1
+ * inputs before the root, oldest first):
+ *   seq_i = state[0..W-2] ++ u[s_i]
+ *   out[i][c] = act( bias[c] + sum_{w=0}^{W-1} weight[c][w] * seq_i[len(seq_i)-W+w][c] )
+ * i.e. the ordinary causal conv1d of Mamba-2 (weight[c][W-1] multiplies the current
+ * input) run on the path that leads to i.  act = SiLU(z) = z / (1 + e^-z) if act != 0.
+ * state may be NULL (zeros), bias may be NULL (zeros).  Trees failing PAPER.md:90
+ * get status 1/2 and out = 0.
+ */
+int oracle_tree_conv(int B, int T, int C, int W, const double *u, const double *weight, const double *bias,
+                     const double *state, const int32_t *parent, int act, double *out, int32_t *status) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int b = 0; b < B; ++b) {
+        const int32_t *par = parent + (size_t)b * T;
+        int st = check_tree(par, T);
+        status[b] = st;
+        double *ob = out + (size_t)b * T * C;
+        if (st) {
+            memset(ob, 0, sizeof(double) * (size_t)T * C);
+            continue;
+        }
+        int *path = (int *)malloc(sizeof(int) * (size_t)T);
+        double *seq = (double *)malloc(sizeof(double) * (size_t)(T + W));
+        for (int i = 0; i < T; ++i) {
+            int len = path_to(par, i, path, T);
+            for (int c = 0; c < C; ++c) {
+                int n = 0;
+                for (int j = 0; j < W - 1; ++j)
+                    seq[n++] = state ? state[((size_t)b * (W - 1) + j) * C + c] : 0.0;
+                for (int k = 0; k < len; ++k) seq[n++] = u[((size_t)b * T + path[k]) * C + c];
+                double z = bias ? bias[c] : 0.0;
+                for (int w = 0; w < W; ++w) z += weight[(size_t)c * W + w] * seq[n - W + w];
+                ob[(size_t)i * C + c] = act ? z / (1.0 + exp(-z)) : z;
+            }
+        }
+        free(path);
+        free(seq);
+    }
+    return 0;
+}
+
+/*
+ * Conv-state commit along the accepted path: the new state is the last W-1
+ * entries of state ++ u[path[0..r-1]] (oldest first).  Path checks as in
+ * oracle_commit; an invalid path leaves the state unchanged (status 3).
+ */
+int oracle_conv_commit(int B, int T, int C, int W, const double *u, const double *state,
+                       const int32_t *parent, const int32_t *path, const int32_t *path_len,
+                       double *state_new, int32_t *status) {
+    for (int b = 0; b < B; ++b) {
+        const int32_t *pa = path + (size_t)b * T;
+        int r = path_len[b], st = 0;
+        if (r < 1 || r > T || pa[0] != 0) st = 3;
+        for (int k = 1; !st && k < r; ++k) {
+            if (pa[k] <= pa[k - 1] || pa[k] >= T) st = 3;
+            else if (parent && parent[(size_t)b * T + pa[k]] != pa[k - 1]) st = 3;
+        }
+        status[b] = st;
+        const int L = (W - 1) + (st ? 0 : r);   /* length of state ++ path */
+        for (int j = 0; j < W - 1; ++j) {
+            int q = L - (W - 1) + j;               /* index into state ++ path */
+            for (int c = 0; c < C; ++c) {
+                double v;
+                if (q < W - 1) v = state ? state[((size_t)b * (W - 1) + q) * C + c] : 0.0;
+                else v = u[((size_t)b * T + pa[q - (W - 1)]) * C + c];
+                state_new[((size_t)b * (W - 1) + j) * C + c] = v;
+            }
+        }
+    }
+    return 0;
+}
+

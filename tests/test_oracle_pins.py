@@ -410,3 +410,132 @@ def test_graft_invariant():
         assert st[0] == 0
         y2, _ = oracle.tree_scan(s2(x), s2(dt), A, s2(Bm), s2(Cm), D, hk, p2[None])
         np.testing.assert_allclose(y2[0], yg[0, T1:], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Tree-causal depthwise conv1d (reading R-conv)
+# Pins: the chain reduces to the library causal conv1d (torch CPU, grouped conv,
+# state as left context); every node equals the library conv run on its own
+# root-to-node path; W = 1 is pointwise; the commit is list slicing.
+# ---------------------------------------------------------------------------
+def _torch_causal_conv(seq, weight, bias, act):
+    """Library reference: depthwise causal conv1d over seq [L][C] (no padding: seq already holds the
+    left context), torch.nn.functional.conv1d on CPU in float64; returns [L - W + 1][C]."""
+    import torch
+    C, W = weight.shape
+    x = torch.from_numpy(np.ascontiguousarray(seq.T[None]))                 # [1][C][L]
+    w = torch.from_numpy(np.ascontiguousarray(weight[:, None, :]))          # [C][1][W]
+    b = None if bias is None else torch.from_numpy(bias)
+    z = torch.nn.functional.conv1d(x, w, b, groups=C)[0].T                  # [L-W+1][C]
+    if act:
+        z = torch.nn.functional.silu(z)
+    return z.numpy()
+
+
+def _conv_inputs(B, T, C, W, seed):
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal((B, T, C))
+    weight = rng.standard_normal((C, W)) * 0.5
+    bias = rng.standard_normal(C) * 0.1
+    state = rng.standard_normal((B, W - 1, C))
+    return u, weight, bias, state
+
+
+@pytest.mark.parametrize("W,act", [(4, True), (4, False), (2, True), (3, True)])
+def test_conv_chain_equals_library_causal_conv(W, act):
+    B, T, C = 2, 23, 5
+    u, weight, bias, state = _conv_inputs(B, T, C, W, seed=W)
+    par = np.stack([trees.chain(T)] * B)
+    out, st = oracle.tree_conv(u, weight, bias, state, par, act=act)
+    assert not st.any()
+    for b in range(B):
+        ref = _torch_causal_conv(np.concatenate([state[b], u[b]]), weight, bias, act)
+        np.testing.assert_allclose(out[b], ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["random", "heap2", "star"])
+def test_conv_every_node_is_the_conv_of_its_path(kind):
+    B, T, C, W = 3, 31, 4, 4
+    rng = np.random.default_rng(7)
+    mk = {"random": lambda: trees.random_recursive(T, 3, rng), "heap2": lambda: trees.heap_kary(T, 2),
+          "star": lambda: np.array([-1] + [0] * (T - 1), np.int32)}[kind]
+    par = np.stack([mk() for _ in range(B)])
+    u, weight, bias, state = _conv_inputs(B, T, C, W, seed=11)
+    out, st = oracle.tree_conv(u, weight, bias, state, par)
+    assert not st.any()
+    for b in range(B):
+        for i in range(T):
+            path = []
+            v = i
+            while v >= 0:
+                path.append(v)
+                v = int(par[b, v])
+            seq = np.concatenate([state[b], u[b, path[::-1]]])
+            ref = _torch_causal_conv(seq, weight, bias, True)[-1]
+            np.testing.assert_allclose(out[b, i], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_conv_special_cases():
+    B, T, C = 2, 9, 3
+    u, weight, bias, state = _conv_inputs(B, T, C, 1, seed=3)
+    par = np.stack([trees.random_recursive(T, 3, np.random.default_rng(1)) for _ in range(B)])
+    out, _ = oracle.tree_conv(u, weight, bias, None, par, act=False)
+    np.testing.assert_allclose(out, u * weight[None, None, :, 0] + bias, rtol=1e-14)   # W = 1: pointwise
+    u, weight, bias, state = _conv_inputs(B, T, C, 4, seed=4)
+    o1, _ = oracle.tree_conv(u, weight, None, None, par, act=False)
+    o2, _ = oracle.tree_conv(u, weight, None, np.zeros_like(state), par, act=False)
+    assert np.array_equal(o1, o2)                                                       # NULL state = zeros
+    bad = par.copy()
+    bad[1, 4] = 6
+    o3, st = oracle.tree_conv(u, weight, bias, state, bad)
+    assert list(st) == [0, 2] and not o3[1].any()
+
+
+def test_conv_commit_is_slicing_of_state_and_path():
+    B, T, C, W = 3, 12, 4, 4
+    u, _, _, state = _conv_inputs(B, T, C, W, seed=5)
+    par = np.stack([trees.chain(T)] * B)
+    path = np.full((B, T), -1, np.int32)
+    plen = np.array([12, 2, 1], np.int32)
+    for b in range(B):
+        path[b, : plen[b]] = np.arange(plen[b])
+    new, st = oracle.conv_commit(u, state, path, plen, W, parent=par)
+    assert not st.any()
+    for b in range(B):
+        full = np.concatenate([state[b], u[b, path[b, : plen[b]]]])
+        np.testing.assert_array_equal(new[b], full[-(W - 1):])
+    path2 = path.copy()
+    path2[1, 1] = 3                                    # not parent-linked
+    new2, st2 = oracle.conv_commit(u, state, path2, plen, W, parent=par)
+    assert list(st2) == [0, 3, 0]
+    np.testing.assert_array_equal(new2[1], state[1])
+
+
+def test_conv_commit_then_conv_equals_grafted_tree():
+    """Losslessness of the conv state across iterations (the conv analogue of Alg. 1): the conv of a
+    second tree from the committed state equals the conv of that tree grafted under the last accepted
+    node of the first tree, from the original state."""
+    C, W = 3, 4
+    rng = np.random.default_rng(9)
+    T1, T2 = 10, 8
+    p1 = trees.random_recursive(T1, 3, rng)
+    p2 = trees.random_recursive(T2, 3, rng)
+    u1 = rng.standard_normal((1, T1, C))
+    u2 = rng.standard_normal((1, T2, C))
+    weight = rng.standard_normal((C, W))
+    bias = rng.standard_normal(C)
+    state = rng.standard_normal((1, W - 1, C))
+    k = T1 - 1
+    path = []
+    v = k
+    while v >= 0:
+        path.append(v)
+        v = int(p1[v])
+    path = path[::-1]
+    pa = np.full((1, T1), -1, np.int32)
+    pa[0, : len(path)] = path
+    s1, _ = oracle.conv_commit(u1, state, pa, np.array([len(path)], np.int32), W, parent=p1[None])
+    o2, _ = oracle.tree_conv(u2, weight, bias, s1, p2[None])
+    pg = np.concatenate([p1, np.where(p2 < 0, k, p2 + T1)]).astype(np.int32)
+    og, _ = oracle.tree_conv(np.concatenate([u1, u2], 1), weight, bias, state, pg[None])
+    np.testing.assert_allclose(o2[0], og[0, T1:], rtol=1e-12, atol=1e-12)
