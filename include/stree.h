@@ -193,6 +193,47 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
 enum { STREE_LAUNCH_PDL = 1, STREE_LAUNCH_EARLY_STATE = 2, STREE_LAUNCH_EARLY_REPLAY = 4 };
 stree_status stree_set_launch_flags(uint32_t flags);
 
+/*
+ * stree_tree_conv — tree-causal depthwise conv1d over the xBC channels (the
+ * paper is silent on the convolution, reading R-conv): Mamba-2's causal conv of width W
+ * run along each node's root-to-node path, the committed conv state prepended:
+ *   seq_i        = conv_state[b] (W-1 rows, oldest first) ++ u[b][root .. i]
+ *   out[b][i][c] = act( bias[c] + sum_{w<W} weight[c][w] * seq_i[len(seq_i) - W + w][c] )
+ * act = SiLU (z / (1 + e^-z)) when act != 0, identity otherwise.
+ *   u          [B][T][C]    io dtype   (xBC after in_proj)
+ *   weight     [C][W]       f32        (W = width, 1..4; weight[c][W-1] multiplies the node itself)
+ *   bias       [C]          f32 or NULL
+ *   conv_state [B][W-1][C]  io dtype or NULL (zeros)
+ *   parent     [B][T]       i32
+ *   out        [B][T][C]    io dtype (must not overlap u)
+ * C must be a multiple of 8 (bf16) / 4 (f32); arrays 16-byte aligned.  Invalid tree b: dev_status
+ * <- 1 / 2 and out[b] = 0.
+ */
+typedef struct {
+    int32_t batch;        /* B */
+    int32_t n_nodes;      /* T, 0..256 */
+    int32_t channels;     /* C (conv_dim = H*P + 2*G*N for Mamba-2) */
+    int32_t width;        /* W, 1..4 (d_conv) */
+    stree_dtype io_dtype; /* dtype of u, conv_state, out */
+} stree_conv_dims;
+
+stree_status stree_tree_conv(const stree_conv_dims* d, const void* u, const float* weight, const float* bias,
+                             const void* conv_state, const int32_t* parent, int32_t act, void* out,
+                             int32_t* dev_status, void* stream);
+
+/*
+ * stree_conv_commit — conv-state commit along the accepted path (reading R-conv):
+ *   conv_state_new[b] = last W-1 rows of (conv_state[b] ++ u[b][path[0 .. path_len-1]])
+ *   conv_state     [B][W-1][C] io dtype or NULL (zeros)
+ *   parent         [B][T] or NULL: if given, each path[m] must have parent path[m-1]
+ *   path, path_len as produced by stree_accept
+ *   conv_state_new [B][W-1][C] io dtype; == conv_state (in place) allowed, partial overlap not.
+ * Invalid path for tree b: dev_status <- 3 and conv_state_new[b] = conv_state[b].
+ */
+stree_status stree_conv_commit(const stree_conv_dims* d, const void* u, const void* conv_state,
+                               const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                               void* conv_state_new, int32_t* dev_status, void* stream);
+
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
 

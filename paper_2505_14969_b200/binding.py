@@ -35,6 +35,11 @@ class stree_dims(ctypes.Structure):
                 ("io_dtype", ctypes.c_int32)]
 
 
+class stree_conv_dims(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("channels", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("io_dtype", ctypes.c_int32)]
+
+
 _lib = None
 
 
@@ -56,6 +61,8 @@ def lib():
             "stree_replay_scan": [vp] * 19,
             "stree_scan_kernel_for": [vp],
             "stree_commit_kernel_for": [vp, i32],
+            "stree_tree_conv": [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp],
+            "stree_conv_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -73,7 +80,7 @@ STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY = 1, 2, 4
 
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
                     "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",
-                    "stree_replay_scan", "stree_commit_kernel_for")
+                    "stree_replay_scan", "stree_commit_kernel_for", "stree_tree_conv", "stree_conv_commit")
 
 
 def status_string(s: int) -> str:
@@ -171,3 +178,25 @@ def stree_scan_kernel_for(dims: stree_dims) -> int:
 
 def stree_commit_kernel_for(dims: stree_dims, has_h0: bool = True) -> int:
     return lib().stree_commit_kernel_for(ctypes.byref(dims), int(bool(has_h0)))
+
+
+def make_conv_dims(u: torch.Tensor, weight: torch.Tensor) -> stree_conv_dims:
+    B, T, C = u.shape
+    return stree_conv_dims(B, T, C, weight.shape[1], io_code(u.dtype))
+
+
+def stree_tree_conv(u, weight, bias, conv_state, parent, out, act=True, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_conv_dims(u, weight)
+    _check("stree_tree_conv", lib().stree_tree_conv(ctypes.byref(d), _ptr(u), _ptr(weight), _ptr(bias),
+                                                    _ptr(conv_state), _ptr(parent), int(bool(act)), _ptr(out),
+                                                    _ptr(dev_status), _stream(stream)))
+
+
+def stree_conv_commit(u, conv_state, parent, path, path_len, conv_state_new, width, dev_status=None, stream=None,
+                      dims=None):
+    B, T, C = u.shape
+    d = dims if dims is not None else stree_conv_dims(B, T, C, int(width), io_code(u.dtype))
+    _check("stree_conv_commit", lib().stree_conv_commit(ctypes.byref(d), _ptr(u), _ptr(conv_state), _ptr(parent),
+                                                        _ptr(path), _ptr(path_len), _ptr(conv_state_new),
+                                                        _ptr(dev_status), _stream(stream)))
+

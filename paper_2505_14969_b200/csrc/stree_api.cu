@@ -19,6 +19,10 @@ extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*
                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
                                     cudaStream_t);
 extern "C" int stree_tc_supports(const stree_dims*);
+extern "C" int stree_launch_tree_conv(const stree_conv_dims*, const void*, const float*, const float*, const void*,
+                                      const int32_t*, int, void*, int32_t*, cudaStream_t);
+extern "C" int stree_launch_conv_commit(const stree_conv_dims*, const void*, const void*, const int32_t*,
+                                        const int32_t*, const int32_t*, void*, int32_t*, cudaStream_t);
 extern "C" int stree_tc_commit_supports(const stree_dims*);
 extern "C" int stree_launch_commit_tc(const stree_dims*, const void*, const float*, const float*, const void*,
                                       const float*, const int32_t*, const int32_t*, const int32_t*, float*, int32_t*,
@@ -211,6 +215,55 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
         if (p && !aligned16(p)) return STREE_ERR_ALIGN;
     return finish(stree_launch_replay_scan_tc(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt,
                                               A, Bm, Cm, D, h, parent, y, dev_status, s),
+                  dev_status, s);
+}
+
+namespace {
+stree_status check_conv_dims(const stree_conv_dims* d) {
+    if (!d) return STREE_ERR_NULL;
+    if (d->batch < 0 || d->n_nodes < 0 || d->n_nodes > STREE_MAX_NODES || d->channels <= 0 || d->width < 1 ||
+        d->width > 4)
+        return STREE_ERR_SHAPE;
+    if (d->io_dtype != STREE_F32 && d->io_dtype != STREE_BF16) return STREE_ERR_DTYPE;
+    const int v = d->io_dtype == STREE_BF16 ? 8 : 4;   // 16-byte channel chunks
+    if (d->channels % v) return STREE_ERR_SHAPE;
+    return STREE_OK;
+}
+}  // namespace
+
+stree_status stree_tree_conv(const stree_conv_dims* d, const void* u, const float* weight, const float* bias,
+                             const void* conv_state, const int32_t* parent, int32_t act, void* out,
+                             int32_t* dev_status, void* stream) {
+    stree_status st = check_conv_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!u || !weight || !parent || !out) return STREE_ERR_NULL;
+    if (!aligned16(u) || !aligned16(out) || (conv_state && !aligned16(conv_state))) return STREE_ERR_ALIGN;
+    const size_t es = d->io_dtype == STREE_BF16 ? 2 : 4;
+    const size_t bytes = (size_t)d->batch * d->n_nodes * d->channels * es;
+    const char *a = (const char*)u, *o = (const char*)out;
+    if (a < o + bytes && o < a + bytes) return STREE_ERR_SHAPE;   // out must not overlap u
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_tree_conv(d, u, weight, bias, conv_state, parent, act, out, dev_status, s), dev_status,
+                  s);
+}
+
+stree_status stree_conv_commit(const stree_conv_dims* d, const void* u, const void* conv_state,
+                               const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                               void* conv_state_new, int32_t* dev_status, void* stream) {
+    stree_status st = check_conv_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0 || d->width == 1) return STREE_OK;
+    if (!u || !path || !path_len || !conv_state_new) return STREE_ERR_NULL;
+    if (!aligned16(u) || !aligned16(conv_state_new) || (conv_state && !aligned16(conv_state))) return STREE_ERR_ALIGN;
+    if (conv_state && conv_state != conv_state_new) {
+        const size_t es = d->io_dtype == STREE_BF16 ? 2 : 4;
+        const size_t bytes = (size_t)d->batch * (d->width - 1) * d->channels * es;
+        const char *a = (const char*)conv_state, *o = (const char*)conv_state_new;
+        if (a < o + bytes && o < a + bytes) return STREE_ERR_SHAPE;   // partial overlap
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_conv_commit(d, u, conv_state, parent, path, path_len, conv_state_new, dev_status, s),
                   dev_status, s);
 }
 

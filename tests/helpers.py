@@ -34,3 +34,10 @@ def assert_h_close(h_gpu, h_ref, tol):
     r1, r2 = blockwise_relerr(h_gpu, h_ref, (2, 3))
     assert r1 <= tol and r2 <= tol, f"h rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
     return r1, r2
+
+
+def assert_conv_close(o_gpu, o_ref, tol):
+    """tree conv output [B][T][C]: blocks are (tree, channel)."""
+    r1, r2 = blockwise_relerr(o_gpu, o_ref, (1,))
+    assert r1 <= tol and r2 <= tol, f"conv rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
+    return r1, r2
