@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-fuse", action="store_true",
                     help="separate commit kernels instead of the fused replay+scan (stree_replay_scan)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true",
+                    help="skip the SURVEY §8(f) rows (tree attention, KV commit, tree conv, conv commit; bench_next.py)")
     ap.add_argument("--p-match", type=float, default=0.9)
     ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
                     help="N>1: batch = each rank verifies its own trees (no collective, weak scaling); "
@@ -450,6 +452,10 @@ def run_stree(args):
             "clocks": sampler.summary(),
             "parallelism": (f"heads x{world} (+NCCL all-gather of y)" if heads_mode else
                             f"batch-replicas x{world}") if world > 1 else "single"}
+    if world == 1 and not args.no_next:
+        # §8(f) rows measured beside the step (their own graphs, after the timed region)
+        import bench_next
+        line["next_rows"] = bench_next.measure(dev, hbm_peak, bf16_peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(base, tok, vt)
     if rank == 0:

@@ -55,7 +55,8 @@ typedef enum {
 
 typedef enum { STREE_F32 = 0, STREE_BF16 = 1 } stree_dtype;
 
-enum { STREE_DEV_OK = 0, STREE_DEV_BAD_ROOT = 1, STREE_DEV_BAD_PARENT = 2, STREE_DEV_BAD_PATH = 3 };
+enum { STREE_DEV_OK = 0, STREE_DEV_BAD_ROOT = 1, STREE_DEV_BAD_PARENT = 2, STREE_DEV_BAD_PATH = 3,
+       STREE_DEV_CAPACITY = 5 /* KV cache: cache_len outside [0, cache_cap], or a commit would overflow it */ };
 
 enum { STREE_MAX_NODES = 256 };
 
@@ -233,6 +234,60 @@ stree_status stree_tree_conv(const stree_conv_dims* d, const void* u, const floa
 stree_status stree_conv_commit(const stree_conv_dims* d, const void* u, const void* conv_state,
                                const int32_t* parent, const int32_t* path, const int32_t* path_len,
                                void* conv_state_new, int32_t* dev_status, void* stream);
+
+/*
+ * Tree attention for the attention layers of a hybrid SSM/Transformer stack (
+ * PAPER.md:19, :54 topology-aware mask, :63-66 L_ij, :318 MambaInLlama; reading R-attn).
+ * Node i of tree b attends to every committed cache position and to the tree nodes on its own
+ * root-to-i path:
+ *   keys(i)    = k_cache[b][0 : cache_len[b]]  ++  k_new[b][path(i)]
+ *   o[b][i][h] = Σ_j softmax_j(scale · <q[b][i][h], key_j>) · value_j,   kv head of h = h / (Hq/Hkv)
+ * Positional encodings (RoPE at position cache_len + depth(i)) are applied upstream to q / k_new.
+ */
+typedef struct {
+    int32_t batch;        /* B */
+    int32_t n_nodes;      /* T, 0..256 */
+    int32_t n_q_heads;    /* Hq */
+    int32_t n_kv_heads;   /* Hkv, divides Hq (GQA) */
+    int32_t head_dim;     /* D, 1..256 (the tcgen05 kernel serves D = 128, bf16, (Hq/Hkv) | 128) */
+    int32_t cache_cap;    /* S: rows allocated per sequence in k_cache / v_cache */
+    stree_dtype io_dtype; /* dtype of q, k_new, v_new, k_cache, v_cache, o */
+} stree_attn_dims;
+
+/*
+ * stree_tree_attn — o for every node of every tree (no cache write).
+ *   q              [B][T][Hq][D]   io dtype
+ *   k_new, v_new   [B][T][Hkv][D]  io dtype (the tree nodes' keys / values)
+ *   k_cache, v_cache [B][S][Hkv][D] io dtype (rows >= cache_len[b] are ignored)
+ *   cache_len      [B] int32, device, 0 <= cache_len[b] <= S
+ *   parent         [B][T] int32
+ *   scale          softmax scale (typically 1/sqrt(D))
+ *   o              [B][T][Hq][D]   io dtype; must not alias an input.
+ * Invalid tree b: dev_status <- 1/2 and o[b] = 0; cache_len[b] out of range: dev_status <- 5, o[b] = 0.
+ * Alignment: all pointers 16-byte aligned.
+ */
+stree_status stree_tree_attn(const stree_attn_dims* d, const void* q, const void* k_new, const void* v_new,
+                             const void* k_cache, const void* v_cache, const int32_t* cache_len,
+                             const int32_t* parent, float scale, void* o, int32_t* dev_status, void* stream);
+
+/*
+ * stree_kv_commit — KV-cache commit of the accepted path (the attention analogue of activation
+ * replay, Alg. 1 l.123; reading R-attn):
+ *   k_cache[b][cache_len[b] + r] = k_new[b][path[b][r]],  same for v,  r < path_len[b];
+ *   cache_len[b] += path_len[b]                                        (cache_len updated in place)
+ *   parent [B][T] or NULL: if given, each path[m] must have parent path[m-1]
+ *   path, path_len as produced by stree_accept
+ * Invalid path for tree b: dev_status <- 3, cache and cache_len[b] unchanged; overflow
+ * (cache_len + path_len > S): dev_status <- 5, unchanged.
+ * Row size Hkv·D·sizeof(io) must be a multiple of 4 bytes; pointers 16-byte aligned.
+ */
+stree_status stree_kv_commit(const stree_attn_dims* d, const void* k_new, const void* v_new,
+                             const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                             void* k_cache, void* v_cache, int32_t* cache_len, int32_t* dev_status,
+                             void* stream);
+
+/* Which kernel stree_tree_attn would launch: 1 = SIMT (any shape, fp32), 2 = tcgen05, 0 = invalid. */
+int32_t stree_attn_kernel_for(const stree_attn_dims* d);
 
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_PKG, "libstree.so")
 
 STREE_F32, STREE_BF16 = 0, 1
 STREE_SCAN_AUTO, STREE_SCAN_SIMT, STREE_SCAN_TC = 0, 1, 2
-DEV_BAD_ROOT, DEV_BAD_PARENT, DEV_BAD_PATH = 1, 2, 3
+DEV_BAD_ROOT, DEV_BAD_PARENT, DEV_BAD_PATH, DEV_CAPACITY = 1, 2, 3, 5
 MAX_NODES = 256
 
 
@@ -32,6 +32,12 @@ class StreeError(RuntimeError):
 class stree_dims(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("d_state", ctypes.c_int32), ("n_groups", ctypes.c_int32),
+                ("io_dtype", ctypes.c_int32)]
+
+
+class stree_attn_dims(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("cache_cap", ctypes.c_int32),
                 ("io_dtype", ctypes.c_int32)]
 
 
@@ -63,6 +69,9 @@ def lib():
             "stree_commit_kernel_for": [vp, i32],
             "stree_tree_conv": [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp],
             "stree_conv_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "stree_tree_attn": [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, vp],
+            "stree_kv_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "stree_attn_kernel_for": [vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -80,7 +89,8 @@ STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY = 1, 2, 4
 
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
                     "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",
-                    "stree_replay_scan", "stree_commit_kernel_for", "stree_tree_conv", "stree_conv_commit")
+                    "stree_replay_scan", "stree_commit_kernel_for", "stree_tree_conv", "stree_conv_commit",
+                    "stree_tree_attn", "stree_kv_commit", "stree_attn_kernel_for")
 
 
 def status_string(s: int) -> str:
@@ -200,3 +210,30 @@ def stree_conv_commit(u, conv_state, parent, path, path_len, conv_state_new, wid
                                                         _ptr(path), _ptr(path_len), _ptr(conv_state_new),
                                                         _ptr(dev_status), _stream(stream)))
 
+
+
+def make_attn_dims(q: torch.Tensor, k_new: torch.Tensor, k_cache: torch.Tensor) -> stree_attn_dims:
+    B, T, Hq, D = q.shape
+    return stree_attn_dims(B, T, Hq, k_new.shape[2], D, k_cache.shape[1], io_code(q.dtype))
+
+
+def stree_tree_attn(q, k_new, v_new, k_cache, v_cache, cache_len, parent, scale, o, dev_status=None, stream=None,
+                    dims=None):
+    d = dims if dims is not None else make_attn_dims(q, k_new, k_cache)
+    _check("stree_tree_attn", lib().stree_tree_attn(ctypes.byref(d), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(k_cache),
+                                                    _ptr(v_cache), _ptr(cache_len), _ptr(parent), float(scale),
+                                                    _ptr(o), _ptr(dev_status), _stream(stream)))
+
+
+def stree_kv_commit(k_new, v_new, parent, path, path_len, k_cache, v_cache, cache_len, dev_status=None, stream=None,
+                    dims=None):
+    d = dims if dims is not None else make_attn_dims(k_new, k_new, k_cache)
+    if dims is None:
+        d.n_q_heads = k_new.shape[2]
+    _check("stree_kv_commit", lib().stree_kv_commit(ctypes.byref(d), _ptr(k_new), _ptr(v_new), _ptr(parent),
+                                                    _ptr(path), _ptr(path_len), _ptr(k_cache), _ptr(v_cache),
+                                                    _ptr(cache_len), _ptr(dev_status), _stream(stream)))
+
+
+def stree_attn_kernel_for(dims: stree_attn_dims) -> int:
+    return lib().stree_attn_kernel_for(ctypes.byref(dims))

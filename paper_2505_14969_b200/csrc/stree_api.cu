@@ -32,6 +32,13 @@ extern "C" int stree_launch_replay_scan_tc(const stree_dims*, const void*, const
                                            const float*, const float*, const void*, const void*, const float*, float*,
                                            const int32_t*, void*, int32_t*, cudaStream_t);
 
+extern "C" int stree_attn_tc_supports(const stree_attn_dims*);
+extern "C" int stree_launch_tree_attn(const stree_attn_dims*, const void*, const void*, const void*, const void*,
+                                      const void*, const int32_t*, const int32_t*, float, void*, int32_t*, int,
+                                      cudaStream_t);
+extern "C" int stree_launch_kv_commit(const stree_attn_dims*, const void*, const void*, const int32_t*,
+                                      const int32_t*, const int32_t*, void*, void*, int32_t*, int32_t*, cudaStream_t);
+
 namespace {
 
 std::atomic<int> g_scan_impl{STREE_SCAN_AUTO};
@@ -268,3 +275,61 @@ stree_status stree_conv_commit(const stree_conv_dims* d, const void* u, const vo
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// tree attention + KV commit
+// ---------------------------------------------------------------------------
+namespace {
+stree_status check_attn_dims(const stree_attn_dims* d) {
+    if (!d) return STREE_ERR_NULL;
+    if (d->batch < 0 || d->n_nodes < 0 || d->n_nodes > STREE_MAX_NODES) return STREE_ERR_SHAPE;
+    if (d->n_q_heads < 1 || d->n_kv_heads < 1 || d->n_q_heads % d->n_kv_heads) return STREE_ERR_SHAPE;
+    if (d->head_dim < 1 || d->head_dim > 256 || d->cache_cap < 0) return STREE_ERR_SHAPE;
+    if (d->io_dtype != STREE_F32 && d->io_dtype != STREE_BF16) return STREE_ERR_DTYPE;
+    return STREE_OK;
+}
+int attn_use_tc(const stree_attn_dims* d) {
+    const int impl = g_scan_impl.load();
+    if (impl == STREE_SCAN_SIMT) return 0;
+    return stree_attn_tc_supports(d) ? 1 : 0;
+}
+}  // namespace
+
+int32_t stree_attn_kernel_for(const stree_attn_dims* d) {
+    if (check_attn_dims(d) != STREE_OK) return 0;
+    return attn_use_tc(d) ? 2 : 1;
+}
+
+stree_status stree_tree_attn(const stree_attn_dims* d, const void* q, const void* k_new, const void* v_new,
+                             const void* k_cache, const void* v_cache, const int32_t* cache_len,
+                             const int32_t* parent, float scale, void* o, int32_t* dev_status, void* stream) {
+    stree_status st = check_attn_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!q || !k_new || !v_new || !cache_len || !parent || !o) return STREE_ERR_NULL;
+    if (d->cache_cap > 0 && (!k_cache || !v_cache)) return STREE_ERR_NULL;
+    for (const void* p : {q, k_new, v_new, k_cache, v_cache, (const void*)o})
+        if (p && !aligned16(p)) return STREE_ERR_ALIGN;
+    const int tc = attn_use_tc(d);
+    if (!tc && g_scan_impl.load() == STREE_SCAN_TC) return STREE_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_tree_attn(d, q, k_new, v_new, k_cache, v_cache, cache_len, parent, scale, o,
+                                         dev_status, tc, s),
+                  dev_status, s);
+}
+
+stree_status stree_kv_commit(const stree_attn_dims* d, const void* k_new, const void* v_new, const int32_t* parent,
+                             const int32_t* path, const int32_t* path_len, void* k_cache, void* v_cache,
+                             int32_t* cache_len, int32_t* dev_status, void* stream) {
+    stree_status st = check_attn_dims(d);
+    if (st != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!k_new || !v_new || !path || !path_len || !k_cache || !v_cache || !cache_len) return STREE_ERR_NULL;
+    if (((size_t)d->n_kv_heads * d->head_dim * (d->io_dtype == STREE_BF16 ? 2 : 4)) % 4) return STREE_ERR_SHAPE;
+    for (const void* p : {k_new, v_new, (const void*)k_cache, (const void*)v_cache})
+        if (!aligned16(p)) return STREE_ERR_ALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_kv_commit(d, k_new, v_new, parent, path, path_len, k_cache, v_cache, cache_len,
+                                         dev_status, s),
+                  dev_status, s);
+}

@@ -1,0 +1,597 @@
+// K7 stree_tree_attn / K8 stree_kv_commit: tree-masked attention for the attention layers of a
+// hybrid SSM/Transformer stack and the KV-cache commit of the accepted path (
+// DESIGN.md reading R-attn).  PAPER.md:19, :54 (topology-aware mask), :63-66 (L_ij = 1 iff t_j on
+// the root-to-t_i path), :318 (MambaInLlama hybrid):
+//
+//   o[b][i][h] = softmax_j( scale <q_i,h , key_j> ) value_j,
+//   keys(i)    = k_cache[b][0 : cache_len[b]]  ++  k_new[b][path(i)]        (kv head h / (Hq/Hkv))
+//
+// Two kernels serve stree_tree_attn:
+//   attn_tc_kernel   bf16, head dim 128, (Hq/Hkv) | 128: flash attention on tcgen05.  One CTA per
+//                    (tree, kv head, pair of 128-row query tiles); query rows are (node, q head of
+//                    the group) so the GQA group shares every K/V tile.  Warp 0: TMA producer
+//                    (Q once, then K/V tiles of 128 keys into a 2-stage ring: the committed prefix
+//                    first, then the tree's own nodes).  Warp 1: MMA issuer + TMEM allocator
+//                    (S_w = Q_w·Kᵀ into TMEM columns [128w, 128w+128), P_w written back over S_w as
+//                    bf16, O_w += P_w·V from TMEM (TS MMA) into columns [256+128w, ...)).  Warps 2-5
+//                    and 6-9: softmax of query tile 0 / 1 (thread = row = TMEM lane): mask (prefix
+//                    length, ancestor bits of the row's node), online max with lazy rescaling,
+//                    exp2, P to TMEM, and the final O/l epilogue.  The two tiles ping-pong: the
+//                    tensor core computes S_1 while tile 0's softmax runs, and so on.
+//   attn_simt_kernel any shape / fp32 (the 1e-4 fp32 path): one warp per (tree, node, q head),
+//                    lanes over keys, online softmax, fp32 throughout.
+#include <cuda.h>
+
+#include "stree_common.cuh"
+#include "stree_tc_ptx.cuh"
+
+namespace stree {
+namespace attn {
+
+using namespace stree::tc;
+
+constexpr int kDev_Capacity = STREE_DEV_CAPACITY;   // cache_len out of [0, cache_cap] / commit overflow
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---------------------------------------------------------------------------
+// SIMT kernel (any head dim <= 256, fp32 or bf16 io)
+// ---------------------------------------------------------------------------
+constexpr int kSimtMaxD = 256;
+
+template <typename IO>
+__global__ void __launch_bounds__(32) attn_simt_kernel(const IO* __restrict__ q, const IO* __restrict__ k_new,
+                                                       const IO* __restrict__ v_new, const IO* __restrict__ k_cache,
+                                                       const IO* __restrict__ v_cache,
+                                                       const int32_t* __restrict__ cache_len,
+                                                       const int32_t* __restrict__ parent, float scale, IO* o, int T,
+                                                       int Hq, int Hkv, int D, int S, int32_t* dev_status) {
+    __shared__ float sq[kSimtMaxD];
+    __shared__ int spath[kMaxNodes];
+    __shared__ int snp, sbad;
+    pdl_trigger();
+    pdl_wait();
+    const int h = blockIdx.x, i = blockIdx.y, b = blockIdx.z, lane = threadIdx.x;
+    const int g = h / (Hq / Hkv);
+    const int32_t* par = parent + (size_t)b * T;
+    if (lane == 0) {
+        int bad = par[0] != -1 ? 1 : 0;
+        for (int v = 1; v < T && !bad; ++v)
+            if (par[v] < 0 || par[v] >= v) bad = 2;
+        const int L = cache_len[b];
+        if (!bad && (L < 0 || L > S)) bad = kDev_Capacity;
+        int n = 0;
+        if (!bad)
+            for (int v = i; v >= 0; v = par[v]) spath[n++] = v;   // i .. root (order is irrelevant to softmax)
+        snp = n;
+        sbad = bad;
+        if (bad && i == 0 && h == 0) report(dev_status, bad);
+    }
+    for (int d = lane; d < D; d += 32) sq[d] = to_f32<IO>(q[(((size_t)b * T + i) * Hq + h) * D + d]);
+    __syncwarp();
+    IO* orow = o + (((size_t)b * T + i) * Hq + h) * D;
+    if (sbad) {
+        for (int d = lane; d < D; d += 32) orow[d] = from_f32<IO>(0.f);
+        return;
+    }
+    const int L = cache_len[b], np = snp, nk = L + np;
+    constexpr int kE = kSimtMaxD / 32;
+    float acc[kE];
+#pragma unroll
+    for (int e = 0; e < kE; ++e) acc[e] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    auto krow = [&](int j) -> const IO* {
+        return j < L ? k_cache + (((size_t)b * S + j) * Hkv + g) * D
+                     : k_new + (((size_t)b * T + spath[j - L]) * Hkv + g) * D;
+    };
+    auto vrow = [&](int j) -> const IO* {
+        return j < L ? v_cache + (((size_t)b * S + j) * Hkv + g) * D
+                     : v_new + (((size_t)b * T + spath[j - L]) * Hkv + g) * D;
+    };
+    for (int j0 = 0; j0 < nk; j0 += 32) {
+        const int j = j0 + lane;
+        float s = -INFINITY;
+        if (j < nk) {
+            const IO* kr = krow(j);
+            float dot = 0.f;
+            for (int d = 0; d < D; ++d) dot = fmaf(sq[d], to_f32<IO>(kr[d]), dot);
+            s = dot * scale;
+        }
+        float mc = s;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+        const float mn = fmaxf(m, mc);
+        const float alpha = m == -INFINITY ? 0.f : expf(m - mn);
+        const float p = j < nk ? expf(s - mn) : 0.f;
+        float ps = p;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+        l = l * alpha + ps;
+        m = mn;
+#pragma unroll
+        for (int e = 0; e < kE; ++e) acc[e] *= alpha;
+        const int nj = min(32, nk - j0);
+        for (int jj = 0; jj < nj; ++jj) {
+            const float pj = __shfl_sync(0xffffffffu, p, jj);
+            const IO* vr = vrow(j0 + jj);
+#pragma unroll
+            for (int e = 0; e < kE; ++e) {
+                const int d = lane + 32 * e;
+                if (d < D) acc[e] = fmaf(pj, to_f32<IO>(vr[d]), acc[e]);
+            }
+        }
+    }
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+        const int d = lane + 32 * e;
+        if (d < D) orow[d] = from_f32<IO>(acc[e] * inv);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 kernel (bf16, D = 128)
+// ---------------------------------------------------------------------------
+constexpr int kD = 128;
+constexpr int kBM = 128;            // query rows per tile
+constexpr int kBN = 128;            // keys per K/V tile
+constexpr int kStages = 2;
+constexpr int kThreads = 320;       // warp 0 TMA, warp 1 MMA, warps 2-5 softmax tile 0, 6-9 softmax tile 1
+constexpr int kHalf = kBM * 128;    // one 128-row x 64-element (128 B) swizzle-128B box = 16 KB
+constexpr int kTile = 2 * kHalf;    // 128 rows x 128 elements
+constexpr uint32_t kTmemCols = 512;
+
+struct Smem {
+    static constexpr int Q = 0;                          // 2 query tiles
+    static constexpr int K = Q + 2 * kTile;              // kStages key tiles
+    static constexpr int V = K + kStages * kTile;        // kStages value tiles
+    static constexpr int PAR = V + kStages * kTile;      // parent[256] int
+    static constexpr int BAR = PAR + kMaxNodes * 4;
+    // barriers: qfull, kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], pfull[2], ofull[2]
+    static constexpr int NBAR = 1 + 4 * kStages + 6;
+    static constexpr int TMEMP = BAR + NBAR * 8;
+    static constexpr int MISC = TMEMP + 16;              // int: bad flag, L
+    static constexpr int TOTAL = MISC + 16;
+    static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2,
+                                            int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] · B[smem desc], kind::f16 (A: M lanes x K bf16 packed two per 32-bit column)
+__device__ __forceinline__ void mma_f16_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+struct AttnParams {
+    const int32_t* cache_len;
+    const int32_t* parent;
+    __nv_bfloat16* o;
+    int32_t* dev_status;
+    int T, Hq, Hkv, S, npairs;
+    float scale_log2;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
+                   const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
+                   const __grid_constant__ CUtensorMap tm_vn, const AttnParams prm) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sb = smem_u32(sm);
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+    const int T = prm.T, Hq = prm.Hq, Hkv = prm.Hkv, grp = Hq / Hkv;
+    const int b = blockIdx.x / (Hkv * prm.npairs);
+    const int rem = blockIdx.x % (Hkv * prm.npairs);
+    const int kvh = rem / prm.npairs, pr = rem % prm.npairs;
+    const int nmt = (T * grp + kBM - 1) / kBM;
+    const int nw = min(2, nmt - 2 * pr);               // query tiles of this CTA (1 or 2)
+    pdl_trigger();
+
+    const uint32_t bar0 = sb + Smem::BAR;
+    const uint32_t BAR_Q = bar0;
+    auto bar_kfull = [&](int s) { return bar0 + 8 + 8 * s; };
+    auto bar_kempty = [&](int s) { return bar0 + 8 + 8 * kStages + 8 * s; };
+    auto bar_vfull = [&](int s) { return bar0 + 8 + 16 * kStages + 8 * s; };
+    auto bar_vempty = [&](int s) { return bar0 + 8 + 24 * kStages + 8 * s; };
+    auto bar_sfull = [&](int w) { return bar0 + 8 + 32 * kStages + 8 * w; };
+    auto bar_pfull = [&](int w) { return bar0 + 8 + 32 * kStages + 16 + 8 * w; };
+    auto bar_ofull = [&](int w) { return bar0 + 8 + 32 * kStages + 32 + 8 * w; };
+    uint32_t* tmem_slot = (uint32_t*)(sm + Smem::TMEMP);
+    int* sp = (int*)(sm + Smem::PAR);
+
+    if (tid == 0) {
+        mbar_init(BAR_Q, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(bar_kfull(s), 1);
+            mbar_init(bar_kempty(s), 1);
+            mbar_init(bar_vfull(s), 1);
+            mbar_init(bar_vempty(s), 1);
+        }
+        for (int w = 0; w < 2; ++w) {
+            mbar_init(bar_sfull(w), 1);
+            mbar_init(bar_pfull(w), 128);
+            mbar_init(bar_ofull(w), 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_q); tma_prefetch(&tm_kc); tma_prefetch(&tm_vc); tma_prefetch(&tm_kn); tma_prefetch(&tm_vn);
+    }
+    pdl_wait();
+    // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length
+    int bad = 0;
+    for (int v = tid; v < T; v += kThreads) {
+        const int p = prm.parent[(size_t)b * T + v];
+        sp[v] = p;
+        if (v == 0 ? p != -1 : (p < 0 || p >= v)) bad = v == 0 ? 1 : 2;
+    }
+    const int L = prm.cache_len[b];
+    const int any1 = __syncthreads_or(bad == 1);
+    const int any2 = __syncthreads_or(bad == 2);
+    int code = any1 ? 1 : (any2 ? 2 : ((L < 0 || L > prm.S) ? kDev_Capacity : 0));
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int npre = code ? 0 : (L + kBN - 1) / kBN;   // prefix tiles
+    const int ntr = (T + kBN - 1) / kBN;               // tree tiles
+    const int nt = npre + ntr;
+
+    if (code) {
+        if (tid == 0 && rem == 0) report(prm.dev_status, code);
+        // zero this CTA's output rows
+        if (warp >= 2) {
+            const int w = (warp - 2) >> 2, r = 32 * (warp & 3) + lane;
+            if (w < nw) {
+                const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
+                if (i < T) {
+                    uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD);
+#pragma unroll
+                    for (int c = 0; c < kD / 8; ++c) orow[c] = make_uint4(0, 0, 0, 0);
+                }
+            }
+        }
+    } else if (warp == 0) {
+        // ---- TMA producer ----
+        if (lane == 0) {
+            mbar_expect_tx(BAR_Q, nw * kTile);
+            for (int w = 0; w < nw; ++w) {
+                const int node0 = (2 * pr + w) * (kBM / grp);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(sb + Smem::Q + w * kTile + hf * kHalf, &tm_q, BAR_Q, 64 * hf, kvh * grp, node0, b);
+            }
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % kStages, u = j / kStages;
+                const bool pre = j < npre;
+                const int key0 = pre ? j * kBN : (j - npre) * kBN;
+                mbar_wait(bar_kempty(s), (u & 1) ^ 1);
+                mbar_expect_tx(bar_kfull(s), kTile);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(sb + Smem::K + s * kTile + hf * kHalf, pre ? &tm_kc : &tm_kn, bar_kfull(s), 64 * hf,
+                                kvh, key0, b);
+                mbar_wait(bar_vempty(s), (u & 1) ^ 1);
+                mbar_expect_tx(bar_vfull(s), kTile);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(sb + Smem::V + s * kTile + hf * kHalf, pre ? &tm_vc : &tm_vn, bar_vfull(s), 64 * hf,
+                                kvh, key0, b);
+            }
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer (whole warp converged, one elected lane issues) ----
+        const uint32_t id_s = idesc(kFmtBF16, 0, kBM, kBN);   // S = Q·Kᵀ: A, B K-major
+        const uint32_t id_o = idesc(kFmtBF16, 1, kBM, kD);    // O += P·V: A in TMEM, B (V) MN-major
+        auto issue_s = [&](int w, int s) {
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint64_t ad = sdesc(sb + Smem::Q + w * kTile + (kk >> 2) * kHalf, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                const uint64_t bd = sdesc(sb + Smem::K + s * kTile + (kk >> 2) * kHalf, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                mma_f16_w(tmem + 128 * w, ad, bd, id_s, kk > 0);
+            }
+            tc_commit_w(bar_sfull(w));
+        };
+        mbar_wait(BAR_Q, 0);
+        mbar_wait(bar_kfull(0), 0);
+        tc_fence_after();
+        for (int w = 0; w < nw; ++w) issue_s(w, 0);
+        tc_commit_w(bar_kempty(0));
+        for (int j = 0; j < nt; ++j) {
+            const int s = j % kStages, u = j / kStages;
+            const int s1 = (j + 1) % kStages, u1 = (j + 1) / kStages;
+            for (int w = 0; w < nw; ++w) {
+                mbar_wait(bar_pfull(w), j & 1);
+                if (w == 0) mbar_wait(bar_vfull(s), u & 1);
+                tc_fence_after();
+                const uint64_t vd = sdesc(sb + Smem::V + s * kTile, kHalf, 1024);
+#pragma unroll
+                for (int kk = 0; kk < kBN / 16; ++kk)
+                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 8 * kk, vd + (uint64_t)(kk * 128), id_o,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+                if (w == nw - 1) tc_commit_w(bar_vempty(s));
+                if (j == nt - 1) tc_commit_w(bar_ofull(w));
+                if (j + 1 < nt) {
+                    if (w == 0) {
+                        mbar_wait(bar_kfull(s1), u1 & 1);
+                        tc_fence_after();
+                    }
+                    issue_s(w, s1);
+                    if (w == nw - 1) tc_commit_w(bar_kempty(s1));
+                }
+            }
+        }
+    } else {
+        // ---- softmax: thread = query row = TMEM lane ----
+        const int w = (warp - 2) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
+        if (w < nw) {
+            const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
+            const bool vrow = i < T;
+            uint32_t anc[kMaxWords];
+#pragma unroll
+            for (int q = 0; q < kMaxWords; ++q) anc[q] = 0u;
+            if (vrow)
+                for (int v = i; v >= 0; v = sp[v]) {
+#pragma unroll
+                    for (int q = 0; q < kMaxWords; ++q) anc[q] |= ((v >> 5) == q) ? (1u << (v & 31)) : 0u;
+                }
+            const uint32_t lane_base = tmem + ((uint32_t)(32 * q4) << 16);
+            const uint32_t t_s = lane_base + 128 * w, t_o = lane_base + 256 + 128 * w;
+            const float sl2 = prm.scale_log2;
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < nt; ++j) {
+                mbar_wait(bar_sfull(w), j & 1);
+                tc_fence_after();
+                uint32_t sr[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(t_s + 32 * c, sr + 32 * c);
+                tmem_wait();
+                float x[128];
+                const bool pre = j < npre;
+                if (pre) {
+                    const int lim = L - j * kBN;   // keys [0, lim) of this tile are committed
+#pragma unroll
+                    for (int c = 0; c < 128; ++c) x[c] = c < lim ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
+                } else {
+                    const int jt = j - npre, lim = T - jt * kBN;
+                    uint32_t aw[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) aw[q] = jt == 0 ? anc[q] : anc[4 + q];
+#pragma unroll
+                    for (int c = 0; c < 128; ++c)
+                        x[c] = (c < lim && ((aw[c >> 5] >> (c & 31)) & 1u)) ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
+                }
+                float mx = x[0];
+#pragma unroll
+                for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
+                // lazy rescaling: keep the running max unless the new one exceeds it by > 8 (log2 units).
+                // tcgen05.ld/st are warp-collective: the O rescale runs warp-wide whenever any lane needs
+                // it (alpha = 1 for the others).
+                const bool need = mx > m_run + 8.f;
+                const float alpha = need ? (m_run == -INFINITY ? 0.f : ex2(m_run - mx)) : 1.f;
+                if (need) m_run = mx;
+                l_run *= alpha;
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t orr[32];
+                        tmem_ld32(t_o + 32 * c, orr);
+                        tmem_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+                        tmem_st32(t_o + 32 * c, orr);
+                    }
+                    tmem_st_wait();
+                }
+                const float mu = m_run == -INFINITY ? 0.f : m_run;
+                uint32_t pk[64];
+                float ls = 0.f;
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const float p0 = ex2(x[2 * c] - mu), p1 = ex2(x[2 * c + 1] - mu);
+                    ls += p0 + p1;
+                    pk[c] = pack_bf16(p0, p1);
+                }
+                l_run += ls;
+                tmem_st32(t_s, pk);
+                tmem_st32(t_s + 32, pk + 32);
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(bar_pfull(w));
+            }
+            // epilogue: O / l -> bf16 -> global
+            mbar_wait(bar_ofull(w), 0);
+            tc_fence_after();
+            const float inv = 1.f / l_run;
+            uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD);
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t orr[32];
+                tmem_ld32(t_o + 32 * c, orr);
+                tmem_wait();
+                if (vrow) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float* f = reinterpret_cast<const float*>(orr + 8 * e);
+                        orow[4 * c + e] = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                                                     pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K8 KV commit: append the accepted path's K/V rows to the cache (one CTA per tree)
+// ---------------------------------------------------------------------------
+template <typename W>
+__global__ void __launch_bounds__(256) kv_commit_kernel(const W* __restrict__ k_new, const W* __restrict__ v_new,
+                                                        const int32_t* __restrict__ parent,
+                                                        const int32_t* __restrict__ path,
+                                                        const int32_t* __restrict__ path_len, W* k_cache, W* v_cache,
+                                                        int32_t* cache_len, int T, int S, int row_words,
+                                                        int32_t* dev_status) {
+    __shared__ int s_ok, s_L, s_r;
+    __shared__ int s_path[kMaxNodes];
+    pdl_trigger();
+    pdl_wait();
+    const int b = blockIdx.x, tid = threadIdx.x;
+    if (tid == 0) {
+        const int r = path_len[b], L = cache_len[b];
+        int ok = (r >= 1 && r <= T) ? 1 : 0;
+        for (int s = 0; ok && s < r; ++s) {
+            const int v = path[(size_t)b * T + s];
+            if (v < 0 || v >= T) ok = 0;
+            else if (s == 0 ? v != 0 : (parent && parent[(size_t)b * T + v] != s_path[s - 1])) ok = 0;
+            else s_path[s] = v;
+        }
+        int code = ok ? 0 : STREE_DEV_BAD_PATH;
+        if (ok && (L < 0 || L + r > S)) code = kDev_Capacity;
+        if (code) report(dev_status, code);
+        s_ok = code == 0;
+        s_L = L;
+        s_r = r;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    const int L = s_L, r = s_r;
+    for (int k = tid; k < r * row_words; k += blockDim.x) {
+        const int s = k / row_words, c = k % row_words;
+        const size_t src = ((size_t)b * T + s_path[s]) * row_words + c;
+        const size_t dst = ((size_t)b * S + L + s) * row_words + c;
+        k_cache[dst] = k_new[src];
+        v_cache[dst] = v_new[src];
+    }
+    __syncthreads();
+    if (tid == 0) cache_len[b] = L + r;
+}
+
+}  // namespace attn
+}  // namespace stree
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn attn_encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// bf16 4-D map over [d3][d2][d1][d0] (d0 innermost, contiguous), box {64, b1, b2, 1}, swizzle 128B
+bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b1,
+               uint32_t b2) {
+    EncodeTiledFn fn = attn_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {d0, d1, d2, d3};
+    cuuint64_t strides[3] = {d0 * 2, d0 * d1 * 2, d0 * d1 * d2 * 2};
+    cuuint32_t box[4] = {64, b1, b2, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" int stree_attn_tc_supports(const stree_attn_dims* d) {
+    if (!d || d->io_dtype != STREE_BF16 || d->head_dim != stree::attn::kD) return 0;
+    if (d->n_kv_heads < 1 || d->n_q_heads % d->n_kv_heads) return 0;
+    const int grp = d->n_q_heads / d->n_kv_heads;
+    if (grp > 128 || stree::attn::kBM % grp) return 0;
+    if (d->n_nodes < 1 || d->n_nodes > stree::kMaxNodes || d->cache_cap < 1) return 0;
+    return 1;
+}
+
+extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, const void* k_new, const void* v_new,
+                                      const void* k_cache, const void* v_cache, const int32_t* cache_len,
+                                      const int32_t* parent, float scale, void* o, int32_t* dev_status, int use_tc,
+                                      cudaStream_t s) {
+    using namespace stree::attn;
+    const int B = d->batch, T = d->n_nodes, Hq = d->n_q_heads, Hkv = d->n_kv_heads, D = d->head_dim, S = d->cache_cap;
+    cudaError_t e;
+    if (use_tc) {
+        const int grp = Hq / Hkv;
+        CUtensorMap mq, mkc, mvc, mkn, mvn;
+        bool ok = make_map4(&mq, q, D, Hq, T, B, grp, kBM / grp) &&
+                  make_map4(&mkc, k_cache, D, Hkv, S, B, 1, kBN) && make_map4(&mvc, v_cache, D, Hkv, S, B, 1, kBN) &&
+                  make_map4(&mkn, k_new, D, Hkv, T, B, 1, kBN) && make_map4(&mvn, v_new, D, Hkv, T, B, 1, kBN);
+        if (!ok) return (int)cudaErrorInvalidValue;
+        AttnParams prm{};
+        prm.cache_len = cache_len; prm.parent = parent; prm.o = (__nv_bfloat16*)o; prm.dev_status = dev_status;
+        prm.T = T; prm.Hq = Hq; prm.Hkv = Hkv; prm.S = S;
+        const int nmt = (T * grp + kBM - 1) / kBM;
+        prm.npairs = (nmt + 1) / 2;
+        prm.scale_log2 = scale * 1.4426950408889634f;
+        const size_t smem = Smem::TOTAL + 1024;
+        e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        e = stree::launch_k(attn_tc_kernel, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem, s, mq, mkc, mvc, mkn, mvn,
+                            prm);
+    } else {
+        dim3 grid(Hq, T, B);
+        if (d->io_dtype == STREE_BF16)
+            e = stree::launch_k(attn_simt_kernel<__nv_bfloat16>, grid, dim3(32), 0, s, (const __nv_bfloat16*)q,
+                                (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
+                                (const __nv_bfloat16*)k_cache, (const __nv_bfloat16*)v_cache, cache_len, parent, scale,
+                                (__nv_bfloat16*)o, T, Hq, Hkv, D, S, dev_status);
+        else
+            e = stree::launch_k(attn_simt_kernel<float>, grid, dim3(32), 0, s, (const float*)q, (const float*)k_new,
+                                (const float*)v_new, (const float*)k_cache, (const float*)v_cache, cache_len, parent,
+                                scale, (float*)o, T, Hq, Hkv, D, S, dev_status);
+    }
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int stree_launch_kv_commit(const stree_attn_dims* d, const void* k_new, const void* v_new,
+                                      const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                                      void* k_cache, void* v_cache, int32_t* cache_len, int32_t* dev_status,
+                                      cudaStream_t s) {
+    using namespace stree::attn;
+    const size_t row_bytes = (size_t)d->n_kv_heads * d->head_dim * (d->io_dtype == STREE_BF16 ? 2 : 4);
+    cudaError_t e;
+    if (row_bytes % 16 == 0)
+        e = stree::launch_k(kv_commit_kernel<uint4>, dim3(d->batch), dim3(256), 0, s, (const uint4*)k_new,
+                            (const uint4*)v_new, parent, path, path_len, (uint4*)k_cache, (uint4*)v_cache, cache_len,
+                            d->n_nodes, d->cache_cap, (int)(row_bytes / 16), dev_status);
+    else
+        e = stree::launch_k(kv_commit_kernel<uint32_t>, dim3(d->batch), dim3(256), 0, s, (const uint32_t*)k_new,
+                            (const uint32_t*)v_new, parent, path, path_len, (uint32_t*)k_cache, (uint32_t*)v_cache,
+                            cache_len, d->n_nodes, d->cache_cap, (int)(row_bytes / 4), dev_status);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
