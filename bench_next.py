@@ -72,6 +72,8 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
 
     stream = torch.cuda.Stream(device=dev)
     out = {}
+    # decode-loop launch promise: a layer's KV cache / conv state is not written by the kernel right before it
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE)
 
     # ---------------- tree attention + KV commit ----------------
     prob = attn_config("hyb8b")

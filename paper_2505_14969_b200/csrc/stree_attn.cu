@@ -22,6 +22,8 @@
 //                    lanes over keys, online softmax, fp32 throughout.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "stree_common.cuh"
 #include "stree_tc_ptx.cuh"
 
@@ -36,6 +38,53 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 2^x on the FMA pipe (offloads the 16/clk/SM MUFU): x = n + f, n = rint(x), f in [-1/2, 1/2];
+// 2^f by a degree-3 fit (max rel err 1.1e-4, below the bf16 rounding of P); 2^n added to the exponent.
+// Inputs below -126 are clamped (2^-126: the caller zeroes masked entries itself).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.f;                 // 1.5 * 2^23: rint(x) in the low mantissa bits
+    const float f = x - (t - 12582912.f);
+    const float p = fmaf(f, fmaf(f, fmaf(f, 0.05459818f, 0.24221842f), 0.69336758f), 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+    return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// two 2^x on the FMA pipe with paired fp32 ops (FADD2 / FFMA2): same split and polynomial as ex2_poly
+__device__ __forceinline__ void ex2_poly2(uint64_t a2, float& p0, float& p1) {
+    const uint64_t x = f2pack(fmaxf(__uint_as_float((uint32_t)a2), -126.f), fmaxf(__uint_as_float((uint32_t)(a2 >> 32)), -126.f));
+    const uint64_t t = fadd2(x, f2pack(12582912.f, 12582912.f));
+    const uint64_t r = fadd2(t, f2pack(-12582912.f, -12582912.f));
+    const uint64_t f = ffma2(r, f2pack(-1.f, -1.f), x);
+    uint64_t p = ffma2(f, f2pack(0.05459818f, 0.05459818f), f2pack(0.24221842f, 0.24221842f));
+    p = ffma2(p, f, f2pack(0.69336758f, 0.69336758f));
+    p = ffma2(p, f, f2pack(1.f, 1.f));
+    p0 = __int_as_float((int)(uint32_t)p + ((int)(uint32_t)t << 23));
+    p1 = __int_as_float((int)(uint32_t)(p >> 32) + ((int)(uint32_t)(t >> 32) << 23));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -150,7 +199,8 @@ struct Smem {
     static constexpr int K = Q + 2 * kTile;              // kStages key tiles
     static constexpr int V = K + kStages * kTile;        // kStages value tiles
     static constexpr int PAR = V + kStages * kTile;      // parent[256] int
-    static constexpr int BAR = PAR + kMaxNodes * 4;
+    static constexpr int ANC = PAR + kMaxNodes * 4;      // ancestor bits of each softmax row: [8 words][256 rows]
+    static constexpr int BAR = ANC + kMaxWords * 256 * 4;
     // barriers: qfull, kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], pfull[2], ofull[2]
     static constexpr int NBAR = 1 + 4 * kStages + 6;
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -181,10 +231,12 @@ struct AttnParams {
     const int32_t* parent;
     __nv_bfloat16* o;
     int32_t* dev_status;
-    int T, Hq, Hkv, S, npairs;
+    int T, Hq, Hkv, S, npairs, early;
+    unsigned long long* trace;
     float scale_log2;
 };
 
+template <int POLY>   // exp2: 0 = all on the MUFU, 1 = every 4th pair on the FMA pipe (ex2_poly2), 2 = every 2nd
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                    const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
@@ -199,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kvh = rem / prm.npairs, pr = rem % prm.npairs;
     const int nmt = (T * grp + kBM - 1) / kBM;
     const int nw = min(2, nmt - 2 * pr);               // query tiles of this CTA (1 or 2)
+    unsigned long long* tr = (prm.trace && blockIdx.x == 0) ? prm.trace : nullptr;   // debug timeline
     pdl_trigger();
 
     const uint32_t bar0 = sb + Smem::BAR;
@@ -233,8 +286,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // EARLY_STATE promise (stree_set_launch_flags): the KV cache and cache_len are not written by the kernel
+    // immediately preceding this one (true in a decode loop: the cache was committed an iteration earlier),
+    // so the first prefix tiles stream in before the dependency wait, overlapping the previous kernel
+    int n_early = 0;
+    auto issue_kv = [&](int j, bool pre, int key0) {
+        const int s = j % kStages;
+        mbar_expect_tx(bar_kfull(s), kTile);
+        for (int hf = 0; hf < 2; ++hf)
+            tma_load_4d(sb + Smem::K + s * kTile + hf * kHalf, pre ? &tm_kc : &tm_kn, bar_kfull(s), 64 * hf, kvh, key0, b);
+        mbar_expect_tx(bar_vfull(s), kTile);
+        for (int hf = 0; hf < 2; ++hf)
+            tma_load_4d(sb + Smem::V + s * kTile + hf * kHalf, pre ? &tm_vc : &tm_vn, bar_vfull(s), 64 * hf, kvh, key0, b);
+    };
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_q); tma_prefetch(&tm_kc); tma_prefetch(&tm_vc); tma_prefetch(&tm_kn); tma_prefetch(&tm_vn);
+        if (prm.early) {
+            const int Le = prm.cache_len[b];
+            if (Le > 0 && Le <= prm.S) {
+                n_early = min(kStages, (Le + kBN - 1) / kBN);
+                for (int j = 0; j < n_early; ++j) issue_kv(j, true, j * kBN);
+            }
+        }
     }
     pdl_wait();
     // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length
@@ -256,6 +329,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (code) {
         if (tid == 0 && rem == 0) report(prm.dev_status, code);
+        if (warp == 0 && lane == 0)   // drain the early loads before the CTA exits
+            for (int j = 0; j < n_early; ++j) {
+                mbar_wait(bar_kfull(j), 0);
+                mbar_wait(bar_vfull(j), 0);
+            }
         // zero this CTA's output rows
         if (warp >= 2) {
             const int w = (warp - 2) >> 2, r = 32 * (warp & 3) + lane;
@@ -277,20 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int hf = 0; hf < 2; ++hf)
                     tma_load_4d(sb + Smem::Q + w * kTile + hf * kHalf, &tm_q, BAR_Q, 64 * hf, kvh * grp, node0, b);
             }
-            for (int j = 0; j < nt; ++j) {
+            for (int j = n_early; j < nt; ++j) {
                 const int s = j % kStages, u = j / kStages;
                 const bool pre = j < npre;
                 const int key0 = pre ? j * kBN : (j - npre) * kBN;
                 mbar_wait(bar_kempty(s), (u & 1) ^ 1);
-                mbar_expect_tx(bar_kfull(s), kTile);
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_4d(sb + Smem::K + s * kTile + hf * kHalf, pre ? &tm_kc : &tm_kn, bar_kfull(s), 64 * hf,
-                                kvh, key0, b);
                 mbar_wait(bar_vempty(s), (u & 1) ^ 1);
-                mbar_expect_tx(bar_vfull(s), kTile);
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_4d(sb + Smem::V + s * kTile + hf * kHalf, pre ? &tm_vc : &tm_vn, bar_vfull(s), 64 * hf,
-                                kvh, key0, b);
+                if (tr && j < 64) tr[j] = gtimer();
+                issue_kv(j, pre, key0);
             }
         }
     } else if (warp == 1) {
@@ -316,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s1 = (j + 1) % kStages, u1 = (j + 1) / kStages;
             for (int w = 0; w < nw; ++w) {
                 mbar_wait(bar_pfull(w), j & 1);
+                if (tr && lane == 0 && j < 64) tr[128 + 2 * j + w] = gtimer();
                 if (w == 0) mbar_wait(bar_vfull(s), u & 1);
                 tc_fence_after();
                 const uint64_t vd = sdesc(sb + Smem::V + s * kTile, kHalf, 1024);
@@ -328,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (j + 1 < nt) {
                     if (w == 0) {
                         mbar_wait(bar_kfull(s1), u1 & 1);
+                        if (tr && lane == 0 && j < 64) tr[256 + j] = gtimer();
                         tc_fence_after();
                     }
                     issue_s(w, s1);
@@ -341,43 +415,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (w < nw) {
             const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
             const bool vrow = i < T;
-            uint32_t anc[kMaxWords];
+            // ancestor bits of the row's node, word-major in smem (conflict-free reads)
+            uint32_t* sanc = (uint32_t*)(sm + Smem::ANC) + 128 * w + r;
+            {
+                uint32_t anc[kMaxWords];
 #pragma unroll
-            for (int q = 0; q < kMaxWords; ++q) anc[q] = 0u;
-            if (vrow)
-                for (int v = i; v >= 0; v = sp[v]) {
+                for (int q = 0; q < kMaxWords; ++q) anc[q] = 0u;
+                if (vrow)
+                    for (int v = i; v >= 0; v = sp[v]) {
 #pragma unroll
-                    for (int q = 0; q < kMaxWords; ++q) anc[q] |= ((v >> 5) == q) ? (1u << (v & 31)) : 0u;
-                }
+                        for (int q = 0; q < kMaxWords; ++q) anc[q] |= ((v >> 5) == q) ? (1u << (v & 31)) : 0u;
+                    }
+#pragma unroll
+                for (int q = 0; q < kMaxWords; ++q) sanc[256 * q] = anc[q];
+            }
             const uint32_t lane_base = tmem + ((uint32_t)(32 * q4) << 16);
             const uint32_t t_s = lane_base + 128 * w, t_o = lane_base + 256 + 128 * w;
             const float sl2 = prm.scale_log2;
             float m_run = -INFINITY, l_run = 0.f;
             for (int j = 0; j < nt; ++j) {
                 mbar_wait(bar_sfull(w), j & 1);
+                if (tr && lane == 0 && q4 == 0 && j < 64) tr[384 + 2 * j + w] = gtimer();
                 tc_fence_after();
+                // valid-key bits of this row in the tile, one word per 32-column chunk: committed prefix
+                // keys [0, lim), or tree nodes on the row's root path
+                const bool pre = j < npre;
+                const int lim = pre ? L - j * kBN : T - (j - npre) * kBN;
+                const uint32_t* aw = sanc + 256 * 4 * (pre ? 0 : j - npre);
+                const bool full = pre && lim >= kBN;   // full prefix tile: no masking
                 uint32_t sr[128];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_ld32(t_s + 32 * c, sr + 32 * c);
                 tmem_wait();
-                float x[128];
-                const bool pre = j < npre;
-                if (pre) {
-                    const int lim = L - j * kBN;   // keys [0, lim) of this tile are committed
+                if (!full) {   // partial tile: masked scores -> -inf
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) x[c] = c < lim ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
-                } else {
-                    const int jt = j - npre, lim = T - jt * kBN;
-                    uint32_t aw[4];
+                    for (int c = 0; c < 4; ++c) {
+                        const int n = lim - 32 * c;
+                        uint32_t vw = n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+                        if (!pre) vw &= aw[256 * c];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) aw[q] = jt == 0 ? anc[q] : anc[4 + q];
-#pragma unroll
-                    for (int c = 0; c < 128; ++c)
-                        x[c] = (c < lim && ((aw[c >> 5] >> (c & 31)) & 1u)) ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
+                        for (int e = 0; e < 32; ++e) sr[32 * c + e] = ((vw >> e) & 1u) ? sr[32 * c + e] : 0xff800000u;
+                    }
                 }
-                float mx = x[0];
+                // row max: 8 independent FMNMX3 chains (latency, not throughput, bounds this step)
+                float m8[8];
 #pragma unroll
-                for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
+                for (int k = 0; k < 8; ++k) m8[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+                for (int e = 16; e < 128; e += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2)
+                        m8[k >> 1] = fmax3(m8[k >> 1], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+#pragma unroll
+                for (int e = 8; e < 128; e += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2)
+                        m8[4 + (k >> 1)] = fmax3(m8[4 + (k >> 1)], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+                float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                mx *= sl2;   // scale > 0
                 // lazy rescaling: keep the running max unless the new one exceeds it by > 8 (log2 units).
                 // tcgen05.ld/st are warp-collective: the O rescale runs warp-wide whenever any lane needs
                 // it (alpha = 1 for the others).
@@ -398,19 +493,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_st_wait();
                 }
                 const float mu = m_run == -INFINITY ? 0.f : m_run;
-                uint32_t pk[64];
-                float ls = 0.f;
+                // p = 2^(s·scale·log2e - m) (masked: 2^-inf = 0); paired FFMA2, 4 FADD2 sum chains; bf16 P
+                // packed in place over the consumed scores, then written over S's first 64 columns
+                const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(-mu, -mu);
+                uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const float p0 = ex2(x[2 * c] - mu), p1 = ex2(x[2 * c + 1] - mu);
-                    ls += p0 + p1;
-                    pk[c] = pack_bf16(p0, p1);
+                for (int e = 0; e < 64; ++e) {
+                    const uint64_t a2 = ffma2(f2pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nm2);
+                    float p0, p1;
+                    if (POLY == 2 ? (e & 1) : (POLY == 1 ? (e & 3) == 3 : false)) {
+                        ex2_poly2(a2, p0, p1);
+                        if (!full) {   // the polynomial does not map -inf to 0
+                            p0 = sr[2 * e] == 0xff800000u ? 0.f : p0;
+                            p1 = sr[2 * e + 1] == 0xff800000u ? 0.f : p1;
+                        }
+                    } else {
+                        p0 = ex2(__uint_as_float((uint32_t)a2));
+                        p1 = ex2(__uint_as_float((uint32_t)(a2 >> 32)));
+                    }
+                    acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
+                    sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
                 }
-                l_run += ls;
-                tmem_st32(t_s, pk);
-                tmem_st32(t_s + 32, pk + 32);
+                const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                l_run += __uint_as_float((uint32_t)a01) + __uint_as_float((uint32_t)(a01 >> 32));
+                tmem_st32(t_s, sr);
+                tmem_st32(t_s + 32, sr + 32);
                 tmem_st_wait();
                 tc_fence_before();
+                if (tr && lane == 0 && q4 == 0 && j < 64) tr[512 + 2 * j + w] = gtimer();
                 mbar_arrive(bar_pfull(w));
             }
             // epilogue: O / l -> bf16 -> global
@@ -527,6 +637,12 @@ bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 
 }  // namespace
 
+namespace {
+unsigned long long* g_attn_trace = nullptr;
+}
+// Debug hook (not part of the ABI): globaltimer stamps of CTA 0's pipeline events, 640 u64.
+extern "C" void stree_debug_attn_trace(unsigned long long* dev_buf) { g_attn_trace = dev_buf; }
+
 extern "C" int stree_attn_tc_supports(const stree_attn_dims* d) {
     if (!d || d->io_dtype != STREE_BF16 || d->head_dim != stree::attn::kD) return 0;
     if (d->n_kv_heads < 1 || d->n_q_heads % d->n_kv_heads) return 0;
@@ -556,11 +672,17 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
         const int nmt = (T * grp + kBM - 1) / kBM;
         prm.npairs = (nmt + 1) / 2;
         prm.scale_log2 = scale * 1.4426950408889634f;
+        prm.trace = g_attn_trace;
+        prm.early = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
         const size_t smem = Smem::TOTAL + 1024;
-        e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        static const int poly = [] {
+            const char* v = std::getenv("STREE_ATTN_POLY");   // tuning knob; default 0 (measured best)
+            return v && v[0] ? std::atoi(v) : 0;
+        }();
+        auto k = poly == 0 ? attn_tc_kernel<0> : (poly == 2 ? attn_tc_kernel<2> : attn_tc_kernel<1>);
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        e = stree::launch_k(attn_tc_kernel, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem, s, mq, mkc, mvc, mkn, mvn,
-                            prm);
+        e = stree::launch_k(k, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem, s, mq, mkc, mvc, mkn, mvn, prm);
     } else {
         dim3 grid(Hq, T, B);
         if (d->io_dtype == STREE_BF16)

@@ -234,3 +234,21 @@ def test_verify_commit_decode_matches_oracle():
     ref, _ = oattn.tree_attn(_f64(nxt, "q"), _f64(nxt, "k_new"), _f64(nxt, "v_new"), rk, rv, rcl, nxt.parent,
                              nxt.scale)
     check(o2.float().cpu().numpy().astype(np.float64), ref, TOL_BF16)
+
+
+def test_early_kv_prefetch_flag():
+    """STREE_LAUNCH_EARLY_STATE: the first K/V tiles stream before the PDL wait (decode-loop promise);
+    results unchanged, and an invalid tree still drains its early loads and reports."""
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE)
+    try:
+        prob = make_case(3, 64, 32, 8, 128, 1024, "bf16", 61, cache_len=[1000, 129, 0])
+        o, st = run_gpu(prob, expect_kernel=2)
+        ref, _ = run_oracle(prob)
+        assert st == 0
+        check(o, ref, TOL_BF16)
+        prob.parent[0, 3] = 7
+        o, st = run_gpu(prob, expect_kernel=2)
+        assert st == 2 and not o[0].any()
+        check(o[1:], ref[1:], TOL_BF16)
+    finally:
+        binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)

@@ -1,0 +1,52 @@
+"""Timeline of CTA 0 of the tcgen05 tree-attention kernel (globaltimer stamps; debug hook
+stree_debug_attn_trace).  Prints per-KV-tile event times relative to the first stamp (us)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from gen.attn import attn_config  # noqa: E402
+from paper_2505_14969_b200 import binding  # noqa: E402
+
+
+def main():
+    prob = attn_config("hyb8b")
+    dev = torch.device("cuda", 0)
+
+    def t(a):
+        return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).to(dev)
+    q, kn, vn, kc, vc = (t(getattr(prob, n)) for n in ("q", "k_new", "v_new", "k_cache", "v_cache"))
+    cl = torch.from_numpy(prob.cache_len).to(dev)
+    par = torch.from_numpy(prob.parent).to(dev)
+    o = torch.empty_like(q)
+    buf = torch.zeros(640, dtype=torch.int64, device=dev)
+    L = binding.lib()
+    L.stree_debug_attn_trace.argtypes = [ctypes.c_void_p]
+    for it in range(3):
+        binding.stree_tree_attn(q, kn, vn, kc, vc, cl, par, prob.scale, o)
+    torch.cuda.synchronize()
+    buf.zero_()
+    L.stree_debug_attn_trace(ctypes.c_void_p(buf.data_ptr()))
+    binding.stree_tree_attn(q, kn, vn, kc, vc, cl, par, prob.scale, o)
+    torch.cuda.synchronize()
+    L.stree_debug_attn_trace(None)
+    a = buf.cpu().numpy().astype(np.int64)
+    nz = a[a > 0]
+    t0 = nz.min()
+    f = lambda v: f"{(v - t0) / 1e3:7.2f}" if v > 0 else "    -  "
+    print("cache_len[0] =", prob.cache_len[0])
+    print(" j | kempty  vempty | kfull  | pfull0  pfull1 | sfull0  sfull1 | parr0   parr1")
+    for j in range(64):
+        row = [a[j], a[64 + j], a[256 + j], a[128 + 2 * j], a[129 + 2 * j], a[384 + 2 * j], a[385 + 2 * j],
+               a[512 + 2 * j], a[513 + 2 * j]]
+        if not any(row):
+            continue
+        print(f"{j:2d} | {f(row[0])} {f(row[1])} | {f(row[2])} | {f(row[3])} {f(row[4])} | {f(row[5])} {f(row[6])} | "
+              f"{f(row[7])} {f(row[8])}")
+
+
+if __name__ == "__main__":
+    main()
