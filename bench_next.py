@@ -11,6 +11,7 @@ replays, median over K replays; algorithmic bytes per call / time against the me
   kv_commit  stree_kv_commit of the accepted paths of those trees into each layer's cache
   tree_conv  stree_tree_conv on the Mamba-2 2.7B conv (conv_dim 5376 = H*P + 2*G*N, W = 4), c4 trees
   conv_commit stree_conv_commit along the accepted paths
+  accept_mss stree_accept_mss (multi-step speculative sampling) on the c4 trees, V = 50,280
 """
 from __future__ import annotations
 
@@ -173,10 +174,29 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
     ccbytes = B * (W - 1) * C * 2 * 2
     out["conv_commit"] = {"us": us_cc, "bytes": ccbytes, "GB/s": ccbytes / (us_cc * 1e-6) / 1e9,
                           "frac": ccbytes / (us_cc * 1e-6) / 1e9 / hbm_peak, "bound": "latency"}
-    torch.cuda.synchronize()
-    assert status.item() == 0, f"device status {status.item()}"
     del cl
     torch.cuda.empty_cache()
+
+    # ---------------- MSS verification (once per iteration) ----------------
+    from gen.mss import mss_config
+    mp = mss_config("c4")
+    md = {k: torch.from_numpy(getattr(mp, k)).to(dev) for k in ("tokens", "parent", "p_target", "q_draft",
+                                                                  "u_accept", "u_bonus")}
+    B, T = mp.parent.shape
+    mpath = torch.empty((B, T), dtype=torch.int32, device=dev)
+    mplen = torch.empty((B,), dtype=torch.int32, device=dev)
+    mbonus = torch.empty((B,), dtype=torch.int32, device=dev)
+
+    def mss_once():
+        binding.stree_accept_mss(md["tokens"], md["parent"], md["p_target"], md["q_draft"], md["u_accept"],
+                                 md["u_bonus"], mpath, mplen, mbonus, status)
+
+    us_m = _graph_time_us(mss_once, 1, stream)
+    out["accept_mss"] = {"us": us_m, "bound": "latency", "mean_path_len": float(mplen.float().mean().item()),
+                         "workload": "c4 trees (16 x 64 nodes), V=50280, target sigma=3, draft noise 1",
+                         "note": "one call per verify iteration; vocab rows touched depend on the rejections"}
+    torch.cuda.synchronize()
+    assert status.item() == 0, f"device status {status.item()}"
     return out
 
 

@@ -289,6 +289,27 @@ stree_status stree_kv_commit(const stree_attn_dims* d, const void* k_new, const 
 /* Which kernel stree_tree_attn would launch: 1 = SIMT (any shape, fp32), 2 = tcgen05, 0 = invalid. */
 int32_t stree_attn_kernel_for(const stree_attn_dims* d);
 
+/*
+ * stree_accept_mss — multi-step speculative sampling verification (SpecInfer MSS; SURVEY
+ * §8(f) NEXT #4; reading R-mss).  From the root, children are tried in increasing index order:
+ *   child c (token t) of cur is accepted iff u_accept[c]·q_draft[cur][t] < p[t]   (u < min(1, p/q));
+ *   on rejection p <- max(0, p - q_draft[cur]) / Σ (kept if that mass is 0);
+ *   on acceptance cur <- c and p <- p_target[c].
+ * When no child of cur is accepted: bonus = smallest v with Σ_{w<=v} p[w] > u_bonus·Σ_w p[w].
+ *   tokens   [B][T] int32       drafted tokens (tokens[0] is not compared); out-of-range tokens are rejected
+ *   parent   [B][T] int32
+ *   p_target [B][T][V] f32      target distribution after each node (post-temperature)
+ *   q_draft  [B][T][V] f32      draft distribution each node's children were drawn from
+ *   u_accept [B][T] f32 in [0,1) one uniform per child trial (indexed by the child node)
+ *   u_bonus  [B] f32 in [0,1)   the bonus sample's uniform
+ *   path, path_len, bonus       as for stree_accept
+ * Invalid tree b: dev_status <- 1/2, path_len = 0, path = -1, bonus = -1.  V <= 450,000.
+ */
+stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, const float* p_target,
+                              const float* q_draft, const float* u_accept, const float* u_bonus, int32_t batch,
+                              int32_t n_nodes, int32_t vocab, int32_t* path, int32_t* path_len, int32_t* bonus,
+                              int32_t* dev_status, void* stream);
+
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05, 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
 

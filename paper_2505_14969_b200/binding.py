@@ -72,6 +72,7 @@ def lib():
             "stree_tree_attn": [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, vp],
             "stree_kv_commit": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
             "stree_attn_kernel_for": [vp],
+            "stree_accept_mss": [vp, vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -90,7 +91,7 @@ STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY = 1, 2, 4
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
                     "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",
                     "stree_replay_scan", "stree_commit_kernel_for", "stree_tree_conv", "stree_conv_commit",
-                    "stree_tree_attn", "stree_kv_commit", "stree_attn_kernel_for")
+                    "stree_tree_attn", "stree_kv_commit", "stree_attn_kernel_for", "stree_accept_mss")
 
 
 def status_string(s: int) -> str:
@@ -237,3 +238,13 @@ def stree_kv_commit(k_new, v_new, parent, path, path_len, k_cache, v_cache, cach
 
 def stree_attn_kernel_for(dims: stree_attn_dims) -> int:
     return lib().stree_attn_kernel_for(ctypes.byref(dims))
+
+
+def stree_accept_mss(tokens, parent, p_target, q_draft, u_accept, u_bonus, path, path_len, bonus, dev_status=None,
+                     stream=None):
+    B, T = parent.shape
+    V = p_target.shape[-1]
+    _check("stree_accept_mss", lib().stree_accept_mss(_ptr(tokens), _ptr(parent), _ptr(p_target), _ptr(q_draft),
+                                                      _ptr(u_accept), _ptr(u_bonus), B, T, V, _ptr(path),
+                                                      _ptr(path_len), _ptr(bonus), _ptr(dev_status),
+                                                      _stream(stream)))

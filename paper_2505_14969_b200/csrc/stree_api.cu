@@ -39,6 +39,10 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims*, const void*, const
 extern "C" int stree_launch_kv_commit(const stree_attn_dims*, const void*, const void*, const int32_t*,
                                       const int32_t*, const int32_t*, void*, void*, int32_t*, int32_t*, cudaStream_t);
 
+extern "C" int stree_launch_accept_mss(const int32_t*, const int32_t*, const float*, const float*, const float*,
+                                       const float*, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
+                                       cudaStream_t);
+
 namespace {
 
 std::atomic<int> g_scan_impl{STREE_SCAN_AUTO};
@@ -331,5 +335,20 @@ stree_status stree_kv_commit(const stree_attn_dims* d, const void* k_new, const 
     cudaStream_t s = (cudaStream_t)stream;
     return finish(stree_launch_kv_commit(d, k_new, v_new, parent, path, path_len, k_cache, v_cache, cache_len,
                                          dev_status, s),
+                  dev_status, s);
+}
+
+stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, const float* p_target,
+                              const float* q_draft, const float* u_accept, const float* u_bonus, int32_t batch,
+                              int32_t n_nodes, int32_t vocab, int32_t* path, int32_t* path_len, int32_t* bonus,
+                              int32_t* dev_status, void* stream) {
+    if (batch < 0 || n_nodes < 0 || n_nodes > STREE_MAX_NODES || vocab < 0 || vocab > 450000) return STREE_ERR_SHAPE;
+    if (batch == 0 || n_nodes == 0) return STREE_OK;
+    if (vocab < 1) return STREE_ERR_SHAPE;
+    if (!tokens || !parent || !p_target || !q_draft || !u_accept || !u_bonus || !path || !path_len || !bonus)
+        return STREE_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    return finish(stree_launch_accept_mss(tokens, parent, p_target, q_draft, u_accept, u_bonus, batch, n_nodes, vocab,
+                                          path, path_len, bonus, dev_status, s),
                   dev_status, s);
 }

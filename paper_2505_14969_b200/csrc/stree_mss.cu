@@ -1,0 +1,259 @@
+// K9 stree_accept_mss: multi-step speculative sampling verification of a drafted tree (SURVEY §8(f)
+// NEXT #4; "MSS sampling" for temperature > 0; reading R-mss):
+//
+//   cur = root, p = p_target[cur]
+//   for each child c of cur (increasing index): t = tokens[c], q = q_draft[cur]
+//       accept iff u_accept[c]·q[t] < p[t]  -> path += c, cur = c, p = p_target[c], next level
+//       reject: r = max(0, p - q); if Σr > 0: p = r / Σr
+//   no child accepted: bonus = smallest v with Σ_{w<=v} p[w] > u_bonus·Σ p
+//
+// One thread-block CLUSTER of 8 CTAs per tree; CTA k keeps the vocabulary slice [k·S, (k+1)·S) of
+// the current distribution p in its shared memory (S = ceil(V/8): 25 KB at V = 50,280), so the
+// vocab-wide steps (residual, normalisation, inverse CDF) run on 8 SMs with reductions exchanged
+// through distributed shared memory (st.shared::cluster + barrier.cluster).  An acceptance test
+// needs only p[t] and q[t]: q[t] from global memory, p[t] from the owning CTA's slice (DSMEM) or,
+// for a fresh distribution, from global memory — accepted chains never touch the vocabulary.
+// Every CTA of the cluster takes every decision itself from bit-identical operands, so control
+// flow stays uniform across the cluster without broadcasts.
+#include "stree_common.cuh"
+
+namespace stree {
+namespace mss {
+
+constexpr int kCl = 8;          // CTAs per tree
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_cluster(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+// block-wide sum, deterministic order; every thread gets the result
+__device__ __forceinline__ float block_sum(float v, float* s_warp) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) s_warp[w] = v;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t += s_warp[i];
+    return t;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    mss_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+               const float* __restrict__ p_target, const float* __restrict__ q_draft,
+               const float* __restrict__ u_accept, const float* __restrict__ u_bonus, int T, int V, int slice,
+               int32_t* path, int32_t* path_len, int32_t* bonus, int32_t* dev_status) {
+    extern __shared__ __align__(16) float ps[];          // [slice]: this CTA's part of p
+    __shared__ int s_par[kMaxNodes];
+    __shared__ float s_warp[kWarps];
+    __shared__ float s_red[2][kCl];                      // cluster exchange of partial sums (double buffer)
+    __shared__ float s_scan[kWarps];
+    __shared__ int s_found;
+    pdl_trigger();
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_rank();
+    const int b = blockIdx.x / kCl;
+    const int v0 = rank * slice, v1 = min(V, v0 + slice), n = max(0, v1 - v0);
+    pdl_wait();
+    int bad = 0;
+    for (int i = tid; i < T; i += kThreads) {
+        const int p = parent[(size_t)b * T + i];
+        s_par[i] = p;
+        if (i == 0 ? p != -1 : (p < 0 || p >= i)) bad = i == 0 ? 1 : 2;
+    }
+    const int any1 = __syncthreads_or(bad == 1), any2 = __syncthreads_or(bad == 2);
+    if (any1 || any2) {
+        if (rank == 0) {
+            if (tid == 0) {
+                report(dev_status, any1 ? 1 : 2);
+                path_len[b] = 0;
+                bonus[b] = -1;
+            }
+            for (int i = tid; i < T; i += kThreads) path[(size_t)b * T + i] = -1;
+        }
+        return;   // uniform across the cluster (same parent array)
+    }
+    int red_buf = 0;
+    // cluster-wide sum of one float per CTA (every CTA gets the same value, same order)
+    auto cluster_sum = [&](float part) -> float {
+        if (tid < kCl) st_cluster(map_rank(&s_red[red_buf][rank], tid), part);
+        cluster_sync();
+        float z = 0.f;
+#pragma unroll
+        for (int k = 0; k < kCl; ++k) z += s_red[red_buf][k];
+        red_buf ^= 1;
+        return z;
+    };
+    auto load_fresh = [&](int node) {
+        const float* src = p_target + ((size_t)b * T + node) * V + v0;
+        for (int v = tid; v < n; v += kThreads) ps[v] = src[v];
+    };
+
+    int cur = 0, plen = 1;
+    bool loaded = false;          // ps holds the current (residual) distribution of cur
+    if (rank == 0 && tid == 0) path[(size_t)b * T] = 0;
+    for (;;) {
+        const float* qrow = q_draft + ((size_t)b * T + cur) * V;
+        int acc = -1;
+        for (int c = cur + 1; c < T; ++c) {
+            if (s_par[c] != cur) continue;
+            const int t = tokens[(size_t)b * T + c];
+            const bool tok_ok = t >= 0 && t < V;   // precondition; an out-of-range draft is simply rejected
+            const float qt = tok_ok ? qrow[t] : 1.f;
+            float pt;
+            if (!tok_ok) {
+                pt = 0.f;
+            } else if (loaded) {
+                const int owner = t / slice;
+                pt = ld_cluster(map_rank(&ps[t - owner * slice], owner));
+            } else {
+                pt = p_target[((size_t)b * T + cur) * V + t];
+            }
+            if (u_accept[(size_t)b * T + c] * qt < pt) {
+                acc = c;
+                break;
+            }
+            // rejected: residual r = max(0, p - q), renormalised when its mass is positive
+            if (!loaded) {
+                load_fresh(cur);
+                loaded = true;
+            }
+            float part = 0.f;
+            for (int v = tid; v < n; v += kThreads) part += fmaxf(0.f, ps[v] - qrow[v0 + v]);
+            part = block_sum(part, s_warp);
+            const float z = cluster_sum(part);   // also orders every CTA's reads of ps before the writes
+            if (z > 0.f) {
+                const float inv = 1.f / z;
+                for (int v = tid; v < n; v += kThreads) ps[v] = fmaxf(0.f, ps[v] - qrow[v0 + v]) * inv;
+            }
+            cluster_sync();                      // writes visible before any remote p[t] read
+        }
+        if (acc < 0) break;
+        if (loaded) cluster_sync();   // peers' remote reads of p[t] complete before ps is reloaded
+        if (rank == 0 && tid == 0) path[(size_t)b * T + plen] = acc;
+        ++plen;
+        cur = acc;
+        loaded = false;
+    }
+    // bonus: inverse CDF of p over the vocabulary, slice by slice
+    if (!loaded) {
+        load_fresh(cur);
+        __syncthreads();
+    }
+    // each thread owns a contiguous chunk of the slice
+    const int per = (n + kThreads - 1) / kThreads;
+    const int c0 = min(n, tid * per), c1 = min(n, c0 + per);
+    float tsum = 0.f;
+    for (int v = c0; v < c1; ++v) tsum += ps[v];
+    const float part = block_sum(tsum, s_warp);
+    // slice sums of all ranks (same values in every CTA)
+    if (tid < kCl) st_cluster(map_rank(&s_red[red_buf][rank], tid), part);
+    cluster_sync();
+    float sums[kCl], z = 0.f;
+#pragma unroll
+    for (int k = 0; k < kCl; ++k) {
+        sums[k] = s_red[red_buf][k];
+        z += sums[k];
+    }
+    const float thr = u_bonus[b] * z;
+    int target = -1, last_pos = -1;
+    float before = 0.f, cum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kCl; ++k) {
+        if (target < 0 && cum + sums[k] > thr) { target = k; before = cum; }
+        cum += sums[k];
+        if (sums[k] > 0.f) last_pos = k;
+    }
+    const bool fallback = target < 0;   // rounding left no CDF step above the threshold
+    if (fallback) target = last_pos;
+    if ((int)rank == target) {
+        // exclusive scan of the thread chunk sums (deterministic: warp scan + warp totals)
+        const int w = tid >> 5, l = tid & 31;
+        float x = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        if (l == 31) s_scan[w] = x;
+        if (tid == 0) s_found = -1;
+        __syncthreads();
+        float wbase = 0.f;
+        for (int i = 0; i < w; ++i) wbase += s_scan[i];
+        float run = before + wbase + x - tsum;   // cumulative mass before this thread's chunk
+        if (!fallback) {
+            for (int v = c0; v < c1; ++v) {
+                run += ps[v];
+                if (run > thr) { atomicMin(reinterpret_cast<unsigned*>(&s_found), (unsigned)(v0 + v)); break; }
+            }
+        }
+        __syncthreads();
+        if (s_found == -1) {   // fallback (or the threshold fell past this slice's last step): last v with p > 0
+            int lp = -1;
+            for (int v = c0; v < c1; ++v)
+                if (ps[v] > 0.f) lp = v0 + v;
+            atomicMax(&s_found, lp);
+            __syncthreads();
+        }
+        if (tid == 0) bonus[b] = s_found;
+    }
+    if (rank == 0) {
+        for (int i = plen + tid; i < T; i += kThreads) path[(size_t)b * T + i] = -1;
+        if (tid == 0) path_len[b] = plen;
+    }
+    cluster_sync();   // no CTA exits while a peer may still read its shared memory
+}
+
+}  // namespace mss
+}  // namespace stree
+
+extern "C" int stree_launch_accept_mss(const int32_t* tokens, const int32_t* parent, const float* p_target,
+                                       const float* q_draft, const float* u_accept, const float* u_bonus, int B,
+                                       int T, int V, int32_t* path, int32_t* path_len, int32_t* bonus,
+                                       int32_t* dev_status, cudaStream_t s) {
+    using namespace stree::mss;
+    const int slice = (V + kCl - 1) / kCl;
+    const size_t smem = (size_t)slice * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B * kCl);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (stree_launch_flags_get() & STREE_LAUNCH_PDL) ? 2 : 1;
+    e = cudaLaunchKernelEx(&cfg, mss_kernel, tokens, parent, p_target, q_draft, u_accept, u_bonus, T, V, slice, path,
+                           path_len, bonus, dev_status);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
