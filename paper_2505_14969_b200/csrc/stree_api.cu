@@ -249,7 +249,8 @@ stree_status stree_tree_conv(const stree_conv_dims* d, const void* u, const floa
     if (st != STREE_OK) return st;
     if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
     if (!u || !weight || !parent || !out) return STREE_ERR_NULL;
-    if (!aligned16(u) || !aligned16(out) || (conv_state && !aligned16(conv_state))) return STREE_ERR_ALIGN;
+    if (!aligned16(u) || !aligned16(out) || !aligned16(weight) || (conv_state && !aligned16(conv_state)))
+        return STREE_ERR_ALIGN;
     const size_t es = d->io_dtype == STREE_BF16 ? 2 : 4;
     const size_t bytes = (size_t)d->batch * d->n_nodes * d->channels * es;
     const char *a = (const char*)u, *o = (const char*)out;

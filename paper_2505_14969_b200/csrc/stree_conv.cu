@@ -57,7 +57,7 @@ __host__ __device__ constexpr size_t tree_conv_smem(int T, int W) {
 }
 
 template <typename IO, int W>
-__global__ void __launch_bounds__(kThreads) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
+__global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
                                                              const float* __restrict__ bias, const IO* __restrict__ state,
                                                              const int32_t* __restrict__ parent, int act,
                                                              IO* __restrict__ out, int T, int C, int32_t* dev_status) {
@@ -71,49 +71,79 @@ __global__ void __launch_bounds__(kThreads) tree_conv_kernel(const IO* __restric
     const bool cv = c0 + lane * V < C;                                     // this lane's chunk exists
     pdl_trigger();
     if (tid == 0) s_bad = 0;
-    // the thread's channels: weights and bias in registers (model parameters, not produced upstream)
+    // the block's weights and bias (model parameters, not produced upstream: loaded before the dependency
+    // wait) staged through shared memory with coalesced loads, [w][v][lane] so the per-thread reads below
+    // are conflict-free, then each thread's channels into registers
+    __shared__ float s_w[4 * 8 * kChunks];
+    __shared__ float s_b[8 * kChunks];
+    {
+        const int nc = min(kChunks * V, C - c0);   // channels of this block
+        for (int k = tid; k < nc * W; k += kThreads) {
+            const int cl = k / W, w = k % W;
+            s_w[(w * V + cl % V) * kChunks + cl / V] = weight[(size_t)c0 * W + k];
+        }
+        for (int k = tid; k < nc; k += kThreads) s_b[(k % V) * kChunks + k / V] = bias ? bias[c0 + k] : 0.f;
+    }
+    __syncthreads();
     float wt[W][V], bs[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-        const int c = c0 + lane * V + v;
 #pragma unroll
-        for (int w = 0; w < W; ++w) wt[w][v] = cv ? weight[(size_t)c * W + w] : 0.f;
-        bs[v] = (cv && bias) ? bias[c] : 0.f;
+        for (int w = 0; w < W; ++w) wt[w][v] = cv ? s_w[(w * V + v) * kChunks + lane] : 0.f;
+        bs[v] = cv ? s_b[v * kChunks + lane] : 0.f;
     }
     pdl_wait();
     for (int i = tid; i < T; i += kThreads) sp[i] = parent[(size_t)b * T + i];
     // stage the state rows and the tree's rows of this channel block (one coalesced pass)
-    for (int r = wy; r < (W - 1) + T; r += kThreads / 32) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (cv) {
-            if (r < W - 1) {
-                if (state) v = *reinterpret_cast<const uint4*>(state + ((size_t)b * (W - 1) + r) * C + c0 + lane * V);
-            } else {
-                v = *reinterpret_cast<const uint4*>(u + ((size_t)b * T + (r - (W - 1))) * C + c0 + lane * V);
-            }
+    // batches of kBatch independent 16-byte loads per thread in flight (one latency per batch, not per
+    // row): addresses are clamped to valid rows so the loads are unconditional, zeros selected after
+    constexpr int kBatch = 9, kWy = kThreads / 32;   // 9 x 8 warps = 72 >= 3 + 64 rows: one batch at T = 64
+    const int nrows = (W - 1) + T;
+    const size_t cofs = (size_t)c0 + (cv ? lane * V : 0);
+    for (int r0 = wy; r0 < nrows; r0 += kWy * kBatch) {
+        uint4 v[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const int r = min(r0 + kWy * k, nrows - 1);
+            const IO* src = (r < W - 1) ? (state ? state + ((size_t)b * (W - 1) + r) * C : u + (size_t)b * T * C)
+                                        : u + ((size_t)b * T + (r - (W - 1))) * C;
+            v[k] = __ldg(reinterpret_cast<const uint4*>(src + cofs));
         }
-        rows[r * kChunks + lane] = v;
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const int r = r0 + kWy * k;
+            const bool zero = !cv || (r < W - 1 && !state);
+            if (r < nrows) rows[r * kChunks + lane] = zero ? make_uint4(0, 0, 0, 0) : v[k];
+        }
     }
     __syncthreads();
-    // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i (root error takes precedence)
+    // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i (root error takes precedence); the same
+    // pass tabulates every node's window rows (oldest first: ancestors at distance W-1 .. 1, then the node;
+    // above the root the chain continues into the state rows W-2, W-3, ...) so the main loop's shared-memory
+    // loads are independent
+    __shared__ int s_win[kMaxNodes * 4];
     for (int i = tid; i < T; i += kThreads) {
         const int p = sp[i];
         if (i == 0 ? p != -1 : (p < 0 || p >= i)) atomicMax(&s_bad, i == 0 ? 2 : 1);
+        int v = i, srow = W - 1;
+        s_win[i * W + W - 1] = (W - 1) + i;
+#pragma unroll
+        for (int k = 1; k < W; ++k) {
+            if (v >= 0) {
+                const int pv = sp[v];
+                v = (pv >= 0 && pv < v) ? pv : -1;
+            }
+            s_win[i * W + W - 1 - k] = v >= 0 ? (W - 1) + v : --srow;
+        }
     }
     __syncthreads();
     const int bad = s_bad;
     if (bad && tid == 0 && blockIdx.x == 0) report(dev_status, bad == 2 ? 1 : 2);
+#pragma unroll 2
     for (int i = wy; i < T; i += kThreads / 32) {
-        // rows of the window, oldest first: ancestors at distance W-1 .. 1, then the node itself;
-        // above the root the chain continues into the state rows W-2, W-3, ...
         int rw[W];
-        rw[W - 1] = (W - 1) + i;
-        int v = i, srow = W - 1;
 #pragma unroll
-        for (int k = 1; k < W; ++k) {
-            if (v >= 0) v = bad ? -1 : sp[v];
-            rw[W - 1 - k] = v >= 0 ? (W - 1) + v : --srow;
-        }
+        for (int k = 0; k < W; ++k) rw[k] = s_win[i * W + k];
         float z[V];
 #pragma unroll
         for (int q = 0; q < V; ++q) z[q] = bs[q];
@@ -126,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) tree_conv_kernel(const IO* __restric
         }
         if (act) {
 #pragma unroll
-            for (int q = 0; q < V; ++q) z[q] = z[q] / (1.f + __expf(-z[q]));
+            for (int q = 0; q < V; ++q) z[q] = __fdividef(z[q], 1.f + __expf(-z[q]));
         }
         if (bad) {
 #pragma unroll
@@ -196,7 +226,10 @@ cudaError_t launch_conv(const stree_conv_dims* d, const void* u, const float* we
     dim3 grid((C / V + kChunks - 1) / kChunks, d->batch);
     const size_t smem = tree_conv_smem(T, W);
     auto k = tree_conv_kernel<IO, W>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_conv_smem(kMaxNodes, 4));
+    // one wave at the 2.7B shape (336 CTAs over 148 SMs needs 3 resident per SM): registers capped by the
+    // launch bounds, shared-memory carveout at its maximum
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     return launch_k(k, grid, dim3(kThreads), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent, act,
                     (IO*)out, T, C, dev_status);
