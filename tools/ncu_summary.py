@@ -25,7 +25,9 @@ API = {"scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "
        "scan_tc_kernel<128, 0>": "stree_tree_scan", "scan_tc_kernel<64, 0>": "stree_tree_scan",
        "scan_tc_kernel<128, 2>": "stree_commit", "scan_tc_kernel<64, 2>": "stree_commit",
        "commit_ring_kernel": "stree_commit", "commit_block_kernel": "stree_commit",
-       "build_mask_kernel": "stree_build_mask", "accept_kernel": "stree_accept"}
+       "build_mask_kernel": "stree_build_mask", "accept_kernel": "stree_accept",
+       "attn_tc_kernel": "stree_tree_attn", "attn_simt_kernel": "stree_tree_attn", "kv_commit_kernel": "stree_kv_commit",
+       "tree_conv_kernel": "stree_tree_conv", "conv_commit_kernel": "stree_conv_commit", "mss_kernel": "stree_accept_mss"}
 
 
 def api_name(k):
@@ -49,6 +51,18 @@ if os.path.exists(nf):
         wr = sum(m["dram__bytes_write.sum"]) / len(t)
         print(f"{k[:60]:60s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  share={sum(t) / tn * 100:5.1f}%  "
               f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB")
+        traffic.setdefault(api_name(k), rd + wr)
+nx = os.path.join(out, "launches_next.csv")
+if os.path.exists(nx):
+    print("== launch list, SURVEY §8(f) rows (tools/prof_attn.py = bench_next at 4 layers) ==")
+    px = launches(nx)
+    for k, m in sorted(px.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
+        t = m["gpu__time_duration.sum"]
+        rd = sum(m["dram__bytes_read.sum"]) / len(t)
+        wr = sum(m["dram__bytes_write.sum"]) / len(t)
+        tp = m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", [0.0])
+        print(f"{api_name(k):18s} {k[:50]:50s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  "
+              f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB  tensor pipe {sum(tp) / len(tp):5.1f}%")
         traffic.setdefault(api_name(k), rd + wr)
 print("== launch list (ncu --cache-control none, serialised): per-kernel mean over launches ==")
 per = launches(os.path.join(out, "launches.csv"))
