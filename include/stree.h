@@ -303,7 +303,8 @@ int32_t stree_attn_kernel_for(const stree_attn_dims* d);
  *   u_accept [B][T] f32 in [0,1) one uniform per child trial (indexed by the child node)
  *   u_bonus  [B] f32 in [0,1)   the bonus sample's uniform
  *   path, path_len, bonus       as for stree_accept
- * Invalid tree b: dev_status <- 1/2, path_len = 0, path = -1, bonus = -1.  V <= 450,000.
+ * Invalid tree b: dev_status <- 1/2, path_len = 0, path = -1, bonus = -1.  V <= 150,000 (three vocabulary
+ * slices of V/8 floats per CTA in shared memory).
  */
 stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, const float* p_target,
                               const float* q_draft, const float* u_accept, const float* u_bonus, int32_t batch,

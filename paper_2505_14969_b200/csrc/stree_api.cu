@@ -343,7 +343,7 @@ stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, cons
                               const float* q_draft, const float* u_accept, const float* u_bonus, int32_t batch,
                               int32_t n_nodes, int32_t vocab, int32_t* path, int32_t* path_len, int32_t* bonus,
                               int32_t* dev_status, void* stream) {
-    if (batch < 0 || n_nodes < 0 || n_nodes > STREE_MAX_NODES || vocab < 0 || vocab > 450000) return STREE_ERR_SHAPE;
+    if (batch < 0 || n_nodes < 0 || n_nodes > STREE_MAX_NODES || vocab < 0 || vocab > 150000) return STREE_ERR_SHAPE;
     if (batch == 0 || n_nodes == 0) return STREE_OK;
     if (vocab < 1) return STREE_ERR_SHAPE;
     if (!tokens || !parent || !p_target || !q_draft || !u_accept || !u_bonus || !path || !path_len || !bonus)

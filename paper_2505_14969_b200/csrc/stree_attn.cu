@@ -236,7 +236,8 @@ struct AttnParams {
     float scale_log2;
 };
 
-template <int POLY>   // exp2: 0 = all on the MUFU, 1 = every 4th pair on the FMA pipe (ex2_poly2), 2 = every 2nd
+template <int POLY>   // exp2: 0 = all on the MUFU; on the FMA pipe (ex2_poly2): 1 = every 4th pair, 3 = every 3rd,
+                      // 2 = every 2nd
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                    const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
@@ -447,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) tmem_ld32(t_s + 32 * c, sr + 32 * c);
                 tmem_wait();
+                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 0] = gtimer();
                 if (!full) {   // partial tile: masked scores -> -inf
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -473,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         m8[4 + (k >> 1)] = fmax3(m8[4 + (k >> 1)], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
                 float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
                 mx *= sl2;   // scale > 0
+                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 1] = gtimer();
                 // lazy rescaling: keep the running max unless the new one exceeds it by > 8 (log2 units).
                 // tcgen05.ld/st are warp-collective: the O rescale runs warp-wide whenever any lane needs
                 // it (alpha = 1 for the others).
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int e = 0; e < 64; ++e) {
                     const uint64_t a2 = ffma2(f2pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nm2);
                     float p0, p1;
-                    if (POLY == 2 ? (e & 1) : (POLY == 1 ? (e & 3) == 3 : false)) {
+                    if (POLY == 2 ? (e & 1) : (POLY == 1 ? (e & 3) == 3 : (POLY == 3 ? (e % 3) == 2 : false))) {
                         ex2_poly2(a2, p0, p1);
                         if (!full) {   // the polynomial does not map -inf to 0
                             p0 = sr[2 * e] == 0xff800000u ? 0.f : p0;
@@ -513,12 +516,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
                     sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
+                    if (e == 31) tmem_st32(t_s, sr);   // P columns [0, 32) (S columns [0, 64) consumed): frees sr[0..31]
                 }
+                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 2] = gtimer();
                 const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 l_run += __uint_as_float((uint32_t)a01) + __uint_as_float((uint32_t)(a01 >> 32));
-                tmem_st32(t_s, sr);
                 tmem_st32(t_s + 32, sr + 32);
                 tmem_st_wait();
+                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 3] = gtimer();
                 tc_fence_before();
                 if (tr && lane == 0 && q4 == 0 && j < 64) tr[512 + 2 * j + w] = gtimer();
                 mbar_arrive(bar_pfull(w));
@@ -640,7 +645,7 @@ bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 namespace {
 unsigned long long* g_attn_trace = nullptr;
 }
-// Debug hook (not part of the ABI): globaltimer stamps of CTA 0's pipeline events, 640 u64.
+// Debug hook (not part of the ABI): globaltimer stamps of CTA 0's pipeline events, 1024 u64.
 extern "C" void stree_debug_attn_trace(unsigned long long* dev_buf) { g_attn_trace = dev_buf; }
 
 extern "C" int stree_attn_tc_supports(const stree_attn_dims* d) {
@@ -679,7 +684,8 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
             const char* v = std::getenv("STREE_ATTN_POLY");   // tuning knob; default 0 (measured best)
             return v && v[0] ? std::atoi(v) : 0;
         }();
-        auto k = poly == 0 ? attn_tc_kernel<0> : (poly == 2 ? attn_tc_kernel<2> : attn_tc_kernel<1>);
+        auto k = poly == 1 ? attn_tc_kernel<1>
+                           : (poly == 2 ? attn_tc_kernel<2> : (poly == 3 ? attn_tc_kernel<3> : attn_tc_kernel<0>));
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem, s, mq, mkc, mvc, mkn, mvn, prm);
