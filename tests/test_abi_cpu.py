@@ -78,3 +78,47 @@ def test_scan_kernel_selection(L):
     assert b.stree_scan_kernel_for(big) in (1, 2)
     with pytest.raises(b.StreeError):
         b.stree_set_scan_impl(9)
+
+
+def test_host_validation_next_rows(L):
+    """§8(f) calls: tree attention, KV commit, MSS verification, tree conv — host-side codes."""
+    from paper_2505_14969_b200 import binding as b
+    vp = ctypes.c_void_p
+    fake, mis = vp(0x10000), vp(0x10004)
+    f = ctypes.c_float(0.125)
+    d = b.stree_attn_dims(2, 16, 32, 8, 128, 1024, b.STREE_BF16)
+    z = b.stree_attn_dims(0, 16, 32, 8, 128, 1024, b.STREE_BF16)
+    assert L.stree_tree_attn(ctypes.byref(z), None, None, None, None, None, None, None, f, None, None, None) == 0
+    assert L.stree_tree_attn(None, fake, fake, fake, fake, fake, fake, fake, f, fake, None, None) == 1
+    assert L.stree_tree_attn(ctypes.byref(d), fake, fake, fake, fake, fake, None, fake, f, fake, None, None) == 1
+    gqa = b.stree_attn_dims(2, 16, 30, 8, 128, 1024, b.STREE_BF16)      # Hq % Hkv != 0
+    assert L.stree_tree_attn(ctypes.byref(gqa), fake, fake, fake, fake, fake, fake, fake, f, fake, None, None) == 2
+    wide = b.stree_attn_dims(2, 16, 32, 8, 512, 1024, b.STREE_BF16)     # D > 256
+    assert L.stree_tree_attn(ctypes.byref(wide), fake, fake, fake, fake, fake, fake, fake, f, fake, None, None) == 2
+    dtb = b.stree_attn_dims(2, 16, 32, 8, 128, 1024, 9)
+    assert L.stree_tree_attn(ctypes.byref(dtb), fake, fake, fake, fake, fake, fake, fake, f, fake, None, None) == 3
+    assert L.stree_tree_attn(ctypes.byref(d), mis, fake, fake, fake, fake, fake, fake, f, fake, None, None) == 4
+    # kernel selection: bf16 D=128 with (Hq/Hkv) | 128 -> tcgen05; fp32 or grp=3 -> SIMT
+    assert b.stree_attn_kernel_for(d) == 2
+    assert b.stree_attn_kernel_for(b.stree_attn_dims(2, 16, 32, 8, 128, 1024, b.STREE_F32)) == 1
+    assert b.stree_attn_kernel_for(b.stree_attn_dims(2, 16, 12, 4, 128, 1024, b.STREE_BF16)) == 1
+    # KV commit: NULL / row size not a multiple of 4 bytes / alignment
+    assert L.stree_kv_commit(ctypes.byref(d), fake, fake, None, fake, fake, fake, fake, None, None, None) == 1
+    odd = b.stree_attn_dims(2, 16, 1, 1, 1, 64, b.STREE_BF16)             # 2-byte rows
+    assert L.stree_kv_commit(ctypes.byref(odd), fake, fake, None, fake, fake, fake, fake, fake, None, None) == 2
+    assert L.stree_kv_commit(ctypes.byref(d), mis, fake, None, fake, fake, fake, fake, fake, None, None) == 4
+    # MSS: vocabulary bound, NULLs, empty
+    i32 = ctypes.c_int32
+    assert L.stree_accept_mss(fake, fake, fake, fake, fake, fake, i32(2), i32(8), i32(200000), fake, fake, fake,
+                              None, None) == 2
+    assert L.stree_accept_mss(fake, fake, None, fake, fake, fake, i32(2), i32(8), i32(1000), fake, fake, fake,
+                              None, None) == 1
+    assert L.stree_accept_mss(None, None, None, None, None, None, i32(0), i32(8), i32(1000), None, None, None,
+                              None, None) == 0
+    # tree conv: width out of range, channels not a multiple of the vector width, misaligned weight
+    cd = b.stree_conv_dims(2, 16, 5376, 4, b.STREE_BF16)
+    w5 = b.stree_conv_dims(2, 16, 5376, 5, b.STREE_BF16)
+    assert L.stree_tree_conv(ctypes.byref(w5), fake, fake, None, None, fake, 1, fake, None, None) == 2
+    c7 = b.stree_conv_dims(2, 16, 5377, 4, b.STREE_BF16)
+    assert L.stree_tree_conv(ctypes.byref(c7), fake, fake, None, None, fake, 1, fake, None, None) == 2
+    assert L.stree_tree_conv(ctypes.byref(cd), fake, mis, None, None, fake, 1, fake, None, None) == 4
