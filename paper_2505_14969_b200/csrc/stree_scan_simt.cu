@@ -63,10 +63,10 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
     const int code = build_tree_rows(sp, T, W, rows, (uint32_t*)(smem_raw + L.rows2), (int*)(smem_raw + L.jmp),
                                      (int*)(smem_raw + L.jmp2));
     if (code) {
-        if (tid == 0 && h == 0) report(dev_status, code);
+        if (tid == 0 && h == 0 && blockIdx.z == 0) report(dev_status, code);
         for (int k = tid; k < T * P; k += 256) {
             int i = k / P, p = k % P;
-            y[(((size_t)b * T + i) * H + h) * P + p] = from_f32<IO>(0.f);
+            if ((i / kTile) % (int)gridDim.z == (int)blockIdx.z) y[(((size_t)b * T + i) * H + h) * P + p] = from_f32<IO>(0.f);
         }
         return;
     }
@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
     }
     __syncthreads();
 
+    // row tiles are spread over blockIdx.z (one 64-node tile of rows per CTA) so that a single tree still
+    // fills the machine; every CTA rebuilds the (cheap) tree prologue
     for (int pc = 0; pc < P; pc += kTile) {
-        for (int rc = 0; rc < T; rc += kTile) {
+        for (int rc = blockIdx.z * kTile; rc < T; rc += kTile * gridDim.z) {
             const int jmax = min(T, rc + kTile);   // columns j <= i < rc + 64
             float acc[4][4];
 #pragma unroll
@@ -130,17 +132,50 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
                 }
             }
             // ---- decay-masked weights M[i][j] = L_ij e^{Λ_i-Λ_j} dt_j (C_i·B_j) ----
-            for (int k = tid; k < kTile * jmax; k += 256) {
-                int rr = k / jmax, j = k % jmax, i = rc + rr;
-                float w = 0.f;
-                if (i < T && mask_bit(rows, W, i, j)) {
-                    const IO* ci = Cm + (((size_t)b * T + i) * G + g) * N;
-                    const IO* bj = Bm + (((size_t)b * T + j) * G + g) * N;
-                    float dot = 0.f;
-                    for (int n = 0; n < N; ++n) dot = fmaf(to_f32(ci[n]), to_f32(bj[n]), dot);
-                    w = expf(fminf(lam[i] - lam[j], 0.f)) * dtv[j] * dot;
+            // G = C·Bᵀ for this row tile, 64 x 64 register-tiled over N chunks staged in shared memory
+            // (the same pattern as Y0; CsT holds C chunk [n][row], HsT is reused for B chunk [n][j])
+            for (int jc = 0; jc < jmax; jc += kTile) {
+                float gacc[4][4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) gacc[r][c] = 0.f;
+                for (int nc = 0; nc < N; nc += kTile) {
+                    __syncthreads();
+                    for (int k = tid; k < kTile * kTile; k += 256) {
+                        int rr = k / kTile, nn = k % kTile;
+                        int i = rc + rr, j = jc + rr, n = nc + nn;
+                        CsT[nn * kPitch + rr] =
+                            (i < T && n < N) ? to_f32(Cm[(((size_t)b * T + i) * G + g) * N + n]) : 0.f;
+                        HsT[nn * kPitch + rr] =
+                            (j < jmax && n < N) ? to_f32(Bm[(((size_t)b * T + j) * G + g) * N + n]) : 0.f;
+                    }
+                    __syncthreads();
+#pragma unroll 8
+                    for (int nn = 0; nn < kTile; ++nn) {
+                        float4 a = *reinterpret_cast<const float4*>(&CsT[nn * kPitch + ty * 4]);
+                        float4 bb = *reinterpret_cast<const float4*>(&HsT[nn * kPitch + tx * 4]);
+                        float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) gacc[r][c] = fmaf(av[r], bv[c], gacc[r][c]);
+                    }
                 }
-                Ms[rr * mp + j] = w;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int rr = ty * 4 + r, i = rc + rr;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int j = jc + tx * 4 + c;
+                        if (j < jmax) {
+                            float w = 0.f;
+                            if (i < T && mask_bit(rows, W, i, j))
+                                w = expf(fminf(lam[i] - lam[j], 0.f)) * dtv[j] * gacc[r][c];
+                            Ms[rr * mp + j] = w;
+                        }
+                    }
+                }
             }
             for (int k = tid; k < jmax * kTile; k += 256) {
                 int j = k / kTile, pp = k % kTile, p = pc + pp;
@@ -186,7 +221,7 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
                                       const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s) {
     const int T = d->n_nodes;
     size_t smem = stree::SimtSmem(T).total;
-    dim3 grid(d->n_heads, d->batch);
+    dim3 grid(d->n_heads, d->batch, (T + stree::kTile - 1) / stree::kTile);
     cudaError_t e;
     if (d->io_dtype == STREE_BF16) {
         auto k = stree::scan_simt_kernel<__nv_bfloat16>;
