@@ -56,6 +56,19 @@ __host__ __device__ constexpr size_t tree_conv_smem(int T, int W) {
     return (size_t)kMaxNodes * 4 + (size_t)((W - 1) + T) * kChunks * 16;
 }
 
+// SiLU: bf16 outputs take x·σ(x) with σ(x) = ½ tanh(x/2) + ½ (one MUFU op; tanh.approx's 2^-11 error is
+// far below the bf16 rounding of the output); fp32 outputs keep the exp + division form (the 1e-4 path)
+template <typename IO>
+__device__ __forceinline__ float silu(float z);
+template <>
+__device__ __forceinline__ float silu<__nv_bfloat16>(float z) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
+    return z * fmaf(0.5f, t, 0.5f);
+}
+template <>
+__device__ __forceinline__ float silu<float>(float z) { return __fdividef(z, 1.f + __expf(-z)); }
+
 template <typename IO, int W>
 __global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
                                                              const float* __restrict__ bias, const IO* __restrict__ state,
@@ -71,28 +84,20 @@ __global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __rest
     const bool cv = c0 + lane * V < C;                                     // this lane's chunk exists
     pdl_trigger();
     if (tid == 0) s_bad = 0;
-    // the block's weights and bias (model parameters, not produced upstream: loaded before the dependency
-    // wait) staged through shared memory with coalesced loads, [w][v][lane] so the per-thread reads below
-    // are conflict-free, then each thread's channels into registers
+    // the block's weights and bias: coalesced loads issued together with the parent and staging loads below
+    // (one memory latency for all of them), then through shared memory, [w][v][lane] so the per-thread reads
+    // are conflict-free
     __shared__ float s_w[4 * 8 * kChunks];
     __shared__ float s_b[8 * kChunks];
-    {
-        const int nc = min(kChunks * V, C - c0);   // channels of this block
-        for (int k = tid; k < nc * W; k += kThreads) {
-            const int cl = k / W, w = k % W;
-            s_w[(w * V + cl % V) * kChunks + cl / V] = weight[(size_t)c0 * W + k];
-        }
-        for (int k = tid; k < nc; k += kThreads) s_b[(k % V) * kChunks + k / V] = bias ? bias[c0 + k] : 0.f;
-    }
-    __syncthreads();
-    float wt[W][V], bs[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) wt[w][v] = cv ? s_w[(w * V + v) * kChunks + lane] : 0.f;
-        bs[v] = cv ? s_b[v * kChunks + lane] : 0.f;
-    }
     pdl_wait();
+    const int nc = min(kChunks * V, C - c0);   // channels of this block (nc * W <= 4 * kThreads)
+    float wv[4], bv;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = tid + q * kThreads;
+        wv[q] = k < nc * W ? __ldg(weight + (size_t)c0 * W + k) : 0.f;
+    }
+    bv = (tid < nc && bias) ? __ldg(bias + c0 + tid) : 0.f;
     for (int i = tid; i < T; i += kThreads) sp[i] = parent[(size_t)b * T + i];
     // stage the state rows and the tree's rows of this channel block (one coalesced pass)
     // batches of kBatch independent 16-byte loads per thread in flight (one latency per batch, not per
@@ -116,7 +121,23 @@ __global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __rest
             if (r < nrows) rows[r * kChunks + lane] = zero ? make_uint4(0, 0, 0, 0) : v[k];
         }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = tid + q * kThreads;
+        if (k < nc * W) {
+            const int cl = k / W, w = k % W;
+            s_w[(w * V + cl % V) * kChunks + cl / V] = wv[q];
+        }
+    }
+    if (tid < nc) s_b[(tid % V) * kChunks + tid / V] = bv;
     __syncthreads();
+    float wt[W][V], bs[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) wt[w][v] = cv ? s_w[(w * V + v) * kChunks + lane] : 0.f;
+        bs[v] = cv ? s_b[v * kChunks + lane] : 0.f;
+    }
     // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i (root error takes precedence); the same
     // pass tabulates every node's window rows (oldest first: ancestors at distance W-1 .. 1, then the node;
     // above the root the chain continues into the state rows W-2, W-3, ...) so the main loop's shared-memory
@@ -156,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __rest
         }
         if (act) {
 #pragma unroll
-            for (int q = 0; q < V; ++q) z[q] = __fdividef(z[q], 1.f + __expf(-z[q]));
+            for (int q = 0; q < V; ++q) z[q] = silu<IO>(z[q]);
         }
         if (bad) {
 #pragma unroll

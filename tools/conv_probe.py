@@ -49,8 +49,8 @@ st = torch.randn((B, 3, C), device=dev).to(torch.bfloat16)
 out = torch.empty_like(u)
 par = torch.from_numpy(par_np.astype(np.int32)).to(dev)
 binding.stree_set_launch_flags(0)
-for it in range(3):
-    binding.stree_tree_conv(u, w, bias, st, par, out, True)
+for it in range(4):
+    binding.stree_tree_conv(u, w, bias, st, par, out, it < 2)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 8)()
     L.stree_debug_conv_trace(buf)
