@@ -27,7 +27,7 @@ cat $OUT/profile_summary.txt
 # launch list of bench_next (attention, KV commit, conv, conv commit, MSS) and a --set full
 # capture of the tree-attention kernel
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed \
-    --clock-control none -k regex:'attn_|kv_commit|tree_conv|conv_commit|mss_' -c 200 --csv \
+    --clock-control none -k regex:'attn_|kv_commit|tree_conv|conv_commit|mss_' -c 400 --csv \
     --log-file $OUT/launches_next.csv python tools/prof_attn.py > $OUT/ncu_launches_next.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 4 -c 1 -o $OUT/prof_attn \
     python tools/prof_attn.py > $OUT/ncu_attn.log 2>&1
