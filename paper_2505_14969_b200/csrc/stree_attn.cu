@@ -190,6 +190,7 @@ constexpr int kBM = 128;            // query rows per tile
 constexpr int kBN = 128;            // keys per K/V tile
 constexpr int kStages = 2;
 constexpr int kThreads = 320;       // warp 0 TMA, warp 1 MMA, warps 2-5 softmax tile 0, 6-9 softmax tile 1
+constexpr int kThreadsSplit = 576;  // warp 0 TMA, warp 1 MMA, warps 2-9 softmax tile 0, 10-17 softmax tile 1
 constexpr int kHalf = kBM * 128;    // one 128-row x 64-element (128 B) swizzle-128B box = 16 KB
 constexpr int kTile = 2 * kHalf;    // 128 rows x 128 elements
 constexpr uint32_t kTmemCols = 512;
@@ -205,7 +206,8 @@ struct Smem {
     static constexpr int NBAR = 1 + 4 * kStages + 6;
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int MISC = TMEMP + 16;              // int: bad flag, L
-    static constexpr int TOTAL = MISC + 16;
+    static constexpr int XCH = MISC + 16;                // float [2 parity][2 tiles][2 halves][128 rows]
+    static constexpr int TOTAL = XCH + 2 * 2 * 2 * 128 * 4;
     static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
 };
 
@@ -236,9 +238,12 @@ struct AttnParams {
     float scale_log2;
 };
 
-template <int POLY>   // exp2: 0 = all on the MUFU; on the FMA pipe (ex2_poly2): 1 = every 4th pair, 3 = every 3rd,
-                      // 2 = every 2nd
-__global__ void __launch_bounds__(kThreads, 1)
+// POLY: exp2 on the MUFU (0) or every 4th pair on the FMA pipe (1).  SPLIT: two softmax warps per TMEM lane
+// quadrant and query tile, each owning 64 of the 128 score columns of its 32 rows (18 warps), so the exp
+// phase of a tile runs at MUFU throughput instead of one warp's latency; row max and row sum are combined
+// through shared memory with a 64-thread named barrier per (tile, quadrant).
+template <int POLY, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? kThreadsSplit : kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                    const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
                    const __grid_constant__ CUtensorMap tm_vn, const AttnParams prm) {
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int w = 0; w < 2; ++w) {
             mbar_init(bar_sfull(w), 1);
-            mbar_init(bar_pfull(w), 128);
+            mbar_init(bar_pfull(w), SPLIT ? 256 : 128);
             mbar_init(bar_ofull(w), 1);
         }
         fence_barrier_init();
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();
     // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length
     int bad = 0;
-    for (int v = tid; v < T; v += kThreads) {
+    for (int v = tid; v < T; v += (int)blockDim.x) {
         const int p = prm.parent[(size_t)b * T + v];
         sp[v] = p;
         if (v == 0 ? p != -1 : (p < 0 || p >= v)) bad = v == 0 ? 1 : 2;
@@ -336,8 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(bar_vfull(j), 0);
             }
         // zero this CTA's output rows
-        if (warp >= 2) {
-            const int w = (warp - 2) >> 2, r = 32 * (warp & 3) + lane;
+        if (warp >= 2 && (!SPLIT || ((warp - 2) & 7) < 4)) {
+            const int w = SPLIT ? (warp - 2) >> 3 : (warp - 2) >> 2, r = 32 * (warp & 3) + lane;
             if (w < nw) {
                 const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
                 if (i < T) {
@@ -395,8 +400,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t vd = sdesc(sb + Smem::V + s * kTile, kHalf, 1024);
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
-                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 8 * kk, vd + (uint64_t)(kk * 128), id_o,
-                                 (j > 0 || kk > 0) ? 1u : 0u);
+                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 8 * kk + ((SPLIT && kk >= 4) ? 32 : 0),
+                                 vd + (uint64_t)(kk * 128), id_o, (j > 0 || kk > 0) ? 1u : 0u);
                 if (w == nw - 1) tc_commit_w(bar_vempty(s));
                 if (j == nt - 1) tc_commit_w(bar_ofull(w));
                 if (j + 1 < nt) {
@@ -411,12 +416,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ---- softmax: thread = query row = TMEM lane ----
-        const int w = (warp - 2) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
+        // ---- softmax: thread = query row = TMEM lane (SPLIT: and one half of the score columns) ----
+        constexpr int kCols = SPLIT ? 64 : 128;            // score columns per thread
+        const int sw = SPLIT ? (warp - 2) & 7 : (warp - 2) & 3;
+        const int w = SPLIT ? (warp - 2) >> 3 : (warp - 2) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
+        const int hh = SPLIT ? sw >> 2 : 0;                 // column half
         if (w < nw) {
             const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
             const bool vrow = i < T;
-            // ancestor bits of the row's node, word-major in smem (conflict-free reads)
+            // ancestor bits of the row's node, word-major in smem (conflict-free reads); the
+            // two halves write identical values
             uint32_t* sanc = (uint32_t*)(sm + Smem::ANC) + 128 * w + r;
             {
                 uint32_t anc[kMaxWords];
@@ -430,13 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < kMaxWords; ++q) sanc[256 * q] = anc[q];
             }
+            float* xch = (float*)(sm + Smem::XCH);          // [parity][tile][half][row]
+            auto pair_sync = [&]() { if (SPLIT) named_bar(1 + 4 * w + q4, 64); };
             const uint32_t lane_base = tmem + ((uint32_t)(32 * q4) << 16);
             const uint32_t t_s = lane_base + 128 * w, t_o = lane_base + 256 + 128 * w;
             const float sl2 = prm.scale_log2;
+            const bool tr0 = tr && w == 0 && hh == 0 && lane == 0 && q4 == 0;
             float m_run = -INFINITY, l_run = 0.f;
             for (int j = 0; j < nt; ++j) {
                 mbar_wait(bar_sfull(w), j & 1);
-                if (tr && lane == 0 && q4 == 0 && j < 64) tr[384 + 2 * j + w] = gtimer();
+                if (tr && hh == 0 && lane == 0 && q4 == 0 && j < 64) tr[384 + 2 * j + w] = gtimer();
                 tc_fence_after();
                 // valid-key bits of this row in the tile, one word per 32-column chunk: committed prefix
                 // keys [0, lim), or tree nodes on the row's root path
@@ -444,99 +456,170 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int lim = pre ? L - j * kBN : T - (j - npre) * kBN;
                 const uint32_t* aw = sanc + 256 * 4 * (pre ? 0 : j - npre);
                 const bool full = pre && lim >= kBN;   // full prefix tile: no masking
-                uint32_t sr[128];
+                // valid-key word of global 32-column chunk cg
+                auto valid_word = [&](int cg) -> uint32_t {
+                    const int n = lim - 32 * cg;
+                    uint32_t vw = n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+                    if (!pre) vw &= aw[256 * cg];
+                    return vw;
+                };
+                float mx;
+                uint32_t sr[SPLIT ? 32 : 128];
+                if (SPLIT) {
+                    // two chunks of 32 columns, scores reloaded for the exp pass (TMEM reads are cheap;
+                    // registers are not at 18 warps)
+                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(t_s + 32 * c, sr + 32 * c);
-                tmem_wait();
-                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 0] = gtimer();
-                if (!full) {   // partial tile: masked scores -> -inf
+                    for (int c = 0; c < 2; ++c) {
+                        tmem_ld32(t_s + 64 * hh + 32 * c, sr);
+                        tmem_wait();
+                        const uint32_t vw = full ? 0xffffffffu : valid_word(2 * hh + c);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int n = lim - 32 * c;
-                        uint32_t vw = n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
-                        if (!pre) vw &= aw[256 * c];
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) sr[32 * c + e] = ((vw >> e) & 1u) ? sr[32 * c + e] : 0xff800000u;
+                        for (int e = 0; e < 32; e += 2)
+                            m4[(e >> 1) & 3] = fmax3(m4[(e >> 1) & 3], ((vw >> e) & 1u) ? __uint_as_float(sr[e]) : -INFINITY,
+                                                     ((vw >> (e + 1)) & 1u) ? __uint_as_float(sr[e + 1]) : -INFINITY);
                     }
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                    if (tr0 && j < 64) tr[640 + 4 * j + 0] = gtimer();
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) tmem_ld32(t_s + 32 * c, sr + 32 * c);
+                    tmem_wait();
+                    if (tr0 && j < 64) tr[640 + 4 * j + 0] = gtimer();
+                    if (!full) {   // partial tile: masked scores -> -inf
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint32_t vw = valid_word(c);
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) sr[32 * c + e] = ((vw >> e) & 1u) ? sr[32 * c + e] : 0xff800000u;
+                        }
+                    }
+                    // row max: 8 independent FMNMX3 chains (latency, not throughput, bounds this step)
+                    float m8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) m8[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+                    for (int e = 16; e < 128; e += 16)
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2)
+                            m8[k >> 1] = fmax3(m8[k >> 1], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+#pragma unroll
+                    for (int e = 8; e < 128; e += 16)
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2)
+                            m8[4 + (k >> 1)] = fmax3(m8[4 + (k >> 1)], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+                    mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
                 }
-                // row max: 8 independent FMNMX3 chains (latency, not throughput, bounds this step)
-                float m8[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) m8[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
-#pragma unroll
-                for (int e = 16; e < 128; e += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; k += 2)
-                        m8[k >> 1] = fmax3(m8[k >> 1], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
-#pragma unroll
-                for (int e = 8; e < 128; e += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; k += 2)
-                        m8[4 + (k >> 1)] = fmax3(m8[4 + (k >> 1)], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
-                float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                if (SPLIT) {   // combine with the other half (double-buffered by tile parity: no WAR barrier)
+                    float* xm = xch + (((j & 1) * 2 + w) * 2) * 128;
+                    xm[hh * 128 + r] = mx;
+                    pair_sync();
+                    mx = fmaxf(mx, xm[(hh ^ 1) * 128 + r]);
+                }
                 mx *= sl2;   // scale > 0
-                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 1] = gtimer();
+                if (tr0 && j < 64) tr[640 + 4 * j + 1] = gtimer();
                 // lazy rescaling: keep the running max unless the new one exceeds it by > 8 (log2 units).
                 // tcgen05.ld/st are warp-collective: the O rescale runs warp-wide whenever any lane needs
-                // it (alpha = 1 for the others).
+                // it (alpha = 1 for the others); each half rescales its own O columns.
                 const bool need = mx > m_run + 8.f;
                 const float alpha = need ? (m_run == -INFINITY ? 0.f : ex2(m_run - mx)) : 1.f;
                 if (need) m_run = mx;
                 l_run *= alpha;
                 if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < kCols / 32; ++c) {
                         uint32_t orr[32];
-                        tmem_ld32(t_o + 32 * c, orr);
+                        tmem_ld32(t_o + kCols * hh + 32 * c, orr);
                         tmem_wait();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-                        tmem_st32(t_o + 32 * c, orr);
+                        tmem_st32(t_o + kCols * hh + 32 * c, orr);
                     }
                     tmem_st_wait();
                 }
                 const float mu = m_run == -INFINITY ? 0.f : m_run;
                 // p = 2^(s·scale·log2e - m) (masked: 2^-inf = 0); paired FFMA2, 4 FADD2 sum chains; bf16 P
-                // packed in place over the consumed scores, then written over S's first 64 columns
+                // packed in place over the consumed scores, then written over S's columns (this half's keys
+                // land in packed columns [kCols/2·hh, +kCols/2); with SPLIT both halves have loaded their S
+                // before the max exchange, so neither overwrites the other's unread scores)
+                // SPLIT: the two query tiles' exp phases alternate (tile 0 of KV tile j, tile 1 of j, tile 0 of
+                // j+1, ...): the MUFU is shared by the whole SM, so each phase runs alone at its throughput
+                // while the tensor core works on the other tile's PV + next S
+                if (SPLIT && nw == 2) {
+                    if (w == 1) mbar_wait(bar_pfull(0), j & 1);
+                    else if (j > 0) mbar_wait(bar_pfull(1), (j - 1) & 1);
+                }
                 const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(-mu, -mu);
                 uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int e = 0; e < 64; ++e) {
-                    const uint64_t a2 = ffma2(f2pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nm2);
-                    float p0, p1;
-                    if (POLY == 2 ? (e & 1) : (POLY == 1 ? (e & 3) == 3 : (POLY == 3 ? (e % 3) == 2 : false))) {
+                auto exp_pair = [&](uint32_t s0, uint32_t s1, int e, float& p0, float& p1) {
+                    const uint64_t a2 = ffma2(f2pack(__uint_as_float(s0), __uint_as_float(s1)), sc2, nm2);
+                    if (POLY == 1 && (e & 3) == 3) {
                         ex2_poly2(a2, p0, p1);
                         if (!full) {   // the polynomial does not map -inf to 0
-                            p0 = sr[2 * e] == 0xff800000u ? 0.f : p0;
-                            p1 = sr[2 * e + 1] == 0xff800000u ? 0.f : p1;
+                            p0 = s0 == 0xff800000u ? 0.f : p0;
+                            p1 = s1 == 0xff800000u ? 0.f : p1;
                         }
                     } else {
                         p0 = ex2(__uint_as_float((uint32_t)a2));
                         p1 = ex2(__uint_as_float((uint32_t)(a2 >> 32)));
                     }
-                    acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
-                    sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
-                    if (e == 31) tmem_st32(t_s, sr);   // P columns [0, 32) (S columns [0, 64) consumed): frees sr[0..31]
+                };
+                if (SPLIT) {
+                    // this half's 64 keys -> packed P columns [32·hh, 32·hh + 32), 16 per chunk
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t pk[16];
+                        tmem_ld32(t_s + 64 * hh + 32 * c, sr);
+                        tmem_wait();
+                        const uint32_t vw = full ? 0xffffffffu : valid_word(2 * hh + c);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            float p0, p1;
+                            exp_pair(((vw >> (2 * e)) & 1u) ? sr[2 * e] : 0xff800000u,
+                                     ((vw >> (2 * e + 1)) & 1u) ? sr[2 * e + 1] : 0xff800000u, e, p0, p1);
+                            acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
+                            pk[e] = pack_bf16(p0, p1);
+                        }
+                        // P of this half's keys goes over its own first score chunk (already consumed): keys
+                        // [64·hh, +64) -> columns [64·hh, 64·hh + 32); the PV MMA reads them from there
+                        tmem_st16(t_s + 64 * hh + 16 * c, pk);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) {
+                        float p0, p1;
+                        exp_pair(sr[2 * e], sr[2 * e + 1], e, p0, p1);
+                        acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
+                        sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
+                        if (e == 31) tmem_st32(t_s, sr);   // P columns [0, 32): frees sr[0..31]
+                    }
+                    tmem_st32(t_s + 32, sr + 32);
                 }
-                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 2] = gtimer();
+                if (tr0 && j < 64) tr[640 + 4 * j + 2] = gtimer();
                 const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 l_run += __uint_as_float((uint32_t)a01) + __uint_as_float((uint32_t)(a01 >> 32));
-                tmem_st32(t_s + 32, sr + 32);
                 tmem_st_wait();
-                if (tr && w == 0 && lane == 0 && q4 == 0 && j < 64) tr[640 + 4 * j + 3] = gtimer();
+                if (tr0 && j < 64) tr[640 + 4 * j + 3] = gtimer();
                 tc_fence_before();
-                if (tr && lane == 0 && q4 == 0 && j < 64) tr[512 + 2 * j + w] = gtimer();
+                if (tr && hh == 0 && lane == 0 && q4 == 0 && j < 64) tr[512 + 2 * j + w] = gtimer();
                 mbar_arrive(bar_pfull(w));
             }
-            // epilogue: O / l -> bf16 -> global
+            // epilogue: O / l -> bf16 -> global (SPLIT: each half stores its 64 output columns; l = the sum of
+            // the two halves' partial sums, which were rescaled identically)
             mbar_wait(bar_ofull(w), 0);
             tc_fence_after();
+            if (SPLIT) {
+                float* xl = xch + ((((nt & 1) * 2 + w) * 2) * 128);
+                xl[hh * 128 + r] = l_run;
+                pair_sync();
+                l_run += xl[(hh ^ 1) * 128 + r];
+            }
             const float inv = 1.f / l_run;
-            uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD);
+            uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD) + (kCols / 8) * hh;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < kCols / 32; ++c) {
                 uint32_t orr[32];
-                tmem_ld32(t_o + 32 * c, orr);
+                tmem_ld32(t_o + kCols * hh + 32 * c, orr);
                 tmem_wait();
                 if (vrow) {
 #pragma unroll
@@ -684,11 +767,16 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
             const char* v = std::getenv("STREE_ATTN_POLY");   // tuning knob; default 0 (measured best)
             return v && v[0] ? std::atoi(v) : 0;
         }();
-        auto k = poly == 1 ? attn_tc_kernel<1>
-                           : (poly == 2 ? attn_tc_kernel<2> : (poly == 3 ? attn_tc_kernel<3> : attn_tc_kernel<0>));
+        static const int split = [] {
+            const char* v = std::getenv("STREE_ATTN_SPLIT");   // tuning knob; default 0 (measured faster)
+            return v && v[0] ? std::atoi(v) : 0;
+        }();
+        auto k = split ? (poly == 1 ? attn_tc_kernel<1, true> : attn_tc_kernel<0, true>)
+                       : (poly == 1 ? attn_tc_kernel<1, false> : attn_tc_kernel<0, false>);
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        e = stree::launch_k(k, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem, s, mq, mkc, mvc, mkn, mvn, prm);
+        e = stree::launch_k(k, dim3(B * Hkv * prm.npairs), dim3(split ? kThreadsSplit : kThreads), smem, s, mq, mkc,
+                            mvc, mkn, mvn, prm);
     } else {
         dim3 grid(Hq, T, B);
         if (d->io_dtype == STREE_BF16)

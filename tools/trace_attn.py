@@ -14,6 +14,9 @@ from paper_2505_14969_b200 import binding  # noqa: E402
 
 def main():
     prob = attn_config("hyb8b")
+    if "--one-tile" in sys.argv:   # T = 32 nodes x 4 heads = 128 rows: one query tile per CTA (no ping-pong)
+        from gen.attn import AttnDims, make_attn_problem
+        prob = make_attn_problem(AttnDims(16, 32), prob.parent[:, :32], 7, cache_len=[1280] * 16)
     dev = torch.device("cuda", 0)
 
     def t(a):
@@ -22,7 +25,7 @@ def main():
     cl = torch.from_numpy(prob.cache_len).to(dev)
     par = torch.from_numpy(prob.parent).to(dev)
     o = torch.empty_like(q)
-    buf = torch.zeros(640, dtype=torch.int64, device=dev)
+    buf = torch.zeros(1024, dtype=torch.int64, device=dev)
     L = binding.lib()
     L.stree_debug_attn_trace.argtypes = [ctypes.c_void_p]
     for it in range(3):
@@ -44,8 +47,9 @@ def main():
                a[512 + 2 * j], a[513 + 2 * j]]
         if not any(row):
             continue
+        sm = [a[640 + 4 * j + k] for k in range(4)]
         print(f"{j:2d} | {f(row[0])} {f(row[1])} | {f(row[2])} | {f(row[3])} {f(row[4])} | {f(row[5])} {f(row[6])} | "
-              f"{f(row[7])} {f(row[8])}")
+              f"{f(row[7])} {f(row[8])} | softmax0: ld {f(sm[0])} max {f(sm[1])} exp {f(sm[2])} st {f(sm[3])}")
 
 
 if __name__ == "__main__":
