@@ -19,6 +19,10 @@ extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*
                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
                                     cudaStream_t);
 extern "C" int stree_tc_supports(const stree_dims*);
+extern "C" int stree_tc128_supports(const stree_dims*);
+extern "C" int stree_launch_scan_tc128(const stree_dims*, const void*, const float*, const float*, const void*,
+                                       const void*, const float*, const float*, const int32_t*, void*, int32_t*,
+                                       cudaStream_t);
 extern "C" int stree_launch_tree_conv(const stree_conv_dims*, const void*, const float*, const float*, const void*,
                                       const int32_t*, int, void*, int32_t*, cudaStream_t);
 extern "C" int stree_launch_conv_commit(const stree_conv_dims*, const void*, const void*, const int32_t*,
@@ -128,6 +132,7 @@ int32_t stree_scan_kernel_for(const stree_dims* d) {
     int impl = g_scan_impl.load();
     if (impl == STREE_SCAN_SIMT) return 1;
     if (stree_tc_supports(d)) return 2;
+    if (stree_tc128_supports(d)) return 3;
     return impl == STREE_SCAN_TC ? 0 : 1;
 }
 
@@ -153,8 +158,9 @@ stree_status stree_tree_scan(const stree_dims* d, const void* x, const float* dt
     cudaStream_t s = (cudaStream_t)stream;
     int which = stree_scan_kernel_for(d);
     if (which == 0) return STREE_ERR_UNSUPPORTED;
-    int rc = (which == 2) ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
-                          : stree_launch_scan_simt(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s);
+    int rc = (which == 2)   ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
+             : (which == 3) ? stree_launch_scan_tc128(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
+                            : stree_launch_scan_simt(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s);
     return finish(rc, dev_status, s);
 }
 

@@ -1,0 +1,468 @@
+// K2b stree_tree_scan for 64 < T <= 128 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Same method as K2 (stree_scan_tc.cu, Mamba-2 realisation SURVEY R1-R3):
+//     G   = C·Bᵀ                 (T x T, K = N)    kind::f16   once per tree
+//     Y0  = C·h0_hᵀ              (T x P, K = N)    kind::tf32  per head (A = C as tf32 in TMEM)
+//     Y'  = (L∘G∘c_h)·X_h        (T x P, K = T)    kind::f16   per head
+//     y_i = e^{Λ_i} (Y0 + Y')_i + D_h x_i     (factorised decay, c_j = e^{-Λ_j} dt_j, when min Λ >= -64)
+//     y_i = e^{Λ_i} Y0_i + Y'_i + D_h x_i     (direct decay, M'_ij = e^{min(Λ_i-Λ_j,0)} dt_j G_ij, otherwise)
+// but with the tree's nodes in all 128 TMEM lanes (K2 puts them in lanes 0-63 and a copy of G in 64-127),
+// so trees of up to 128 nodes stay on the tensor cores instead of the FP32 SIMT kernel.  A simpler pipeline
+// than K2: one CTA per (tree, chunk of <= 10 heads of one group), 192 threads —
+//   warps 0-3  thread = node = TMEM lane: tree prologue (validation, ancestor bits and Λ of every head by
+//              pointer jumping), C -> tf32 into TMEM, then per head the masked weights M' (G row from TMEM
+//              -> bf16 swizzle-128B K-major smem tile) and the epilogue of the previous head
+//   warp 4     TMA producer: C, B once; per head the 32 KB fp32 state (4 boxes) and the x tile, 2-stage rings
+//   warp 5     tcgen05.mma issuer + TMEM allocator (512 columns: G 0-127, C tf32 128-255, two head slots of
+//              Y0 / Y' accumulators 256-511)
+// Served: bf16 io, P = 64, N = 128, 1 <= T <= 128 (dispatched for T > 64).
+#include <cuda.h>
+
+#include "stree_common.cuh"
+#include "stree_tc_ptx.cuh"
+
+namespace stree {
+namespace tc128 {
+
+using namespace stree::tc;
+
+constexpr int kT = 128, kP = 64, kN = 128;
+constexpr int kHPC = 10;
+constexpr int kThreads = 192;
+constexpr int kTile = 16384;          // 128 rows x 128 bytes, swizzle-128B
+constexpr uint32_t kCols = 512;
+constexpr int kGCol = 0, kCCol = 128, kAccCol = 256;   // accumulator slot a: Y0 at 256 + 128a, Y' at +64
+
+struct Sm {
+    static constexpr int C = 0;                    // C bf16: 2 k-chunks x 16 KB
+    static constexpr int B = C + 2 * kTile;        // B bf16: 2 k-chunks (dead after G: M' buffer 1)
+    static constexpr int M0 = B + 2 * kTile;       // M' buffer 0: 2 k-chunks (keys 0-63, 64-127)
+    static constexpr int H = M0 + 2 * kTile;       // state ring: 2 x 32 KB (4 boxes of 64 rows x 32 fp32)
+    static constexpr int X = H + 2 * 32768;        // x ring: 2 x 16 KB (128 rows x 64 bf16)
+    static constexpr int PAR = X + 2 * kTile / 2 * 2;
+    static constexpr int ANC = PAR + kT * 4;       // u32 [2][4][128]
+    static constexpr int JMP = ANC + 2 * 4 * kT * 4;   // int [2][128]
+    static constexpr int LAM = JMP + 2 * kT * 4;   // float [2][kHPC][128]
+    static constexpr int DTS = LAM + 2 * kHPC * kT * 4;   // float [kHPC][128]
+    static constexpr int CJ = DTS + kHPC * kT * 4;        // float [kHPC][128]
+    static constexpr int AS = CJ + kHPC * kT * 4;         // float [kHPC]
+    static constexpr int DS = AS + kHPC * 4;               // float [kHPC]
+    static constexpr int MODE = DS + kHPC * 4;             // int: bit k = factorised decay for head k
+    static constexpr int BADF = MODE + 4;                  // int
+    static constexpr int WOK = BADF + 4;                   // u32 [4] per-warp factorisable-head masks
+    static constexpr int BAR = (WOK + 16 + 7) & ~7;
+    // tree, g, ctf, hfull[2], hempty[2], xfull[2], xempty[2], mfull[2], mempty[2], accfull[2], accempty[2]
+    static constexpr int NBAR = 3 + 14;
+    static constexpr int TMEMP = BAR + NBAR * 8;
+    static constexpr int TOTAL = TMEMP + 16;
+    static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+struct Params {
+    const float* dt;
+    const float* A;
+    const float* D;
+    const int32_t* parent;
+    __nv_bfloat16* y;
+    int32_t* dev_status;
+    int B, T, H, G, cpg, hpc, has_h0;
+};
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    scan_tc128_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
+                      const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
+                      const Params prm) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sb = smem_u32(sm);
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+    const int T = prm.T, H = prm.H;
+    const int b = blockIdx.x / (prm.G * prm.cpg);
+    const int rem = blockIdx.x % (prm.G * prm.cpg);
+    const int g = rem / prm.cpg, chunk = rem % prm.cpg;
+    const int hpg = H / prm.G;
+    const int hbeg = g * hpg + chunk * prm.hpc;
+    const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
+    if (nh <= 0) return;
+    const int Tp16 = (T + 15) & ~15;
+    pdl_trigger();
+
+    const uint32_t bar0 = sb + Sm::BAR;
+    const uint32_t BAR_TREE = bar0, BAR_G = bar0 + 8, BAR_CTF = bar0 + 16;
+    auto bar_hfull = [&](int s) { return bar0 + 24 + 8 * s; };
+    auto bar_hempty = [&](int s) { return bar0 + 40 + 8 * s; };
+    auto bar_xfull = [&](int s) { return bar0 + 56 + 8 * s; };
+    auto bar_xempty = [&](int s) { return bar0 + 72 + 8 * s; };
+    auto bar_mfull = [&](int a) { return bar0 + 88 + 8 * a; };
+    auto bar_mempty = [&](int a) { return bar0 + 104 + 8 * a; };
+    auto bar_accfull = [&](int a) { return bar0 + 120 + 8 * a; };
+    auto bar_accempty = [&](int a) { return bar0 + 136 + 8 * a; };
+    uint32_t* tmem_slot = (uint32_t*)(sm + Sm::TMEMP);
+    auto mbuf = [&](int a) { return sb + (a ? Sm::B : Sm::M0); };
+
+    if (tid == 0) {
+        mbar_init(BAR_TREE, 1);
+        mbar_init(BAR_G, 1);
+        mbar_init(BAR_CTF, 128);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(bar_hfull(s), 1);
+            mbar_init(bar_hempty(s), 1);
+            mbar_init(bar_xfull(s), 1);
+            mbar_init(bar_xempty(s), 128);
+            mbar_init(bar_mfull(s), 128);
+            mbar_init(bar_mempty(s), 1);
+            mbar_init(bar_accfull(s), 1);
+            mbar_init(bar_accempty(s), 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 4 && lane == 0) {
+        tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+
+    if (warp == 4) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            mbar_expect_tx(BAR_TREE, 4 * kTile);
+            for (int a = 0; a < 2; ++a) {
+                tma_load_2d(sb + Sm::C + a * kTile, &tm_c, BAR_TREE, g * kN + 64 * a, b * T);
+                tma_load_2d(sb + Sm::B + a * kTile, &tm_b, BAR_TREE, g * kN + 64 * a, b * T);
+            }
+            for (int k = 0; k < nh; ++k) {
+                const int s = k & 1, u = k >> 1;
+                const int h = hbeg + k;
+                if (prm.has_h0) {
+                    mbar_wait(bar_hempty(s), (u & 1) ^ 1);
+                    mbar_expect_tx(bar_hfull(s), 32768);
+                    for (int a = 0; a < 4; ++a)
+                        tma_load_2d(sb + Sm::H + s * 32768 + a * 8192, &tm_h0, bar_hfull(s), 32 * a, (b * H + h) * kP);
+                }
+                mbar_wait(bar_xempty(s), (u & 1) ^ 1);
+                mbar_expect_tx(bar_xfull(s), kTile);
+                tma_load_2d(sb + Sm::X + s * kTile, &tm_x, bar_xfull(s), h * kP, b * T);
+            }
+        }
+    } else if (warp == 5) {
+        // ================= MMA issuer (warp converged, elected lane issues) =================
+        mbar_wait(BAR_TREE, 0);
+        tc_fence_after();
+        const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
+#pragma unroll 1
+        for (int kk = 0; kk < kN / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kTile + (kk & 3) * 32;
+            mma_f16_w(tmem + kGCol, sdesc(sb + Sm::C + off, 16, 1024), sdesc(sb + Sm::B + off, 16, 1024), id_g, kk > 0);
+        }
+        tc_commit_w(BAR_G);
+        mbar_wait(BAR_CTF, 0);   // C as tf32 in TMEM (and B tile free for M' buffer 1 once G completed)
+        tc_fence_after();
+        const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
+        const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
+        for (int k = 0; k < nh; ++k) {
+            const int s = k & 1, a = k & 1, u = k >> 1;
+            const uint32_t d0 = tmem + kAccCol + 128 * a, d1 = d0 + 64;
+            mbar_wait(bar_accempty(a), (u & 1) ^ 1);
+            tc_fence_after();
+            if (prm.has_h0) {
+                mbar_wait(bar_hfull(s), u & 1);
+                tc_fence_after();
+                const uint64_t bd = sdesc(sb + Sm::H + s * 32768, 16, 1024);
+#pragma unroll 2
+                for (int kk = 0; kk < kN / 8; ++kk)
+                    mma_tf32_ts_w(d0, tmem + kCCol + 8 * kk, bd + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4),
+                                  id_y0, kk > 0);
+                tc_commit_w(bar_hempty(s));
+            }
+            mbar_wait(bar_mfull(a), u & 1);
+            mbar_wait(bar_xfull(s), u & 1);
+            tc_fence_after();
+            const uint64_t xd = sdesc(sb + Sm::X + s * kTile, kTile, 1024);
+#pragma unroll 1
+            for (int kk = 0; kk < Tp16 / 16; ++kk)
+                mma_f16_w(d1, sdesc(mbuf(a) + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024), xd + (uint64_t)(kk * 128),
+                          id_y, kk > 0);
+            tc_commit_w(bar_mempty(a));
+            tc_commit_w(bar_accfull(a));
+        }
+    } else {
+        // ================= math warps: thread = node i = TMEM lane =================
+        const int i = tid;                       // 0..127
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+        uint32_t* anc = (uint32_t*)(sm + Sm::ANC);    // [buf][word][node]
+        int* jmp = (int*)(sm + Sm::JMP);              // [buf][node]
+        float* lam = (float*)(sm + Sm::LAM);          // [buf][head][node]
+        float* dts = (float*)(sm + Sm::DTS);          // [head][node]
+        float* cj = (float*)(sm + Sm::CJ);
+        float* as = (float*)(sm + Sm::AS);
+        float* ds = (float*)(sm + Sm::DS);
+        int* sbad = (int*)(sm + Sm::BADF);
+        uint32_t* wok = (uint32_t*)(sm + Sm::WOK);
+        auto mbar = [&]() { named_bar(1, 128); };
+        // ---- tree prologue: validation (PAPER.md:90 / R5), ancestor bits and Λ of every head
+        //      (Eq. a_tree) by pointer jumping ----
+        const int p = i < T ? prm.parent[(size_t)b * T + i] : -1;
+        int bad = 0;
+        if (i < T && (i == 0 ? p != -1 : (p < 0 || p >= i))) bad = (i == 0) ? 1 : 2;
+        if (i < nh) {
+            as[i] = prm.A[hbeg + i];
+            ds[i] = prm.D ? prm.D[hbeg + i] : 0.f;
+        }
+        if (i == 0) *sbad = 0;
+        mbar();
+        if (bad) atomicMax(sbad, bad == 1 ? 2 : 1);   // root error takes precedence
+        for (int k = 0; k < nh; ++k) {
+            const float d = i < T ? prm.dt[((size_t)b * T + i) * H + hbeg + k] : 0.f;
+            dts[k * kT + i] = d;
+        }
+        mbar();
+        const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);
+        if (badcode && i == 0 && rem == 0) report(prm.dev_status, badcode);
+        const bool valid = badcode == 0;
+        int cur = 0;
+        {
+            const int pp = (valid && i < T) ? p : -1;
+            for (int w = 0; w < 4; ++w) anc[(0 * 4 + w) * kT + i] = (i < T && (i >> 5) == w) ? (1u << (i & 31)) : 0u;
+            jmp[i] = pp;
+            for (int k = 0; k < nh; ++k) lam[(0 * kHPC + k) * kT + i] = dts[k * kT + i] * as[k];
+            mbar();
+            for (int r = 0; r < 7; ++r) {
+                const int j = jmp[cur * kT + i], nx = cur ^ 1;
+                for (int w = 0; w < 4; ++w)
+                    anc[(nx * 4 + w) * kT + i] = anc[(cur * 4 + w) * kT + i] | (j >= 0 ? anc[(cur * 4 + w) * kT + j] : 0u);
+                for (int k = 0; k < nh; ++k)
+                    lam[(nx * kHPC + k) * kT + i] =
+                        lam[(cur * kHPC + k) * kT + i] + (j >= 0 ? lam[(cur * kHPC + k) * kT + j] : 0.f);
+                jmp[nx * kT + i] = j >= 0 ? jmp[cur * kT + j] : -1;
+                mbar();
+                cur = nx;
+            }
+        }
+        // decay mode per head: factorised iff min Λ >= -64 over the tree (both factors within e^{±64})
+        uint32_t okm = 0;
+        for (int k = 0; k < nh; ++k) {
+            const float l = lam[(cur * kHPC + k) * kT + i];
+            if (i >= T || l >= -64.f) okm |= 1u << k;
+            cj[k * kT + i] = i < T ? __expf(-l) * dts[k * kT + i] : 0.f;
+        }
+        okm = __reduce_and_sync(0xffffffffu, okm);
+        if (lane == 0) wok[warp] = okm;
+        // C -> tf32 into TMEM columns [128, 256) (row i)
+        mbar_wait(BAR_TREE, 0);
+        {
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {   // 32 columns per store
+                uint32_t r32[32];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 bf16
+                    const int col = 32 * c4 + 8 * q;
+                    const uint4 v = *reinterpret_cast<const uint4*>(sm + Sm::C + (col >> 6) * kTile + swz(i, (col & 63) >> 3));
+                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        r32[8 * q + 2 * e] = __float_as_uint(bf_lo(wv[e]));
+                        r32[8 * q + 2 * e + 1] = __float_as_uint(bf_hi(wv[e]));
+                    }
+                }
+                tmem_st32(lane_base + kCCol + 32 * c4, r32);
+            }
+            tmem_st_wait();
+        }
+        mbar();
+        const uint32_t fmask = wok[0] & wok[1] & wok[2] & wok[3];
+        const uint32_t* ar = anc + cur * 4 * kT;   // final ancestor words: ar[w * kT + i]
+        uint32_t myanc[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) myanc[w] = ar[w * kT + i];
+        tc_fence_before();
+        mbar_arrive(BAR_CTF);
+        mbar_wait(BAR_G, 0);
+        tc_fence_after();
+        const float* laml = lam + cur * kHPC * kT;
+
+        auto epilogue = [&](int k) {
+            const int a = k & 1, s = k & 1, u = k >> 1;
+            mbar_wait(bar_accfull(a), u & 1);
+            tc_fence_after();
+            uint32_t y0[32], y1[32];
+            const float li = laml[k * kT + i], ei = __expf(li), dh = ds[k];
+            const bool fac = (fmask >> k) & 1u;
+            __nv_bfloat16* yrow = prm.y + (((size_t)b * T + i) * H + hbeg + k) * kP;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                tmem_ld32(lane_base + kAccCol + 128 * a + 32 * hf, y0);
+                tmem_ld32(lane_base + kAccCol + 128 * a + 64 + 32 * hf, y1);
+                tmem_wait();
+                uint32_t out[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {   // 8 columns per 16-byte x chunk
+                    const int col = 32 * hf + 8 * q;
+                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + Sm::X + s * kTile + swz(i, col >> 3));
+                    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float v[2];
+#pragma unroll
+                        for (int t2 = 0; t2 < 2; ++t2) {
+                            const int cc = 8 * q + 2 * e + t2;
+                            const float a0 = prm.has_h0 ? __uint_as_float(y0[cc]) : 0.f;
+                            const float a1 = __uint_as_float(y1[cc]);
+                            const float xx = t2 ? bf_hi(xw[e]) : bf_lo(xw[e]);
+                            const float base = fac ? ei * (a0 + a1) : fmaf(ei, a0, a1);
+                            v[t2] = valid ? fmaf(dh, xx, base) : 0.f;
+                        }
+                        out[4 * q + e] = pack_bf16(v[0], v[1]);
+                    }
+                }
+                if (i < T) {
+                    uint4* dst = reinterpret_cast<uint4*>(yrow + 32 * hf);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(bar_accempty(a));
+            mbar_arrive(bar_xempty(s));
+        };
+
+        for (int k = 0; k < nh; ++k) {
+            const int a = k & 1, u = k >> 1;
+            // ---- masked weights M'(k) into buffer a: row i = L_i∘G_i∘c (factorised) / direct decay ----
+            mbar_wait(bar_mempty(a), (u & 1) ^ 1);
+            tc_fence_after();
+            const bool fac = (fmask >> k) & 1u;
+            const float li = laml[k * kT + i];
+            const float* cjk = cj + k * kT;
+            const float* lamk = laml + k * kT;
+            const float* dtk = dts + k * kT;
+            const uint32_t mb = mbuf(a);
+#pragma unroll 1
+            for (int c4 = 0; c4 < Tp16 / 32 + ((Tp16 & 31) ? 1 : 0); ++c4) {   // 32 key columns at a time
+                uint32_t gr[32];
+                tmem_ld32(lane_base + kGCol + 32 * c4, gr);
+                tmem_wait();
+                const uint32_t bits = myanc[c4];
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    float wv[2];
+#pragma unroll
+                    for (int t2 = 0; t2 < 2; ++t2) {
+                        const int jj = 2 * e + t2, j = 32 * c4 + jj;
+                        float w = 0.f;
+                        if ((bits >> jj) & 1u) {
+                            const float gv = __uint_as_float(gr[jj]);
+                            w = fac ? gv * cjk[j] : gv * __expf(fminf(li - lamk[j], 0.f)) * dtk[j];
+                        }
+                        wv[t2] = w;
+                    }
+                    pk[e] = pack_bf16(wv[0], wv[1]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 keys -> swizzled 16-byte stores
+                    const int col = 32 * c4 + 8 * q;
+                    *reinterpret_cast<uint4*>(sm + (mb - sb) + (col >> 6) * kTile + swz(i, (col & 63) >> 3)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+            }
+            // keys past Tp16 are never read by the MMA (K = Tp16)
+            fence_proxy_async();
+            mbar_arrive(bar_mfull(a));
+            if (k > 0) epilogue(k - 1);
+        }
+        epilogue(nh - 1);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    }
+}
+
+}  // namespace tc128
+}  // namespace stree
+
+namespace {
+typedef CUresult (*EncodeTiledFn128)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn128 enc128() {
+    static EncodeTiledFn128 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn128) nullptr;
+        return (EncodeTiledFn128)p;
+    }();
+    return fn;
+}
+bool map2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+           uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn128 fn = enc128();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+}  // namespace
+
+extern "C" int stree_tc128_supports(const stree_dims* d) {
+    if (!d || d->io_dtype != STREE_BF16 || d->head_dim != stree::tc128::kP || d->d_state != stree::tc128::kN) return 0;
+    if (d->n_nodes < 1 || d->n_nodes > stree::tc128::kT) return 0;
+    if (d->n_groups < 1 || d->n_heads % d->n_groups) return 0;
+    return 1;
+}
+
+extern "C" int stree_launch_scan_tc128(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                       const void* Bm, const void* Cm, const float* D, const float* h0,
+                                       const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s) {
+    using namespace stree::tc128;
+    if (!stree_tc128_supports(d)) return (int)cudaErrorNotSupported;
+    const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
+    CUtensorMap mc, mb, mx, mh;
+    const uint64_t BT = (uint64_t)B * T;
+    bool ok = map2d(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, kT) &&
+              map2d(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, kT) &&
+              map2d(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, kT);
+    if (h0)
+        ok = ok && map2d(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h0, (uint64_t)N, (uint64_t)B * H * P, (uint64_t)N * 4, 32, 64);
+    else
+        mh = mx;
+    if (!ok) return (int)cudaErrorInvalidValue;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int hpg = H / G;
+    int cpg = nsm / (B * G);
+    if (cpg < 1) cpg = 1;
+    if (cpg > hpg) cpg = hpg;
+    int hpc = (hpg + cpg - 1) / cpg;
+    if (hpc > kHPC) hpc = kHPC;
+    cpg = (hpg + hpc - 1) / hpc;
+    Params prm{};
+    prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
+    prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc; prm.has_h0 = h0 != nullptr;
+    const size_t smem = Sm::TOTAL + 1024;
+    cudaError_t e = cudaFuncSetAttribute(scan_tc128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    e = stree::launch_k(scan_tc128_kernel, dim3(B * G * cpg), dim3(kThreads), smem, s, mc, mb, mx, mh, prm);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}

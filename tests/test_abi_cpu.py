@@ -76,6 +76,10 @@ def test_scan_kernel_selection(L):
     assert b.stree_scan_kernel_for(big) == 1
     b.stree_set_scan_impl(b.STREE_SCAN_AUTO)
     assert b.stree_scan_kernel_for(big) in (1, 2)
+    t100 = b.stree_dims(4, 100, 80, 64, 128, 1, b.STREE_BF16)
+    assert b.stree_scan_kernel_for(t100) == 3       # 128-node tcgen05 kernel
+    t200 = b.stree_dims(4, 200, 80, 64, 128, 1, b.STREE_BF16)
+    assert b.stree_scan_kernel_for(t200) == 1
     with pytest.raises(b.StreeError):
         b.stree_set_scan_impl(9)
 

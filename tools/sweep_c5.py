@@ -114,7 +114,7 @@ def main():
         t_unr, _ = time_scan(np.stack([trees.chain(maxlen)] * len(paths)))
         t_p16, _ = time_scan(np.stack([par] * 16)) if T <= 128 else (None, None)
         rec = {"case": name, "T": T, "leaves": len(paths), "unrolled_tokens": int(sum(len(p) for p in paths)),
-               "kernel": {1: "simt", 2: "tcgen05"}.get(k_packed),
+               "kernel": {1: "simt", 2: "tcgen05", 3: "tcgen05-128"}.get(k_packed),
                "packed_us": t_packed, "chain_us": t_chain, "unrolled_us": t_unr,
                "packed_nodes_per_s": T / (t_packed * 1e-6), "unrolled_nodes_per_s": T / (t_unr * 1e-6),
                "speedup_vs_unrolled": t_unr / t_packed, "tree_over_chain": t_packed / t_chain}
