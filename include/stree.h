@@ -73,7 +73,7 @@ typedef struct {
 /* Kernel family selection for stree_tree_scan and stree_commit (stree_set_scan_impl). */
 typedef enum {
     STREE_SCAN_AUTO = 0,  /* TMA / tcgen05 pipeline kernels when supported, else the CUDA-core kernels.
-                             scan: bf16 io, P == 64, N in {64,128}, T <= 64; or N == 128, T <= 128;
+                             scan: bf16 io, P == 64, N in {64,128}, T <= 64; or N == 128, T <= 256;
                              commit: bf16 io, P == 64, N in {64,128}, T <= 256, h0 given */
     STREE_SCAN_SIMT = 1,  /* CUDA-core kernels (FP32-FMA scan, ring commit; any shape; the fp32 1e-4 path) */
     STREE_SCAN_TC = 2     /* force the pipeline kernels; STREE_ERR_UNSUPPORTED if the shape is not served */
@@ -312,7 +312,7 @@ stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, cons
                               int32_t* dev_status, void* stream);
 
 /* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05 (T <= 64),
- * 3 = tcgen05 128-node kernel (64 < T <= 128, bf16, P = 64, N = 128), 0 = invalid. */
+ * 3 = tcgen05 128-row-tile kernel (64 < T <= 256, bf16, P = 64, N = 128), 0 = invalid. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
 
 /* Which kernel stree_commit would launch (has_h0: h0 != NULL): 1 = CUDA-core ring / block kernel,

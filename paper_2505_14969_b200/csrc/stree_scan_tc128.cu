@@ -15,7 +15,10 @@
 //   warp 4     TMA producer: C, B once; per head the 32 KB fp32 state (4 boxes) and the x tile, 2-stage rings
 //   warp 5     tcgen05.mma issuer + TMEM allocator (512 columns: G 0-127, C tf32 128-255, two head slots of
 //              Y0 / Y' accumulators 256-511)
-// Served: bf16 io, P = 64, N = 128, 1 <= T <= 128 (dispatched for T > 64).
+// Served: bf16 io, P = 64, N = 128, 1 <= T <= 256 (dispatched for T > 64).  NKB = 2 (128 < T <= 256): each
+// CTA owns one 128-row tile of nodes (rt = 0, 1); its keys are the nodes 0 .. 128·rt + 127 (topological order:
+// every ancestor precedes its descendants), G = C_rows·Bᵀ takes 256 TMEM columns, so one accumulator slot,
+// one M' buffer (over the B tile) and the second x stage over the C tile (free once C is in TMEM).
 #include <cuda.h>
 
 #include "stree_common.cuh"
@@ -26,36 +29,40 @@ namespace tc128 {
 
 using namespace stree::tc;
 
-constexpr int kT = 128, kP = 64, kN = 128;
-constexpr int kHPC = 10;
+constexpr int kP = 64, kN = 128;
 constexpr int kThreads = 192;
 constexpr int kTile = 16384;          // 128 rows x 128 bytes, swizzle-128B
 constexpr uint32_t kCols = 512;
-constexpr int kGCol = 0, kCCol = 128, kAccCol = 256;   // accumulator slot a: Y0 at 256 + 128a, Y' at +64
 
+template <int NKB>
 struct Sm {
-    static constexpr int C = 0;                    // C bf16: 2 k-chunks x 16 KB
-    static constexpr int B = C + 2 * kTile;        // B bf16: 2 k-chunks (dead after G: M' buffer 1)
-    static constexpr int M0 = B + 2 * kTile;       // M' buffer 0: 2 k-chunks (keys 0-63, 64-127)
-    static constexpr int H = M0 + 2 * kTile;       // state ring: 2 x 32 KB (4 boxes of 64 rows x 32 fp32)
-    static constexpr int X = H + 2 * 32768;        // x ring: 2 x 16 KB (128 rows x 64 bf16)
-    static constexpr int PAR = X + 2 * kTile / 2 * 2;
-    static constexpr int ANC = PAR + kT * 4;       // u32 [2][4][128]
-    static constexpr int JMP = ANC + 2 * 4 * kT * 4;   // int [2][128]
-    static constexpr int LAM = JMP + 2 * kT * 4;   // float [2][kHPC][128]
-    static constexpr int DTS = LAM + 2 * kHPC * kT * 4;   // float [kHPC][128]
-    static constexpr int CJ = DTS + kHPC * kT * 4;        // float [kHPC][128]
-    static constexpr int AS = CJ + kHPC * kT * 4;         // float [kHPC]
-    static constexpr int DS = AS + kHPC * 4;               // float [kHPC]
-    static constexpr int MODE = DS + kHPC * 4;             // int: bit k = factorised decay for head k
-    static constexpr int BADF = MODE + 4;                  // int
-    static constexpr int WOK = BADF + 4;                   // u32 [4] per-warp factorisable-head masks
+    static constexpr int kKeys = 128 * NKB;        // nodes / keys per tree served
+    static constexpr int kHPC = NKB == 1 ? 10 : 4; // heads per CTA
+    static constexpr int kSlots = NKB == 1 ? 2 : 1;        // accumulator slots / M' buffers
+    static constexpr int kGCol = 0, kCCol = 128 * NKB, kAccCol = kCCol + 128;   // slot a: Y0 +128a, Y' +64
+    static constexpr int XS = kTile * NKB;        // x stage: 128·NKB rows x 128 B
+    static constexpr int C = 0;                    // C rows of this tile: 2 k-chunks x 16 KB
+    static constexpr int B = C + 2 * kTile;        // B rows 0 .. kKeys-1: NKB x 2 k-chunks (dead after G: M')
+    static constexpr int M0 = B + 2 * kTile * NKB; // NKB == 1: second M' buffer
+    static constexpr int H = M0 + (NKB == 1 ? 2 * kTile : 0);   // state ring: 2 x 32 KB
+    static constexpr int X = H + 2 * 32768;        // x stage 0 (NKB == 1: stages 0 and 1)
+    static constexpr int PAR = X + (NKB == 1 ? 2 : 1) * XS;
+    static constexpr int ANC = PAR + kKeys * 4;    // u32 [4·NKB][kKeys]   (updated in place)
+    static constexpr int JMP = ANC + 4 * NKB * kKeys * 4;   // int [2][kKeys]
+    static constexpr int LAM = JMP + 2 * kKeys * 4;         // float [2][kHPC][kKeys]
+    static constexpr int DTS = LAM + 2 * kHPC * kKeys * 4;  // float [kHPC][kKeys]
+    static constexpr int CJ = DTS + kHPC * kKeys * 4;       // float [kHPC][kKeys]
+    static constexpr int AS = CJ + kHPC * kKeys * 4;        // float [kHPC]
+    static constexpr int DS = AS + kHPC * 4;                // float [kHPC]
+    static constexpr int BADF = DS + kHPC * 4;              // int
+    static constexpr int WOK = BADF + 4;                    // u32 [4] per-warp factorisable-head masks
     static constexpr int BAR = (WOK + 16 + 7) & ~7;
     // tree, g, ctf, hfull[2], hempty[2], xfull[2], xempty[2], mfull[2], mempty[2], accfull[2], accempty[2]
     static constexpr int NBAR = 3 + 14;
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
     static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
+    __device__ static constexpr int xstage(int s) { return NKB == 1 ? X + s * XS : (s ? C : X); }
 };
 
 struct Params {
@@ -71,23 +78,31 @@ struct Params {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+template <int NKB>
 __global__ void __launch_bounds__(kThreads, 1)
     scan_tc128_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
                       const Params prm) {
+    using Sm = tc128::Sm<NKB>;
+    constexpr int kT = Sm::kKeys, kHPC = Sm::kHPC, kGCol = Sm::kGCol, kCCol = Sm::kCCol, kAccCol = Sm::kAccCol;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(sm);
     const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
     const int T = prm.T, H = prm.H;
-    const int b = blockIdx.x / (prm.G * prm.cpg);
-    const int rem = blockIdx.x % (prm.G * prm.cpg);
+    const int rt = blockIdx.x % NKB;                  // row tile: nodes r0 .. r0 + 127
+    const int r0 = 128 * rt;
+    const int cta = blockIdx.x / NKB;
+    const int b = cta / (prm.G * prm.cpg);
+    const int rem = cta % (prm.G * prm.cpg);
     const int g = rem / prm.cpg, chunk = rem % prm.cpg;
     const int hpg = H / prm.G;
     const int hbeg = g * hpg + chunk * prm.hpc;
     const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
-    if (nh <= 0) return;
+    if (nh <= 0 || r0 >= T) return;
     const int Tp16 = (T + 15) & ~15;
+    const int kcta = min(Tp16, 128 * (rt + 1));       // keys this tile's rows can see (multiple of 16)
+    const int nkb = rt + 1;                           // key blocks of 128
     pdl_trigger();
 
     const uint32_t bar0 = sb + Sm::BAR;
@@ -101,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto bar_accfull = [&](int a) { return bar0 + 120 + 8 * a; };
     auto bar_accempty = [&](int a) { return bar0 + 136 + 8 * a; };
     uint32_t* tmem_slot = (uint32_t*)(sm + Sm::TMEMP);
-    auto mbuf = [&](int a) { return sb + (a ? Sm::B : Sm::M0); };
+    auto mbuf = [&](int a) { return sb + ((NKB == 1 && a == 0) ? Sm::M0 : Sm::B); };
 
     if (tid == 0) {
         mbar_init(BAR_TREE, 1);
@@ -136,10 +151,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 4) {
         // ================= TMA producer =================
         if (lane == 0) {
-            mbar_expect_tx(BAR_TREE, 4 * kTile);
+            mbar_expect_tx(BAR_TREE, (2 + 2 * nkb) * kTile);
             for (int a = 0; a < 2; ++a) {
-                tma_load_2d(sb + Sm::C + a * kTile, &tm_c, BAR_TREE, g * kN + 64 * a, b * T);
-                tma_load_2d(sb + Sm::B + a * kTile, &tm_b, BAR_TREE, g * kN + 64 * a, b * T);
+                tma_load_2d(sb + Sm::C + a * kTile, &tm_c, BAR_TREE, g * kN + 64 * a, b * T + r0);
+                for (int kb = 0; kb < nkb; ++kb)
+                    tma_load_2d(sb + Sm::B + (2 * kb + a) * kTile, &tm_b, BAR_TREE, g * kN + 64 * a, b * T + 128 * kb);
             }
             for (int k = 0; k < nh; ++k) {
                 const int s = k & 1, u = k >> 1;
@@ -151,19 +167,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_2d(sb + Sm::H + s * 32768 + a * 8192, &tm_h0, bar_hfull(s), 32 * a, (b * H + h) * kP);
                 }
                 mbar_wait(bar_xempty(s), (u & 1) ^ 1);
-                mbar_expect_tx(bar_xfull(s), kTile);
-                tma_load_2d(sb + Sm::X + s * kTile, &tm_x, bar_xfull(s), h * kP, b * T);
+                if (NKB == 2 && k == 1) mbar_wait(BAR_CTF, 0);   // stage 1 lives over the C tile
+                mbar_expect_tx(bar_xfull(s), nkb * kTile);
+                for (int kb = 0; kb < nkb; ++kb)
+                    tma_load_2d(sb + Sm::xstage(s) + kb * kTile, &tm_x, bar_xfull(s), h * kP, b * T + 128 * kb);
             }
         }
     } else if (warp == 5) {
         // ================= MMA issuer (warp converged, elected lane issues) =================
         mbar_wait(BAR_TREE, 0);
         tc_fence_after();
-        const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
+        // G = C_rows·Bᵀ, one N = 128 block per 128 keys (NKB == 1: N = Tp16)
+        for (int kb = 0; kb < nkb; ++kb) {
+            const uint32_t id_g = idesc(kFmtBF16, 0, 128, NKB == 1 ? Tp16 : 128);
 #pragma unroll 1
-        for (int kk = 0; kk < kN / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kTile + (kk & 3) * 32;
-            mma_f16_w(tmem + kGCol, sdesc(sb + Sm::C + off, 16, 1024), sdesc(sb + Sm::B + off, 16, 1024), id_g, kk > 0);
+            for (int kk = 0; kk < kN / 16; ++kk) {
+                const uint32_t off = (kk >> 2) * kTile + (kk & 3) * 32;
+                mma_f16_w(tmem + kGCol + 128 * kb, sdesc(sb + Sm::C + off, 16, 1024),
+                          sdesc(sb + Sm::B + 2 * kb * kTile + off, 16, 1024), id_g, kk > 0);
+            }
         }
         tc_commit_w(BAR_G);
         mbar_wait(BAR_CTF, 0);   // C as tf32 in TMEM (and B tile free for M' buffer 1 once G completed)
@@ -171,9 +193,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
         const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
         for (int k = 0; k < nh; ++k) {
-            const int s = k & 1, a = k & 1, u = k >> 1;
+            const int s = k & 1, a = NKB == 1 ? (k & 1) : 0, u = k >> 1, ua = NKB == 1 ? u : k;
             const uint32_t d0 = tmem + kAccCol + 128 * a, d1 = d0 + 64;
-            mbar_wait(bar_accempty(a), (u & 1) ^ 1);
+            mbar_wait(bar_accempty(a), (ua & 1) ^ 1);
             tc_fence_after();
             if (prm.has_h0) {
                 mbar_wait(bar_hfull(s), u & 1);
@@ -185,22 +207,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   id_y0, kk > 0);
                 tc_commit_w(bar_hempty(s));
             }
-            mbar_wait(bar_mfull(a), u & 1);
+            mbar_wait(bar_mfull(a), ua & 1);
             mbar_wait(bar_xfull(s), u & 1);
             tc_fence_after();
-            const uint64_t xd = sdesc(sb + Sm::X + s * kTile, kTile, 1024);
+            const uint64_t xd = sdesc(sb + Sm::xstage(s), kTile, 1024);
 #pragma unroll 1
-            for (int kk = 0; kk < Tp16 / 16; ++kk)
+            for (int kk = 0; kk < kcta / 16; ++kk)
                 mma_f16_w(d1, sdesc(mbuf(a) + (kk >> 2) * kTile + (kk & 3) * 32, 16, 1024), xd + (uint64_t)(kk * 128),
                           id_y, kk > 0);
             tc_commit_w(bar_mempty(a));
             tc_commit_w(bar_accfull(a));
         }
     } else {
-        // ================= math warps: thread = node i = TMEM lane =================
-        const int i = tid;                       // 0..127
+        // ================= math warps: thread t = row r0 + t = TMEM lane =================
+        const int t = tid;                       // 0..127
+        const int i = r0 + t;                    // this thread's row (node)
         const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
-        uint32_t* anc = (uint32_t*)(sm + Sm::ANC);    // [buf][word][node]
+        uint32_t* anc = (uint32_t*)(sm + Sm::ANC);    // [word][node]
         int* jmp = (int*)(sm + Sm::JMP);              // [buf][node]
         float* lam = (float*)(sm + Sm::LAM);          // [buf][head][node]
         float* dts = (float*)(sm + Sm::DTS);          // [head][node]
@@ -210,55 +233,68 @@ __global__ void __launch_bounds__(kThreads, 1)
         int* sbad = (int*)(sm + Sm::BADF);
         uint32_t* wok = (uint32_t*)(sm + Sm::WOK);
         auto mbar = [&]() { named_bar(1, 128); };
-        // ---- tree prologue: validation (PAPER.md:90 / R5), ancestor bits and Λ of every head
-        //      (Eq. a_tree) by pointer jumping ----
-        const int p = i < T ? prm.parent[(size_t)b * T + i] : -1;
-        int bad = 0;
-        if (i < T && (i == 0 ? p != -1 : (p < 0 || p >= i))) bad = (i == 0) ? 1 : 2;
-        if (i < nh) {
-            as[i] = prm.A[hbeg + i];
-            ds[i] = prm.D ? prm.D[hbeg + i] : 0.f;
+        constexpr int kW = 4 * NKB;              // ancestor words per node
+        // ---- tree prologue over all kT nodes (thread t: nodes t, t + 128): validation (PAPER.md:90 / R5),
+        //      ancestor bits and Λ of every head (Eq. a_tree) by pointer jumping ----
+        if (t < nh) {
+            as[t] = prm.A[hbeg + t];
+            ds[t] = prm.D ? prm.D[hbeg + t] : 0.f;
         }
-        if (i == 0) *sbad = 0;
+        if (t == 0) *sbad = 0;
         mbar();
-        if (bad) atomicMax(sbad, bad == 1 ? 2 : 1);   // root error takes precedence
-        for (int k = 0; k < nh; ++k) {
-            const float d = i < T ? prm.dt[((size_t)b * T + i) * H + hbeg + k] : 0.f;
-            dts[k * kT + i] = d;
+        int pv[NKB];
+#pragma unroll
+        for (int q = 0; q < NKB; ++q) {
+            const int v = t + 128 * q;
+            pv[q] = v < T ? prm.parent[(size_t)b * T + v] : -1;
+            if (v < T && (v == 0 ? pv[q] != -1 : (pv[q] < 0 || pv[q] >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
+            for (int k = 0; k < nh; ++k) dts[k * kT + v] = v < T ? prm.dt[((size_t)b * T + v) * H + hbeg + k] : 0.f;
         }
         mbar();
-        const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);
-        if (badcode && i == 0 && rem == 0) report(prm.dev_status, badcode);
+        const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);   // root error takes precedence
+        if (badcode && t == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
         const bool valid = badcode == 0;
         int cur = 0;
-        {
-            const int pp = (valid && i < T) ? p : -1;
-            for (int w = 0; w < 4; ++w) anc[(0 * 4 + w) * kT + i] = (i < T && (i >> 5) == w) ? (1u << (i & 31)) : 0u;
-            jmp[i] = pp;
-            for (int k = 0; k < nh; ++k) lam[(0 * kHPC + k) * kT + i] = dts[k * kT + i] * as[k];
-            mbar();
-            for (int r = 0; r < 7; ++r) {
-                const int j = jmp[cur * kT + i], nx = cur ^ 1;
-                for (int w = 0; w < 4; ++w)
-                    anc[(nx * 4 + w) * kT + i] = anc[(cur * 4 + w) * kT + i] | (j >= 0 ? anc[(cur * 4 + w) * kT + j] : 0u);
+#pragma unroll
+        for (int q = 0; q < NKB; ++q) {
+            const int v = t + 128 * q;
+            for (int w = 0; w < kW; ++w) anc[w * kT + v] = (v < T && (v >> 5) == w) ? (1u << (v & 31)) : 0u;
+            jmp[v] = (valid && v < T) ? pv[q] : -1;
+            for (int k = 0; k < nh; ++k) lam[k * kT + v] = dts[k * kT + v] * as[k];
+        }
+        mbar();
+        for (int r = 0; r < 7 + NKB - 1; ++r) {
+            const int nx = cur ^ 1;
+#pragma unroll
+            for (int q = 0; q < NKB; ++q) {
+                const int v = t + 128 * q, j = jmp[cur * kT + v];
+                // ancestor sets in place: a concurrently updated row j only ever holds more true ancestors of j
+                if (j >= 0)
+                    for (int w = 0; w < kW; ++w) anc[w * kT + v] |= anc[w * kT + j];
                 for (int k = 0; k < nh; ++k)
-                    lam[(nx * kHPC + k) * kT + i] =
-                        lam[(cur * kHPC + k) * kT + i] + (j >= 0 ? lam[(cur * kHPC + k) * kT + j] : 0.f);
-                jmp[nx * kT + i] = j >= 0 ? jmp[cur * kT + j] : -1;
-                mbar();
-                cur = nx;
+                    lam[(nx * kHPC + k) * kT + v] =
+                        lam[(cur * kHPC + k) * kT + v] + (j >= 0 ? lam[(cur * kHPC + k) * kT + j] : 0.f);
+                jmp[nx * kT + v] = j >= 0 ? jmp[cur * kT + j] : -1;
             }
+            mbar();
+            cur = nx;
         }
         // decay mode per head: factorised iff min Λ >= -64 over the tree (both factors within e^{±64})
         uint32_t okm = 0;
         for (int k = 0; k < nh; ++k) {
-            const float l = lam[(cur * kHPC + k) * kT + i];
-            if (i >= T || l >= -64.f) okm |= 1u << k;
-            cj[k * kT + i] = i < T ? __expf(-l) * dts[k * kT + i] : 0.f;
+            bool ok = true;
+#pragma unroll
+            for (int q = 0; q < NKB; ++q) {
+                const int v = t + 128 * q;
+                const float l = lam[(cur * kHPC + k) * kT + v];
+                if (v < T && l < -64.f) ok = false;
+                cj[k * kT + v] = v < T ? __expf(-l) * dts[k * kT + v] : 0.f;
+            }
+            if (ok) okm |= 1u << k;
         }
         okm = __reduce_and_sync(0xffffffffu, okm);
         if (lane == 0) wok[warp] = okm;
-        // C -> tf32 into TMEM columns [128, 256) (row i)
+        // C -> tf32 into TMEM columns [kCCol, kCCol + 128) (row t of this tile)
         mbar_wait(BAR_TREE, 0);
         {
 #pragma unroll
@@ -267,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 bf16
                     const int col = 32 * c4 + 8 * q;
-                    const uint4 v = *reinterpret_cast<const uint4*>(sm + Sm::C + (col >> 6) * kTile + swz(i, (col & 63) >> 3));
+                    const uint4 v = *reinterpret_cast<const uint4*>(sm + Sm::C + (col >> 6) * kTile + swz(t, (col & 63) >> 3));
                     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -281,19 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar();
         const uint32_t fmask = wok[0] & wok[1] & wok[2] & wok[3];
-        const uint32_t* ar = anc + cur * 4 * kT;   // final ancestor words: ar[w * kT + i]
-        uint32_t myanc[4];
+        uint32_t myanc[kW];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) myanc[w] = ar[w * kT + i];
+        for (int w = 0; w < kW; ++w) myanc[w] = anc[w * kT + i];
         tc_fence_before();
-        mbar_arrive(BAR_CTF);
+        mbar_arrive(BAR_CTF);   // (NKB == 2: the C tile is free for x stage 1 from here)
         mbar_wait(BAR_G, 0);
         tc_fence_after();
         const float* laml = lam + cur * kHPC * kT;
 
         auto epilogue = [&](int k) {
-            const int a = k & 1, s = k & 1, u = k >> 1;
-            mbar_wait(bar_accfull(a), u & 1);
+            const int a = NKB == 1 ? (k & 1) : 0, s = k & 1, u = k >> 1, ua = NKB == 1 ? u : k;
+            mbar_wait(bar_accfull(a), ua & 1);
             tc_fence_after();
             uint32_t y0[32], y1[32];
             const float li = laml[k * kT + i], ei = __expf(li), dh = ds[k];
@@ -306,9 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait();
                 uint32_t out[16];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {   // 8 columns per 16-byte x chunk
+                for (int q = 0; q < 4; ++q) {   // 8 columns per 16-byte x chunk (x row i of the stage)
                     const int col = 32 * hf + 8 * q;
-                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + Sm::X + s * kTile + swz(i, col >> 3));
+                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + Sm::xstage(s) + (i >> 7) * kTile +
+                                                                     swz(i & 127, col >> 3));
                     const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -337,9 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
 
         for (int k = 0; k < nh; ++k) {
-            const int a = k & 1, u = k >> 1;
-            // ---- masked weights M'(k) into buffer a: row i = L_i∘G_i∘c (factorised) / direct decay ----
-            mbar_wait(bar_mempty(a), (u & 1) ^ 1);
+            const int a = NKB == 1 ? (k & 1) : 0, ua = NKB == 1 ? (k >> 1) : k;
+            // ---- masked weights M'(k): row t = L_i∘G_i∘c (factorised) / direct decay, keys 0 .. kcta-1 ----
+            mbar_wait(bar_mempty(a), (ua & 1) ^ 1);
             tc_fence_after();
             const bool fac = (fmask >> k) & 1u;
             const float li = laml[k * kT + i];
@@ -348,11 +384,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* dtk = dts + k * kT;
             const uint32_t mb = mbuf(a);
 #pragma unroll 1
-            for (int c4 = 0; c4 < Tp16 / 32 + ((Tp16 & 31) ? 1 : 0); ++c4) {   // 32 key columns at a time
+            for (int c4 = 0; c4 < (kcta + 31) / 32; ++c4) {   // 32 key columns at a time
                 uint32_t gr[32];
                 tmem_ld32(lane_base + kGCol + 32 * c4, gr);
                 tmem_wait();
-                const uint32_t bits = myanc[c4];
+                uint32_t bits = 0u;
+#pragma unroll
+                for (int w = 0; w < kW; ++w)
+                    if (w == c4) bits = myanc[w];
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
@@ -372,16 +411,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 keys -> swizzled 16-byte stores
                     const int col = 32 * c4 + 8 * q;
-                    *reinterpret_cast<uint4*>(sm + (mb - sb) + (col >> 6) * kTile + swz(i, (col & 63) >> 3)) =
+                    *reinterpret_cast<uint4*>(sm + (mb - sb) + (col >> 6) * kTile + swz(t, (col & 63) >> 3)) =
                         make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 }
             }
-            // keys past Tp16 are never read by the MMA (K = Tp16)
+            // keys past kcta are never read by the MMA (K = kcta)
             fence_proxy_async();
             mbar_arrive(bar_mfull(a));
-            if (k > 0) epilogue(k - 1);
+            if (NKB == 1) {
+                if (k > 0) epilogue(k - 1);
+            } else {
+                epilogue(k);   // single accumulator slot / M' buffer: head k+1 waits for this one
+            }
         }
-        epilogue(nh - 1);
+        if (NKB == 1) epilogue(nh - 1);
     }
     tc_fence_before();
     __syncthreads();
@@ -425,10 +468,40 @@ bool map2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t in
 
 extern "C" int stree_tc128_supports(const stree_dims* d) {
     if (!d || d->io_dtype != STREE_BF16 || d->head_dim != stree::tc128::kP || d->d_state != stree::tc128::kN) return 0;
-    if (d->n_nodes < 1 || d->n_nodes > stree::tc128::kT) return 0;
+    if (d->n_nodes < 1 || d->n_nodes > 256) return 0;
     if (d->n_groups < 1 || d->n_heads % d->n_groups) return 0;
     return 1;
 }
+
+namespace {
+template <int NKB>
+int launch_tc128(const stree_dims* d, const CUtensorMap& mc, const CUtensorMap& mb, const CUtensorMap& mx,
+                 const CUtensorMap& mh, const stree::tc128::Params& base, cudaStream_t s) {
+    using namespace stree::tc128;
+    using S = Sm<NKB>;
+    const int B = d->batch, H = d->n_heads, G = d->n_groups;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int hpg = H / G;
+    int cpg = nsm / (B * G * NKB);
+    if (cpg < 1) cpg = 1;
+    if (cpg > hpg) cpg = hpg;
+    int hpc = (hpg + cpg - 1) / cpg;
+    if (hpc > S::kHPC) hpc = S::kHPC;
+    cpg = (hpg + hpc - 1) / hpc;
+    Params prm = base;
+    prm.cpg = cpg;
+    prm.hpc = hpc;
+    const size_t smem = S::TOTAL + 1024;
+    auto k = scan_tc128_kernel<NKB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    e = stree::launch_k(k, dim3(B * G * cpg * NKB), dim3(kThreads), smem, s, mc, mb, mx, mh, prm);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+}  // namespace
 
 extern "C" int stree_launch_scan_tc128(const stree_dims* d, const void* x, const float* dt, const float* A,
                                        const void* Bm, const void* Cm, const float* D, const float* h0,
@@ -438,31 +511,16 @@ extern "C" int stree_launch_scan_tc128(const stree_dims* d, const void* x, const
     const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
     CUtensorMap mc, mb, mx, mh;
     const uint64_t BT = (uint64_t)B * T;
-    bool ok = map2d(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, kT) &&
-              map2d(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, kT) &&
-              map2d(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, kT);
+    bool ok = map2d(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, 128) &&
+              map2d(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, 128) &&
+              map2d(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, 128);
     if (h0)
         ok = ok && map2d(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h0, (uint64_t)N, (uint64_t)B * H * P, (uint64_t)N * 4, 32, 64);
     else
         mh = mx;
     if (!ok) return (int)cudaErrorInvalidValue;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int hpg = H / G;
-    int cpg = nsm / (B * G);
-    if (cpg < 1) cpg = 1;
-    if (cpg > hpg) cpg = hpg;
-    int hpc = (hpg + cpg - 1) / cpg;
-    if (hpc > kHPC) hpc = kHPC;
-    cpg = (hpg + hpc - 1) / hpc;
     Params prm{};
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
-    prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc; prm.has_h0 = h0 != nullptr;
-    const size_t smem = Sm::TOTAL + 1024;
-    cudaError_t e = cudaFuncSetAttribute(scan_tc128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    e = stree::launch_k(scan_tc128_kernel, dim3(B * G * cpg), dim3(kThreads), smem, s, mc, mb, mx, mh, prm);
-    if (e != cudaSuccess) return (int)e;
-    return (int)cudaGetLastError();
+    prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.has_h0 = h0 != nullptr;
+    return T <= 128 ? launch_tc128<1>(d, mc, mb, mx, mh, prm, s) : launch_tc128<2>(d, mc, mb, mx, mh, prm, s);
 }

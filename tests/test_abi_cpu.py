@@ -79,7 +79,8 @@ def test_scan_kernel_selection(L):
     t100 = b.stree_dims(4, 100, 80, 64, 128, 1, b.STREE_BF16)
     assert b.stree_scan_kernel_for(t100) == 3       # 128-node tcgen05 kernel
     t200 = b.stree_dims(4, 200, 80, 64, 128, 1, b.STREE_BF16)
-    assert b.stree_scan_kernel_for(t200) == 1
+    assert b.stree_scan_kernel_for(t200) == 3       # two 128-row tiles
+    assert b.stree_scan_kernel_for(b.stree_dims(4, 200, 80, 64, 64, 1, b.STREE_BF16)) == 1   # N = 64: SIMT
     with pytest.raises(b.StreeError):
         b.stree_set_scan_impl(9)
 

@@ -1,5 +1,6 @@
-"""GPU parity of the 128-node tcgen05 scan kernel (stree_scan_tc128.cu: 64 < T <= 128, bf16, P = 64,
-N = 128; BASELINE configs[4] sweep range) against the fp64 oracle, through the C ABI."""
+"""GPU parity of the 128-row-tile tcgen05 scan kernel (stree_scan_tc128.cu: 64 < T <= 256 — one tile up to
+128 nodes, two row tiles above —, bf16, P = 64, N = 128; BASELINE configs[4] sweep range) against the fp64
+oracle, through the C ABI."""
 import numpy as np
 import pytest
 import torch
@@ -45,7 +46,9 @@ def _trees(kind, B, T, seed):
 
 @pytest.mark.parametrize("B,T,H,G,kind", [(2, 65, 8, 1, "random"), (3, 80, 12, 1, "heap2"), (2, 100, 24, 2, "chain"),
                                           (1, 127, 80, 1, "heap8"), (4, 128, 16, 1, "random"), (2, 96, 30, 3, "star"),
-                                          (16, 128, 80, 1, "heap2")])
+                                          (16, 128, 80, 1, "heap2"), (2, 129, 8, 1, "random"),
+                                          (3, 200, 12, 1, "heap2"), (2, 256, 16, 2, "chain"), (2, 256, 8, 1, "heap8"),
+                                          (1, 170, 80, 1, "star"), (4, 256, 80, 1, "random")])
 def test_tc128_matches_oracle(B, T, H, G, kind):
     prob = inputs.make_problem(inputs.Dims(B, T, H, 64, 128, G, "bf16"), _trees(kind, B, T, T + H), seed=T * 7 + H)
     y, st = run(prob)
@@ -55,9 +58,10 @@ def test_tc128_matches_oracle(B, T, H, G, kind):
 
 
 @pytest.mark.parametrize("variant", ["stress_decay", "no_decay", "large_x", "h0_none", "D_none"])
-def test_tc128_stress(variant):
-    d = inputs.Dims(2, 112, 8, 64, 128, 1, "bf16")
-    par = np.stack([trees.heap_kary(112, 2), trees.chain(112)])
+@pytest.mark.parametrize("T", [112, 240])
+def test_tc128_stress(variant, T):
+    d = inputs.Dims(2, T, 8, 64, 128, 1, "bf16")
+    par = np.stack([trees.heap_kary(T, 2), trees.chain(T)])
     kw = dict(stress_decay=dict(dt_range=(0.5, 1.0), A_range=(16.0, 16.0)), no_decay=dict(dt_range=(1e-6, 1e-5)),
               large_x=dict(x_scale=100.0), h0_none=dict(h0_zero=True), D_none=dict(D_none=True)).get(variant, {})
     prob = inputs.make_problem(d, par, seed=99, **kw)
@@ -67,9 +71,10 @@ def test_tc128_stress(variant):
     assert_y_close(y, ref, TOL_BF16)
 
 
-def test_tc128_invalid_tree_zero_and_status():
-    prob = inputs.make_problem(inputs.Dims(3, 90, 8, 64, 128, 1, "bf16"), _trees("random", 3, 90, 5), seed=5)
-    prob.parent[1, 40] = 70
+@pytest.mark.parametrize("T,bad_node", [(90, 40), (220, 180)])
+def test_tc128_invalid_tree_zero_and_status(T, bad_node):
+    prob = inputs.make_problem(inputs.Dims(3, T, 8, 64, 128, 1, "bf16"), _trees("random", 3, T, 5), seed=5)
+    prob.parent[1, bad_node] = bad_node + 5
     y, st = run(prob)
     assert st == 2
     assert not y[1].any()
