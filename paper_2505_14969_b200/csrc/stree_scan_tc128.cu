@@ -30,7 +30,7 @@ namespace tc128 {
 using namespace stree::tc;
 
 constexpr int kP = 64, kN = 128;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // warps 0-7 math (two per TMEM lane quadrant), 8 TMA, 9 MMA
 constexpr int kTile = 16384;          // 128 rows x 128 bytes, swizzle-128B
 constexpr uint32_t kCols = 512;
 
@@ -55,8 +55,8 @@ struct Sm {
     static constexpr int AS = CJ + kHPC * kKeys * 4;        // float [kHPC]
     static constexpr int DS = AS + kHPC * 4;                // float [kHPC]
     static constexpr int BADF = DS + kHPC * 4;              // int
-    static constexpr int WOK = BADF + 4;                    // u32 [4] per-warp factorisable-head masks
-    static constexpr int BAR = (WOK + 16 + 7) & ~7;
+    static constexpr int WOK = BADF + 4;                    // u32 [8] per-warp factorisable-head masks
+    static constexpr int BAR = (WOK + 32 + 7) & ~7;
     // tree, g, ctf, hfull[2], hempty[2], xfull[2], xempty[2], mfull[2], mempty[2], accfull[2], accempty[2]
     static constexpr int NBAR = 3 + 14;
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -121,25 +121,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         mbar_init(BAR_TREE, 1);
         mbar_init(BAR_G, 1);
-        mbar_init(BAR_CTF, 128);
+        mbar_init(BAR_CTF, 256);
         for (int s = 0; s < 2; ++s) {
             mbar_init(bar_hfull(s), 1);
             mbar_init(bar_hempty(s), 1);
             mbar_init(bar_xfull(s), 1);
-            mbar_init(bar_xempty(s), 128);
-            mbar_init(bar_mfull(s), 128);
+            mbar_init(bar_xempty(s), 256);
+            mbar_init(bar_mfull(s), 256);
             mbar_init(bar_mempty(s), 1);
             mbar_init(bar_accfull(s), 1);
-            mbar_init(bar_accempty(s), 128);
+            mbar_init(bar_accempty(s), 256);
         }
         fence_barrier_init();
     }
-    if (warp == 5) {
+    if (warp == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (warp == 4 && lane == 0) {
+    if (warp == 8 && lane == 0) {
         tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0);
     }
     tc_fence_before();
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ================= TMA producer =================
         if (lane == 0) {
             mbar_expect_tx(BAR_TREE, (2 + 2 * nkb) * kTile);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_2d(sb + Sm::xstage(s) + kb * kTile, &tm_x, bar_xfull(s), h * kP, b * T + 128 * kb);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ================= MMA issuer (warp converged, elected lane issues) =================
         mbar_wait(BAR_TREE, 0);
         tc_fence_after();
@@ -219,10 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_commit_w(bar_accfull(a));
         }
     } else {
-        // ================= math warps: thread t = row r0 + t = TMEM lane =================
-        const int t = tid;                       // 0..127
+        // ================= math warps: row t = TMEM lane (warp % 4 quadrant), column half hh =================
+        const int t = tid & 127;                 // row within the tile
+        const int hh = tid >> 7;                 // 0: warps 0-3, 1: warps 4-7 (same lanes, other column half)
         const int i = r0 + t;                    // this thread's row (node)
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
         uint32_t* anc = (uint32_t*)(sm + Sm::ANC);    // [word][node]
         int* jmp = (int*)(sm + Sm::JMP);              // [buf][node]
         float* lam = (float*)(sm + Sm::LAM);          // [buf][head][node]
@@ -232,42 +233,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* ds = (float*)(sm + Sm::DS);
         int* sbad = (int*)(sm + Sm::BADF);
         uint32_t* wok = (uint32_t*)(sm + Sm::WOK);
-        auto mbar = [&]() { named_bar(1, 128); };
+        auto mbar = [&]() { named_bar(1, 256); };
         constexpr int kW = 4 * NKB;              // ancestor words per node
-        // ---- tree prologue over all kT nodes (thread t: nodes t, t + 128): validation (PAPER.md:90 / R5),
-        //      ancestor bits and Λ of every head (Eq. a_tree) by pointer jumping ----
-        if (t < nh) {
-            as[t] = prm.A[hbeg + t];
-            ds[t] = prm.D ? prm.D[hbeg + t] : 0.f;
+        // ---- tree prologue over all kT nodes (thread tid: node tid): validation (PAPER.md:90 / R5), ancestor
+        //      bits and Λ of every head (Eq. a_tree) by pointer jumping ----
+        if (tid < nh) {
+            as[tid] = prm.A[hbeg + tid];
+            ds[tid] = prm.D ? prm.D[hbeg + tid] : 0.f;
         }
-        if (t == 0) *sbad = 0;
+        if (tid == 0) *sbad = 0;
         mbar();
-        int pv[NKB];
-#pragma unroll
-        for (int q = 0; q < NKB; ++q) {
-            const int v = t + 128 * q;
-            pv[q] = v < T ? prm.parent[(size_t)b * T + v] : -1;
-            if (v < T && (v == 0 ? pv[q] != -1 : (pv[q] < 0 || pv[q] >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
+        const int v = tid;                       // node of this thread in the prologue (v < kT iff active)
+        const int pvv = (v < T && v < kT) ? prm.parent[(size_t)b * T + v] : -1;
+        if (v < T && v < kT && (v == 0 ? pvv != -1 : (pvv < 0 || pvv >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
+        if (v < kT)
             for (int k = 0; k < nh; ++k) dts[k * kT + v] = v < T ? prm.dt[((size_t)b * T + v) * H + hbeg + k] : 0.f;
-        }
         mbar();
         const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);   // root error takes precedence
-        if (badcode && t == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
+        if (badcode && tid == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
         const bool valid = badcode == 0;
         int cur = 0;
-#pragma unroll
-        for (int q = 0; q < NKB; ++q) {
-            const int v = t + 128 * q;
+        if (v < kT) {
             for (int w = 0; w < kW; ++w) anc[w * kT + v] = (v < T && (v >> 5) == w) ? (1u << (v & 31)) : 0u;
-            jmp[v] = (valid && v < T) ? pv[q] : -1;
+            jmp[v] = (valid && v < T) ? pvv : -1;
             for (int k = 0; k < nh; ++k) lam[k * kT + v] = dts[k * kT + v] * as[k];
         }
         mbar();
         for (int r = 0; r < 7 + NKB - 1; ++r) {
             const int nx = cur ^ 1;
-#pragma unroll
-            for (int q = 0; q < NKB; ++q) {
-                const int v = t + 128 * q, j = jmp[cur * kT + v];
+            if (v < kT) {
+                const int j = jmp[cur * kT + v];
                 // ancestor sets in place: a concurrently updated row j only ever holds more true ancestors of j
                 if (j >= 0)
                     for (int w = 0; w < kW; ++w) anc[w * kT + v] |= anc[w * kT + j];
@@ -283,9 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t okm = 0;
         for (int k = 0; k < nh; ++k) {
             bool ok = true;
-#pragma unroll
-            for (int q = 0; q < NKB; ++q) {
-                const int v = t + 128 * q;
+            if (v < kT) {
                 const float l = lam[(cur * kHPC + k) * kT + v];
                 if (v < T && l < -64.f) ok = false;
                 cj[k * kT + v] = v < T ? __expf(-l) * dts[k * kT + v] : 0.f;
@@ -298,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(BAR_TREE, 0);
         {
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {   // 32 columns per store
+            for (int c4 = 2 * hh; c4 < 2 * hh + 2; ++c4) {   // this half's 64 columns, 32 per store
                 uint32_t r32[32];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 bf16
@@ -316,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
         }
         mbar();
-        const uint32_t fmask = wok[0] & wok[1] & wok[2] & wok[3];
+        const uint32_t fmask = wok[0] & wok[1] & wok[2] & wok[3] & wok[4] & wok[5] & wok[6] & wok[7];
         uint32_t myanc[kW];
 #pragma unroll
         for (int w = 0; w < kW; ++w) myanc[w] = anc[w * kT + i];
@@ -334,8 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float li = laml[k * kT + i], ei = __expf(li), dh = ds[k];
             const bool fac = (fmask >> k) & 1u;
             __nv_bfloat16* yrow = prm.y + (((size_t)b * T + i) * H + hbeg + k) * kP;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
+            {
+                const int hf = hh;   // this half's 32 output columns
                 tmem_ld32(lane_base + kAccCol + 128 * a + 32 * hf, y0);
                 tmem_ld32(lane_base + kAccCol + 128 * a + 64 + 32 * hf, y1);
                 tmem_wait();
@@ -384,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* dtk = dts + k * kT;
             const uint32_t mb = mbuf(a);
 #pragma unroll 1
-            for (int c4 = 0; c4 < (kcta + 31) / 32; ++c4) {   // 32 key columns at a time
+            for (int c4 = hh; c4 < (kcta + 31) / 32; c4 += 2) {   // 32 key columns at a time, halves interleaved
                 uint32_t gr[32];
                 tmem_ld32(lane_base + kGCol + 32 * c4, gr);
                 tmem_wait();
@@ -428,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
     }
