@@ -198,7 +198,26 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
                          "note": "one call per verify iteration; vocab rows touched depend on the rejections"}
     torch.cuda.synchronize()
     assert status.item() == 0, f"device status {status.item()}"
+    out["c5_sweep"] = measure_c5()
     return out
+
+
+def measure_c5():
+    """BASELINE configs[4] headline shapes (full sweep: tools/sweep_c5.py): packed tree vs the unrolled
+    baseline (every root-to-leaf path its own sequence from the same h0), batch 1, us per layer."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sweep_c5
+    from gen import trees
+    res = {}
+    for T in (64, 128, 256):
+        par = trees.heap_kary(T, 2)
+        paths = sweep_c5.leaf_paths(par)
+        maxlen = max(len(p) for p in paths)
+        t_p, k_p = sweep_c5.time_scan(par[None], L=16)
+        t_u, _ = sweep_c5.time_scan(np.stack([trees.chain(maxlen)] * len(paths)), L=16)
+        res[f"heap2_T{T}"] = {"packed_us": t_p, "unrolled_us": t_u, "speedup_vs_unrolled": t_u / t_p,
+                              "kernel": {1: "simt", 2: "tcgen05", 3: "tcgen05-128"}.get(k_p)}
+    return res
 
 
 if __name__ == "__main__":
