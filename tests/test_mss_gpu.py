@@ -61,7 +61,7 @@ def test_bench_config_c4():
 
 @pytest.mark.parametrize("T,V,kind,seed", [(16, 1000, "random", 1), (31, 997, "heap", 2), (64, 4096, "random", 3),
                                            (7, 7, "heap", 4), (5, 3, "chain", 5), (256, 257, "random", 6),
-                                           (40, 50280, "star", 7)])
+                                           (40, 50280, "star", 7), (15, 128256, "heap", 8)])
 def test_random_trees(T, V, kind, seed):
     rng = np.random.default_rng(seed)
     mk = {"random": lambda: trees.random_recursive(T, 4, rng), "heap": lambda: trees.heap_kary(T, 2),
