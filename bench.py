@@ -416,7 +416,7 @@ def run_stree(args):
         fu_us = ph_mean[1] * 1e3 / L
         fu_gbs = fb / (fu_us * 1e-6) / 1e9
         kernels["stree_replay_scan"] = {"us": fu_us, "bytes": fb, "GB/s": fu_gbs, "frac": fu_gbs / hbm_peak,
-                                        "impl": {1: "simt+commit", 2: "tcgen05 fused"}.get(kernel),
+                                        "impl": {1: "simt+commit", 2: "tcgen05 fused", 4: "tcgen05 small-batch fused"}.get(kernel),
                                         "mean_path_len": float(plen_host.mean())}
         dominant, dom_gbs, dom_bytes = "stree_replay_scan", fu_gbs, fb
     else:
@@ -425,7 +425,7 @@ def run_stree(args):
         scan_gbs = sb / (scan_us * 1e-6) / 1e9
         commit_gbs = cb / (commit_us * 1e-6) / 1e9
         kernels["stree_tree_scan"] = {"us": scan_us, "bytes": sb, "GB/s": scan_gbs, "frac": scan_gbs / hbm_peak,
-                                      "impl": {1: "simt", 2: "tcgen05"}.get(kernel)}
+                                      "impl": {1: "simt", 2: "tcgen05", 3: "tcgen05 128-row", 4: "tcgen05 small-batch"}.get(kernel)}
         kernels["stree_commit"] = {"us": commit_us, "bytes": cb, "GB/s": commit_gbs, "frac": commit_gbs / hbm_peak,
                                    "impl": {1: "ring (CUDA cores)", 2: "TMA pipeline"}.get(
                                        binding.stree_commit_kernel_for(dims, True)),

@@ -76,7 +76,8 @@ typedef enum {
                              scan: bf16 io, P == 64, N in {64,128}, T <= 64; or N == 128, T <= 256;
                              commit: bf16 io, P == 64, N in {64,128}, T <= 256, h0 given */
     STREE_SCAN_SIMT = 1,  /* CUDA-core kernels (FP32-FMA scan, ring commit; any shape; the fp32 1e-4 path) */
-    STREE_SCAN_TC = 2     /* force the pipeline kernels; STREE_ERR_UNSUPPORTED if the shape is not served */
+    STREE_SCAN_TC = 2,    /* force the tcgen05 kernels; STREE_ERR_UNSUPPORTED if the shape is not served */
+    STREE_SCAN_TC_PIPELINE = 3   /* as STREE_SCAN_TC but never the small-batch kernel (A/B comparisons) */
 } stree_scan_impl;
 
 /*
@@ -177,19 +178,31 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
 
 /*
  * Launch options (process-wide, default STREE_LAUNCH_PDL).
- *  STREE_LAUNCH_PDL          launch with programmatic dependent launch: each kernel lets the next
- *                            grid in the stream be scheduled early and waits (griddepcontrol.wait)
- *                            before its first access to argument memory.  Always safe.
- *  STREE_LAUNCH_EARLY_STATE  promise: the state h0 passed to stree_tree_scan / stree_commit is not
- *                            written by the kernel immediately preceding the call in its stream
- *                            (true in a decode loop: the state was committed an iteration earlier).
- *                            The kernels then start streaming h0 before that wait.
+ *  STREE_LAUNCH_PDL          launch with programmatic dependent launch: each kernel may be scheduled
+ *                            while the kernel before it in the stream is still running and waits
+ *                            (griddepcontrol.wait) for that kernel to complete before its first access
+ *                            to argument memory.  Every kernel of this library lets its successor launch
+ *                            only after passing its own wait, so a library kernel can overlap only the
+ *                            kernel IMMEDIATELY preceding it in the stream — never an older one (an
+ *                            older kernel has completed before the preceding kernel's wait returned; a
+ *                            foreign kernel without PDL completes before ours starts).  Always safe.
+ *  STREE_LAUNCH_EARLY_STATE  promise: the state operands of a call are not written by the kernel
+ *                            immediately preceding the call in its stream (true in a decode loop: the
+ *                            state was committed an iteration earlier).  Covered operands:
+ *                              stree_tree_scan, stree_commit, stree_replay_scan: h0 / h;
+ *                              stree_tree_attn: k_cache, v_cache and cache_len.
+ *                            The kernels then start streaming them before the dependency wait.  A call
+ *                            that launches two kernels (stree_replay_scan on shapes the fused kernel does
+ *                            not serve: commit, then scan) applies the promise to its first kernel only.
  *  STREE_LAUNCH_EARLY_REPLAY promise: the previous tree's operands of stree_replay_scan (path,
  *                            path_len, x_prev, dt_prev, Bm_prev, parent_prev) are not written by the
- *                            kernel immediately preceding the call (true in a decode loop: they are
- *                            the previous iteration's inputs and acceptance).  The replay prologue
- *                            (path validation, coefficients, staging) then runs before that wait;
- *                            every global write still follows it.
+ *                            kernel immediately preceding the call (true in a decode loop where the
+ *                            accept kernel is followed by at least one other kernel — e.g. the next
+ *                            iteration's stree_build_mask — before the first replay).  The replay
+ *                            prologue (path validation, coefficients, staging) then runs before that
+ *                            wait; every global write still follows it.  Only stree_replay_scan honours
+ *                            this flag; stree_commit ignores it (its path normally comes from the accept
+ *                            kernel just before it).
  */
 enum { STREE_LAUNCH_PDL = 1, STREE_LAUNCH_EARLY_STATE = 2, STREE_LAUNCH_EARLY_REPLAY = 4 };
 stree_status stree_set_launch_flags(uint32_t flags);
@@ -311,8 +324,9 @@ stree_status stree_accept_mss(const int32_t* tokens, const int32_t* parent, cons
                               int32_t n_nodes, int32_t vocab, int32_t* path, int32_t* path_len, int32_t* bonus,
                               int32_t* dev_status, void* stream);
 
-/* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05 (T <= 64),
- * 3 = tcgen05 128-row-tile kernel (64 < T <= 256, bf16, P = 64, N = 128), 0 = invalid. */
+/* Which kernel stree_tree_scan would launch for these dims: 1 = SIMT, 2 = tcgen05 pipeline (T <= 64),
+ * 3 = tcgen05 128-row-tile kernel (64 < T <= 256, bf16, P = 64, N = 128), 4 = tcgen05 small-batch kernel
+ * (T <= 64, one head per CTA: B·H <= #SMs), 0 = invalid.  stree_replay_scan fuses the commit for 2 and 4. */
 int32_t stree_scan_kernel_for(const stree_dims* d);
 
 /* Which kernel stree_commit would launch (has_h0: h0 != NULL): 1 = CUDA-core ring / block kernel,

@@ -18,7 +18,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libstree.so")
 
 STREE_F32, STREE_BF16 = 0, 1
-STREE_SCAN_AUTO, STREE_SCAN_SIMT, STREE_SCAN_TC = 0, 1, 2
+STREE_SCAN_AUTO, STREE_SCAN_SIMT, STREE_SCAN_TC, STREE_SCAN_TC_PIPELINE = 0, 1, 2, 3
 DEV_BAD_ROOT, DEV_BAD_PARENT, DEV_BAD_PATH, DEV_CAPACITY = 1, 2, 3, 5
 MAX_NODES = 256
 

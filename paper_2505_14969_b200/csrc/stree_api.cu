@@ -19,6 +19,14 @@ extern "C" int stree_launch_scan_tc(const stree_dims*, const void*, const float*
                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
                                     cudaStream_t);
 extern "C" int stree_tc_supports(const stree_dims*);
+extern "C" int stree_lat_supports(const stree_dims*);
+extern "C" int stree_launch_scan_lat(const stree_dims*, const void*, const float*, const float*, const void*,
+                                     const void*, const float*, const float*, const int32_t*, void*, int32_t*,
+                                     cudaStream_t, const void*);
+extern "C" int stree_launch_replay_scan_lat(const stree_dims*, const void*, const float*, const void*,
+                                            const int32_t*, const int32_t*, const int32_t*, const stree_dims*,
+                                            const void*, const float*, const float*, const void*, const void*,
+                                            const float*, float*, const int32_t*, void*, int32_t*, cudaStream_t);
 extern "C" int stree_tc128_supports(const stree_dims*);
 extern "C" int stree_launch_scan_tc128(const stree_dims*, const void*, const float*, const float*, const void*,
                                        const void*, const float*, const float*, const int32_t*, void*, int32_t*,
@@ -51,6 +59,16 @@ namespace {
 
 std::atomic<int> g_scan_impl{STREE_SCAN_AUTO};
 std::atomic<uint32_t> g_launch_flags{STREE_LAUNCH_PDL};
+// Launch flags withheld from the kernels of the call in progress on this thread: an EARLY_* promise
+// covers the operands of one call and the kernel immediately preceding it, so a call that launches
+// two kernels (or whose operands the promise does not cover) clears the flag for that launch.
+thread_local uint32_t tl_flags_mask = ~0u;
+thread_local bool tl_replay_allowed = false;   // set by stree_replay_scan around its internal commit
+struct FlagsMask {
+    uint32_t saved;
+    explicit FlagsMask(uint32_t clear) : saved(tl_flags_mask) { tl_flags_mask &= ~clear; }
+    ~FlagsMask() { tl_flags_mask = saved; }
+};
 
 bool sync_check_enabled() {
     static int v = [] {
@@ -90,7 +108,7 @@ extern "C" {
 
 const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
 
-uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed); }
+uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed) & tl_flags_mask; }
 
 stree_status stree_set_launch_flags(uint32_t flags) {
     if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE | STREE_LAUNCH_EARLY_REPLAY))
@@ -114,7 +132,8 @@ const char* stree_status_string(stree_status s) {
 }
 
 stree_status stree_set_scan_impl(stree_scan_impl impl) {
-    if (impl != STREE_SCAN_AUTO && impl != STREE_SCAN_SIMT && impl != STREE_SCAN_TC) return STREE_ERR_UNSUPPORTED;
+    if (impl != STREE_SCAN_AUTO && impl != STREE_SCAN_SIMT && impl != STREE_SCAN_TC && impl != STREE_SCAN_TC_PIPELINE)
+        return STREE_ERR_UNSUPPORTED;
     g_scan_impl.store((int)impl);
     return STREE_OK;
 }
@@ -124,16 +143,17 @@ int32_t stree_commit_kernel_for(const stree_dims* d, int32_t has_h0) {
     int impl = g_scan_impl.load();
     if (impl == STREE_SCAN_SIMT) return 1;
     if (has_h0 && stree_tc_commit_supports(d)) return 2;
-    return impl == STREE_SCAN_TC ? 0 : 1;
+    return (impl == STREE_SCAN_TC || impl == STREE_SCAN_TC_PIPELINE) ? 0 : 1;
 }
 
 int32_t stree_scan_kernel_for(const stree_dims* d) {
     if (check_dims(d) != STREE_OK) return 0;
     int impl = g_scan_impl.load();
     if (impl == STREE_SCAN_SIMT) return 1;
+    if (impl != STREE_SCAN_TC_PIPELINE && stree_lat_supports(d)) return 4;
     if (stree_tc_supports(d)) return 2;
     if (stree_tc128_supports(d)) return 3;
-    return impl == STREE_SCAN_TC ? 0 : 1;
+    return (impl == STREE_SCAN_TC || impl == STREE_SCAN_TC_PIPELINE) ? 0 : 1;
 }
 
 stree_status stree_build_mask(const int32_t* parent, int32_t batch, int32_t n_nodes, uint32_t* mask,
@@ -158,7 +178,8 @@ stree_status stree_tree_scan(const stree_dims* d, const void* x, const float* dt
     cudaStream_t s = (cudaStream_t)stream;
     int which = stree_scan_kernel_for(d);
     if (which == 0) return STREE_ERR_UNSUPPORTED;
-    int rc = (which == 2)   ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
+    int rc = (which == 4)   ? stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s, nullptr)
+             : (which == 2) ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
              : (which == 3) ? stree_launch_scan_tc128(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
                             : stree_launch_scan_simt(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s);
     return finish(rc, dev_status, s);
@@ -191,6 +212,9 @@ stree_status stree_commit(const stree_dims* d, const void* x, const float* dt, c
         if (a < b + bytes && b < a + bytes) return STREE_ERR_SHAPE;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    // EARLY_REPLAY is a promise about stree_replay_scan's previous-tree operands only: the path of a plain
+    // commit is normally written by the stree_accept kernel immediately before it
+    FlagsMask fm(tl_replay_allowed ? 0u : (uint32_t)STREE_LAUNCH_EARLY_REPLAY);
     const int which = stree_commit_kernel_for(d, h0 != nullptr);
     if (which == 0) return STREE_ERR_UNSUPPORTED;
     if (which == 2) {
@@ -216,12 +240,19 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
     if (d->batch == 0) return STREE_OK;
     if (!h) return STREE_ERR_NULL;
     cudaStream_t s = (cudaStream_t)stream;
-    const bool fused = d->n_nodes > 0 && d_prev->n_nodes > 0 && stree_scan_kernel_for(d) == 2;
+    const int which = stree_scan_kernel_for(d);
+    const bool fused = d->n_nodes > 0 && d_prev->n_nodes > 0 && (which == 2 || which == 4);
     if (!fused) {   // two launches: commit (in place), then scan from the committed state
         if (d_prev->n_nodes > 0) {
+            // the commit is the call's first kernel: the caller's EARLY_REPLAY / EARLY_STATE promises hold for it
+            tl_replay_allowed = true;
             st = stree_commit(d_prev, x_prev, dt_prev, A, Bm_prev, h, parent_prev, path, path_len, h, dev_status,
                               stream);
+            tl_replay_allowed = false;
             if (st != STREE_OK) return st;
+            // ... but the scan's carry-in h was just written by that commit: no early state stream
+            FlagsMask fm(STREE_LAUNCH_EARLY_STATE);
+            return stree_tree_scan(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, stream);
         }
         return stree_tree_scan(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, stream);
     }
@@ -230,8 +261,9 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
     const void* ptrs[] = {x_prev, dt_prev, Bm_prev, x, dt, A, Bm, Cm, D, h, parent, y};
     for (const void* p : ptrs)
         if (p && !aligned16(p)) return STREE_ERR_ALIGN;
-    return finish(stree_launch_replay_scan_tc(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt,
-                                              A, Bm, Cm, D, h, parent, y, dev_status, s),
+    auto launch = which == 4 ? stree_launch_replay_scan_lat : stree_launch_replay_scan_tc;
+    return finish(launch(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt, A, Bm, Cm, D, h,
+                         parent, y, dev_status, s),
                   dev_status, s);
 }
 
@@ -322,7 +354,7 @@ stree_status stree_tree_attn(const stree_attn_dims* d, const void* q, const void
     for (const void* p : {q, k_new, v_new, k_cache, v_cache, (const void*)o})
         if (p && !aligned16(p)) return STREE_ERR_ALIGN;
     const int tc = attn_use_tc(d);
-    if (!tc && g_scan_impl.load() == STREE_SCAN_TC) return STREE_ERR_UNSUPPORTED;
+    if (!tc && (g_scan_impl.load() == STREE_SCAN_TC || g_scan_impl.load() == STREE_SCAN_TC_PIPELINE)) return STREE_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     return finish(stree_launch_tree_attn(d, q, k_new, v_new, k_cache, v_cache, cache_len, parent, scale, o,
                                          dev_status, tc, s),

@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 #include "stree_tc_ptx.cuh"
 
 namespace stree {
@@ -102,7 +103,6 @@ __global__ void __launch_bounds__(32) attn_simt_kernel(const IO* __restrict__ q,
     __shared__ float sq[kSimtMaxD];
     __shared__ int spath[kMaxNodes];
     __shared__ int snp, sbad;
-    pdl_trigger();
     pdl_wait();
     const int h = blockIdx.x, i = blockIdx.y, b = blockIdx.z, lane = threadIdx.x;
     const int g = h / (Hq / Hkv);
@@ -258,7 +258,6 @@ __global__ void __launch_bounds__(SPLIT ? kThreadsSplit : kThreads, 1)
     const int nmt = (T * grp + kBM - 1) / kBM;
     const int nw = min(2, nmt - 2 * pr);               // query tiles of this CTA (1 or 2)
     unsigned long long* tr = (prm.trace && blockIdx.x == 0) ? prm.trace : nullptr;   // debug timeline
-    pdl_trigger();
 
     const uint32_t bar0 = sb + Smem::BAR;
     const uint32_t BAR_Q = bar0;
@@ -652,7 +651,6 @@ __global__ void __launch_bounds__(256) kv_commit_kernel(const W* __restrict__ k_
                                                         int32_t* dev_status) {
     __shared__ int s_ok, s_L, s_r;
     __shared__ int s_path[kMaxNodes];
-    pdl_trigger();
     pdl_wait();
     const int b = blockIdx.x, tid = threadIdx.x;
     if (tid == 0) {
@@ -693,34 +691,10 @@ __global__ void __launch_bounds__(256) kv_commit_kernel(const W* __restrict__ k_
 // ---------------------------------------------------------------------------
 namespace {
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn attn_encode_fn() {
-    static EncodeTiledFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return (EncodeTiledFn) nullptr;
-        return (EncodeTiledFn)p;
-    }();
-    return fn;
-}
-
 // bf16 4-D map over [d3][d2][d1][d0] (d0 innermost, contiguous), box {64, b1, b2, 1}, swizzle 128B
 bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b1,
                uint32_t b2) {
-    EncodeTiledFn fn = attn_encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[4] = {d0, d1, d2, d3};
-    cuuint64_t strides[3] = {d0 * 2, d0 * d1 * 2, d0 * d1 * d2 * 2};
-    cuuint32_t box[4] = {64, b1, b2, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return stree::host::tmap_4d_bf16(m, base, d0, d1, d2, d3, b1, b2);
 }
 
 }  // namespace
@@ -773,7 +747,7 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
         }();
         auto k = split ? (poly == 1 ? attn_tc_kernel<1, true> : attn_tc_kernel<0, true>)
                        : (poly == 1 ? attn_tc_kernel<1, false> : attn_tc_kernel<0, false>);
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = stree::host::smem_attr((const void*)k, (int)smem);
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, dim3(B * Hkv * prm.npairs), dim3(split ? kThreadsSplit : kThreads), smem, s, mq, mkc,
                             mvc, mkn, mvn, prm);

@@ -14,6 +14,7 @@
 // path prologue.  Accepted paths longer than kRMax (and shapes the ring cannot
 // hold) use the simple per-(tree, head) kernel below.
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 
 namespace stree {
 
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     const int g = rem / prm.cpg, chunk = rem % prm.cpg;
     const int hpg = H / prm.G, hbeg = g * hpg + chunk * prm.hpc;
     const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
-    if (nh <= 0) return;
+    if (nh <= 0) { pdl_wait(); return; }
     const int blk = P * N;                              // floats per state block
     const uint32_t blk_bytes = (uint32_t)blk * 4;
     // shared layout: ring | u[nh][kRMax][P] (long paths: coef[kCHPC][kMaxNodes]) | Bs[kRMax][N] |
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     float* ring = (float*)csm;
     float* u = (float*)(csm + (size_t)prm.slots * blk_bytes);
     float* coefl = u;
-    float* Bs = u + kCHPC * kRMax * P;
+    // the u region is max(u staging, long-path coefficients) wide, as the host sizes it
+    float* Bs = u + max(kCHPC * kRMax * P, kCHPC * kMaxNodes);
     float* decay = Bs + kRMax * N;                      // [kCHPC]
     int* spath = (int*)(decay + kCHPC);                 // [kMaxNodes]
     int* sr = spath + kMaxNodes;                        // [1]
@@ -96,7 +98,6 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     const size_t base = ((size_t)b * H + hbeg) * (size_t)blk;
     unsigned long long* tr = prm.trace ? prm.trace + (size_t)blockIdx.x * 64 : nullptr;
     if (tr && tid == 0) tr[0] = c_gtimer();
-    pdl_trigger();
 
     if (tid == 0) {
         for (int s = 0; s < prm.slots; ++s) {
@@ -299,7 +300,6 @@ __global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, 
     __shared__ float s_decay;
     __shared__ int s_r;
     const int h = blockIdx.x, b = blockIdx.y, g = h / (H / G), tid = threadIdx.x;
-    pdl_trigger();
     pdl_wait();
     const int r0 = path_len[b];
     if (tid < 32) {
@@ -367,15 +367,7 @@ namespace {
 
 unsigned long long* g_commit_trace = nullptr;
 
-int commit_sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
-}
+int commit_sms() { return stree::host::num_sms(); }
 
 template <typename IO>
 int launch(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm, const float* h0,
@@ -409,7 +401,7 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
     const size_t smem = (size_t)slots * blk_bytes + ustage + (size_t)stree::kRMax * N * 4 + stree::kCHPC * 4 +
                         (stree::kMaxNodes + 1) * 4 + 16 + (size_t)2 * slots * 8 + 64;
     auto k = stree::commit_ring_kernel<IO>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return (int)e;
     return (int)stree::launch_k(k, dim3(B * G * cpg), dim3(stree::kCThreads), smem, s, prm);
 }

@@ -14,11 +14,17 @@ constexpr int kMaxNodes = STREE_MAX_NODES;          // T <= 256
 constexpr int kMaxWords = (kMaxNodes + 31) / 32;    // mask words per row
 
 // ---- Programmatic dependent launch (PDL) ----
-// Every kernel calls pdl_trigger() at entry (the next grid in the stream may be scheduled as SMs free
-// up) and pdl_wait() before its first global read or write of call arguments; setup that touches
-// no argument memory (barrier init, TMEM alloc, descriptor prefetch) runs before the wait.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Every kernel calls pdl_wait() before its first global read or write of call arguments (setup that
+// touches no argument memory — barrier init, TMEM allocation, descriptor prefetch — runs before it).
+// The wait is followed by griddepcontrol.launch_dependents: the next grid in the stream may be
+// scheduled only once every CTA of this grid has passed its own dependency wait (or exited), i.e. once
+// the grid before this one has completed.  So a kernel launched by this library can overlap only the
+// kernel immediately preceding it in the stream, never an older one — the scope of the
+// STREE_LAUNCH_EARLY_* promises (include/stree.h).
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ void report(int32_t* dev_status, int code) {
     if (dev_status) atomicCAS(dev_status, 0, code);

@@ -10,6 +10,7 @@
 // walked in shared memory, stepping into the state rows above the root), and the output row is
 // written once, coalesced.
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 
 namespace stree {
 namespace conv {
@@ -82,7 +83,6 @@ __global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __rest
     const int b = blockIdx.y, c0 = blockIdx.x * kChunks * V;
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
     const bool cv = c0 + lane * V < C;                                     // this lane's chunk exists
-    pdl_trigger();
     if (tid == 0) s_bad = 0;
     // the block's weights and bias: coalesced loads issued together with the parent and staging loads below
     // (one memory latency for all of them), then through shared memory, [w][v][lane] so the per-thread reads
@@ -198,7 +198,6 @@ __global__ void __launch_bounds__(32) conv_commit_kernel(const IO* __restrict__ 
     constexpr int V = Pack<IO>::V;
     const int b = blockIdx.y, c0 = blockIdx.x * kChunks * V, lane = threadIdx.x;
     const bool cv = c0 + lane * V < C;
-    pdl_trigger();
     pdl_wait();
     const int r = path_len[b];
     const int32_t* pa = path + (size_t)b * T;
@@ -249,7 +248,7 @@ cudaError_t launch_conv(const stree_conv_dims* d, const void* u, const float* we
     auto k = tree_conv_kernel<IO, W>;
     // one wave at the 2.7B shape (336 CTAs over 148 SMs needs 3 resident per SM): registers capped by the
     // launch bounds, shared-memory carveout at its maximum
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     return launch_k(k, grid, dim3(kThreads), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent, act,

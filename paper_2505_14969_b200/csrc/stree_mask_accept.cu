@@ -17,7 +17,6 @@ __global__ void __launch_bounds__(256) build_mask_kernel(const int32_t* __restri
     __shared__ int sp[kMaxNodes], jmp[kMaxNodes], jmp2[kMaxNodes];
     __shared__ uint32_t rows[kMaxNodes * kMaxWords], rows2[kMaxNodes * kMaxWords];
     const int b = blockIdx.x, W = (T + 31) >> 5;
-    pdl_trigger();
     pdl_wait();
     for (int i = threadIdx.x; i < T; i += blockDim.x) sp[i] = parent[(size_t)b * T + i];
     __syncthreads();
@@ -43,7 +42,6 @@ __global__ void __launch_bounds__(128) accept_kernel(const int32_t* __restrict__
                                                      int32_t* __restrict__ bonus, int32_t* dev_status) {
     __shared__ int s_par[4][kMaxNodes], s_tok[4][kMaxNodes], s_vt[4][kMaxNodes];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    pdl_trigger();
     pdl_wait();
     const int b = blockIdx.x * 4 + warp;
     if (b >= B) return;

@@ -17,6 +17,7 @@
 // rejection, and accepted chains never touch the vocabulary.  Every CTA takes every decision itself
 // from bit-identical operands, so control flow stays uniform across the cluster.
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 
 namespace stree {
 namespace mss {
@@ -90,7 +91,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ float s_red[2][kCl];                      // cluster exchange of partial sums (double buffer)
     __shared__ float s_scan[kWarps];
     __shared__ int s_found;
-    pdl_trigger();
     const int tid = threadIdx.x;
     const uint32_t rank = cluster_rank();
     const int b = blockIdx.x / kCl;
@@ -194,7 +194,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         loaded = false;
         for (int k = 0; k < nch; ++k) {
             const int c = s_child[k];
-            const float pt = loaded ? pt_next : s_pt[k];
+            // after a rejection p[t] of this sibling comes from the CTA owning t; an out-of-range token has
+            // no owner and is rejected (p = 0), as before any rejection (s_pt)
+            const int tc = s_tok[c];
+            const float pt = loaded ? ((tc >= 0 && tc < V) ? pt_next : 0.f) : s_pt[k];
             if (s_u[c] * s_qt[k] < pt) {
                 acc = c;
                 break;
@@ -303,13 +306,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncthreads();
-        if (s_found == -1) {   // fallback (or the threshold fell past this slice's last step): last v with p > 0
+        // read the search result into a register before any thread may change it: the fallback branch
+        // below is then uniform across the CTA and its barrier is never divergent
+        const bool none = s_found == -1;
+        __syncthreads();
+        if (none) {   // fallback (or the threshold fell past this slice's last step): last v with p > 0
             int lp = -1;
             for (int v = c0; v < c1; ++v)
                 if (ps[v] > 0.f) lp = v0 + v;
             atomicMax(&s_found, lp);
-            __syncthreads();
         }
+        __syncthreads();
         if (tid == 0) bonus[b] = s_found;
     }
     if (rank == 0) {
@@ -331,7 +338,7 @@ extern "C" int stree_launch_accept_mss(const int32_t* tokens, const int32_t* par
     using namespace stree::mss;
     const int slice = (V + kCl - 1) / kCl;
     const size_t smem = (size_t)3 * slice * sizeof(float);
-    cudaError_t e = cudaFuncSetAttribute(mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = stree::host::smem_attr((const void*)mss_kernel, (int)smem);
     if (e != cudaSuccess) return (int)e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(B * kCl);

@@ -9,6 +9,7 @@
 // with Λ = L·(dt A_h) the tree segsum and the decay mask
 // applied before exp (off-path entries are never exponentiated).
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 
 namespace stree {
 
@@ -55,7 +56,6 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
     const int W = L.W, mp = L.mpitch;
     const int h = blockIdx.x, b = blockIdx.y, g = h / (H / G);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    pdl_trigger();
     pdl_wait();
 
     for (int i = tid; i < T; i += 256) sp[i] = parent[(size_t)b * T + i];
@@ -225,7 +225,7 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
     cudaError_t e;
     if (d->io_dtype == STREE_BF16) {
         auto k = stree::scan_simt_kernel<__nv_bfloat16>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = stree::host::smem_attr((const void*)k, (int)smem);
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
                             (const __nv_bfloat16*)x, dt, A, (const __nv_bfloat16*)Bm, (const __nv_bfloat16*)Cm, D, h0,
@@ -233,7 +233,7 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
         if (e != cudaSuccess) return (int)e;
     } else {
         auto k = stree::scan_simt_kernel<float>;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = stree::host::smem_attr((const void*)k, (int)smem);
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
                             (const float*)x, dt, A, (const float*)Bm, (const float*)Cm, D, h0, parent, (float*)y,

@@ -30,6 +30,7 @@
 #include <cuda.h>
 
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 #include "stree_tc_ptx.cuh"
 
 namespace stree {
@@ -396,9 +397,8 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     const int hpg = H / prm.G;
     const int hbeg = g * hpg + chunk * prm.hpc;
     const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
-    if (nh <= 0) return;
+    if (nh <= 0) { pdl_wait(); return; }
     int* sp = (int*)(sm + S::PAR);
-    pdl_trigger();
 
     const uint32_t bar0 = sb + S::BAR;
     const uint32_t BAR_TREE = bar0, BAR_CTF = bar0 + 8, BAR_G = bar0 + 16;
@@ -952,46 +952,14 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
 // ---------------------------------------------------------------------------
 namespace {
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return (EncodeTiledFn) nullptr;
-        return (EncodeTiledFn)p;
-    }();
-    return fn;
-}
-
 bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
-    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return stree::host::tmap_2d(m, dt, base, inner, outer, row_bytes, box_inner, box_outer);
 }
 
 unsigned long long* g_trace = nullptr;
 
-int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
-}
+int num_sms() { return stree::host::num_sms(); }
 
 }  // namespace
 
@@ -1017,7 +985,7 @@ cudaError_t launch_tc_inst(dim3 grid, cudaStream_t s, const CUtensorMap& mc, con
     using namespace stree::tc;
     auto k = scan_tc_kernel<NS, MODE>;
     const size_t smem = Smem<NS, (MODE >= 1)>::TOTAL + 1024;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return e;
     return stree::launch_k(k, grid, dim3(MODE ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, prm);
 }

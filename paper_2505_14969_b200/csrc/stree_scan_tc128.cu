@@ -22,6 +22,7 @@
 #include <cuda.h>
 
 #include "stree_common.cuh"
+#include "stree_host.cuh"
 #include "stree_tc_ptx.cuh"
 
 namespace stree {
@@ -99,11 +100,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hpg = H / prm.G;
     const int hbeg = g * hpg + chunk * prm.hpc;
     const int nh = min(prm.hpc, g * hpg + hpg - hbeg);
-    if (nh <= 0 || r0 >= T) return;
+    if (nh <= 0 || r0 >= T) { pdl_wait(); return; }
     const int Tp16 = (T + 15) & ~15;
     const int kcta = min(Tp16, 128 * (rt + 1));       // keys this tile's rows can see (multiple of 16)
     const int nkb = rt + 1;                           // key blocks of 128
-    pdl_trigger();
 
     const uint32_t bar0 = sb + Sm::BAR;
     const uint32_t BAR_TREE = bar0, BAR_G = bar0 + 8, BAR_CTF = bar0 + 16;
@@ -431,31 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace stree
 
 namespace {
-typedef CUresult (*EncodeTiledFn128)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn128 enc128() {
-    static EncodeTiledFn128 fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return (EncodeTiledFn128) nullptr;
-        return (EncodeTiledFn128)p;
-    }();
-    return fn;
-}
 bool map2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
            uint32_t box_inner, uint32_t box_outer) {
-    EncodeTiledFn128 fn = enc128();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
-    return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
+    return stree::host::tmap_2d(m, dt, base, inner, outer, row_bytes, box_inner, box_outer);
 }
 }  // namespace
 
@@ -488,7 +466,7 @@ int launch_tc128(const stree_dims* d, const CUtensorMap& mc, const CUtensorMap& 
     prm.hpc = hpc;
     const size_t smem = S::TOTAL + 1024;
     auto k = scan_tc128_kernel<NKB>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return (int)e;
     e = stree::launch_k(k, dim3(B * G * cpg * NKB), dim3(kThreads), smem, s, mc, mb, mx, mh, prm);
     if (e != cudaSuccess) return (int)e;

@@ -11,3 +11,11 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    try:
+        from tests import helpers
+    except Exception:
+        return
+    helpers.write_log()

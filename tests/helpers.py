@@ -1,43 +1,96 @@
 """Comparison helpers for parity tests (tolerances: BASELINE north_star;
-metric: SURVEY.md §8(c) C20)."""
+metric: SURVEY.md §8(c) C20, R13).
+
+Every floating-point comparison applies three checks:
+  1. normwise per block (tree, head) / (tree, channel):  ‖a−b‖₂ / ‖b‖₂ ≤ tol      (C20 primary)
+  2. elementwise per block:  max|a−b| ≤ tol · max|b|                             (C20 secondary guard)
+  3. per node (one row of the block, e.g. y[b, i, h, :]):  ‖a_i−b_i‖₂ ≤ tol · max(‖b_i‖₂, rms_block)
+     — a defect confined to a few nodes (e.g. the deepest nodes of a long chain) cannot hide in a
+     block norm.
+Blocks whose reference is exactly zero (zero-filled invalid trees, zero inputs) are not skipped: the
+result must be zero up to tol · (largest |reference| of the whole array).
+The bf16 path must in addition stay inside the error model of SURVEY §8(c) (bf16 output rounding 2⁻⁹,
+bf16 masked weights, tf32 carry-in): normwise ≤ ERR_MODEL_BF16, 4x below the 2e-2 tolerance, so a
+several-fold regression of the kernels' accuracy fails even while it is still inside the tolerance.
+Observed errors are recorded (and written as JSON lines to $STREE_PARITY_LOG at session end).
+"""
+import os
+
 import numpy as np
 
 TOL_F32 = 1e-4   # fp32 path
 TOL_BF16 = 2e-2  # bf16 inputs, fp32 accumulation
+ERR_MODEL_BF16 = 5e-3   # SURVEY §8(c) "bf16 tolerance": expected ≲ 5e-3 normwise
+
+OBSERVED = []   # (test id, kind, normwise, elementwise, per-node)
 
 
-def blockwise_relerr(got, ref, block_axes):
-    """Normwise rel-err per block (blocks = all indices except block_axes reduced).
-    Returns (max normwise rel err, max of max|a-b|/max|b|)."""
+def _record(kind, r1, r2, r3):
+    OBSERVED.append((os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], kind, r1, r2, r3))
+
+
+def blockwise_relerr(got, ref, block_axes, row_axes=None):
+    """Errors per block (blocks = all indices except block_axes reduced).
+    Returns (max normwise rel err, max of max|a-b|/max|b|, max per-row error, max |a| over zero blocks
+    relative to the array's max |b|).  row_axes: the axes of one node's row (subset of block_axes)."""
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    assert np.isfinite(got).all(), "non-finite values"
     diff = got - ref
     num = np.sqrt((diff ** 2).sum(axis=block_axes))
     den = np.sqrt((ref ** 2).sum(axis=block_axes))
     mx = np.abs(diff).max(axis=block_axes)
     mref = np.abs(ref).max(axis=block_axes)
     ok = den > 0
-    r1 = float((num[ok] / den[ok]).max()) if ok.any() else float(num.max())
-    r2 = float((mx[ok] / mref[ok]).max()) if ok.any() else float(mx.max())
+    scale = max(float(np.abs(ref).max()), 1e-30)
+    r1 = float((num[ok] / den[ok]).max()) if ok.any() else 0.0
+    r2 = float((mx[ok] / mref[ok]).max()) if ok.any() else 0.0
+    rz = float(mx[~ok].max() / scale) if (~ok).any() else 0.0
+    r3 = 0.0
+    if row_axes is not None:
+        rnum = np.sqrt((diff ** 2).sum(axis=row_axes, keepdims=True))
+        rden = np.sqrt((ref ** 2).sum(axis=row_axes, keepdims=True))
+        # rms row norm of the row's block: block norm / sqrt(rows per block)
+        n_rows = int(np.prod([ref.shape[a] for a in block_axes])) // int(np.prod([ref.shape[a] for a in row_axes]))
+        bden = np.sqrt((ref ** 2).sum(axis=block_axes, keepdims=True)) / np.sqrt(max(n_rows, 1))
+        floor = np.maximum(rden, bden)
+        okr = floor > 0
+        r3 = float((rnum[okr] / floor[okr]).max()) if okr.any() else 0.0
+    return r1, r2, r3, rz
+
+
+def _assert(kind, got, ref, tol, block_axes, row_axes):
+    r1, r2, r3, rz = blockwise_relerr(got, ref, block_axes, row_axes)
+    _record(kind, r1, r2, r3)
+    assert r1 <= tol and r2 <= tol, f"{kind} rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
+    assert r3 <= tol, f"{kind} per-node rel-err {r3:.3e} > tol {tol:.0e}"
+    assert rz <= tol, f"{kind}: a block whose reference is zero has |value| {rz:.3e} (relative) > tol {tol:.0e}"
+    if tol == TOL_BF16:
+        assert r1 <= ERR_MODEL_BF16, f"{kind} normwise {r1:.3e} outside the bf16 error model {ERR_MODEL_BF16:.0e}"
     return r1, r2
 
 
 def assert_y_close(y_gpu, y_ref, tol):
-    """y [B][T][H][P]: blocks are (tree, head)."""
-    r1, r2 = blockwise_relerr(y_gpu, y_ref, (1, 3))
-    assert r1 <= tol and r2 <= tol, f"y rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
-    return r1, r2
+    """y [B][T][H][P]: blocks are (tree, head), rows are nodes (P values)."""
+    return _assert("y", y_gpu, y_ref, tol, (1, 3), (3,))
 
 
 def assert_h_close(h_gpu, h_ref, tol):
-    """h [B][H][P][N]: blocks are (tree, head)."""
-    r1, r2 = blockwise_relerr(h_gpu, h_ref, (2, 3))
-    assert r1 <= tol and r2 <= tol, f"h rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
-    return r1, r2
+    """h [B][H][P][N]: blocks are (tree, head), rows are state rows p (N values)."""
+    return _assert("h", h_gpu, h_ref, tol, (2, 3), (3,))
 
 
 def assert_conv_close(o_gpu, o_ref, tol):
-    """tree conv output [B][T][C]: blocks are (tree, channel)."""
-    r1, r2 = blockwise_relerr(o_gpu, o_ref, (1,))
-    assert r1 <= tol and r2 <= tol, f"conv rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
-    return r1, r2
+    """tree conv output [B][T][C]: blocks are (tree, channel), rows are single nodes."""
+    return _assert("conv", o_gpu, o_ref, tol, (1,), None)
+
+
+def write_log():
+    path = os.environ.get("STREE_PARITY_LOG")
+    if not path or not OBSERVED:
+        return
+    import json
+    with open(path, "a") as f:
+        for t, kind, r1, r2, r3 in OBSERVED:
+            f.write(json.dumps({"test": t, "kind": kind, "normwise": r1, "elementwise": r2, "per_node": r3}) + "\n")

@@ -7,7 +7,7 @@ import torch
 from gen import trees
 from gen.attn import AttnDims, attn_config, make_attn_problem
 from oracle import attn as oattn
-from tests.helpers import TOL_BF16, TOL_F32, blockwise_relerr
+from tests.helpers import TOL_BF16, TOL_F32, _assert
 
 pytestmark = pytest.mark.gpu
 
@@ -57,9 +57,8 @@ def run_oracle(prob):
 
 
 def check(o, ref, tol):
-    r1, r2 = blockwise_relerr(o, ref, (1, 3))
-    assert r1 <= tol and r2 <= tol, f"attn rel-err normwise {r1:.3e} max {r2:.3e} > tol {tol:.0e}"
-    return r1, r2
+    """o [B][T][Hq][D]: blocks (tree, head), rows = nodes (tests/helpers.py checks)."""
+    return _assert("attn", o, ref, tol, (1, 3), (3,))
 
 
 def _tree(kind, T, rng):

@@ -347,44 +347,62 @@ def test_graft_invariant_two_iterations():
 # tcgen05 kernel specifically (forced), incl. N=64, G>1, ragged T, NULL h0/D
 # ---------------------------------------------------------------------------
 def test_tc_kernel_selected_for_mamba2_shapes():
-    for cfg in ("c2", "c3", "c4"):
+    # batch-1 layers (c2, c3: B·H <= #SMs) take the small-batch kernel, c4 the pipelined one
+    for cfg, k in (("c2", 4), ("c3", 4), ("c4", 2)):
         d, _ = inputs.config_trees(cfg, 0)
         dims = binding.stree_dims(d.batch, d.n_nodes, d.n_heads, d.head_dim, d.d_state, d.n_groups, 1)
-        assert binding.stree_scan_kernel_for(dims) == 2, cfg
+        assert binding.stree_scan_kernel_for(dims) == k, cfg
+        binding.stree_set_scan_impl(binding.STREE_SCAN_TC_PIPELINE)
+        try:
+            assert binding.stree_scan_kernel_for(dims) == 2, cfg
+        finally:
+            binding.stree_set_scan_impl(binding.STREE_SCAN_AUTO)
+
+
+# the forced tcgen05 tests run both the small-batch kernel (where B·H <= #SMs) and the pipelined one
+TC_IMPLS = pytest.mark.parametrize("impl", ["tc", "pipeline"])
+
+
+def _impl(name):
+    return {"tc": binding.STREE_SCAN_TC, "pipeline": binding.STREE_SCAN_TC_PIPELINE}[name]
 
 
 @pytest.mark.parametrize("shape", [(1, 64, 80, 64, 128, 1), (16, 64, 80, 64, 128, 1), (3, 1, 5, 64, 128, 1),
                                    (2, 13, 7, 64, 64, 1), (4, 50, 24, 64, 128, 2), (2, 33, 30, 64, 64, 3),
                                    (5, 17, 40, 64, 128, 1), (16, 50, 80, 64, 128, 1), (12, 37, 96, 64, 128, 1)])
-def test_tc_forced_shapes(shape):
+@TC_IMPLS
+def test_tc_forced_shapes(shape, impl):
     B, T, H, P, N, G = shape
     rng = np.random.default_rng(B * 1000 + T)
     par = np.stack([trees.random_recursive(T, 3, rng) for _ in range(B)])
     prob = inputs.make_problem(inputs.Dims(B, T, H, P, N, G, "bf16"), par, seed=T * 31 + H)
-    y, ref, st, _ = scan_both(prob, binding.STREE_SCAN_TC)
+    y, ref, st, _ = scan_both(prob, _impl(impl))
     assert st == 0
     assert_y_close(y, ref, TOL_BF16)
 
 
 @pytest.mark.parametrize("variant", ["stress_decay", "no_decay", "large_x", "h0_zero", "D_none"])
-def test_tc_forced_stress(variant):
+@TC_IMPLS
+def test_tc_forced_stress(variant, impl):
     d = inputs.Dims(2, 64, 8, 64, 128, 1, "bf16")
     par = np.stack([trees.heap_kary(64, 2), trees.chain(64)])
     kw = dict(stress_decay=dict(dt_range=(0.5, 1.0), A_range=(16.0, 16.0)),
               no_decay=dict(dt_range=(1e-6, 1e-5)),
               large_x=dict(x_scale=100.0), h0_zero=dict(h0_zero=True), D_none=dict(D_none=True))[variant]
     prob = inputs.make_problem(d, par, seed=98, **kw)
-    y, ref, st, _ = scan_both(prob, binding.STREE_SCAN_TC)
+    y, ref, st, _ = scan_both(prob, _impl(impl))
     assert_y_close(y, ref, TOL_BF16)
 
 
 @pytest.mark.parametrize("with_h0", [True, False])
-def test_tc_mixed_decay_modes(with_h0):
+@pytest.mark.parametrize("B", [16, 2])
+def test_tc_mixed_decay_modes(with_h0, B):
     """Heads of one CTA alternate between the factorised decay (Y' accumulated onto Y0) and the
     direct per-element decay (Y' in its own TMEM columns): A_h spans 1..16 over a chain, so
-    min Λ crosses the -64 switch within the head range."""
-    d = inputs.Dims(16, 64, 48, 64, 128, 1, "bf16")      # 16 trees: several heads per CTA
-    par = np.stack([trees.chain(64) if i % 2 == 0 else trees.heap_kary(64, 2) for i in range(16)])
+    min Λ crosses the -64 switch within the head range.  B = 2: the small-batch kernel (one head per
+    CTA, the direct Y' in the G columns)."""
+    d = inputs.Dims(B, 64, 48, 64, 128, 1, "bf16")      # 16 trees: several heads per CTA
+    par = np.stack([trees.chain(64) if i % 2 == 0 else trees.heap_kary(64, 2) for i in range(B)])
     prob = inputs.make_problem(d, par, seed=77, dt_range=(0.05, 0.2), A_range=(1.0, 24.0))
     lam_min = (prob.dt[0] * prob.A[None, :]).sum(axis=0)
     assert (lam_min < -64).any() and (lam_min > -64).any()
@@ -406,10 +424,11 @@ def test_tc_mixed_decay_modes(with_h0):
     assert_y_close(y, ref, TOL_BF16)
 
 
-def test_tc_null_h0_D_and_invalid_tree():
+@TC_IMPLS
+def test_tc_null_h0_D_and_invalid_tree(impl):
     prob = inputs.config_problem("c2")
     t = api.upload(prob)
-    binding.stree_set_scan_impl(binding.STREE_SCAN_TC)
+    binding.stree_set_scan_impl(_impl(impl))
     try:
         y = torch.empty_like(t["x"])
         binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], None, None, t["parent"], y)

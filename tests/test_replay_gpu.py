@@ -63,12 +63,18 @@ def oracle_pair(prev, new, path, plen):
 @pytest.mark.parametrize("shape", [(16, 64, 64, 80, 64, 128, 1), (1, 64, 64, 80, 64, 128, 1),
                                    (3, 40, 24, 16, 64, 64, 1), (4, 32, 50, 24, 64, 128, 2),
                                    (2, 13, 64, 12, 64, 128, 1), (16, 64, 50, 80, 64, 128, 1), (12, 30, 37, 96, 64, 128, 1)])
-def test_replay_scan_matches_oracle(shape):
+@pytest.mark.parametrize("impl", ["auto", "pipeline"])
+def test_replay_scan_matches_oracle(shape, impl):
     B, Tp, T, H, P, N, G = shape
     prev, new, path, plen = make_pair(B, Tp, T, H, P, N, G, "bf16", seed=Tp * 7 + T)
     d = binding.stree_dims(B, T, H, P, N, G, 1)
-    assert binding.stree_scan_kernel_for(d) == 2      # the fused tcgen05 kernel serves this shape
-    y, h, st = run_fused(prev, new, path, plen)
+    binding.stree_set_scan_impl(binding.STREE_SCAN_TC_PIPELINE if impl == "pipeline" else binding.STREE_SCAN_AUTO)
+    try:
+        # a fused tcgen05 kernel serves this shape: the small-batch one (4) when B·H <= #SMs
+        assert binding.stree_scan_kernel_for(d) in ((2,) if impl == "pipeline" else (2, 4))
+        y, h, st = run_fused(prev, new, path, plen)
+    finally:
+        binding.stree_set_scan_impl(binding.STREE_SCAN_AUTO)
     yr, hr, hst, yst = oracle_pair(prev, new, path, plen)
     assert st == 0 and not hst.any() and not yst.any()
     assert_h_close(h, hr, TOL_F32)
@@ -76,27 +82,31 @@ def test_replay_scan_matches_oracle(shape):
 
 
 @pytest.mark.parametrize("flags", [0, 7])
-def test_replay_launch_flags(flags):
+@pytest.mark.parametrize("B", [16, 1])
+def test_replay_launch_flags(flags, B):
     """PDL off, and PDL with the EARLY_STATE + EARLY_REPLAY promises (state ring and replay prologue
     ahead of the dependency wait): same result, including an invalid path's status."""
-    prev, new, path, plen = make_pair(16, 64, 64, 80, 64, 128, 1, "bf16", seed=31)
+    prev, new, path, plen = make_pair(B, 64, 64, 80, 64, 128, 1, "bf16", seed=31)
     path = path.copy()
-    path[3, 0] = 2
+    bad = min(3, B - 1)
+    path[bad, 0] = 2
     binding.stree_set_launch_flags(flags)
     try:
         y, h, st = run_fused(prev, new, path, plen)
     finally:
         binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
     yr, hr, hst, _ = oracle_pair(prev, new, path, plen)
-    assert st == 3 and hst[3] == 3
+    assert st == 3 and hst[bad] == 3
     assert_h_close(h, hr, TOL_F32)
     assert_y_close(y, yr, TOL_BF16)
 
 
-def test_replay_long_paths_use_l2_path():
-    """Accepted paths longer than the 16 staged nodes (full chains)."""
-    prev, new, path, plen = make_pair(2, 64, 64, 8, 64, 128, 1, "bf16", seed=5, prev_kind="chain")
-    assert (plen == 64).all()
+@pytest.mark.parametrize("B,H,Tp", [(2, 8, 64), (2, 8, 200), (16, 80, 130), (1, 80, 256)])
+def test_replay_long_paths_use_l2_path(B, H, Tp):
+    """Accepted paths longer than the staged nodes (full chains), including previous trees of more than 64
+    accepted nodes (the chunked path-cumsum), through both fused kernels (small-batch: B·H <= #SMs)."""
+    prev, new, path, plen = make_pair(B, Tp, 64, H, 64, 128, 1, "bf16", seed=5 + Tp, prev_kind="chain")
+    assert (plen == Tp).all()
     y, h, st = run_fused(prev, new, path, plen, use_parent=False)
     yr, hr, _, _ = oracle_pair(prev, new, path, plen)
     assert_h_close(h, hr, TOL_F32)
