@@ -228,9 +228,22 @@ def cpu_baseline(prob, tok, vt, budget_s=15.0):
         tot += oracle_sample(prob, tok, vt, n)
         reps += 1
     cores = oracle.num_threads()
-    return {"value": n * prob.dims.n_nodes * reps / tot, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} trees x 1 layer (mask+scan+accept+commit) x {reps} reps of {args_cfg_name(prob)}, "
-                      f"fp64, {tot:.1f} s, OpenMP {cores} threads"}
+    out = {"value": n * prob.dims.n_nodes * reps / tot, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{n} trees x 1 layer (mask+scan+accept+commit) x {reps} reps of {args_cfg_name(prob)}, "
+                     f"fp64, {tot:.1f} s, OpenMP {cores} threads",
+           "cpu_model": oracle.cpu_model(), "build": "gcc -O3 -march=native -ffp-contract=off -fopenmp"}
+    # the same oracle on one thread: one tree per sample, ~1/3 of the budget
+    oracle.set_threads(1)
+    try:
+        reps1, tot1 = 0, 0.0
+        while tot1 < budget_s / 3 and reps1 < 20:
+            tot1 += oracle_sample(prob, tok, vt, 1)
+            reps1 += 1
+    finally:
+        oracle.set_threads(0)
+    out["single_thread"] = {"value": prob.dims.n_nodes * reps1 / tot1, "unit": UNIT, "cores": 1,
+                            "sample": f"1 tree x 1 layer x {reps1} reps, {tot1:.1f} s"}
+    return out
 
 
 def args_cfg_name(prob):
@@ -257,7 +270,8 @@ def run_stree(args):
     # writes layer l's state, so the state stream may start before the dependency wait (EARLY_STATE)
     binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL |
                                    (0 if args.no_early_state else
-                                    binding.STREE_LAUNCH_EARLY_STATE | binding.STREE_LAUNCH_EARLY_REPLAY))
+                                    binding.STREE_LAUNCH_EARLY_STATE | binding.STREE_LAUNCH_EARLY_REPLAY |
+                                    binding.STREE_LAUNCH_EARLY_TREE | binding.STREE_LAUNCH_EARLY_DT))
     L = args.layers
     # every rank verifies its own batch of trees (weak scaling; no data-path collective)
     from paper_2505_14969_b200 import dist as sdist
@@ -476,6 +490,12 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
     host = []
     for t in layers:
         host.append({k: t[k].cpu().pin_memory() for k in ("x", "dt", "Bm", "Cm")})
+    # the verified tree's x, dt, B are the cache the next step's replay reads, so the
+    # fused loop double-buffers them: step k uploads into set k % 2 and replays from set (k - 1) % 2
+    bufs = [[{k: t[k] for k in ("x", "dt", "Bm", "Cm")} for t in layers]]
+    if fused:
+        bufs.append([{k: (t[k].clone() if k != "Cm" else t[k]) for k in ("x", "dt", "Bm", "Cm")} for t in layers])
+    it = [0]
     hp = parent.cpu().pin_memory()
     htok, hvt = tok_d.cpu().pin_memory(), vt_d.cpu().pin_memory()
     out = [torch.empty(path.shape, dtype=torch.int32).pin_memory(),
@@ -491,33 +511,36 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
     evs = [torch.cuda.Event() for _ in range(len(layers) + 1)]
 
     def step():
+        cur = bufs[it[0] % len(bufs)]
+        prv = bufs[(it[0] - 1) % len(bufs)]
+        it[0] += 1
         cstream.wait_stream(stream)   # previous step's kernels are done with the buffers
         with torch.cuda.stream(cstream):
             parent.copy_(hp, non_blocking=True)
             tok_d.copy_(htok, non_blocking=True)
             vt_d.copy_(hvt, non_blocking=True)
             evs[-1].record(cstream)
-            for t, hh, ev in zip(layers, host, evs):
+            for c, hh, ev in zip(cur, host, evs):
                 for k, v in hh.items():
-                    t[k].copy_(v, non_blocking=True)
+                    c[k].copy_(v, non_blocking=True)
                 ev.record(cstream)
         with torch.cuda.stream(stream):
             stream.wait_event(evs[-1])
             binding.stree_build_mask(parent, torch.empty((d.batch, d.n_nodes, (d.n_nodes + 31) // 32),
                                                          dtype=torch.int32, device=dev), None, status)
-            for t, ev in zip(layers, evs):
+            for t, c, p, ev in zip(layers, cur, prv, evs):
                 stream.wait_event(ev)
-                if fused:
-                    binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
-                                              t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status,
+                if fused:   # (the tree topology is the same every step here, so parent serves both trees)
+                    binding.stree_replay_scan(p["x"], p["dt"], p["Bm"], parent, path, plen, c["x"], c["dt"], t["A"],
+                                              c["Bm"], c["Cm"], t["D"], t["h0"], parent, t["y"], status,
                                               dims_prev=dims, dims=dims)
                 else:
-                    binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent,
+                    binding.stree_tree_scan(c["x"], c["dt"], t["A"], c["Bm"], c["Cm"], t["D"], t["h0"], parent,
                                             t["y"], status, dims=dims)
             binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
             if not fused:
-                for t in layers:
-                    binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"],
+                for t, c in zip(layers, cur):
+                    binding.stree_commit(c["x"], c["dt"], t["A"], c["Bm"], t["h0"], parent, path, plen, t["h0"],
                                          status, dims=dims)
             for o, s in zip(out, (path, plen, bonus)):
                 o.copy_(s, non_blocking=True)

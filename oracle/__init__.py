@@ -21,16 +21,47 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "stree_oracle.c")
-_LIB = os.path.join(_HERE, "libstree_oracle.so")
 _lib = None
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _host_key() -> str:
+    """-march=native code is specific to the host's ISA: the library name carries a hash of the CPU
+    model and flags, so a build made on one host (the CPU container) is never executed on another
+    (the GPU box), where it is rebuilt on first use (gcc is in both images)."""
+    import hashlib
+    flags = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    flags = line
+                    break
+    except OSError:
+        pass
+    return hashlib.sha1((cpu_model() + flags).encode()).hexdigest()[:10]
+
+
+_LIB = os.path.join(_HERE, f"libstree_oracle.{_host_key()}.so")
+
+
 def build(force: bool = False) -> str:
-    """Compile the C oracle (gcc, -O2 -fopenmp).  No -ffast-math: fp64 semantics kept."""
+    """Compile the C oracle (gcc -O3 -march=native -fopenmp).  No -ffast-math: fp64 semantics kept
+    (gcc does not contract a*b+c into an FMA across statements without -ffp-contract=fast in ISO C mode)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
-                               "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-ffp-contract=off", "-fopenmp", "-fPIC",
+                               "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -47,6 +78,7 @@ def _load():
         lib.oracle_accept.argtypes = [P, P, P, i, i, P, P, P, P]
         lib.oracle_commit.argtypes = [i, i, i, i, i, i, P, P, P, P, P, P, P, P, P, P]
         lib.oracle_num_threads.argtypes = []
+        lib.oracle_set_threads.argtypes = [i]
         lib.oracle_tree_conv.argtypes = [i, i, i, i, P, P, P, P, P, i, P, P]
         lib.oracle_conv_commit.argtypes = [i, i, i, i, P, P, P, P, P, P, P]
         for f in (lib.oracle_build_mask, lib.oracle_tree_scan, lib.oracle_accept,
@@ -70,6 +102,11 @@ def _i32(a):
 
 def num_threads() -> int:
     return _load().oracle_num_threads()
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count of later oracle calls (n <= 0: the runtime default)."""
+    _load().oracle_set_threads(int(n))
 
 
 def build_mask(parent):

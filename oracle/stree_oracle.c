@@ -69,6 +69,17 @@ int oracle_num_threads(void) {
 #endif
 }
 
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+    static int dflt = 0;
+    if (!dflt) dflt = omp_get_max_threads();
+    omp_set_num_threads(n > 0 ? n : dflt);
+#else
+    (void)n;
+#endif
+    return 0;
+}
+
 /* L: bit j%32 of word j/32 of row i, W = ceil(T/32) words. */
 int oracle_build_mask(const int32_t *parent, int B, int T, uint32_t *mask, int32_t *depth,
                       int32_t *status) {

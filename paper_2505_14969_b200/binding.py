@@ -86,7 +86,8 @@ def lib():
     return _lib
 
 
-STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY = 1, 2, 4
+(STREE_LAUNCH_PDL, STREE_LAUNCH_EARLY_STATE, STREE_LAUNCH_EARLY_REPLAY, STREE_LAUNCH_EARLY_TREE,
+ STREE_LAUNCH_EARLY_DT) = 1, 2, 4, 8, 16
 
 EXPORTED_SYMBOLS = ("stree_build_mask", "stree_tree_scan", "stree_accept", "stree_commit",
                     "stree_status_string", "stree_set_scan_impl", "stree_set_launch_flags", "stree_scan_kernel_for", "stree_version",

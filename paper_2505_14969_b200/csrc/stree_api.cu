@@ -111,7 +111,8 @@ const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
 uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed) & tl_flags_mask; }
 
 stree_status stree_set_launch_flags(uint32_t flags) {
-    if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE | STREE_LAUNCH_EARLY_REPLAY))
+    if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE | STREE_LAUNCH_EARLY_REPLAY |
+                          STREE_LAUNCH_EARLY_TREE | STREE_LAUNCH_EARLY_DT))
         return STREE_ERR_UNSUPPORTED;
     g_launch_flags.store(flags);
     return STREE_OK;

@@ -30,7 +30,7 @@ EncodeTiledFn encode_fn() {
 // the whole geometry of a map: a map is a pure function of it (the address is a UVA virtual address)
 struct Key {
     uint64_t base, dims[4], strides[3];
-    uint32_t box[4], dt, rank;
+    uint32_t box[4], dt, rank, swz, pad;
     bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
 };
 struct KeyHash {
@@ -50,12 +50,13 @@ std::unordered_map<Key, CUtensorMap, KeyHash>& cache() {
 }
 
 bool encode(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const cuuint64_t* dims,
-            const cuuint64_t* strides, const cuuint32_t* box) {
+            const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     Key k;
     std::memset(&k, 0, sizeof(k));
     k.base = reinterpret_cast<uint64_t>(base);
     k.dt = (uint32_t)dt;
     k.rank = rank;
+    k.swz = (uint32_t)swz;
     for (uint32_t i = 0; i < rank; ++i) {
         k.dims[i] = dims[i];
         k.box[i] = box[i];
@@ -73,7 +74,7 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* b
     if (!fn) return false;
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (fn(m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     std::lock_guard<std::mutex> lk(g_mu);
@@ -85,11 +86,12 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* b
 }  // namespace
 
 bool tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
-             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
-    return encode(m, dt, 2, base, dims, strides, box);
+    return encode(m, dt, 2, base, dims, strides, box,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 bool tmap_4d_bf16(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b1,

@@ -11,9 +11,10 @@
 namespace stree {
 namespace host {
 
-// 2-D tiled map: dims (inner, outer), row pitch row_bytes, box (box_inner, box_outer), SWIZZLE_128B.
+// 2-D tiled map: dims (inner, outer), row pitch row_bytes, box (box_inner, box_outer), SWIZZLE_128B
+// (or no swizzle: the box lands row after row, box_inner elements each).
 bool tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
-             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle128 = true);
 // 4-D bf16 map (d0 contiguous), box (64, b1, b2, 1), SWIZZLE_128B (tree attention).
 bool tmap_4d_bf16(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b1,
                   uint32_t b2);

@@ -2,29 +2,41 @@
 // latency (the paper's batch-1 setting; BASELINE configs c2 / c3).
 //
 // Same arithmetic as K2 (stree_scan_tc.cu; PAPER.md:91-102 with the Mamba-2 realisation of SURVEY R1-R3):
-//     G   = C·Bᵀ                 (T x T, K = N)    tcgen05 kind::f16    bf16 -> fp32 TMEM
-//     Y0  = C·h0ᵀ                (T x P, K = N)    tcgen05 kind::tf32   A = C from TMEM, B = fp32 state (TMA)
-//     Y'  = (L∘G∘c)·X            (T x P, K = T)    tcgen05 kind::f16    masked weights (bf16) x x
-//     y   = e^{Λ_i}(Y0 + Y') + D x                 (factorised decay; direct e^{Λi-Λj} when min Λ < -64)
+//     G   = C·Bᵀ                 (T x T, K = N)      tcgen05 kind::f16, A = C, B = B (smem)
+//     Y0  = C·h0ᵀ                (T x P, K = N)      tcgen05 kind::f16, h0 = hi + lo split into two bf16
+//                                                    tiles: C·hiᵀ + C·loᵀ in one accumulator
+//     Y'  = (L∘G∘c)·X            (T x P, K = T)      tcgen05 kind::f16, A = masked weights in TMEM (TS)
+//     y   = e^{Λ_i}(Y0 + Y') + D x                   (factorised decay; direct e^{Λi-Λj} when min Λ < -64)
 // and, in the replay variant, the activation replay of the previous tree's accepted path applied on chip
 // to the state tile before Y0 reads it (Alg. 1 l.123-124), the committed tile TMA-stored in
-// place.
+// place.  The hi/lo split keeps 16 mantissa bits of the fp32 state (tf32 keeps 10), so Y0 is more
+// accurate than a kind::tf32 product, and it needs no conversion of C after the inputs land.
 //
 // Why a separate kernel: with B·H ≤ #SMs there is one head per CTA and nothing to pipeline; a layer's
-// time is its dependency chain (inputs -> G -> Y0 -> Y' -> y) plus the launch boundary.  So:
-//  * 97 KB of shared memory and 256 TMEM columns per CTA: two CTAs fit on an SM, so under PDL the next
-//    layer's CTAs are resident while this layer runs and do everything that does not depend on the
-//    previous kernel before their dependency wait (barriers, TMEM, state tile and — with
-//    STREE_LAUNCH_EARLY_REPLAY — the whole replay of the previous path);
-//  * small code (one pass, no rings, no head loop) that stays in the SM's instruction cache from one
-//    layer to the next;
-//  * G first on the tensor pipe, then Y0, while two warps build the masked weights; y is written
-//    straight from registers (64 contiguous bytes per thread), no staging and no TMA store.
-// Warps: 0-3 math (tree prologue redundantly per warp, C -> tf32 into TMEM, masked weights (0-1),
-// epilogue), 4 TMA + MMA issue, 5-8 replay (replay variant only).
+// time is its dependency chain after the PDL wait (inputs land -> G -> masked weights -> Y' -> y) plus
+// the launch boundary (measured floor of an empty dependent kernel in a graph: 0.71 us, tools/pdl_floor.cu).
+// Everything that does not depend on the preceding kernel runs before the wait, and the chain after it is
+// one DRAM latency plus the tensor-core work:
+//  * ≈ 105 KB of shared memory and 256 TMEM columns per CTA: two CTAs fit on an SM, so under PDL the next
+//    layer's CTAs are resident while this layer runs;
+//  * before the wait: barriers, TMEM, the state tile (STREE_LAUNCH_EARLY_STATE), the whole activation
+//    replay of the previous path (STREE_LAUNCH_EARLY_REPLAY; its operands gathered with cp.async, one DRAM
+//    latency after the path) and the hi/lo split of the state, and the tree topology — validation,
+//    ancestor bits, and the jump pointers of every pointer-jumping round — plus A_h, D_h
+//    (STREE_LAUNCH_EARLY_TREE);
+//  * after the wait: C, B, x by TMA and dt by the row warps, all in flight together; G = C·Bᵀ and then
+//    Y0 are issued the moment C, B land; the segsum Λ replays the recorded jump pointers (6 shuffle
+//    rounds); four warps (two per TMEM lane quadrant of the 64 node rows, on key-column halves) build the
+//    masked weights straight into TMEM (no shared memory, no proxy fence) for a TS-form Y'; the same warps
+//    write y from registers (64 contiguous bytes per thread).
+// Warps: 0, 1, 4, 5 row warps (tree, Λ, masked weights, epilogue); 2, 3, 6, 7 aux (replay, state split);
+// 8 TMA producer + MMA issuer (its own warp: the replay of the fused variant must never delay the MMAs).
+// Accumulator rows 64-127 are never read (M = 128 MMAs, T ≤ 64 rows).
 //
 // Served: bf16 io, P = 64, N in {64, 128}, 1 <= T <= 64 (the launcher picks this kernel when B·H ≤ #SMs).
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "stree_common.cuh"
 #include "stree_host.cuh"
@@ -36,12 +48,15 @@ using namespace stree::tc;
 
 constexpr int kP = 64;
 constexpr int kAtom = 8192;               // 64 rows x 128 B, swizzle-128B
-constexpr int kMathT = 128;               // warps 0-3
-constexpr int kIssW = 4;                  // warp 4
-constexpr int kRep0 = 160;                // first replay thread (warp 5)
+constexpr int kIssW = 8;                  // TMA producer + MMA issuer
+constexpr int kThreads = 288;
 constexpr int kRStage = 8;                // previous-path nodes staged on chip
-constexpr uint32_t kCols = 256;           // TMEM columns: G / direct Y' [0,64), C tf32 [64, 64+N), acc [64+N, 128+N)
-constexpr int kColG = 0, kColC = 64;
+constexpr int kRounds = 6;                // pointer-jumping rounds for T <= 64
+constexpr uint32_t kCols = 256;           // TMEM columns
+constexpr int kColG = 0;                  // G = C·Bᵀ, fp32 [0, 64)
+constexpr int kColM = 64;                 // masked weights, bf16 packed two per column [64, 96)
+constexpr int kColAcc = 128;              // Y0 (+ factorised Y') [128, 192)
+constexpr int kColYd = 0;                 // direct-decay Y' over G's columns (G is dead once M' is built)
 constexpr int kTraceWords = 32;           // debug timeline: u64 globaltimer stamps per CTA (STREE_TRACE builds)
 #ifdef STREE_TRACE
 constexpr bool kTrace = true;
@@ -54,20 +69,22 @@ struct Lay {
     static constexpr int kCbAtoms = NS / 64;
     static constexpr int CB = 0;                              // C bf16: atom a = columns [64a, 64a+64)
     static constexpr int BB = CB + kCbAtoms * kAtom;          // B bf16
-    static constexpr int H0 = BB + kCbAtoms * kAtom;          // state tile: atom a = columns [32a, 32a+32), fp32
+    static constexpr int HL = BB + kCbAtoms * kAtom;          // split state, 64-column atoms of 128 rows:
+                                                              // rows 0-63 = bf16(h0), rows 64-127 = bf16(h0 - hi)
+    static constexpr int H0 = HL + kCbAtoms * 2 * kAtom;      // state tile: atom a = columns [32a, 32a+32), fp32
     static constexpr int X = H0 + (NS / 32) * kAtom;          // x tile (64 rows of 64 bf16)
-    static constexpr int MB = X + kAtom;                      // masked weights, 128 rows (rows 64-127 = copy)
-    static constexpr int CJ = MB + 2 * kAtom;                 // float [4 warps][64]  c_j
-    static constexpr int LM = CJ + 4 * 64 * 4;                // float [4 warps][64]  Λ_j (direct decay)
+    static constexpr int DT = X + kAtom;                      // dt of heads (h & ~3) .. +3, T rows of 16 B (TMA)
+    static constexpr int CJ = DT + 64 * 16;                   // float [4 row warps][64]  c_j
+    static constexpr int LM = CJ + 4 * 64 * 4;                // float [4 row warps][64]  Λ_j (direct decay)
     static constexpr int MODE = LM + 4 * 64 * 4;              // int
     static constexpr int RPATH = MODE + 16;                   // int [kMaxNodes]
     static constexpr int RINFO = RPATH + (R ? kMaxNodes * 4 : 0);   // int [2]: r (0 = nothing), bad path
     static constexpr int RCOEF = RINFO + 16;                  // float [kRStage]
-    static constexpr int RLAM = RCOEF + 64;                   // float [4]: λ_last, λ_{kRStage-1}, e^{λ_last}
+    static constexpr int RLAM = RCOEF + 32;                   // float [4]: λ_last, λ_{kRStage-1}, e^{λ_last}
     static constexpr int XPREV = RLAM + 16;                   // bf16 [kRStage][64]
-    static constexpr int BPREV = XPREV + (R ? kRStage * kP * 2 : 0);    // float [kRStage][NS]
-    static constexpr int BAR = (BPREV + (R ? kRStage * NS * 4 : 0) + 7) & ~7;
-    static constexpr int NBAR = 8;                            // cb, x, h, ctf, g, m, acc, upd
+    static constexpr int BPREV = XPREV + (R ? kRStage * kP * 2 : 0);    // bf16 [kRStage][NS]
+    static constexpr int BAR = (BPREV + (R ? kRStage * NS * 2 : 0) + 7) & ~7;
+    static constexpr int NBAR = 7;                            // cb, x, h, hs, g, m, acc
     static constexpr int TMEMP = BAR + NBAR * 8;
     static constexpr int TOTAL = TMEMP + 16;
     static_assert(2 * (TOTAL + 1024 + 1024) <= 228 * 1024, "two CTAs per SM");
@@ -81,7 +98,9 @@ struct Params {
     const int32_t* parent;
     __nv_bfloat16* y;
     int32_t* dev_status;
-    int has_h0, early_state, early_replay;
+    int has_h0, early_state, early_replay, early_tree;
+    int early_dt;                // STREE_LAUNCH_EARLY_DT: the segsum runs before the dependency wait
+    int dt_tma;                  // dt staged by TMA (needs H·4 % 16 == 0), else read by the row warps
     // replay (previous tree)
     int Tp;
     const __nv_bfloat16* x_prev;
@@ -93,10 +112,49 @@ struct Params {
     unsigned long long* trace;   // [grid][kTraceWords] or NULL (STREE_TRACE builds only)
 };
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// Masked weights of one row warp (node row i = its TMEM lane, key columns [c0, c0 + 32)):
+// M'_ij = L_ij G_ij c_j (factorised) or L_ij e^{min(Λi-Λj,0)} dt_j G_ij (direct), bf16, packed two keys per
+// 32-bit TMEM column at [kColM + c0/2, +16) — the A operand of the TS-form Y' MMA.
+template <bool FAC>
+__device__ __forceinline__ void build_weights(uint32_t tq, int c0, uint64_t bits, float li, const float* cjw,
+                                              const float* lmw, unsigned long long* tr) {
+    uint32_t o[16];
+#pragma unroll
+    for (int h16 = 0; h16 < 2; ++h16) {   // 16 key columns at a time (registers)
+        uint32_t gv[16];
+        tmem_ld16r(tq + kColG + c0 + 16 * h16, gv);
+        tmem_wait();
+        if (kTrace && tr && h16 == 0) tr[25] = gtimer();
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) {
+            const int j = c0 + 16 * h16 + k;
+            float v0 = cjw[j] * __uint_as_float(gv[k]);
+            float v1 = cjw[j + 1] * __uint_as_float(gv[k + 1]);
+            if (!FAC) {
+                v0 *= __expf(fminf(li - lmw[j], 0.f));
+                v1 *= __expf(fminf(li - lmw[j + 1], 0.f));
+            }
+            o[8 * h16 + (k >> 1)] = pack_bf16(((bits >> j) & 1ull) ? v0 : 0.f, ((bits >> (j + 1)) & 1ull) ? v1 : 0.f);
+        }
+    }
+    if (kTrace && tr) tr[26] = gtimer();
+    tmem_st16(tq + kColM + (c0 >> 1), o);
+    tmem_st_wait();
+    if (kTrace && tr) tr[27] = gtimer();
+}
+
 template <int NS, bool R>
-__global__ void __launch_bounds__(R ? 288 : 160, 2)
+__global__ void __launch_bounds__(kThreads, 2)
     lat_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
-               const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h, const Params prm) {
+               const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h,
+               const __grid_constant__ CUtensorMap tm_dt, const Params prm) {
     using L = Lay<NS, R>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -106,8 +164,8 @@ __global__ void __launch_bounds__(R ? 288 : 160, 2)
     const int b = blockIdx.x / H, h = blockIdx.x % H;
     const int g = h / (H / prm.G);                        // group of head h (heads of a group contiguous)
     const uint32_t bar0 = sb + L::BAR;
-    const uint32_t BAR_CB = bar0, BAR_X = bar0 + 8, BAR_H = bar0 + 16, BAR_CTF = bar0 + 24, BAR_G = bar0 + 32,
-                   BAR_M = bar0 + 40, BAR_ACC = bar0 + 48, BAR_UPD = bar0 + 56;
+    const uint32_t BAR_CB = bar0, BAR_X = bar0 + 8, BAR_H = bar0 + 16, BAR_HS = bar0 + 24, BAR_G = bar0 + 32,
+                   BAR_M = bar0 + 40, BAR_ACC = bar0 + 48;
     const int Tp16 = (T + 15) & ~15;
     const bool early_h = prm.early_state && prm.has_h0;
     unsigned long long* const trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
@@ -121,11 +179,10 @@ __global__ void __launch_bounds__(R ? 288 : 160, 2)
         mbar_init(BAR_CB, 1);
         mbar_init(BAR_X, 1);
         mbar_init(BAR_H, 1);
-        mbar_init(BAR_CTF, 4);
+        mbar_init(BAR_HS, 1);
         mbar_init(BAR_G, 1);
-        mbar_init(BAR_M, 2);
+        mbar_init(BAR_M, 4);
         mbar_init(BAR_ACC, 1);
-        mbar_init(BAR_UPD, 1);
         fence_barrier_init();
     }
     if (warp == kIssW) {
@@ -134,429 +191,506 @@ __global__ void __launch_bounds__(R ? 288 : 160, 2)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     // K padding of Y' = M'·X: x rows T .. Tp16-1 (outside the TMA box) must be zero, not stale
-    if (tid < kMathT)
-        for (int k = tid; k < (Tp16 - T) * 8; k += kMathT)
+    if (tid < 128)
+        for (int k = tid; k < (Tp16 - T) * 8; k += 128)
             *reinterpret_cast<uint4*>(sm + L::X + swz(T + k / 8, k & 7)) = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + L::TMEMP);
-    if (warp == kIssW && lane == 0) {
+    const bool row_warp = warp < 8 && (warp & 2) == 0;   // 0, 1, 4, 5
+
+    if (warp == kIssW && lane == 0) {   // state stream first: the replay (aux warps) waits on it
         tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h);
+        if (prm.dt_tma) tma_prefetch(&tm_dt);
         if (early_h) {   // caller's promise: the state is not written by the preceding kernel
             mbar_expect_tx(BAR_H, NS * kP * 4);
 #pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
                 tma_load_2d(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP);
         }
+        stamp(1);
     }
-    if (tid == 0) stamp(1);
-    if (!(R && warp > kIssW && prm.early_replay)) pdl_wait();
-    if (tid == 0) stamp(2);
-
-    if (warp == kIssW) {
-        // ================= TMA producer + MMA issuer (warp converged, elected lane issues) =================
-        if (lane == 0) {
-            const uint64_t ef = policy_evict_first();
-            mbar_expect_tx(BAR_CB, 2 * L::kCbAtoms * T * 128);
-#pragma unroll 1
-            for (int a = 0; a < L::kCbAtoms; ++a) {
-                tma_load_2d(sb + L::CB + a * kAtom, &tm_c, BAR_CB, g * NS + 64 * a, b * T);
-                tma_load_2d(sb + L::BB + a * kAtom, &tm_b, BAR_CB, g * NS + 64 * a, b * T);
-            }
-            mbar_expect_tx(BAR_X, T * 128);
-            tma_load_2d_ef(sb + L::X, &tm_x, BAR_X, h * kP, b * T, ef);
-            if (prm.has_h0 && !early_h) {
+    if (warp < 8) {
+        // ================= warps 0-7: row warps 0, 1, 4, 5 (TMEM lane quadrant qd = node rows 32 qd + lane,
+        // column half ch) and aux warps 2, 3, 6, 7 (u = 0..127)
+        const bool rowr = row_warp;
+        const int qd = warp & 1, ch = warp >> 2, wi = qd + 2 * ch;
+        const int u = 32 * ((warp & 1) + 2 * (warp >> 2)) + lane;
+        bool waited = false, loaded = false;
+        // without STREE_LAUNCH_EARLY_STATE the state is streamed after the dependency wait (aux warp 7)
+        auto wait_and_load_state = [&]() {
+            if (!waited) { pdl_wait(); waited = true; }
+            if (prm.has_h0 && !early_h && !loaded && warp == 7 && lane == 0) {
                 mbar_expect_tx(BAR_H, NS * kP * 4);
 #pragma unroll 1
                 for (int a = 0; a < NS / 32; ++a)
-                    tma_load_2d_ef(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP, ef);
+                    tma_load_2d_ef(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP, policy_evict_first());
             }
-        }
-        __syncwarp();
-        mbar_wait(BAR_CB, 0);
-        tc_fence_after();
-        if (lane == 0) stamp(3);
-        // G = C·Bᵀ, M = 128 (rows >= T, and rows 64-127 read past the C tile, are ignored), N = Tp16, K = NS
-        const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
-#pragma unroll 1
-        for (int kk = 0; kk < NS / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-            mma_f16_w(tmem + kColG, sdesc(sb + L::CB + off, 16, 1024), sdesc(sb + L::BB + off, 16, 1024), id_g, kk > 0);
-        }
-        tc_commit_w(BAR_G);
-        constexpr int kColAcc = 64 + NS;
-        if (prm.has_h0) {
-            // Y0 = C·h0ᵀ, kind::tf32, A = C (tf32) from TMEM, B = state tile (K-major, 32 fp32 per atom row)
-            mbar_wait(BAR_CTF, 0);
-            if (lane == 0) stamp(4);
-            mbar_wait(R ? BAR_UPD : BAR_H, 0);
-            tc_fence_after();
-            if (lane == 0) stamp(5);
-            const uint64_t bd = sdesc(sb + L::H0, 16, 1024);
-            const uint32_t id_y0 = idesc(kFmtTF32, 0, 128, kP);
-#pragma unroll 1
-            for (int kk = 0; kk < NS / 8; ++kk)
-                mma_tf32_ts_w(tmem + kColAcc, tmem + kColC + 8 * kk,
-                              bd + (uint64_t)((((kk >> 2) * kAtom) + (kk & 3) * 32) >> 4), id_y0, kk > 0);
-        }
-        if (lane == 0) stamp(6);
-        mbar_wait(BAR_M, 0);
-        if (lane == 0) stamp(7);
-        mbar_wait(BAR_X, 0);
-        tc_fence_after();
-        if (lane == 0) stamp(8);
-        // Y' = M'·X, kind::f16, A K-major (masked weights), B MN-major (x rows j); factorised decay accumulates
-        // onto Y0, direct decay into the G columns (all builders have read G before BAR_M)
-        const bool fac = *reinterpret_cast<volatile int*>(sm + L::MODE) != 0;
-        const uint32_t dy = tmem + (fac ? kColAcc : kColG);
-        const uint32_t acc0 = (fac && prm.has_h0) ? 1u : 0u;
-        const uint64_t ad = sdesc(sb + L::MB, 16, 1024);
-        const uint64_t xd = sdesc(sb + L::X, kAtom, 1024);
-        const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
-#pragma unroll 1
-        for (int kk = 0; kk < Tp16 / 16; ++kk)
-            mma_f16_w(dy, ad + (uint64_t)(kk * 2), xd + (uint64_t)(kk * 128), id_y, (kk > 0) | acc0);
-        tc_commit_w(BAR_ACC);
-        if (lane == 0) stamp(9);
-    } else if (warp < kIssW) {
-        // ================= math warps 0-3 =================
-        const int q = warp;
-        // ---- tree prologue, redundantly in every math warp (lane holds nodes lane and lane + 32): validation
-        //      (PAPER.md:90 precondition), ancestor rows and the segsum Λ = L·(dt A_h) by pointer jumping
-        //       ----
-        int par[2];
-        float dtv[2];
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-            const int i = lane + 32 * hf;
-            par[hf] = i < T ? prm.parent[(size_t)b * T + i] : -1;
-            dtv[hf] = i < T ? prm.dt[((size_t)b * T + i) * H + h] : 0.f;
-        }
-        const float Ah = prm.A[h];
-        const float Dh = prm.D ? prm.D[h] : 0.f;
-        const bool root_bad = __any_sync(0xffffffffu, lane == 0 && par[0] != -1);
-        const bool par_bad = __any_sync(0xffffffffu, (lane > 0 && lane < T && (par[0] < 0 || par[0] >= lane)) ||
-                                                        (lane + 32 < T && (par[1] < 0 || par[1] >= lane + 32)));
-        const bool bad = root_bad || par_bad;
-        if (bad && q == 0 && lane == 0 && h == 0) report(prm.dev_status, root_bad ? STREE_DEV_BAD_ROOT : STREE_DEV_BAD_PARENT);
-        uint64_t rw[2];
-        int jp[2];
-        float lm[2];
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-            const int i = lane + 32 * hf;
-            rw[hf] = i < T ? (1ull << i) : 0ull;
-            jp[hf] = (i < T && !bad) ? par[hf] : -1;
-            lm[hf] = dtv[hf] * Ah;
-        }
-        int rounds = 0;
-        while ((1 << rounds) < T) ++rounds;
-#pragma unroll 1
-        for (int r = 0; r < rounds; ++r) {
-            uint64_t nrw[2];
-            int njp[2];
-            float nlm[2];
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int j = jp[hf];
-                const int sl = (j >= 0) ? (j & 31) : lane;
-                const bool hi = j >= 32;
-                const uint64_t r0 = __shfl_sync(0xffffffffu, rw[0], sl), r1 = __shfl_sync(0xffffffffu, rw[1], sl);
-                const int j0 = __shfl_sync(0xffffffffu, jp[0], sl), j1 = __shfl_sync(0xffffffffu, jp[1], sl);
-                const float v0 = __shfl_sync(0xffffffffu, lm[0], sl), v1 = __shfl_sync(0xffffffffu, lm[1], sl);
-                nrw[hf] = rw[hf] | ((j >= 0) ? (hi ? r1 : r0) : 0ull);
-                njp[hf] = (j >= 0) ? (hi ? j1 : j0) : -1;
-                nlm[hf] = lm[hf] + ((j >= 0) ? (hi ? v1 : v0) : 0.f);
-            }
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                rw[hf] = nrw[hf];
-                jp[hf] = njp[hf];
-                lm[hf] = nlm[hf];
-            }
-        }
-        float mn = fminf(lm[0], lm[1]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        const bool fac = mn >= -64.f;   // e^{Λi-Λj} = e^{Λi}·e^{-Λj} with both factors inside fp32 range
-        float* cjw = reinterpret_cast<float*>(sm + L::CJ) + 64 * q;
-        float* lmw = reinterpret_cast<float*>(sm + L::LM) + 64 * q;
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-            const int i = lane + 32 * hf;
-            cjw[i] = fac ? __expf(-lm[hf]) * dtv[hf] : dtv[hf];
-            lmw[i] = lm[hf];
-        }
-        if (q == 0 && lane == 0) *reinterpret_cast<volatile int*>(sm + L::MODE) = fac ? 1 : 0;
-        __syncwarp();
-        if (q == 0 && lane == 0) stamp(10);
-        const int rs = q & 1, half = q >> 1;
-        const int row = 32 * rs + lane;                 // tree node of this thread's TMEM lane (lanes 64+ = copy)
-        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
-        // ---- C (bf16, TMA) -> fp32 -> TMEM lanes of this warp, columns [kColC, kColC + NS) ----
-        if (prm.has_h0) {
-            mbar_wait(BAR_CB, 0);
-#pragma unroll 1
-            for (int c32 = 0; c32 < NS / 32; ++c32) {
-                uint32_t f[32];
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const int c = 4 * c32 + cc;   // 16-byte chunk along the row
-                    uint4 v = make_uint4(0, 0, 0, 0);
-                    if (row < T) v = *reinterpret_cast<const uint4*>(sm + L::CB + (c >> 3) * kAtom + swz(row, c & 7));
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        f[8 * cc + 2 * k] = w[k] << 16;
-                        f[8 * cc + 2 * k + 1] = w[k] & 0xFFFF0000u;
-                    }
-                }
-                tmem_st32(tq + kColC + 32 * c32, f);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR_CTF);
-            if (q == 0 && lane == 0) stamp(11);
-        }
-        // ---- masked weights (warps 0, 1 = TMEM lanes 0-63 = nodes): M'_ij = L_ij G_ij c_j (factorised) or
-        //      L_ij e^{Λi-Λj} dt_j G_ij (direct), bf16, swizzle-128B K-major, rows 64-127 a copy ----
-        if (q < 2) {
-            mbar_wait(BAR_G, 0);
-            tc_fence_after();
-            if (q == 0 && lane == 0) stamp(12);
-            const uint64_t bits = rw[q];
-            const float li = lm[q];
-#pragma unroll 1
-            for (int c32 = 0; c32 < Tp16; c32 += 32) {
-                uint32_t gv[32];
-                tmem_ld32(tq + kColG + c32, gv);
-                tmem_wait();
-#pragma unroll
-                for (int c16 = 0; c16 < 2; ++c16) {
-                    uint32_t o[8];
-#pragma unroll
-                    for (int k = 0; k < 16; k += 2) {
-                        const int j = c32 + 16 * c16 + k;
-                        float v0 = cjw[j] * __uint_as_float(gv[16 * c16 + k]);
-                        float v1 = cjw[j + 1] * __uint_as_float(gv[16 * c16 + k + 1]);
-                        if (!fac) {
-                            v0 *= __expf(fminf(li - lmw[j], 0.f));
-                            v1 *= __expf(fminf(li - lmw[j + 1], 0.f));
-                        }
-                        o[k >> 1] = pack_bf16(((bits >> j) & 1ull) ? v0 : 0.f, ((bits >> (j + 1)) & 1ull) ? v1 : 0.f);
-                    }
-                    const int ch = (c32 >> 3) + 2 * c16;
-                    const uint4 lo = make_uint4(o[0], o[1], o[2], o[3]), hi = make_uint4(o[4], o[5], o[6], o[7]);
-                    *reinterpret_cast<uint4*>(sm + L::MB + swz(row, ch)) = lo;
-                    *reinterpret_cast<uint4*>(sm + L::MB + swz(row, ch + 1)) = hi;
-                    *reinterpret_cast<uint4*>(sm + L::MB + kAtom + swz(row, ch)) = lo;
-                    *reinterpret_cast<uint4*>(sm + L::MB + kAtom + swz(row, ch + 1)) = hi;
-                }
-            }
-            fence_proxy_async();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR_M);
-            if (q == 0 && lane == 0) stamp(13);
-        }
-        // ---- epilogue: warp q = node rows 32 (q & 1) .. +31 (TMEM lanes 32q..), output columns
-        //      [32 half, 32 half + 32): y = e^{Λ_i}·acc (+ Y'_direct) + D_h x, bf16 (RNE), straight to HBM ----
-        mbar_wait(BAR_ACC, 0);
-        tc_fence_after();
-        if (q == 0 && lane == 0) stamp(14);
-        constexpr int kColAcc = 64 + NS;
-        const bool has0 = prm.has_h0 || fac;
-        uint32_t v0[32], v1[32];
-        if (has0) tmem_ld32(tq + kColAcc + 32 * half, v0);
-        if (!fac) tmem_ld32(tq + kColG + 32 * half, v1);
-        tmem_wait();
-        if (row < T) {
-            const float s0 = bad ? 0.f : __expf(lm[rs]);
-            const float dh = bad ? 0.f : Dh;
-            uint32_t o[16];
-#pragma unroll
-            for (int qc = 0; qc < 4; ++qc) {
-                const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, 4 * half + qc));
-                const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int p = 8 * qc + 2 * k;
-                    const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
-                    const float a0 = has0 ? __uint_as_float(v0[p]) : 0.f, a1 = has0 ? __uint_as_float(v0[p + 1]) : 0.f;
-                    const float d0 = (!fac && !bad) ? __uint_as_float(v1[p]) : 0.f;
-                    const float d1 = (!fac && !bad) ? __uint_as_float(v1[p + 1]) : 0.f;
-                    o[4 * qc + k] = pack_bf16(fmaf(s0, a0, fmaf(dh, xa, d0)), fmaf(s0, a1, fmaf(dh, xb, d1)));
-                }
-            }
-            uint4* dst = reinterpret_cast<uint4*>(prm.y + (((size_t)b * T + row) * H + h) * kP + 32 * half);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) dst[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
-        }
-        if (q == 0 && lane == 0) stamp(15);
-    } else if (R) {
-        // ================= replay warps 5-8: activation replay of the previous tree's accepted path
-        //   h <- e^{λ_{r-1}} h + Σ_m c_m x_prev[s_m] B_prev[s_m]ᵀ,  c_m = e^{λ_{r-1} - λ_m} dt_prev[s_m],
-        //   λ_m = Σ_{q<=m} dt_prev[s_q] A_h  (PAPER.md:113, 86-90 along the path) =================
-        const int u = tid - kRep0;      // 0..127
-        const int Tp = prm.Tp, G = prm.G;
-        int* rpath = reinterpret_cast<int*>(sm + L::RPATH);
-        int* rinfo = reinterpret_cast<int*>(sm + L::RINFO);
-        float* rcoef = reinterpret_cast<float*>(sm + L::RCOEF);
-        float* rlam = reinterpret_cast<float*>(sm + L::RLAM);
-        __nv_bfloat16* xprev = reinterpret_cast<__nv_bfloat16*>(sm + L::XPREV);
-        float* bprev = reinterpret_cast<float*>(sm + L::BPREV);
-        const int r_raw = prm.path_len[b];
-#pragma unroll 1
-        for (int m = u; m < Tp; m += 128) rpath[m] = prm.path[(size_t)b * Tp + m];
-        named_bar(3, 128);
-        const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
-        const int rs = min(rr, kRStage);
-        auto node = [&](int m) {   // clamped into the tree: loads stay in bounds before validation
-            const int v = rpath[m];
-            return (v >= 0 && v < Tp) ? v : 0;
+            loaded = true;
         };
-        // staged operands of the first kRStage path nodes (all issued together: one DRAM latency)
-#pragma unroll 1
-        for (int k = u; k < rs * NS; k += 128) {
-            const int m = k / NS, n = k % NS;
-            bprev[k] = __bfloat162float(prm.b_prev[(((size_t)b * Tp + node(m)) * G + g) * NS + n]);
-        }
-        for (int k = u; k < rs * (kP / 2); k += 128) {
-            const int m = k / (kP / 2), w = k % (kP / 2);
-            reinterpret_cast<uint32_t*>(xprev)[k] =
-                reinterpret_cast<const uint32_t*>(prm.x_prev)[(((size_t)b * Tp + node(m)) * H + h) * (kP / 2) + w];
-        }
-        if (u < 32) {
-            // path validation (root-anchored, increasing, parent-linked: PAPER.md:90 on the accepted path)
-            int ok = rr > 0;
-            for (int m = lane; m < rr; m += 32) {
+        // ---- tree topology (PAPER.md:90 precondition; ancestor rows PAPER.md:63-66): lane holds nodes lane
+        //      and lane + 32; pointer jumping, the jump pointer of every round recorded for the segsum ----
+        bool root_bad = false, par_bad = false;
+        uint64_t bits = 0ull;                  // ancestor row of this thread's node (row 32 qd + lane)
+        uint32_t jpk[3] = {0u, 0u, 0u};        // jump pointer + 1 of round r, half hf: byte 2r + hf
+        float Ah = 0.f, Dh = 0.f;
+        auto jump = [&](int r, int hf) { return (int)((jpk[(2 * r + hf) >> 2] >> (8 * ((2 * r + hf) & 3))) & 0xFFu) - 1; };
+        auto topology = [&]() {
+            int par[2];
+            uint64_t rw[2];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                par[hf] = i < T ? prm.parent[(size_t)b * T + i] : -1;
+            }
+            Ah = prm.A[h];
+            Dh = prm.D ? prm.D[h] : 0.f;
+            root_bad = __any_sync(0xffffffffu, lane == 0 && par[0] != -1);
+            par_bad = __any_sync(0xffffffffu, (lane > 0 && lane < T && (par[0] < 0 || par[0] >= lane)) ||
+                                                  (lane + 32 < T && (par[1] < 0 || par[1] >= lane + 32)));
+            const bool bad = root_bad || par_bad;
+            int jp[2];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                rw[hf] = i < T ? (1ull << i) : 0ull;
+                jp[hf] = (i < T && !bad) ? par[hf] : -1;
+            }
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                uint64_t nrw[2];
+                int njp[2];
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int j = jp[hf];
+                    jpk[(2 * r + hf) >> 2] |= (uint32_t)(j + 1) << (8 * ((2 * r + hf) & 3));
+                    const int sl = (j >= 0) ? (j & 31) : lane;
+                    const bool hi = j >= 32;
+                    const uint64_t r0 = __shfl_sync(0xffffffffu, rw[0], sl), r1 = __shfl_sync(0xffffffffu, rw[1], sl);
+                    const int j0 = __shfl_sync(0xffffffffu, jp[0], sl), j1 = __shfl_sync(0xffffffffu, jp[1], sl);
+                    nrw[hf] = rw[hf] | ((j >= 0) ? (hi ? r1 : r0) : 0ull);
+                    njp[hf] = (j >= 0) ? (hi ? j1 : j0) : -1;
+                }
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    rw[hf] = nrw[hf];
+                    jp[hf] = njp[hf];
+                }
+            }
+            bits = qd ? rw[1] : rw[0];
+        };
+        const int row = 32 * qd + lane;                 // tree node of this thread's TMEM lane (row warps)
+        const uint32_t tq = tmem + ((uint32_t)(32 * qd) << 16);
+        float* cjw = reinterpret_cast<float*>(sm + L::CJ) + 64 * wi;
+        float* lmw = reinterpret_cast<float*>(sm + L::LM) + 64 * wi;
+        // ---- segsum Λ = L·(dt A_h): the recorded jumps, values only; then c_j and the decay
+        //      mode.  Before the dependency wait under EARLY_TREE + EARLY_DT, else after it. ----
+        float dtv[2], lm[2];
+        bool fac = true;
+        auto segsum = [&](bool from_smem) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                dtv[hf] = 0.f;
+                if (i < T)
+                    dtv[hf] = from_smem ? reinterpret_cast<const float*>(sm + L::DT)[4 * i + (h & 3)]
+                                        : prm.dt[((size_t)b * T + i) * H + h];
+                lm[hf] = dtv[hf] * Ah;
+            }
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const int j0 = jump(r, 0), j1 = jump(r, 1);
+                const int s0 = j0 & 31, s1 = j1 & 31;
+                const float v0 = __shfl_sync(0xffffffffu, lm[0], s0), w0 = __shfl_sync(0xffffffffu, lm[1], s0);
+                const float v1 = __shfl_sync(0xffffffffu, lm[0], s1), w1 = __shfl_sync(0xffffffffu, lm[1], s1);
+                const float n0 = lm[0] + (j0 >= 0 ? (j0 >= 32 ? w0 : v0) : 0.f);
+                const float n1 = lm[1] + (j1 >= 0 ? (j1 >= 32 ? w1 : v1) : 0.f);
+                lm[0] = n0;
+                lm[1] = n1;
+            }
+            float mn = fminf(lm[0], lm[1]);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            fac = mn >= -64.f;   // e^{Λi-Λj} = e^{Λi}·e^{-Λj} with both factors inside fp32 range
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int i = lane + 32 * hf;
+                cjw[i] = fac ? __expf(-lm[hf]) * dtv[hf] : dtv[hf];
+                lmw[i] = lm[hf];
+            }
+            if (wi == 0 && lane == 0) *reinterpret_cast<volatile int*>(sm + L::MODE) = fac ? 1 : 0;
+            __syncwarp();
+        };
+        const bool early_lambda = prm.early_tree && prm.early_dt;
+        int* rinfo = reinterpret_cast<int*>(sm + L::RINFO);
+        // ================= phase A (before the dependency wait where the promises allow) =================
+        if (rowr) {
+            if (prm.early_tree) topology();   // caller's promise: parent, A, D not written by the preceding kernel
+            if (early_lambda) segsum(false);  // caller's promise: dt not written by the preceding kernel
+            if (wi == 0 && lane == 0) stamp(10);
+        } else if (R) {
+            // ---- activation replay of the previous tree's accepted path (PAPER.md:113, 86-90 along the path):
+            //   h <- e^{λ_{r-1}} h + Σ_m c_m x_prev[s_m] B_prev[s_m]ᵀ,  c_m = e^{λ_{r-1} - λ_m} dt_prev[s_m],
+            //   λ_m = Σ_{q<=m} dt_prev[s_q] A_h.  Prologue (aux warps): path, validation, coefficients and the
+            //   staged operands of the first kRStage nodes ----
+            if (!prm.early_replay) wait_and_load_state();
+            const int Tp = prm.Tp, G = prm.G;
+            int* rpath = reinterpret_cast<int*>(sm + L::RPATH);
+            float* rcoef = reinterpret_cast<float*>(sm + L::RCOEF);
+            float* rlam = reinterpret_cast<float*>(sm + L::RLAM);
+            const __nv_bfloat16* xprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::XPREV);
+            const __nv_bfloat16* bprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::BPREV);
+            const int r_raw = prm.path_len[b];
+            {
+                const int p0 = u < Tp ? prm.path[(size_t)b * Tp + u] : 0;
+                const int p1 = u + 128 < Tp ? prm.path[(size_t)b * Tp + u + 128] : 0;
+                if (u < Tp) rpath[u] = p0;
+                if (u + 128 < Tp) rpath[u + 128] = p1;
+            }
+            named_bar(3, 128);
+            const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
+            const int rs = min(rr, kRStage);
+            auto node = [&](int m) {   // clamped into the tree: loads stay in bounds before validation
                 const int v = rpath[m];
-                bool good = (v >= 0 && v < Tp);
-                if (m == 0) good = good && v == 0;
-                else {
-                    const int pu = rpath[m - 1];
-                    good = good && v > pu;
-                    if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
-                }
-                if (!good) ok = 0;
-            }
-            ok = __all_sync(0xffffffffu, ok);
-            const int r = ok ? rr : 0;
-            // path-cumsum of log-decays: inclusive warp scans over m = lane, lane + 32, then 32-node chunks
-            const float Ah = prm.A[h];
-            float a0 = lane < r ? prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h] : 0.f;
-            float a1 = lane + 32 < r ? prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h] : 0.f;
-            const float d0 = a0;
-            a0 *= Ah;
-            a1 *= Ah;
+                return (v >= 0 && v < Tp) ? v : 0;
+            };
+            // staged operands of the first kRStage path nodes: 16-byte cp.async gathers, one DRAM latency
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
-                if (lane >= o) { a0 += t0; a1 += t1; }
+            for (int k = u; k < kRStage * (NS / 8); k += 128) {
+                const int m = k / (NS / 8), c = k % (NS / 8);
+                if (m < rs)
+                    cp_async16(sb + L::BPREV + (m * NS + 8 * c) * 2,
+                               prm.b_prev + (((size_t)b * Tp + node(m)) * G + g) * NS + 8 * c);
             }
-            a1 += __shfl_sync(0xffffffffu, a0, 31);
-            float last = r <= 32 ? __shfl_sync(0xffffffffu, a0, (r - 1) & 31) : __shfl_sync(0xffffffffu, a1, (r - 33) & 31);
-            if (r > 64) {
-                float carry = __shfl_sync(0xffffffffu, a1, 31);
-#pragma unroll 1
-                for (int m0 = 64; m0 < r; m0 += 32) {
-                    const int m = m0 + lane;
-                    float a = m < r ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + h] * Ah : 0.f;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const float t = __shfl_up_sync(0xffffffffu, a, o);
-                        if (lane >= o) a += t;
+            if (u < rs * (kP / 8)) {
+                const int m = u / (kP / 8), c = u % (kP / 8);
+                cp_async16(sb + L::XPREV + (m * kP + 8 * c) * 2,
+                           prm.x_prev + (((size_t)b * Tp + node(m)) * H + h) * kP + 8 * c);
+            }
+            if (u < 32) {
+                // path validation (root-anchored, increasing, parent-linked: PAPER.md:90 on the accepted path)
+                int ok = rr > 0;
+                for (int m = lane; m < rr; m += 32) {
+                    const int v = rpath[m];
+                    bool good = (v >= 0 && v < Tp);
+                    if (m == 0) good = good && v == 0;
+                    else {
+                        const int pu = rpath[m - 1];
+                        good = good && v > pu;
+                        if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
                     }
-                    carry += __shfl_sync(0xffffffffu, a, 31);
+                    if (!good) ok = 0;
                 }
-                last = carry;
+                ok = __all_sync(0xffffffffu, ok);
+                const int rv = ok ? rr : 0;
+                // path-cumsum of log-decays: inclusive warp scans over m = lane, lane + 32, then 32-node chunks
+                const float Ahr = prm.A[h];
+                float a0 = lane < rv ? prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h] : 0.f;
+                float a1 = lane + 32 < rv ? prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h] : 0.f;
+                const float d0 = a0;
+                a0 *= Ahr;
+                a1 *= Ahr;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
+                    if (lane >= o) { a0 += t0; a1 += t1; }
+                }
+                a1 += __shfl_sync(0xffffffffu, a0, 31);
+                float last = rv <= 32 ? __shfl_sync(0xffffffffu, a0, (rv - 1) & 31) : __shfl_sync(0xffffffffu, a1, (rv - 33) & 31);
+                if (rv > 64) {
+                    float carry = __shfl_sync(0xffffffffu, a1, 31);
+#pragma unroll 1
+                    for (int m0 = 64; m0 < rv; m0 += 32) {
+                        const int m = m0 + lane;
+                        float a = m < rv ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + h] * Ahr : 0.f;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const float t = __shfl_up_sync(0xffffffffu, a, o);
+                            if (lane >= o) a += t;
+                        }
+                        carry += __shfl_sync(0xffffffffu, a, 31);
+                    }
+                    last = carry;
+                }
+                const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
+                if (lane < kRStage) rcoef[lane] = __expf(last - a0) * d0;
+                if (lane == 0) {
+                    rlam[0] = last;
+                    rlam[1] = lst;
+                    rlam[2] = __expf(last);
+                    rinfo[0] = rv;
+                    rinfo[1] = ok ? 0 : 1;
+                }
             }
-            const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
-            if (lane < kRStage) rcoef[lane] = __expf(last - a0) * d0;
-            if (lane == 0) {
-                rlam[0] = last;
-                rlam[1] = lst;
-                rlam[2] = __expf(last);
-                rinfo[0] = r;
-                rinfo[1] = ok ? 0 : 1;
-            }
+            cp_async_wait_all();
+            named_bar(3, 128);
+            if (u == 0) stamp(20);
         }
-        named_bar(3, 128);
-        if (u == 0) stamp(20);
-        const int r = rinfo[0];
-        mbar_wait(BAR_H, 0);
-        if (u == 0) stamp(21);
-        if (r > 0) {
-            // thread u owns 16-byte chunk pc of rows (u >> 3) + 16 i of every atom (columns 32 a + 4 pc ..)
-            const int pc = u & 7;
-            constexpr int kAt = NS / 32;
-            const float dk = rlam[2], Ak = prm.A[h], last = rlam[0];
-            float lam_run = rlam[1];
-            float4 hv[4][kAt];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int a = 0; a < kAt; ++a) {
-                    const float4 v = *reinterpret_cast<const float4*>(sm + L::H0 + a * kAtom + swz((u >> 3) + 16 * i, pc));
-                    hv[i][a] = make_float4(dk * v.x, dk * v.y, dk * v.z, dk * v.w);
-                }
-#pragma unroll 1
-            for (int m = 0; m < r; ++m) {
-                float4 bb[kAt];
-                float uu[4];
-                if (m < kRStage) {
-#pragma unroll
-                    for (int a = 0; a < kAt; ++a) bb[a] = *reinterpret_cast<const float4*>(&bprev[m * NS + 32 * a + 4 * pc]);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) uu[i] = rcoef[m] * __bfloat162float(xprev[m * kP + (u >> 3) + 16 * i]);
-                } else {   // long accepted paths: operands from L2, coefficients on the fly
-                    const int s = rpath[m];
-                    const float dm = prm.dt_prev[((size_t)b * Tp + s) * H + h];
-                    lam_run += dm * Ak;
-                    const float cm = __expf(last - lam_run) * dm;
-                    const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + s) * G + g) * NS + 4 * pc;
-#pragma unroll
-                    for (int a = 0; a < kAt; ++a)
-                        bb[a] = make_float4(__bfloat162float(br[32 * a]), __bfloat162float(br[32 * a + 1]),
-                                            __bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
-                    const __nv_bfloat16* xr = prm.x_prev + (((size_t)b * Tp + s) * H + h) * kP;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) uu[i] = cm * __bfloat162float(xr[(u >> 3) + 16 * i]);
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int a = 0; a < kAt; ++a) {
-                        hv[i][a].x = fmaf(uu[i], bb[a].x, hv[i][a].x); hv[i][a].y = fmaf(uu[i], bb[a].y, hv[i][a].y);
-                        hv[i][a].z = fmaf(uu[i], bb[a].z, hv[i][a].z); hv[i][a].w = fmaf(uu[i], bb[a].w, hv[i][a].w);
-                    }
+        // ================= phase B: the state tile, by the 256 threads of warps 0-7: the replay update (R),
+        // the committed fp32 tile written back for its store, and the hi/lo bf16 split (B operand of Y0) =====
+        int r = 0;
+        if (prm.has_h0) {
+            if (!early_h) wait_and_load_state();
+            mbar_wait(BAR_H, 0);
+            if (R) {
+                named_bar(4, 256);                  // replay prologue published (aux warps) to all 8 warps
+                r = rinfo[0];
             }
+            if (tid == 0) stamp(21);
+            const int pc = tid & 7;                 // 16-byte chunk of a 128-byte fp32 atom row
+            constexpr int kAt = NS / 32;
+            float4 hv[2][kAt];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int a = 0; a < kAt; ++a)
-                    *reinterpret_cast<float4*>(sm + L::H0 + a * kAtom + swz((u >> 3) + 16 * i, pc)) = hv[i][a];
-        }
-        fence_proxy_async();
-        named_bar(3, 128);
-        if (u == 0) stamp(22);
-        if (prm.early_replay) pdl_wait();   // every global write follows the dependency wait
-        if (u == 0) stamp(23);
-        if (u == 0) {
-            if (rinfo[1] && h == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
-            mbar_arrive(BAR_UPD);           // Y0 may read the replayed tile (the store below only reads it too)
-            if (r > 0) {                    // the committed state, in place
-                const uint64_t ef = policy_evict_first();
+                    hv[i][a] = *reinterpret_cast<const float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc));
+            if (R && r > 0) {
+                const float* rcoef = reinterpret_cast<const float*>(sm + L::RCOEF);
+                const float* rlam = reinterpret_cast<const float*>(sm + L::RLAM);
+                const int* rpath = reinterpret_cast<const int*>(sm + L::RPATH);
+                const __nv_bfloat16* xprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::XPREV);
+                const __nv_bfloat16* bprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::BPREV);
+                const int Tp = prm.Tp, G = prm.G;
+                const float dk = rlam[2], Ak = prm.A[h], last = rlam[0];
+                float lam_run = rlam[1];
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int a = 0; a < kAt; ++a) {
+                        hv[i][a].x *= dk; hv[i][a].y *= dk; hv[i][a].z *= dk; hv[i][a].w *= dk;
+                    }
 #pragma unroll 1
-                for (int a = 0; a < NS / 32; ++a)
-                    tma_store_2d_ef(&tm_h, sb + L::H0 + a * kAtom, 32 * a, (b * H + h) * kP, ef);
-                bulk_commit();
-                bulk_wait_all();
+                for (int m = 0; m < r; ++m) {
+                    float4 bb[kAt];
+                    float uu[2];
+                    if (m < kRStage) {
+#pragma unroll
+                        for (int a = 0; a < kAt; ++a) {
+                            const uint2 w = *reinterpret_cast<const uint2*>(&bprev[m * NS + 32 * a + 4 * pc]);
+                            bb[a] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                                                __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+                        }
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) uu[i] = rcoef[m] * __bfloat162float(xprev[m * kP + (tid >> 3) + 32 * i]);
+                    } else {   // long accepted paths: operands from L2, coefficients on the fly
+                        const int s = rpath[m];
+                        const float dm = prm.dt_prev[((size_t)b * Tp + s) * H + h];
+                        lam_run += dm * Ak;
+                        const float cm = __expf(last - lam_run) * dm;
+                        const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + s) * G + g) * NS + 4 * pc;
+#pragma unroll
+                        for (int a = 0; a < kAt; ++a)
+                            bb[a] = make_float4(__bfloat162float(br[32 * a]), __bfloat162float(br[32 * a + 1]),
+                                                __bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
+                        const __nv_bfloat16* xr = prm.x_prev + (((size_t)b * Tp + s) * H + h) * kP;
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) uu[i] = cm * __bfloat162float(xr[(tid >> 3) + 32 * i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int a = 0; a < kAt; ++a) {
+                            hv[i][a].x = fmaf(uu[i], bb[a].x, hv[i][a].x); hv[i][a].y = fmaf(uu[i], bb[a].y, hv[i][a].y);
+                            hv[i][a].z = fmaf(uu[i], bb[a].z, hv[i][a].z); hv[i][a].w = fmaf(uu[i], bb[a].w, hv[i][a].w);
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int a = 0; a < kAt; ++a)
+                        *reinterpret_cast<float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc)) = hv[i][a];
+                if (tid == 0) stamp(22);
             }
-            stamp(24);
+            // hi/lo split: fp32 columns 32 a + 4 pc .. +3 -> bf16 atom a / 2, 16-byte chunk (a & 1)·4 + pc / 2,
+            // 8-byte half pc & 1 (rows 0-63 of the split tile = hi, the next 64-row atom = lo)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int a = 0; a < kAt; ++a) {
+                    const float4 v = hv[i][a];
+                    const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
+                    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+                    const uint2 hi = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+                    const uint2 lo = make_uint2(pack_bf16(v.x - f01.x, v.y - f01.y), pack_bf16(v.z - f23.x, v.w - f23.y));
+                    const uint32_t off = (a >> 1) * 2 * kAtom + swz((tid >> 3) + 32 * i, (a & 1) * 4 + (pc >> 1)) + (pc & 1) * 8;
+                    *reinterpret_cast<uint2*>(sm + L::HL + off) = hi;
+                    *reinterpret_cast<uint2*>(sm + L::HL + kAtom + off) = lo;
+                }
+            fence_proxy_async();   // split tiles (and the replayed tile, for its TMA store) -> async proxy
+            named_bar(4, 256);
+            if (tid == 0) {
+                mbar_arrive(BAR_HS);
+                stamp(16);
+            }
+        }
+        // ================= phase C: after the dependency wait =================
+        if (!waited) { pdl_wait(); waited = true; }   // every global write follows the dependency wait
+        if (!rowr) {
+            if (R && u == 0) {
+                stamp(23);
+                if (rinfo[1] && h == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+                if (r > 0) {                    // the committed state, in place
+                    const uint64_t ef = policy_evict_first();
+#pragma unroll 1
+                    for (int a = 0; a < NS / 32; ++a)
+                        tma_store_2d_ef(&tm_h, sb + L::H0 + a * kAtom, 32 * a, (b * H + h) * kP, ef);
+                    bulk_commit();
+                    bulk_wait_read_all();   // the store has read the tile before the CTA releases its shared memory
+                }
+                stamp(24);
+            }
+        } else {
+            const bool live = true;
+            if (!prm.early_tree) topology();
+            const bool bad = root_bad || par_bad;
+            if (bad && wi == 0 && lane == 0 && h == 0)
+                report(prm.dev_status, root_bad ? STREE_DEV_BAD_ROOT : STREE_DEV_BAD_PARENT);
+            if (!early_lambda) {
+                if (prm.dt_tma) mbar_wait(BAR_CB, 0);
+                segsum(prm.dt_tma != 0);
+            }
+            if (live) {
+                if (wi == 0 && lane == 0) stamp(11);
+                // ---- masked weights of key columns [32 ch, 32 ch + 32), straight into TMEM ----
+                mbar_wait(BAR_G, 0);
+                tc_fence_after();
+                if (wi == 0 && lane == 0) stamp(12);
+            }
+            if (32 * ch < Tp16) {
+                unsigned long long* tr = (live && wi == 0 && lane == 0) ? trace : nullptr;
+                if (fac) build_weights<true>(tq, 32 * ch, bits, qd ? lm[1] : lm[0], cjw, lmw, tr);
+                else build_weights<false>(tq, 32 * ch, bits, qd ? lm[1] : lm[0], cjw, lmw, tr);
+            }
+            if (live) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(BAR_M);
+                if (wi == 0 && lane == 0) stamp(13);
+                // ---- epilogue: node row 32 qd + lane, output columns [32 ch, 32 ch + 32):
+                //      y = e^{Λ_i}·acc (+ Y'_direct) + D_h x, bf16 (RNE), straight to HBM ----
+                mbar_wait(BAR_ACC, 0);
+                tc_fence_after();
+                if (wi == 0 && lane == 0) stamp(14);
+            }
+            const bool has0 = prm.has_h0 || fac;
+            const float s0 = bad ? 0.f : __expf(qd ? lm[1] : lm[0]);
+            const float dh = bad ? 0.f : Dh;
+            uint4* dst = reinterpret_cast<uint4*>(prm.y + (((size_t)b * T + row) * H + h) * kP + 32 * ch);
+#pragma unroll
+            for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
+                const int col = 32 * ch + 16 * c16;
+                uint32_t va[16], vb[16];
+                if (has0) tmem_ld16r(tq + kColAcc + col, va);
+                if (!fac) tmem_ld16r(tq + kColYd + col, vb);
+                tmem_wait();
+                float acc[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) acc[k] = has0 ? __uint_as_float(va[k]) : 0.f;
+                if (live && wi == 0 && lane == 0 && c16 == 0) stamp(17);
+                uint32_t o[8];
+#pragma unroll
+                for (int qc = 0; qc < 2; ++qc) {
+                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, (col >> 3) + qc));
+                    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int p = 8 * qc + 2 * k;
+                        const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
+                        const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
+                        const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
+                        o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(dh, xa, d0)), fmaf(s0, acc[p + 1], fmaf(dh, xb, d1)));
+                    }
+                }
+                if (live && wi == 0 && lane == 0 && c16 == 1) stamp(18);
+                if (live && row < T) {
+                    dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
+                    dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+            if (live && wi == 0 && lane == 0) stamp(15);
+        }
+    } else if (warp == kIssW) {
+        // ================= TMA producer + MMA issuer (warp converged, elected lane issues) =================
+        const uint64_t dc = sdesc(sb + L::CB, 16, 1024), db = sdesc(sb + L::BB, 16, 1024);
+        const uint64_t dh = sdesc(sb + L::HL, 16, 1024), xd = sdesc(sb + L::X, kAtom, 1024);
+        const uint32_t id_g = idesc(kFmtBF16, 0, 128, Tp16);
+        const uint32_t id_y0 = idesc(kFmtBF16, 0, 128, kP);
+        const uint32_t id_y = idesc(kFmtBF16, 1, 128, kP);
+        {
+            const uint32_t go = 1;
+            if (go) {
+                pdl_wait();
+                if (lane == 0) {
+                    stamp(2);
+                    const uint64_t ef = policy_evict_first();
+                    // dt rides on the C/B barrier: the segsum needs it at the same time as G
+                    mbar_expect_tx(BAR_CB, 2 * L::kCbAtoms * T * 128 + (prm.dt_tma ? T * 16 : 0));
+                    if (prm.dt_tma) tma_load_2d(sb + L::DT, &tm_dt, BAR_CB, h & ~3, b * T);
+#pragma unroll 1
+                    for (int a = 0; a < L::kCbAtoms; ++a) {
+                        tma_load_2d(sb + L::CB + a * kAtom, &tm_c, BAR_CB, g * NS + 64 * a, b * T);
+                        tma_load_2d(sb + L::BB + a * kAtom, &tm_b, BAR_CB, g * NS + 64 * a, b * T);
+                    }
+                    mbar_expect_tx(BAR_X, T * 128);
+                    tma_load_2d_ef(sb + L::X, &tm_x, BAR_X, h * kP, b * T, ef);
+                }
+                __syncwarp();
+                mbar_wait(BAR_CB, 0);
+                tc_fence_after();
+                if (lane == 0) stamp(3);
+            }
+            // G = C·Bᵀ, M = 128 (rows 64-127 read past the C tile and are never used), N = Tp16, K = NS.
+            // Descriptors = base + offsets, four K steps per unrolled group (one 128-byte swizzle row).
+#pragma unroll 1
+            for (int a = 0; a < NS / 64; ++a)
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    const uint64_t off = (uint64_t)(a * (kAtom >> 4) + k4 * 2);
+                    mma_f16_wp(tmem + kColG, dc + off, db + off, id_g, (a | k4) != 0, go);
+                }
+            tc_commit_wp(BAR_G, go);
+            if (prm.has_h0) {
+                // Y0 = C·h0ᵀ = C·hiᵀ + C·loᵀ: one accumulator, 2·NS/16 MMAs of N = 64 (B = the hi rows, then
+                // the lo rows of the split tile) — the epilogue reads one set of columns (TMEM reads are
+                // 64 B/clk per SM: a second accumulator would add 16 KB to the critical epilogue)
+                if (go) {
+                    mbar_wait(BAR_HS, 0);
+                    tc_fence_after();
+                    if (lane == 0) stamp(4);
+                }
+#pragma unroll 1
+                for (int hl = 0; hl < 2; ++hl)
+#pragma unroll 1
+                    for (int a = 0; a < NS / 64; ++a)
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {
+                            const uint64_t oc = (uint64_t)(a * (kAtom >> 4) + k4 * 2);
+                            const uint64_t oh = (uint64_t)(a * (2 * kAtom >> 4) + hl * (kAtom >> 4) + k4 * 2);
+                            mma_f16_wp(tmem + kColAcc, dc + oc, dh + oh, id_y0, (hl | a | k4) != 0, go);
+                        }
+            }
+            bool fac = true;
+            if (go) {
+                if (lane == 0) stamp(5);
+                mbar_wait(BAR_M, 0);
+                if (lane == 0) stamp(6);
+                mbar_wait(BAR_X, 0);
+                tc_fence_after();
+                if (lane == 0) stamp(7);
+                fac = *reinterpret_cast<volatile int*>(sm + L::MODE) != 0;
+            }
+            // Y' = M'·X, kind::f16 TS: A = masked weights from TMEM, B MN-major (x rows j); factorised decay
+            // accumulates onto Y0 (hi columns), direct decay into its own columns
+            const uint32_t dy = tmem + (fac ? kColAcc : kColYd);
+            const uint32_t acc0 = (fac && prm.has_h0) ? 1u : 0u;
+#pragma unroll 1
+            for (int kk = 0; kk < Tp16 / 16; ++kk)
+                mma_f16_ts_wp(dy, tmem + kColM + 8 * kk, xd + (uint64_t)(kk * 128), id_y, (kk > 0) | acc0, go);
+            tc_commit_wp(BAR_ACC, go);
+            if (go && lane == 0) stamp(8);
         }
     }
     tc_fence_before();
@@ -585,13 +719,18 @@ int g_lat_trace_n = 0;
 
 template <int NS, bool R>
 int launch_lat_inst(int B, int H, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb, const CUtensorMap& mx,
-                    const CUtensorMap& mh, const stree::lat::Params& prm) {
+                    const CUtensorMap& mh, const CUtensorMap& mdt, const stree::lat::Params& prm) {
     using namespace stree::lat;
     auto k = lat_kernel<NS, R>;
-    const size_t smem = Lay<NS, R>::TOTAL + 1024;
+    size_t smem = Lay<NS, R>::TOTAL + 1024;
+    static const bool one_cta = [] {   // debug knob (not part of the ABI): force one CTA per SM
+        const char* e = std::getenv("STREE_LAT_ONE_CTA");
+        return e && e[0] == '1';
+    }();
+    if (one_cta) smem = 120 * 1024;
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    e = stree::launch_k(k, dim3(B * H), dim3(R ? 288 : 160), smem, s, mc, mb, mx, mh, prm);
+    e = stree::launch_k(k, dim3(B * H), dim3(kThreads), smem, s, mc, mb, mx, mh, mdt, prm);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
@@ -616,7 +755,7 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
     if (!stree_lat_supports(d)) return (int)cudaErrorNotSupported;
     const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
     const uint64_t BT = (uint64_t)B * T;
-    CUtensorMap mc, mb, mx, mh;
+    CUtensorMap mc, mb, mx, mh, mdt;
     using stree::host::tmap_2d;
     bool ok = tmap_2d(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
               tmap_2d(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
@@ -626,21 +765,29 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
                            32, 64);
     else
         mh = mx;   // unused
+    // dt [B·T][H] fp32, box = 4 heads x T rows, unswizzled (16-byte rows): needs a 16-byte row pitch
+    const bool dt_tma = (H * 4) % 16 == 0 &&
+                        tmap_2d(&mdt, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dt, (uint64_t)H, BT, (uint64_t)H * 4, 4, T, false);
+    if (!dt_tma) mdt = mx;   // unused
     if (!ok) return (int)cudaErrorInvalidValue;
     Params prm{};
     if (replay) prm = *static_cast<const Params*>(replay);
     prm.B = B; prm.T = T; prm.H = H; prm.G = G;
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.has_h0 = h0 != nullptr;
+    prm.dt_tma = dt_tma ? 1 : 0;
     prm.trace = g_lat_trace ? g_lat_trace + (size_t)(g_lat_trace_n++ % kTraceLaunches) * kTraceStride : nullptr;
     const uint32_t fl = stree_launch_flags_get();
     prm.early_state = (fl & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
     prm.early_replay = (fl & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
+    prm.early_tree = (fl & STREE_LAUNCH_EARLY_TREE) ? 1 : 0;
+    prm.early_dt = (fl & STREE_LAUNCH_EARLY_DT) ? 1 : 0;
+    if (prm.early_tree && prm.early_dt) prm.dt_tma = 0;   // read before the wait by the row warps
     if (replay && !h0) return (int)cudaErrorInvalidValue;
-    if (N == 128) return replay ? launch_lat_inst<128, true>(B, H, s, mc, mb, mx, mh, prm)
-                                : launch_lat_inst<128, false>(B, H, s, mc, mb, mx, mh, prm);
-    return replay ? launch_lat_inst<64, true>(B, H, s, mc, mb, mx, mh, prm)
-                  : launch_lat_inst<64, false>(B, H, s, mc, mb, mx, mh, prm);
+    if (N == 128) return replay ? launch_lat_inst<128, true>(B, H, s, mc, mb, mx, mh, mdt, prm)
+                                : launch_lat_inst<128, false>(B, H, s, mc, mb, mx, mh, mdt, prm);
+    return replay ? launch_lat_inst<64, true>(B, H, s, mc, mb, mx, mh, mdt, prm)
+                  : launch_lat_inst<64, false>(B, H, s, mc, mb, mx, mh, mdt, prm);
 }
 
 extern "C" int stree_launch_replay_scan_lat(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,

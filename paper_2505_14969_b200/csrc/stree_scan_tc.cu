@@ -363,7 +363,7 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
         }
         mbar_arrive(bar_empty(s));
     }
-    bulk_wait_all();
+    bulk_wait_read_all();
 }
 
 // MODE 0: tree scan; 1: replay of the previous tree's accepted path fused with the scan (in place);
@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                     if (trace && k < 12) trace[5 + 2 * k] = gtimer();
                 }
             }
-            if (leader) bulk_wait_all();
+            if (leader) bulk_wait_read_all();
         }
     }
     tc_fence_before();

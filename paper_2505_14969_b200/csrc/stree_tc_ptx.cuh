@@ -77,6 +77,11 @@ __device__ __forceinline__ void tma_store_2d_ef(const CUtensorMap* m, uint32_t s
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Before a CTA exits with bulk stores in flight it only has to wait until they have READ shared memory;
+// their global writes complete on their own (the grid's completion includes them).  Waiting for full
+// completion instead holds the CTA — and the SM slot the next PDL-launched CTA needs — for the DRAM write
+// latency (tools/pdl_floor.cu mode 6: +0.67 us per kernel for a 32 KB store).
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -121,6 +126,42 @@ __device__ __forceinline__ void tc_commit_w(uint32_t bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
         : "memory");
 }
+// Predicated forms (go == 0: the instruction is fetched and decoded but not issued).  A kernel can run its
+// post-dependency-wait issue path once before the wait with go = 0 so that the code is resident in the
+// instruction cache when the live pass needs it (stree_scan_lat.cu).
+__device__ __forceinline__ void mma_f16_wp(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                           uint32_t go) {
+    asm volatile(
+        "{\n\t.reg .pred p, e, g;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 g, %5, 0;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\tand.pred e, e, g;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(go)
+        : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts_wp(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
+                                              uint32_t go) {
+    asm volatile(
+        "{\n\t.reg .pred p, e, g;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 g, %5, 0;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\tand.pred e, e, g;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(go)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_wp(uint32_t bar, uint32_t go) {
+    asm volatile(
+        "{\n\t.reg .pred e, g;\n\t.reg .b32 r;\n\tsetp.ne.b32 g, %1, 0;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "and.pred e, e, g;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar), "r"(go)
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] · B[smem desc], kind::f16 (A: M lanes x K bf16 packed two per 32-bit column)
+__device__ __forceinline__ void mma_f16_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
 // D[tmem] (+)= A[tmem] · B[smem desc]ᵀ  (A in tensor memory: M lanes x K columns of 32 bit)
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -139,6 +180,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
         "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // 32 lanes x 32 bit, 16 consecutive columns per thread
@@ -154,6 +202,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 bit, 16 consecutive columns per thread; caller issues tmem_wait() before use
+__device__ __forceinline__ void tmem_ld16r(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
 // 32 lanes x 32 bit, 32 consecutive columns per thread; caller issues tmem_wait() before use
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
     asm volatile(

@@ -26,7 +26,7 @@ def _lib():
     binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
 
 
-ALL = 7   # PDL | EARLY_STATE | EARLY_REPLAY
+ALL = 31   # PDL | EARLY_STATE | EARLY_REPLAY | EARLY_TREE | EARLY_DT
 
 
 def _iter_problems(B, T, H, L, K, seed):

@@ -81,7 +81,7 @@ def test_replay_scan_matches_oracle(shape, impl):
     assert_y_close(y, yr, TOL_BF16)
 
 
-@pytest.mark.parametrize("flags", [0, 7])
+@pytest.mark.parametrize("flags", [0, 7, 15, 31])
 @pytest.mark.parametrize("B", [16, 1])
 def test_replay_launch_flags(flags, B):
     """PDL off, and PDL with the EARLY_STATE + EARLY_REPLAY promises (state ring and replay prologue

@@ -66,11 +66,12 @@ tr = buf.cpu().numpy().astype(np.int64)[:L]
 ncta = int((tr[0, :, 0] > 0).sum())
 tr = tr[:, :ncta]
 t0 = tr[:, :, 0][tr[:, :, 0] > 0].min()
-names = {0: "start", 1: "setup done", 2: "pdl wait passed", 3: "iss: C,B landed", 4: "iss: ctf done", 5: "iss: state ready",
-         6: "iss: Y0 issued", 7: "iss: M' ready", 8: "iss: x ready", 9: "iss: Y' issued", 10: "math: tree done",
-         11: "math: ctf done", 12: "bld: G ready", 13: "bld: M' done", 14: "epi: acc ready", 15: "epi: stored",
-         20: "rep: prologue", 21: "rep: state landed", 22: "rep: updated", 23: "rep: wait passed", 24: "rep: stored",
-         30: "end"}
+names = {0: "start", 1: "setup done", 2: "pdl wait passed", 3: "iss: C,B landed", 4: "iss: split ready",
+         5: "iss: Y0 issued", 6: "iss: M' ready", 7: "iss: x ready", 8: "iss: Y' issued", 10: "row: tree done",
+         11: "row: lambda done", 12: "row: G ready", 13: "row: M' done", 14: "epi: acc ready", 15: "epi: stored",
+         16: "aux: split done", 17: "epi: tmem loaded", 18: "epi: computed", 25: "bld: G loaded",
+         26: "bld: computed", 27: "bld: stored", 20: "rep: prologue", 21: "rep: state landed", 22: "rep: updated",
+         23: "rep: wait passed", 24: "rep: stored", 30: "end"}
 rel = np.where(tr > 0, tr - t0, -1) / 1000.0
 print(f"{ncta} CTAs per launch")
 for li in range(L):
