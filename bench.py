@@ -60,9 +60,14 @@ def parse():
     ap.add_argument("--no-next", action="store_true",
                     help="skip the SURVEY §8(f) rows (tree attention, KV commit, tree conv, conv commit; bench_next.py)")
     ap.add_argument("--p-match", type=float, default=0.9)
-    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
-                    help="N>1: batch = each rank verifies its own trees (no collective, weak scaling); "
-                         "heads = ranks split the heads of the same trees + NCCL all-gather of y (strong)")
+    ap.add_argument("--shard", default="heads", choices=["batch", "heads"],
+                    help="N>1: heads (default, BASELINE configs[3]) = ranks split the heads of the same 16 trees, "
+                         "the scan epilogue writes every y tile into every rank's full-y buffer over NVLink "
+                         "(symmetric memory; NCCL all-gather if unavailable), strong scaling; batch = each rank "
+                         "verifies its own trees (no collective, weak scaling)")
+    ap.add_argument("--no-p2p", action="store_true", help="heads: NCCL all-gather instead of epilogue P2P stores")
+    ap.add_argument("--force-heads", action="store_true",
+                    help="run the head-sharded code path (symmetric memory, sharded scan, barrier) even at N=1")
     return ap.parse_args()
 
 
@@ -278,13 +283,18 @@ def run_stree(args):
     base = inputs.config_problem(args.config)
     d = base.dims
     par_np = base.parent
-    heads_mode = world > 1 and args.shard == "heads"
+    heads_mode = (world > 1 and args.shard == "heads") or args.force_heads
+    if args.force_heads and not dist.is_initialized():   # one-rank group for the symmetric-memory rendezvous
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     h_lo, h_hi = sdist.shard_heads(d.n_heads, d.n_groups, world, rank) if heads_mode else (0, d.n_heads)
     if world > 1 and not heads_mode:
         rng = np.random.default_rng(inputs.BASE_SEED + 1000 + rank)
         from gen import trees as _t
         par_np = np.stack([_t.random_recursive(d.n_nodes, 4, rng) for _ in range(d.batch)]) \
             if args.config == "c4" else par_np
+    H_full = d.n_heads
     if heads_mode:
         import dataclasses
         d = dataclasses.replace(d, n_heads=h_hi - h_lo, n_groups=max(1, d.n_groups * (h_hi - h_lo) // d.n_heads))
@@ -337,27 +347,53 @@ def run_stree(args):
         for t in layers:
             binding.stree_tree_scan(t["x"], t["dt"], t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"],
                                     status, dims=dims)
-            if heads_mode:   # the layer needs the full y: all-gather the head shards over NVLink (NCCL)
-                t["y_full"] = sdist.gather_heads(t["y"])
 
     def ph_accept():
         binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
 
+    # head-sharded layer: the full y of every layer on every rank (BASELINE configs[3])
+    fully, youts = None, None
+    if heads_mode:
+        fully = sdist.FullY(L, d.batch, d.n_nodes, H_full, d.head_dim, io_t, dev, prefer_p2p=not args.no_p2p,
+                            force_p2p=args.force_heads)
+        if fully.mode == "p2p":
+            youts = [binding.make_yout(fully.peers(li), H_full, h_lo) for li in range(L)]
+        if rank == 0:
+            print(f"[bench] heads x{world}: full y via {fully.mode}" +
+                  (f" (symmetric memory unavailable: {fully.error})" if fully.error else ""), file=sys.stderr)
+
     def ph_replay_scan():
         # commit of the previous step's accepted path (cache = this layer's x, dt, B of that step)
-        # fused with the scan of the current tree, state updated in place
-        for t in layers:
-            binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
-                                      t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status, dims_prev=dims,
-                                      dims=dims)
+        # fused with the scan of the current tree, state updated in place; head-sharded + P2P: the epilogue
+        # stores every y tile into every rank's full y
+        for li, t in enumerate(layers):
+            if youts is not None:
+                binding.stree_replay_scan_sharded(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"],
+                                                  t["A"], t["Bm"], t["Cm"], t["D"], t["h0"], parent, youts[li],
+                                                  status, dims_prev=dims, dims=dims)
+            else:
+                binding.stree_replay_scan(t["x"], t["dt"], t["Bm"], parent, path, plen, t["x"], t["dt"], t["A"],
+                                          t["Bm"], t["Cm"], t["D"], t["h0"], parent, t["y"], status,
+                                          dims_prev=dims, dims=dims)
+
+    def ph_collect():
+        # heads: make the full y of every layer visible on every rank (P2P: the device barrier that publishes
+        # the epilogue stores; NCCL: all-gather of the local shards)
+        if fully.mode == "p2p":
+            fully.publish()
+        else:
+            for li, t in enumerate(layers):
+                fully.gather(li, t["y"])
 
     def ph_commit():
         for t in layers:
             binding.stree_commit(t["x"], t["dt"], t["A"], t["Bm"], t["h0"], parent, path, plen, t["h0"], status,
                                  dims=dims)
 
-    fused = not args.no_fuse and not heads_mode
+    fused = not args.no_fuse
     phases = [ph_mask, ph_replay_scan, ph_accept] if fused else [ph_mask, ph_scan, ph_accept, ph_commit]
+    if heads_mode:
+        phases.insert(2, ph_collect)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         ph_mask()
@@ -419,23 +455,30 @@ def run_stree(args):
     nodes_per_step = d.batch * d.n_nodes * L * (1 if heads_mode else world)
     value = nodes_per_step / (ms_per_step * 1e-3)
     ph_mean = phase_ms.mean(0)
+    ph = dict(zip([f.__name__ for f in phases], ph_mean))   # ms per phase
     hbm_peak, bf16_peak, peak_src = load_peaks()
     sb = scan_bytes(d)
     cb = commit_bytes(d, plen_host)
     traffic = load_traffic(args.config) or {}
-    kernels = {"stree_build_mask": {"us": ph_mean[0] * 1e3}, "stree_accept": {"us": ph_mean[2] * 1e3}}
+    kernels = {"stree_build_mask": {"us": ph["ph_mask"] * 1e3}, "stree_accept": {"us": ph["ph_accept"] * 1e3}}
+    if heads_mode:
+        kernels["collective"] = {"us_per_step": ph["ph_collect"] * 1e3, "mode": fully.mode,
+                                 "y_bytes_per_rank_per_layer": fully.layer_bytes,
+                                 "note": "p2p: the scan epilogue already stored every y tile into every rank's "
+                                         "full y (inside stree_replay_scan_sharded); this is the publishing barrier"
+                                 if fully.mode == "p2p" else "NCCL all_gather of the head shards + layout"}
     if fused:
         # fused bytes: the scan's bytes + the committed state written back + the previous path's rows
         fb = sb + cb - d.batch * d.n_heads * d.head_dim * d.d_state * 4
-        fu_us = ph_mean[1] * 1e3 / L
+        fu_us = ph["ph_replay_scan"] * 1e3 / L
         fu_gbs = fb / (fu_us * 1e-6) / 1e9
         kernels["stree_replay_scan"] = {"us": fu_us, "bytes": fb, "GB/s": fu_gbs, "frac": fu_gbs / hbm_peak,
                                         "impl": {1: "simt+commit", 2: "tcgen05 fused", 4: "tcgen05 small-batch fused"}.get(kernel),
                                         "mean_path_len": float(plen_host.mean())}
         dominant, dom_gbs, dom_bytes = "stree_replay_scan", fu_gbs, fb
     else:
-        scan_us = ph_mean[1] * 1e3 / L
-        commit_us = ph_mean[3] * 1e3 / L
+        scan_us = ph["ph_scan"] * 1e3 / L
+        commit_us = ph["ph_commit"] * 1e3 / L
         scan_gbs = sb / (scan_us * 1e-6) / 1e9
         commit_gbs = cb / (commit_us * 1e-6) / 1e9
         kernels["stree_tree_scan"] = {"us": scan_us, "bytes": sb, "GB/s": scan_gbs, "frac": scan_gbs / hbm_peak,
@@ -454,7 +497,7 @@ def run_stree(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L,
-                      fused)
+                      fused, fully, youts)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if heads_mode else "weak",
@@ -464,7 +507,7 @@ def run_stree(args):
             "step": "mask + L x replay_scan (fused commit+scan) + accept" if fused else
                     "mask + L x scan + accept + L x commit",
             "clocks": sampler.summary(),
-            "parallelism": (f"heads x{world} (+NCCL all-gather of y)" if heads_mode else
+            "parallelism": (f"heads x{world} (full y: {fully.mode})" if heads_mode else
                             f"batch-replicas x{world}") if world > 1 else "single"}
     if world == 1 and not args.no_next:
         # §8(f) rows measured beside the step (their own graphs, after the timed region)
@@ -474,12 +517,13 @@ def run_stree(args):
         line["cpu_baseline"] = cpu_baseline(base, tok, vt)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
 
-def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L, fused):
+def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L, fused,
+            fully=None, youts=None):
     """Same step through the public API, inputs copied from pinned host memory
     every step (x, dt, B, C of every layer + tree + tokens) and the acceptance
     result (path, path_len, bonus) read back."""
@@ -528,15 +572,25 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
             stream.wait_event(evs[-1])
             binding.stree_build_mask(parent, torch.empty((d.batch, d.n_nodes, (d.n_nodes + 31) // 32),
                                                          dtype=torch.int32, device=dev), None, status)
-            for t, c, p, ev in zip(layers, cur, prv, evs):
+            for li, (t, c, p, ev) in enumerate(zip(layers, cur, prv, evs)):
                 stream.wait_event(ev)
-                if fused:   # (the tree topology is the same every step here, so parent serves both trees)
+                if fused and youts is not None:   # head-sharded, epilogue P2P stores into every rank's full y
+                    binding.stree_replay_scan_sharded(p["x"], p["dt"], p["Bm"], parent, path, plen, c["x"], c["dt"],
+                                                      t["A"], c["Bm"], c["Cm"], t["D"], t["h0"], parent, youts[li],
+                                                      status, dims_prev=dims, dims=dims)
+                elif fused:   # (the tree topology is the same every step here, so parent serves both trees)
                     binding.stree_replay_scan(p["x"], p["dt"], p["Bm"], parent, path, plen, c["x"], c["dt"], t["A"],
                                               c["Bm"], c["Cm"], t["D"], t["h0"], parent, t["y"], status,
                                               dims_prev=dims, dims=dims)
                 else:
                     binding.stree_tree_scan(c["x"], c["dt"], t["A"], c["Bm"], c["Cm"], t["D"], t["h0"], parent,
                                             t["y"], status, dims=dims)
+            if fully is not None:   # heads: the full y of every layer on every rank
+                if fully.mode == "p2p":
+                    fully.publish()
+                else:
+                    for li, t in enumerate(layers):
+                        fully.gather(li, t["y"])
             binding.stree_accept(tok_d, parent, vt_d, path, plen, bonus, status)
             if not fused:
                 for t, c in zip(layers, cur):
@@ -563,7 +617,8 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    return {"value": d.batch * d.n_nodes * L * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+    return {"value": d.batch * d.n_nodes * L * (1 if fully is not None else world) / (ms * 1e-3), "unit": UNIT,
+            "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": K}
 
 

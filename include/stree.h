@@ -170,6 +170,44 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
                                const float* D, float* h, const int32_t* parent, void* y,
                                int32_t* dev_status, void* stream);
 
+/*
+ * Head-sharded layers (BASELINE configs[3]: "heads sharded over 2/4/8 GPUs").  Each rank
+ * scans its contiguous shard of the heads; the layer's consumer needs the full y [B][T][H][P] on every
+ * rank.  Instead of a local y followed by an all-gather, the scan epilogue stores each y tile straight
+ * into every rank's full-y buffer at the shard's head offset (P2P stores over NVLink when the peers are
+ * peer-mapped buffers, e.g. torch symmetric memory; the collective then overlaps the scan tile by tile).
+ * The caller makes the stores visible to the consumers (a cross-rank barrier after the call, e.g. the
+ * symmetric-memory handle's barrier); the library does not synchronise ranks.
+ */
+enum { STREE_MAX_Y_PEERS = 8 };
+typedef struct {
+    int32_t n_peers;        /* 1 .. STREE_MAX_Y_PEERS (1 = a local, possibly larger, y buffer)           */
+    int32_t heads_total;    /* H of the full layer: row pitch of every peer buffer, in heads             */
+    int32_t head_offset;    /* index of this call's first head in the full layer                        */
+    int32_t reserved;       /* 0                                                                         */
+    void* peers[STREE_MAX_Y_PEERS];   /* [B][T][heads_total][P] io-dtype, 16-byte aligned; device pointers
+                                         valid in the caller's context (peer-mapped memory for remote ranks) */
+} stree_yout;
+
+/*
+ * stree_tree_scan_sharded / stree_replay_scan_sharded — stree_tree_scan / stree_replay_scan of a head
+ * shard (d->n_heads = the shard's heads; x, dt, A, D, h are the shard's slices), y written to
+ * yout->peers[p][b][t][head_offset + h][:] for every peer p.  Served by the tcgen05 scan kernels (bf16,
+ * P = 64, N in {64, 128}, T <= 64); other shapes return STREE_ERR_UNSUPPORTED (use the plain call and a
+ * collective).  Errors: NULL yout / peer -> STREE_ERR_NULL; n_peers out of range, head_offset + n_heads >
+ * heads_total -> STREE_ERR_SHAPE; misaligned peer -> STREE_ERR_ALIGN.
+ */
+stree_status stree_tree_scan_sharded(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                     const void* Bm, const void* Cm, const float* D, const float* h0,
+                                     const int32_t* parent, const stree_yout* yout, int32_t* dev_status,
+                                     void* stream);
+stree_status stree_replay_scan_sharded(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                       const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                                       const int32_t* path_len, const stree_dims* d, const void* x,
+                                       const float* dt, const float* A, const void* Bm, const void* Cm,
+                                       const float* D, float* h, const int32_t* parent, const stree_yout* yout,
+                                       int32_t* dev_status, void* stream);
+
 /* Human-readable name of a status code (static storage). */
 const char* stree_status_string(stree_status s);
 

@@ -35,6 +35,25 @@ class stree_dims(ctypes.Structure):
                 ("io_dtype", ctypes.c_int32)]
 
 
+STREE_MAX_Y_PEERS = 8
+
+
+class stree_yout(ctypes.Structure):
+    _fields_ = [("n_peers", ctypes.c_int32), ("heads_total", ctypes.c_int32), ("head_offset", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("peers", ctypes.c_void_p * STREE_MAX_Y_PEERS)]
+
+
+def make_yout(peers, heads_total: int, head_offset: int) -> stree_yout:
+    """peers: tensors or raw device addresses (ints) of the [B][T][heads_total][P] y buffers."""
+    yo = stree_yout()
+    if not 1 <= len(peers) <= STREE_MAX_Y_PEERS:
+        raise ValueError(f"1..{STREE_MAX_Y_PEERS} y peers, got {len(peers)}")
+    yo.n_peers, yo.heads_total, yo.head_offset = len(peers), int(heads_total), int(head_offset)
+    for i, p in enumerate(peers):
+        yo.peers[i] = p if isinstance(p, int) else p.data_ptr()
+    return yo
+
+
 class stree_attn_dims(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
                 ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("cache_cap", ctypes.c_int32),
@@ -65,6 +84,8 @@ def lib():
             "stree_set_scan_impl": [ctypes.c_int],
             "stree_set_launch_flags": [ctypes.c_uint32],
             "stree_replay_scan": [vp] * 19,
+            "stree_tree_scan_sharded": [vp] * 12,
+            "stree_replay_scan_sharded": [vp] * 19,
             "stree_scan_kernel_for": [vp],
             "stree_commit_kernel_for": [vp, i32],
             "stree_tree_conv": [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp],
@@ -174,6 +195,23 @@ def stree_replay_scan(x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, x, 
         ctypes.byref(dp), _ptr(x_prev), _ptr(dt_prev), _ptr(Bm_prev), _ptr(parent_prev), _ptr(path),
         _ptr(path_len), ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h),
         _ptr(parent), _ptr(y), _ptr(dev_status), _stream(stream)))
+
+
+def stree_tree_scan_sharded(x, dt, A, Bm, Cm, D, h0, parent, yout, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_tree_scan_sharded", lib().stree_tree_scan_sharded(
+        ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h0), _ptr(parent),
+        ctypes.byref(yout), _ptr(dev_status), _stream(stream)))
+
+
+def stree_replay_scan_sharded(x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, x, dt, A, Bm, Cm, D, h, parent,
+                              yout, dev_status=None, stream=None, dims_prev=None, dims=None):
+    dp = dims_prev if dims_prev is not None else make_dims(x_prev, Bm_prev)
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_replay_scan_sharded", lib().stree_replay_scan_sharded(
+        ctypes.byref(dp), _ptr(x_prev), _ptr(dt_prev), _ptr(Bm_prev), _ptr(parent_prev), _ptr(path),
+        _ptr(path_len), ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h),
+        _ptr(parent), ctypes.byref(yout), _ptr(dev_status), _stream(stream)))
 
 
 def stree_set_scan_impl(impl: int):

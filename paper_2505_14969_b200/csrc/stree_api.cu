@@ -22,11 +22,20 @@ extern "C" int stree_tc_supports(const stree_dims*);
 extern "C" int stree_lat_supports(const stree_dims*);
 extern "C" int stree_launch_scan_lat(const stree_dims*, const void*, const float*, const float*, const void*,
                                      const void*, const float*, const float*, const int32_t*, void*, int32_t*,
-                                     cudaStream_t, const void*);
+                                     cudaStream_t, const void*, const stree_yout*);
 extern "C" int stree_launch_replay_scan_lat(const stree_dims*, const void*, const float*, const void*,
                                             const int32_t*, const int32_t*, const int32_t*, const stree_dims*,
                                             const void*, const float*, const float*, const void*, const void*,
-                                            const float*, float*, const int32_t*, void*, int32_t*, cudaStream_t);
+                                            const float*, float*, const int32_t*, void*, int32_t*, cudaStream_t,
+                                            const stree_yout*);
+extern "C" int stree_launch_scan_tc_sharded(const stree_dims*, const void*, const float*, const float*, const void*,
+                                            const void*, const float*, const float*, const int32_t*,
+                                            const stree_yout*, int32_t*, cudaStream_t);
+extern "C" int stree_launch_replay_scan_tc_sharded(const stree_dims*, const void*, const float*, const void*,
+                                                   const int32_t*, const int32_t*, const int32_t*, const stree_dims*,
+                                                   const void*, const float*, const float*, const void*, const void*,
+                                                   const float*, float*, const int32_t*, const stree_yout*, int32_t*,
+                                                   cudaStream_t);
 extern "C" int stree_tc128_supports(const stree_dims*);
 extern "C" int stree_launch_scan_tc128(const stree_dims*, const void*, const float*, const float*, const void*,
                                        const void*, const float*, const float*, const int32_t*, void*, int32_t*,
@@ -179,7 +188,7 @@ stree_status stree_tree_scan(const stree_dims* d, const void* x, const float* dt
     cudaStream_t s = (cudaStream_t)stream;
     int which = stree_scan_kernel_for(d);
     if (which == 0) return STREE_ERR_UNSUPPORTED;
-    int rc = (which == 4)   ? stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s, nullptr)
+    int rc = (which == 4)   ? stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s, nullptr, nullptr)
              : (which == 2) ? stree_launch_scan_tc(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
              : (which == 3) ? stree_launch_scan_tc128(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s)
                             : stree_launch_scan_simt(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, s);
@@ -262,10 +271,84 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
     const void* ptrs[] = {x_prev, dt_prev, Bm_prev, x, dt, A, Bm, Cm, D, h, parent, y};
     for (const void* p : ptrs)
         if (p && !aligned16(p)) return STREE_ERR_ALIGN;
-    auto launch = which == 4 ? stree_launch_replay_scan_lat : stree_launch_replay_scan_tc;
-    return finish(launch(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt, A, Bm, Cm, D, h,
-                         parent, y, dev_status, s),
-                  dev_status, s);
+    const int rc = which == 4 ? stree_launch_replay_scan_lat(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path,
+                                                             path_len, d, x, dt, A, Bm, Cm, D, h, parent, y,
+                                                             dev_status, s, nullptr)
+                              : stree_launch_replay_scan_tc(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path,
+                                                            path_len, d, x, dt, A, Bm, Cm, D, h, parent, y,
+                                                            dev_status, s);
+    return finish(rc, dev_status, s);
+}
+
+namespace {
+// a head shard's y destinations (stree_yout): served by the tcgen05 scan kernels (2 = pipeline, 4 = small-batch)
+stree_status check_yout(const stree_dims* d, const stree_yout* yo) {
+    if (!yo) return STREE_ERR_NULL;
+    if (yo->n_peers < 1 || yo->n_peers > STREE_MAX_Y_PEERS) return STREE_ERR_SHAPE;
+    if (yo->head_offset < 0 || yo->heads_total < yo->head_offset + d->n_heads) return STREE_ERR_SHAPE;
+    for (int p = 0; p < yo->n_peers; ++p) {
+        if (!yo->peers[p]) return STREE_ERR_NULL;
+        if (!aligned16(yo->peers[p])) return STREE_ERR_ALIGN;
+    }
+    return STREE_OK;
+}
+}  // namespace
+
+stree_status stree_tree_scan_sharded(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                     const void* Bm, const void* Cm, const float* D, const float* h0,
+                                     const int32_t* parent, const stree_yout* yout, int32_t* dev_status,
+                                     void* stream) {
+    stree_status st = check_dims(d);
+    if (st != STREE_OK) return st;
+    if ((st = check_yout(d, yout)) != STREE_OK) return st;
+    if (d->batch == 0 || d->n_nodes == 0) return STREE_OK;
+    if (!x || !dt || !A || !Bm || !Cm || !parent) return STREE_ERR_NULL;
+    const void* ptrs[] = {x, dt, A, Bm, Cm, D, h0, parent};
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return STREE_ERR_ALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int which = stree_scan_kernel_for(d);
+    if (which == 4)
+        return finish(stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h0, parent, nullptr, dev_status, s, nullptr, yout),
+                      dev_status, s);
+    if (which == 2)
+        return finish(stree_launch_scan_tc_sharded(d, x, dt, A, Bm, Cm, D, h0, parent, yout, dev_status, s),
+                      dev_status, s);
+    return STREE_ERR_UNSUPPORTED;
+}
+
+stree_status stree_replay_scan_sharded(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                       const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                                       const int32_t* path_len, const stree_dims* d, const void* x,
+                                       const float* dt, const float* A, const void* Bm, const void* Cm,
+                                       const float* D, float* h, const int32_t* parent, const stree_yout* yout,
+                                       int32_t* dev_status, void* stream) {
+    stree_status st = check_dims(d);
+    if (st != STREE_OK) return st;
+    if ((st = check_dims(d_prev)) != STREE_OK) return st;
+    if (d_prev->batch != d->batch || d_prev->n_heads != d->n_heads || d_prev->head_dim != d->head_dim ||
+        d_prev->d_state != d->d_state || d_prev->n_groups != d->n_groups || d_prev->io_dtype != d->io_dtype)
+        return STREE_ERR_SHAPE;
+    if ((st = check_yout(d, yout)) != STREE_OK) return st;
+    if (d->batch == 0) return STREE_OK;
+    if (d->n_nodes == 0 || d_prev->n_nodes == 0) return STREE_ERR_UNSUPPORTED;   // the fused kernels only
+    if (!h || !x_prev || !dt_prev || !Bm_prev || !path || !path_len || !x || !dt || !A || !Bm || !Cm || !parent)
+        return STREE_ERR_NULL;
+    const void* ptrs[] = {x_prev, dt_prev, Bm_prev, x, dt, A, Bm, Cm, D, h, parent};
+    for (const void* p : ptrs)
+        if (p && !aligned16(p)) return STREE_ERR_ALIGN;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int which = stree_scan_kernel_for(d);
+    int rc;
+    if (which == 4)
+        rc = stree_launch_replay_scan_lat(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt, A,
+                                          Bm, Cm, D, h, parent, nullptr, dev_status, s, yout);
+    else if (which == 2)
+        rc = stree_launch_replay_scan_tc_sharded(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d,
+                                                 x, dt, A, Bm, Cm, D, h, parent, yout, dev_status, s);
+    else
+        return STREE_ERR_UNSUPPORTED;
+    return finish(rc, dev_status, s);
 }
 
 namespace {

@@ -99,6 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto stamp = [&]() { if (trc && ntr < 64) g_mss_trace[ntr++] = gt_mss(); };
     stamp();
     const int v0 = rank * slice, v1 = min(V, v0 + slice), n = max(0, v1 - v0);
+    // every CTA of the cluster must have started before a peer writes its shared memory (DSMEM): arrive
+    // now, wait right before the first remote access (racecheck: "block that might not have entered yet")
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     pdl_wait();
     int bad = 0;
     for (int i = tid; i < T; i += kThreads) {
@@ -120,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return;   // uniform across the cluster (same parent array)
     }
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     int red_buf = 0;
     // cluster-wide sum of one float per CTA (every CTA gets the same value, same order)
     auto cluster_sum = [&](float part) -> float {

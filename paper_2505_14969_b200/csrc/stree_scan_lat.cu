@@ -110,6 +110,10 @@ struct Params {
     const int32_t* path;
     const int32_t* path_len;
     unsigned long long* trace;   // [grid][kTraceWords] or NULL (STREE_TRACE builds only)
+    // y destinations: n_ypeer buffers [B][T][y_heads][P], this call's heads at y_head_off (the local y:
+    // one buffer, y_heads = H, offset 0; a head-sharded layer: every rank's full y, stree_yout)
+    __nv_bfloat16* ypeer[STREE_MAX_Y_PEERS];
+    int n_ypeer, y_heads, y_head_off;
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const bool has0 = prm.has_h0 || fac;
             const float s0 = bad ? 0.f : __expf(qd ? lm[1] : lm[0]);
             const float dh = bad ? 0.f : Dh;
-            uint4* dst = reinterpret_cast<uint4*>(prm.y + (((size_t)b * T + row) * H + h) * kP + 32 * ch);
+            const size_t yoff = (((size_t)b * T + row) * prm.y_heads + prm.y_head_off + h) * kP + 32 * ch;
 #pragma unroll
             for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
                 const int col = 32 * ch + 16 * c16;
@@ -606,8 +610,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 if (live && wi == 0 && lane == 0 && c16 == 1) stamp(18);
                 if (live && row < T) {
-                    dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
-                    dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll 1
+                    for (int pr = 0; pr < prm.n_ypeer; ++pr) {
+                        uint4* dst = reinterpret_cast<uint4*>(prm.ypeer[pr] + yoff);
+                        dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
+                        dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    }
                 }
             }
             if (live && wi == 0 && lane == 0) stamp(15);
@@ -750,7 +758,7 @@ extern "C" int stree_lat_supports(const stree_dims* d) {
 extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const float* dt, const float* A,
                                      const void* Bm, const void* Cm, const float* D, const float* h0,
                                      const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s,
-                                     const void* replay) {
+                                     const void* replay, const stree_yout* yo) {
     using namespace stree::lat;
     if (!stree_lat_supports(d)) return (int)cudaErrorNotSupported;
     const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
@@ -775,6 +783,17 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
     prm.B = B; prm.T = T; prm.H = H; prm.G = G;
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.has_h0 = h0 != nullptr;
+    if (yo) {
+        prm.n_ypeer = yo->n_peers;
+        for (int p = 0; p < yo->n_peers; ++p) prm.ypeer[p] = (__nv_bfloat16*)yo->peers[p];
+        prm.y_heads = yo->heads_total;
+        prm.y_head_off = yo->head_offset;
+    } else {
+        prm.n_ypeer = 1;
+        prm.ypeer[0] = (__nv_bfloat16*)y;
+        prm.y_heads = H;
+        prm.y_head_off = 0;
+    }
     prm.dt_tma = dt_tma ? 1 : 0;
     prm.trace = g_lat_trace ? g_lat_trace + (size_t)(g_lat_trace_n++ % kTraceLaunches) * kTraceStride : nullptr;
     const uint32_t fl = stree_launch_flags_get();
@@ -795,7 +814,7 @@ extern "C" int stree_launch_replay_scan_lat(const stree_dims* d_prev, const void
                                             const int32_t* path_len, const stree_dims* d, const void* x,
                                             const float* dt, const float* A, const void* Bm, const void* Cm,
                                             const float* D, float* h, const int32_t* parent, void* y,
-                                            int32_t* dev_status, cudaStream_t s) {
+                                            int32_t* dev_status, cudaStream_t s, const stree_yout* yo) {
     stree::lat::Params rp{};
     rp.Tp = d_prev->n_nodes;
     rp.x_prev = (const __nv_bfloat16*)x_prev;
@@ -804,7 +823,7 @@ extern "C" int stree_launch_replay_scan_lat(const stree_dims* d_prev, const void
     rp.parent_prev = parent_prev;
     rp.path = path;
     rp.path_len = path_len;
-    return stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, s, &rp);
+    return stree_launch_scan_lat(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, s, &rp, yo);
 }
 
 extern "C" void stree_debug_lat_trace(unsigned long long* dev_buf) {

@@ -130,6 +130,15 @@ struct Params {
     const int32_t* parent_prev;
     const int32_t* path;
     const int32_t* path_len;
+    // head-sharded layer (stree_*_sharded): y tiles go to every peer's full-y buffer at y_head_off + h
+    int n_ypeer, y_head_off;
+};
+// y destinations: the local y map (NoYPeers) or one map per peer buffer (stree_yout)
+struct NoYPeers {
+    int unused;
+};
+struct YPeerMaps {
+    CUtensorMap m[STREE_MAX_Y_PEERS];
 };
 
 // ---------------------------------------------------------------------------
@@ -368,11 +377,12 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
 
 // MODE 0: tree scan; 1: replay of the previous tree's accepted path fused with the scan (in place);
 // 2: replay only (stree_commit): warps 0 (state producer), 6-9 (replay) and 10 (stores to tm_y = h_new)
-template <int NS, int MODE>
+template <int NS, int MODE, typename YM = NoYPeers>
 __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
-                   const __grid_constant__ CUtensorMap tm_y, const Params prm) {
+                   const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ YM ym, const Params prm) {
+    constexpr bool kPeers = sizeof(YM) > sizeof(int);
     constexpr bool kReplay = MODE >= 1, kScan = MODE <= 1;
     // scan only: 8 math warps, two per TMEM lane quadrant, each pair splitting the columns of its rows
     // (builders: j halves of M'; epilogue: p halves of y).  With replay: 4 (warps 6-10 replay / store).
@@ -920,7 +930,14 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                 }
                 named_bar(2, kEpiT);
                 if (leader) {
-                    tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
+                    if constexpr (kPeers) {   // head-sharded layer: this tile into every rank's full y
+#pragma unroll 1
+                        for (int pr = 0; pr < prm.n_ypeer; ++pr)
+                            tma_store_2d_ef(&ym.m[pr], sb + S::YS + a * kAtom, (prm.y_head_off + h) * kP, b * T,
+                                            policy_evict_first());
+                    } else {
+                        tma_store_2d_ef(&tm_y, sb + S::YS + a * kAtom, h * kP, b * T, policy_evict_first());
+                    }
                     bulk_commit();
                     // x slot free (Y' read it before accfull, the epilogue above): refill it with head k + kStX,
                     // so the x stream never waits in the state producer's queue
@@ -978,16 +995,16 @@ extern "C" int stree_tc_supports(const stree_dims* d) {
 
 namespace {
 
-template <int NS, int MODE>
+template <int NS, int MODE, typename YM = stree::tc::NoYPeers>
 cudaError_t launch_tc_inst(dim3 grid, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb,
                            const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& my,
-                           const stree::tc::Params& prm) {
+                           const stree::tc::Params& prm, const YM& ym = YM{}) {
     using namespace stree::tc;
-    auto k = scan_tc_kernel<NS, MODE>;
+    auto k = scan_tc_kernel<NS, MODE, YM>;
     const size_t smem = Smem<NS, (MODE >= 1)>::TOTAL + 1024;
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return e;
-    return stree::launch_k(k, grid, dim3(MODE ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, prm);
+    return stree::launch_k(k, grid, dim3(MODE ? kThreadsReplay : kThreadsScan), smem, s, mc, mb, mx, mh, my, ym, prm);
 }
 
 // work split: one tree per CTA, heads of one group in chunks, ~1 wave over the SMs
@@ -1006,7 +1023,7 @@ void split_heads(int B, int H, int G, int* cpg_out, int* hpc_out) {
 // shared by the scan-only and the fused replay+scan launches
 int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm, const void* Cm,
               const float* D, const float* h0, const int32_t* parent, void* y, int32_t* dev_status, cudaStream_t s,
-              bool replay, const stree::tc::Params* rp) {
+              bool replay, const stree::tc::Params* rp, const stree_yout* yo = nullptr) {
     using namespace stree::tc;
     if (!stree_tc_supports(d)) return (int)cudaErrorNotSupported;
     const int B = d->batch, T = d->n_nodes, H = d->n_heads, P = d->head_dim, N = d->d_state, G = d->n_groups;
@@ -1015,7 +1032,14 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     bool ok = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Cm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
               make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Bm, (uint64_t)G * N, BT, (uint64_t)G * N * 2, 64, T) &&
               make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, T) &&
-              make_map(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, T);
+              (yo || make_map(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y, (uint64_t)H * P, BT, (uint64_t)H * P * 2, 64, T));
+    YPeerMaps ym;
+    if (yo) {   // one map per peer's full y [B·T][heads_total·P], box = one head x T rows
+        const uint64_t HtP = (uint64_t)yo->heads_total * P;
+        for (int p = 0; p < yo->n_peers && ok; ++p)
+            ok = make_map(&ym.m[p], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, yo->peers[p], HtP, BT, HtP * 2, 64, T);
+        my = ym.m[0];
+    }
     if (h0)
         ok = ok && make_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h0, (uint64_t)N, (uint64_t)B * H * P,
                             (uint64_t)N * 4, 32, 64);
@@ -1034,7 +1058,16 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
-    if (N == 128)
+    if (yo) {
+        prm.n_ypeer = yo->n_peers;
+        prm.y_head_off = yo->head_offset;
+        if (N == 128)
+            e = replay ? launch_tc_inst<128, 1>(grid, s, mc, mb, mx, mh, my, prm, ym)
+                       : launch_tc_inst<128, 0>(grid, s, mc, mb, mx, mh, my, prm, ym);
+        else
+            e = replay ? launch_tc_inst<64, 1>(grid, s, mc, mb, mx, mh, my, prm, ym)
+                       : launch_tc_inst<64, 0>(grid, s, mc, mb, mx, mh, my, prm, ym);
+    } else if (N == 128)
         e = replay ? launch_tc_inst<128, 1>(grid, s, mc, mb, mx, mh, my, prm)
                    : launch_tc_inst<128, 0>(grid, s, mc, mb, mx, mh, my, prm);
     else
@@ -1068,6 +1101,30 @@ extern "C" int stree_launch_replay_scan_tc(const stree_dims* d_prev, const void*
     rp.path = path;
     rp.path_len = path_len;
     return launch_tc(d, x, dt, A, Bm, Cm, D, h, parent, y, dev_status, s, true, &rp);
+}
+
+extern "C" int stree_launch_scan_tc_sharded(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                            const void* Bm, const void* Cm, const float* D, const float* h0,
+                                            const int32_t* parent, const stree_yout* yo, int32_t* dev_status,
+                                            cudaStream_t s) {
+    return launch_tc(d, x, dt, A, Bm, Cm, D, h0, parent, nullptr, dev_status, s, false, nullptr, yo);
+}
+
+extern "C" int stree_launch_replay_scan_tc_sharded(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                                   const void* Bm_prev, const int32_t* parent_prev,
+                                                   const int32_t* path, const int32_t* path_len, const stree_dims* d,
+                                                   const void* x, const float* dt, const float* A, const void* Bm,
+                                                   const void* Cm, const float* D, float* h, const int32_t* parent,
+                                                   const stree_yout* yo, int32_t* dev_status, cudaStream_t s) {
+    stree::tc::Params rp{};
+    rp.Tp = d_prev->n_nodes;
+    rp.x_prev = (const __nv_bfloat16*)x_prev;
+    rp.dt_prev = dt_prev;
+    rp.b_prev = (const __nv_bfloat16*)Bm_prev;
+    rp.parent_prev = parent_prev;
+    rp.path = path;
+    rp.path_len = path_len;
+    return launch_tc(d, x, dt, A, Bm, Cm, D, h, parent, nullptr, dev_status, s, true, &rp, yo);
 }
 
 // stree_commit on the same pipeline (MODE 2): bf16 activations, P = 64, N in {64, 128}, any T <= 256,

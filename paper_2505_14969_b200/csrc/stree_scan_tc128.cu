@@ -261,11 +261,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar();
         for (int r = 0; r < 7 + NKB - 1; ++r) {
             const int nx = cur ^ 1;
+            // ancestor sets: read row j of this round, barrier, then OR it in (no row is read while it is
+            // being written: race-free under compute-sanitizer racecheck)
+            uint32_t aj[kW];
+            const int j = v < kT ? jmp[cur * kT + v] : -1;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) aj[w] = j >= 0 ? anc[w * kT + j] : 0u;
+            mbar();
             if (v < kT) {
-                const int j = jmp[cur * kT + v];
-                // ancestor sets in place: a concurrently updated row j only ever holds more true ancestors of j
-                if (j >= 0)
-                    for (int w = 0; w < kW; ++w) anc[w * kT + v] |= anc[w * kT + j];
+#pragma unroll
+                for (int w = 0; w < kW; ++w) anc[w * kT + v] |= aj[w];
                 for (int k = 0; k < nh; ++k)
                     lam[(nx * kHPC + k) * kT + v] =
                         lam[(cur * kHPC + k) * kT + v] + (j >= 0 ? lam[(cur * kHPC + k) * kT + j] : 0.f);

@@ -7,11 +7,15 @@ replicated verifier tokens; commit is per head).  Two layouts:
 * batch sharding (default): rank r verifies its own trees -> no data-path
   collective, weak scaling;
 * head sharding: rank r owns heads [h_lo, h_hi) of every tree (whole groups
-  when G > 1); a layer that needs the full y all-gathers the per-rank head
-  shards over NCCL (`gather_heads`).  Commit stays local (the state of a head
-  lives on the rank that owns the head).
+  when G > 1); the layer's consumer needs the full y on every rank.
+  `FullY` provides it: with peer-mapped symmetric memory (torch symmetric
+  memory over NVLink / NVSwitch) the scan epilogue itself stores each y tile
+  into every rank's full-y buffer (stree_replay_scan_sharded, include/stree.h)
+  and one device-side barrier publishes the stores; without it, the scan
+  writes a local shard and `gather_heads` all-gathers over NCCL.  Commit stays
+  local (the state of a head lives on the rank that owns the head).
 
-Only torch.distributed calls live here; no arithmetic of the method.
+Only torch.distributed plumbing lives here; no arithmetic of the method.
 """
 from __future__ import annotations
 
@@ -57,3 +61,57 @@ def max_over_ranks(value: float, device) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def heads_to_layer(g: torch.Tensor) -> torch.Tensor:
+    """[world][B][T][H_r][P] (gather_heads) -> the layer's [B][T][world·H_r][P] (contiguous shards)."""
+    w, B, T, Hr, P = g.shape
+    return g.permute(1, 2, 0, 3, 4).reshape(B, T, w * Hr, P)
+
+
+class FullY:
+    """Full-y buffers [L][B][T][H][P] of L head-sharded layers on every rank.
+
+    mode "p2p": one symmetric-memory allocation (torch.distributed._symmetric_memory) rendezvoused over the
+    group; `peers(l)` are the device addresses of layer l's buffer on every rank (peer-mapped), the scan
+    epilogue writes into all of them, `publish()` is the device-side barrier that makes the stores visible.
+    mode "nccl": a plain local buffer per layer; the caller scans into a local shard and calls `gather()`.
+    """
+
+    def __init__(self, L, B, T, H, P, dtype, device, group=None, prefer_p2p=True, force_p2p=False):
+        self.L, self.shape = L, (B, T, H, P)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.mode, self.handle = "nccl", None
+        self.error = None
+        if prefer_p2p and (self.world > 1 or force_p2p):   # force_p2p: exercise the path on one rank
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+                buf = symm_mem.empty((L, B, T, H, P), dtype=dtype, device=device)
+                grp = group if group is not None else dist.group.WORLD
+                self.handle = symm_mem.rendezvous(buf, grp)
+                self.buf = buf
+                self.mode = "p2p"
+            except Exception as exc:   # no symmetric memory on this build / topology: NCCL all-gather
+                self.error = f"{type(exc).__name__}: {exc}"
+                self.handle = None
+        if self.mode != "p2p":
+            self.buf = torch.empty((L, B, T, H, P), dtype=dtype, device=device)
+        self.layer_bytes = self.buf[0].numel() * self.buf.element_size()
+
+    def peers(self, layer: int) -> list[int]:
+        """Device addresses of layer `layer`'s full y on every rank (rank order); this rank's own in "nccl"."""
+        if self.mode == "p2p":
+            return [int(p) + layer * self.layer_bytes for p in self.handle.buffer_ptrs]
+        return [self.buf[layer].data_ptr()]
+
+    def publish(self):
+        """p2p: device-side barrier over the group on the current stream (every rank's epilogue stores done and
+        visible before anything after it reads the full y)."""
+        if self.mode == "p2p":
+            self.handle.barrier(channel=0)
+
+    def gather(self, layer: int, y_local: torch.Tensor):
+        """nccl: all-gather of this rank's shard [B][T][H_r][P] into the layer's full y."""
+        g = gather_heads(y_local, self.group)
+        self.buf[layer].copy_(heads_to_layer(g))

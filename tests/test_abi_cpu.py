@@ -127,3 +127,33 @@ def test_host_validation_next_rows(L):
     c7 = b.stree_conv_dims(2, 16, 5377, 4, b.STREE_BF16)
     assert L.stree_tree_conv(ctypes.byref(c7), fake, fake, None, None, fake, 1, fake, None, None) == 2
     assert L.stree_tree_conv(ctypes.byref(cd), fake, mis, None, None, fake, 1, fake, None, None) == 4
+
+
+def test_sharded_yout_validation(L):
+    """stree_*_sharded (include/stree.h, head-sharded layers): the stree_yout descriptor is validated before
+    any CUDA work; shapes the tcgen05 kernels do not serve are STREE_ERR_UNSUPPORTED (no silent fallback)."""
+    from paper_2505_14969_b200 import binding as b
+    vp = ctypes.c_void_p
+    fake = vp(0x10000)
+    d = b.stree_dims(1, 16, 8, 64, 128, 1, b.STREE_BF16)
+    good = b.make_yout([0x20000, 0x30000], heads_total=16, head_offset=8)
+    args = (ctypes.byref(d), fake, fake, fake, fake, fake, None, fake, fake)
+    assert L.stree_tree_scan_sharded(*args, None, None, None) == 1                       # NULL yout
+    zero = b.stree_yout()
+    assert L.stree_tree_scan_sharded(*args, ctypes.byref(zero), None, None) == 2         # n_peers = 0
+    over = b.make_yout([0x20000], heads_total=15, head_offset=8)
+    assert L.stree_tree_scan_sharded(*args, ctypes.byref(over), None, None) == 2         # shard past heads_total
+    nullp = b.make_yout([0x20000, 0], heads_total=16, head_offset=8)
+    assert L.stree_tree_scan_sharded(*args, ctypes.byref(nullp), None, None) == 1        # NULL peer
+    mis = b.make_yout([0x20008], heads_total=16, head_offset=8)
+    assert L.stree_tree_scan_sharded(*args, ctypes.byref(mis), None, None) == 4          # misaligned peer
+    f32 = b.stree_dims(1, 16, 8, 64, 128, 1, b.STREE_F32)
+    assert L.stree_tree_scan_sharded(ctypes.byref(f32), fake, fake, fake, fake, fake, None, fake, fake,
+                                     ctypes.byref(good), None, None) == 5                 # SIMT shape: unsupported
+    with pytest.raises(ValueError):
+        b.make_yout([0x20000] * 9, heads_total=16, head_offset=0)
+    dp = b.stree_dims(1, 16, 8, 64, 128, 1, b.STREE_BF16)
+    rargs = (ctypes.byref(dp), fake, fake, fake, None, fake, fake, ctypes.byref(d), fake, fake, fake, fake, fake,
+             None, fake, fake)
+    assert L.stree_replay_scan_sharded(*rargs, None, None, None) == 1
+    assert L.stree_replay_scan_sharded(*rargs, ctypes.byref(over), None, None) == 2

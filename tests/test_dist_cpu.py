@@ -44,7 +44,13 @@ def _worker(rank, world, port, q):
         lo, hi = sd.shard_heads(H, 1, world, rank)
         g = sd.gather_heads(full[:, :, lo:hi])
         recon = torch.cat(list(g), dim=2)
-        ok_gather = torch.equal(recon, full)
+        ok_gather = torch.equal(recon, full) and torch.equal(sd.heads_to_layer(g), full)
+        # the bench's head-sharded full-y plumbing, NCCL-fallback mode (gloo here): layer buffers filled by gather
+        fy = sd.FullY(2, B, T, H, P, torch.float32, "cpu", prefer_p2p=False)
+        for layer in range(2):
+            fy.gather(layer, (full + layer)[:, :, lo:hi].contiguous())
+        ok_gather = ok_gather and fy.mode == "nccl" and all(torch.equal(fy.buf[l], full + l) for l in range(2))
+        ok_gather = ok_gather and fy.peers(1) == [fy.buf[1].data_ptr()]
         m = sd.max_over_ranks(1.5 + rank, "cpu")
         blo, bhi = sd.shard_range(16, world, rank)
         q.put((rank, ok_gather, m, (blo, bhi)))
