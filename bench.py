@@ -115,7 +115,10 @@ def load_traffic(cfg):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(cfg)
+            j = json.load(f)
+        out = dict(j.get(cfg) or {})
+        out["_source"] = j.get("source", "profiles/traffic.json")
+        return out
     except Exception:
         return None
 
@@ -489,8 +492,13 @@ def run_stree(args):
                                    "mean_path_len": float(plen_host.mean())}
         dominant = "stree_tree_scan" if scan_us >= commit_us else "stree_commit"
         dom_gbs, dom_bytes = (scan_gbs, sb) if dominant == "stree_tree_scan" else (commit_gbs, cb)
+    # one isolated call of the dominant kernel (launch included, GPU idle before it, no PDL overlap): the
+    # latency a single verify step of one layer sees, next to the amortised per-layer time of the graph
+    iso = isolated_call_us(phases[1], layers, stream, L)
+    kernels[dominant]["isolated_call_us"] = iso
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": dom_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": dom_gbs / hbm_peak, "traffic": traffic.get(dominant), "peak_source": peak_src,
+                "traffic_source": traffic.get("_source", "profiles/traffic.json"),
                 "algorithmic_bytes_per_launch": dom_bytes, "kernels": kernels}
 
     # ---- e2e through the public API with host buffers ----
@@ -520,6 +528,29 @@ def run_stree(args):
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def isolated_call_us(phase, layers, stream, L, reps=15):
+    """Median over `reps` trials of ONE layer's call of the phase's kernel, eager, with the device idle before
+    it (synchronize), timed with CUDA events on the launching stream."""
+    import torch
+    one = layers[:1]
+    saved = list(layers)
+    times = []
+    try:
+        layers[:] = one
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                phase()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e3)
+    finally:
+        layers[:] = saved
+    return float(statistics.median(times))
 
 
 def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, stream, world, dev, d, L, fused,
