@@ -57,7 +57,10 @@ struct Sm {
     static constexpr int DS = AS + kHPC * 4;                // float [kHPC]
     static constexpr int BADF = DS + kHPC * 4;              // int
     static constexpr int WOK = BADF + 4;                    // u32 [8] per-warp factorisable-head masks
-    static constexpr int BAR = (WOK + 32 + 7) & ~7;
+    static constexpr int WRB = WOK + 32;                    // u32 [8] per-warp chunk-rebasable-head masks
+    static constexpr int RC = WRB + 32;                     // float [kHPC][8] chunk reference Λ (max over chunk)
+    static constexpr int CR = RC + kHPC * 8 * 4;            // float [kHPC][kKeys] rebased c_j = e^{R_c-Λ_j} dt_j
+    static constexpr int BAR = (CR + kHPC * kKeys * 4 + 7) & ~7;
     // tree, g, ctf, hfull[2], hempty[2], xfull[2], xempty[2], mfull[2], mempty[2], accfull[2], accempty[2]
     static constexpr int NBAR = 3 + 14;
     static constexpr int TMEMP = BAR + NBAR * 8;
@@ -279,19 +282,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar();
             cur = nx;
         }
-        // decay mode per head: factorised iff min Λ >= -64 over the tree (both factors within e^{±64})
-        uint32_t okm = 0;
+        // decay mode per head: factorised iff min Λ >= -64 over the tree (both factors within e^{±64});
+        // otherwise rebased per 32-key chunk (warp = chunk of keys 32w .. 32w+31): R_c = max Λ over the chunk,
+        // e^{Λi-Λj} = e^{Λi-R_c} · e^{R_c-Λj} with e^{R_c-Λj} <= e^{64} when the chunk's Λ range is <= 64
+        // (the row factor may underflow only where the true weight is below e^{-64}); per-element
+        // exponentials remain only for heads with a chunk of wider range (stress inputs)
+        uint32_t okm = 0, rbm = 0;
+        float* rc = (float*)(sm + Sm::RC);
         for (int k = 0; k < nh; ++k) {
             bool ok = true;
+            float l = 0.f;
             if (v < kT) {
-                const float l = lam[(cur * kHPC + k) * kT + v];
+                l = lam[(cur * kHPC + k) * kT + v];
                 if (v < T && l < -64.f) ok = false;
-                cj[k * kT + v] = v < T ? __expf(-l) * dts[k * kT + v] : 0.f;
+            }
+            const bool live = v < T && v < kT;
+            float mx = live ? l : -3.0e38f, mnv = live ? l : 3.0e38f;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                mnv = fminf(mnv, __shfl_xor_sync(0xffffffffu, mnv, o));
+            }
+            const bool chunk_ok = mx - mnv <= 64.f || mx < -1.0e38f;   // (an empty chunk is fine)
+            ok = __all_sync(0xffffffffu, ok);
+            if (lane == 0 && warp < 8) rc[k * 8 + warp] = mx;
+            // both coefficient sets: whether the head factorises is known only once every warp has voted
+            if (v < kT) {
+                cj[k * kT + v] = live ? __expf(-l) * dts[k * kT + v] : 0.f;
+                ((float*)(sm + Sm::CR))[k * kT + v] = live ? __expf(fminf(mx - l, 64.f)) * dts[k * kT + v] : 0.f;
             }
             if (ok) okm |= 1u << k;
+            if (chunk_ok) rbm |= 1u << k;
         }
-        okm = __reduce_and_sync(0xffffffffu, okm);
-        if (lane == 0) wok[warp] = okm;
+        if (lane == 0) {
+            wok[warp] = okm;
+            ((uint32_t*)(sm + Sm::WRB))[warp] = rbm;
+        }
         // C -> tf32 into TMEM columns [kCCol, kCCol + 128) (row t of this tile)
         mbar_wait(BAR_TREE, 0);
         {
@@ -315,6 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar();
         const uint32_t fmask = wok[0] & wok[1] & wok[2] & wok[3] & wok[4] & wok[5] & wok[6] & wok[7];
+        const uint32_t* wrb = (const uint32_t*)(sm + Sm::WRB);
+        const uint32_t rmask = wrb[0] & wrb[1] & wrb[2] & wrb[3] & wrb[4] & wrb[5] & wrb[6] & wrb[7];
+        const float* rcf = (const float*)(sm + Sm::RC);
         uint32_t myanc[kW];
 #pragma unroll
         for (int w = 0; w < kW; ++w) myanc[w] = anc[w * kT + i];
@@ -375,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ---- masked weights M'(k): row t = L_i∘G_i∘c (factorised) / direct decay, keys 0 .. kcta-1 ----
             mbar_wait(bar_mempty(a), (ua & 1) ^ 1);
             tc_fence_after();
-            const bool fac = (fmask >> k) & 1u;
+            const bool fac = (fmask >> k) & 1u, rebased = !fac && ((rmask >> k) & 1u);
             const float li = laml[k * kT + i];
-            const float* cjk = cj + k * kT;
+            const float* cjk = (fac ? cj : (const float*)(sm + Sm::CR)) + k * kT;
             const float* lamk = laml + k * kT;
             const float* dtk = dts + k * kT;
             const uint32_t mb = mbuf(a);
@@ -391,20 +420,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int w = 0; w < kW; ++w)
                     if (w == c4) bits = myanc[w];
                 uint32_t pk[16];
+                if (fac || rebased) {   // one multiply per element (+ the chunk's row factor), select by L
+                    const float fr = rebased ? __expf(fminf(li - rcf[k * 8 + c4], 0.f)) : 1.f;
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    float wv[2];
+                    for (int e = 0; e < 16; ++e) {
+                        float wv[2];
 #pragma unroll
-                    for (int t2 = 0; t2 < 2; ++t2) {
-                        const int jj = 2 * e + t2, j = 32 * c4 + jj;
-                        float w = 0.f;
-                        if ((bits >> jj) & 1u) {
-                            const float gv = __uint_as_float(gr[jj]);
-                            w = fac ? gv * cjk[j] : gv * __expf(fminf(li - lamk[j], 0.f)) * dtk[j];
+                        for (int t2 = 0; t2 < 2; ++t2) {
+                            const int jj = 2 * e + t2, j = 32 * c4 + jj;
+                            const float w = __uint_as_float(gr[jj]) * fr * cjk[j];
+                            wv[t2] = ((bits >> jj) & 1u) ? w : 0.f;
                         }
-                        wv[t2] = w;
+                        pk[e] = pack_bf16(wv[0], wv[1]);
                     }
-                    pk[e] = pack_bf16(wv[0], wv[1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        float wv[2];
+#pragma unroll
+                        for (int t2 = 0; t2 < 2; ++t2) {
+                            const int jj = 2 * e + t2, j = 32 * c4 + jj;
+                            float w = 0.f;
+                            if ((bits >> jj) & 1u) {
+                                const float gv = __uint_as_float(gr[jj]);
+                                w = gv * __expf(fminf(li - lamk[j], 0.f)) * dtk[j];
+                            }
+                            wv[t2] = w;
+                        }
+                        pk[e] = pack_bf16(wv[0], wv[1]);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {   // 4 chunks of 8 keys -> swizzled 16-byte stores
