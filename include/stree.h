@@ -244,15 +244,15 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *  STREE_LAUNCH_EARLY_TREE   promise: the tree topology and the per-head parameters of a scan call
  *                            (parent, A, D of stree_tree_scan / stree_replay_scan) are not written by the
  *                            kernel immediately preceding the call (true in a decode loop: the tree is
- *                            fixed for the iteration, A and D are weights).  The small-batch kernel then
- *                            validates the tree and runs the pointer-jumping rounds of the ancestor mask
- *                            before the dependency wait, so only the segsum of dt and
- *                            the contractions remain after it.  x, B, C are never read early.
+ *                            fixed for the iteration, A and D are weights).  The tcgen05 scan kernels
+ *                            then validate the tree and run the pointer-jumping rounds of the ancestor
+ *                            mask before the dependency wait, so only the segsum of dt
+ *                            and the contractions remain after it.  x, B, C are never read early.
  *  STREE_LAUNCH_EARLY_DT     promise (with EARLY_TREE): dt of a scan call is not written by the kernel
  *                            immediately preceding it.  True in a Mamba-2 layer, where dt comes from the
  *                            input projection and the causal conv1d kernel (which produces x, B, C) runs
  *                            between the projection and the scan; also true in a stack of back-to-back
- *                            scans.  The small-batch kernel then computes the segsum Λ and the decay
+ *                            scans.  The tcgen05 scan kernels then compute the segsum Λ and the decay
  *                            coefficients before the dependency wait, so only the contractions remain
  *                            after it.  Without EARLY_TREE the flag is ignored.
  */

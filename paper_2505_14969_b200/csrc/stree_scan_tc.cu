@@ -121,6 +121,9 @@ struct Params {
     int has_h0;
     int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
     int early_replay;  // STREE_LAUNCH_EARLY_REPLAY: the replay prologue may run before the PDL wait
+    int early_tree;    // STREE_LAUNCH_EARLY_TREE: parent, A, D not written by the preceding kernel
+    int early_dt;      // STREE_LAUNCH_EARLY_DT: dt not written by the preceding kernel (with early_tree: the
+                       // whole tree prologue runs before the wait)
     int store_always;  // commit into a distinct h_new: store the state even when the path is invalid
     // replay (fused commit of the previous tree), kReplay only
     int Tp;
@@ -468,44 +471,12 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     }
     // replay warps with the EARLY_REPLAY promise wait inside their own code (after the prologue's
     // loads of the previous tree's operands, before any global write)
-    if (!(kReplay && warp >= 6 && prm.early_replay)) pdl_wait();
+    // math warps with the EARLY_TREE + EARLY_DT promises run the whole tree prologue (loads, validation,
+    // pointer jumping, Λ, decay coefficients) before their dependency wait
+    const bool math_thread = kScan && tid >= kEpi0 && tid < kEpi0 + kMath;
+    const bool early_tree = math_thread && prm.early_tree && prm.early_dt;
+    if (!(kReplay && warp >= 6 && prm.early_replay) && !early_tree) pdl_wait();
 
-    // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
-    //      The producer issues the tree operands right after the wait; tree validation runs in the
-    //      epilogue warps (an invalid tree yields y = 0), so nothing waits on it ----
-    constexpr int kHPW = (kHPC + kMathW - 1) / kMathW;   // heads per math warp
-    float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
-    int* sbad = (int*)(sm + S::BADF);
-    if (kScan && tid >= kEpi0 && tid < kEpi0 + kMath) {
-        const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
-        if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
-#pragma unroll
-        for (int q = 0; q < kHPW; ++q) {
-            const int hh = ew + kMathW * q;
-            const bool hv = hh < nh;
-            a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
-            d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int i = lane + 32 * hf;
-                dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
-            }
-        }
-        if (e == 0) *sbad = 0;
-        named_bar(1, kMath);
-        if (e < T) {   // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i
-            const int p = sp[e];
-            const int code = (e == 0) ? (p != -1 ? 1 : 0) : ((p < 0 || p >= e) ? 2 : 0);
-            if (code) atomicMax(sbad, code == 1 ? 2 : 1);   // root error takes precedence
-        }
-        named_bar(1, kMath);
-        if (*sbad) {
-            // invalid tree: make the pointer chains harmless; the output stage writes zeros
-            if (e < T) sp[e] = (e == 0) ? -1 : 0;
-            if (e == 0 && chunk == 0 && g == 0) report(prm.dev_status, *sbad == 2 ? 1 : 2);
-        }
-        named_bar(1, kMath);
-    }
     const uint32_t tmem = kScan ? __shfl_sync(0xffffffffu, *tmem_slot, 0) : 0u;
     const int Tp16 = (T + 15) & ~15;
     const int xbytes = T * 128;
@@ -660,46 +631,42 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
         float* cj = (float*)(sm + S::CJ);
         float* e0 = (float*)(sm + S::E0);
         int* mode = (int*)(sm + S::MODE);
-        // ---- C (bf16, TMA) -> tf32 operand tile; zero the padded x rows ----
-        if (trace && e == 0) trace[1] = gtimer();
-        mbar_wait(BAR_TREE, 0);
-        if (trace && e == 0) trace[2] = gtimer();
-        if (quad < 2) {
-            // C row (bf16, swizzled TMA tile) -> fp32 -> TMEM lane = row, columns [kCCol, kCCol + NS)
-            const int i = row;
-            constexpr int kC32 = NS / 32 / (kSplit ? 2 : 1);
+        // ---- per-CTA inputs: epilogue warp ew owns heads ew, ew+4, ew+8; lane owns nodes lane, lane+32.
+        //      The producer issues the tree operands right after the wait; tree validation runs in the
+        //      epilogue warps (an invalid tree yields y = 0), so nothing waits on it ----
+        constexpr int kHPW = (kHPC + kMathW - 1) / kMathW;   // heads per math warp
+        float dtr[kHPW][2], a_h[kHPW], d_h[kHPW];
+        int* sbad = (int*)(sm + S::BADF);
+        if (kScan && tid >= kEpi0 && tid < kEpi0 + kMath) {
+            const int ew = (tid - kEpi0) >> 5, e = tid - kEpi0;
+            if (e < T) sp[e] = prm.parent[(size_t)b * T + e];
 #pragma unroll
-            for (int cq = 0; cq < kC32; ++cq) {
-                const int c32 = half * kC32 + cq;
-                uint32_t f[32];
+            for (int q = 0; q < kHPW; ++q) {
+                const int hh = ew + kMathW * q;
+                const bool hv = hh < nh;
+                a_h[q] = hv ? prm.A[hbeg + hh] : 0.f;
+                d_h[q] = (hv && prm.D) ? prm.D[hbeg + hh] : 0.f;
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const int c = 4 * c32 + cc, a = c >> 3;   // 16-byte bf16 chunk index along the row
-                    uint4 v = make_uint4(0, 0, 0, 0);
-                    if (i < T) v = *reinterpret_cast<const uint4*>(sm + S::CB + 2 * a * kAtom + swz(i, c & 7));
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        f[8 * cc + 2 * q] = w[q] << 16;
-                        f[8 * cc + 2 * q + 1] = w[q] & 0xFFFF0000u;
-                    }
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int i = lane + 32 * hf;
+                    dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
                 }
-                tmem_st32(tmem + ((uint32_t)(quad * 32) << 16) + kCCol + 32 * c32, f);
             }
-            tmem_st_wait();
-            tc_fence_before();
-        } else {
-            const int zi = (quad - 2) * 32 + lane + half * 64;   // 0 .. kMath/2 - 1
-#pragma unroll 1
-            for (int k = zi; k < S::kStX0 * (Tp16 - T) * 8; k += kMath / 2) {
-                const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
-                *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
+            if (e == 0) *sbad = 0;
+            named_bar(1, kMath);
+            if (e < T) {   // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i
+                const int p = sp[e];
+                const int code = (e == 0) ? (p != -1 ? 1 : 0) : ((p < 0 || p >= e) ? 2 : 0);
+                if (code) atomicMax(sbad, code == 1 ? 2 : 1);   // root error takes precedence
             }
+            named_bar(1, kMath);
+            if (*sbad) {
+                // invalid tree: make the pointer chains harmless; the output stage writes zeros
+                if (e < T) sp[e] = (e == 0) ? -1 : 0;
+                if (e == 0 && chunk == 0 && g == 0 && !early_tree) report(prm.dev_status, *sbad == 2 ? 1 : 2);
+            }
+            named_bar(1, kMath);
         }
-        fence_proxy_async();
-        mbar_arrive(BAR_CTF);
-        if (trace && e == 0) trace[46] = gtimer();
-
         int rounds = 0;
         while ((1 << rounds) < T) ++rounds;
         const int ew = warp - 2;
@@ -776,6 +743,50 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             }
         }
         named_bar(1, kMath);
+        if (early_tree) {
+            pdl_wait();   // every global write follows the dependency wait
+            if (*sbad && e == 0 && chunk == 0 && g == 0) report(prm.dev_status, *sbad == 2 ? 1 : 2);
+        }
+        // ---- C (bf16, TMA) -> tf32 operand tile; zero the padded x rows ----
+        if (trace && e == 0) trace[1] = gtimer();
+        mbar_wait(BAR_TREE, 0);
+        if (trace && e == 0) trace[2] = gtimer();
+        if (quad < 2) {
+            // C row (bf16, swizzled TMA tile) -> fp32 -> TMEM lane = row, columns [kCCol, kCCol + NS)
+            const int i = row;
+            constexpr int kC32 = NS / 32 / (kSplit ? 2 : 1);
+#pragma unroll
+            for (int cq = 0; cq < kC32; ++cq) {
+                const int c32 = half * kC32 + cq;
+                uint32_t f[32];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int c = 4 * c32 + cc, a = c >> 3;   // 16-byte bf16 chunk index along the row
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (i < T) v = *reinterpret_cast<const uint4*>(sm + S::CB + 2 * a * kAtom + swz(i, c & 7));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        f[8 * cc + 2 * q] = w[q] << 16;
+                        f[8 * cc + 2 * q + 1] = w[q] & 0xFFFF0000u;
+                    }
+                }
+                tmem_st32(tmem + ((uint32_t)(quad * 32) << 16) + kCCol + 32 * c32, f);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+        } else {
+            const int zi = (quad - 2) * 32 + lane + half * 64;   // 0 .. kMath/2 - 1
+#pragma unroll 1
+            for (int k = zi; k < S::kStX0 * (Tp16 - T) * 8; k += kMath / 2) {
+                const int s = k / ((Tp16 - T) * 8), rr = T + (k / 8) % (Tp16 - T), c = k & 7;
+                *reinterpret_cast<uint4*>(sm + S::X + s * S::XS + swz(rr, c)) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        fence_proxy_async();
+        mbar_arrive(BAR_CTF);
+        if (trace && e == 0) trace[46] = gtimer();
+
         if (trace && e == 0) trace[50] = gtimer();
         // ---- builder warps 2,3 (TMEM lanes 64..127 hold a copy of G) build the masked weights of head
         //      k+1 while warps 4,5 (TMEM lanes 0..63) run the epilogue of head k ----
@@ -1056,6 +1067,8 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     prm.has_h0 = h0 != nullptr;
     prm.early_state = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
     prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
+    prm.early_tree = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_TREE) ? 1 : 0;
+    prm.early_dt = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_DT) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (yo) {
