@@ -171,6 +171,38 @@ stree_status stree_replay_scan(const stree_dims* d_prev, const void* x_prev, con
                                int32_t* dev_status, void* stream);
 
 /*
+ * Scan options (SURVEY §8(f) unranked variants; the plain calls are the *_ex calls with opts = NULL):
+ *   dt_bias        [H] f32 or NULL: dt <- dt + dt_bias[h]                   (Mamba-2's dt bias)
+ *   dt_softplus    1: dt <- softplus(dt) = log(1 + e^dt) after the bias       (Mamba-2's discretisation,
+ *                  P:70-74 with reading R9: the kernels then take the raw projection output)
+ *   d_per_channel  1: D is [H][P], y += D[h][p] x[p]; 0: D is [H]          (Mamba-2's D_has_hdim)
+ * The transform applies to every dt a call reads — the new tree's and, in stree_replay_scan_ex /
+ * stree_commit_ex, the cached tree's — so the committed state equals the recurrence with the effective
+ * dt.  dt_bias and D are per-head parameters: STREE_LAUNCH_EARLY_TREE covers them (read before the
+ * dependency wait).  Errors: misaligned dt_bias -> STREE_ERR_ALIGN (4-byte alignment suffices).
+ */
+typedef struct {
+    const float* dt_bias;
+    int32_t dt_softplus;
+    int32_t d_per_channel;
+} stree_scan_opts;
+
+stree_status stree_tree_scan_ex(const stree_dims* d, const void* x, const float* dt, const float* A,
+                                const void* Bm, const void* Cm, const float* D, const float* h0,
+                                const int32_t* parent, void* y, const stree_scan_opts* opts,
+                                int32_t* dev_status, void* stream);
+stree_status stree_commit_ex(const stree_dims* d, const void* x, const float* dt, const float* A,
+                             const void* Bm, const float* h0, const int32_t* parent, const int32_t* path,
+                             const int32_t* path_len, float* h_new, const stree_scan_opts* opts,
+                             int32_t* dev_status, void* stream);
+stree_status stree_replay_scan_ex(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                  const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                                  const int32_t* path_len, const stree_dims* d, const void* x, const float* dt,
+                                  const float* A, const void* Bm, const void* Cm, const float* D, float* h,
+                                  const int32_t* parent, void* y, const stree_scan_opts* opts,
+                                  int32_t* dev_status, void* stream);
+
+/*
  * Head-sharded layers (BASELINE configs[3]: "heads sharded over 2/4/8 GPUs").  Each rank
  * scans its contiguous shard of the heads; the layer's consumer needs the full y [B][T][H][P] on every
  * rank.  Instead of a local y followed by an all-gather, the scan epilogue stores each y tile straight

@@ -176,6 +176,35 @@ def commit_problem(prob, path, path_len, use_parent=True):
                   parent=prob.parent if use_parent else None, n_groups=prob.dims.n_groups)
 
 
+def effective_dt(dt, dt_bias=None, dt_softplus=False):
+    """The scan options' discretisation (include/stree.h stree_scan_opts; Mamba-2, reading R9 with the raw
+    projection as input): dt <- dt + dt_bias[h], then softplus(v) = log(1 + e^v), in fp64."""
+    v = _f64(dt)
+    if dt_bias is not None:
+        v = v + _f64(dt_bias)[None, None, :]
+    return np.logaddexp(0.0, v) if dt_softplus else v
+
+
+def tree_scan_ex(x, dt, A, Bm, Cm, D, h0, parent, n_groups=1, dt_bias=None, dt_softplus=False,
+                 d_per_channel=False):
+    """tree_scan with the scan options: the effective dt above, and D of shape [H][P] when d_per_channel
+    (y_i += D[h][p] x_i[p], P:45 with a skip weight per channel) — the recurrence itself is unchanged."""
+    dte = effective_dt(dt, dt_bias, dt_softplus)
+    if not d_per_channel:
+        return tree_scan(x, dte, A, Bm, Cm, D, h0, parent, n_groups=n_groups)
+    y, st = tree_scan(x, dte, A, Bm, Cm, None, h0, parent, n_groups=n_groups)
+    if D is not None:
+        y = y + _f64(D)[None, None, :, :] * _f64(x)
+        y[st != 0] = 0.0   # invalid trees stay zero-filled
+    return y, st
+
+
+def commit_ex(x, dt, A, Bm, h0, path, path_len, parent=None, n_groups=1, dt_bias=None, dt_softplus=False):
+    """commit along the accepted path with the effective dt (the same transform as the scan that verified it)."""
+    return commit(x, effective_dt(dt, dt_bias, dt_softplus), A, Bm, h0, path, path_len, parent=parent,
+                  n_groups=n_groups)
+
+
 def tree_conv(u, weight, bias, state, parent, act=True):
     """Tree-causal depthwise conv1d (stree_oracle.c, reading R-conv).
     u [B][T][C], weight [C][W], bias [C] or None, state [B][W-1][C] or None, parent [B][T]

@@ -54,6 +54,15 @@ def make_yout(peers, heads_total: int, head_offset: int) -> stree_yout:
     return yo
 
 
+class stree_scan_opts(ctypes.Structure):
+    _fields_ = [("dt_bias", ctypes.c_void_p), ("dt_softplus", ctypes.c_int32), ("d_per_channel", ctypes.c_int32)]
+
+
+def make_opts(dt_bias=None, dt_softplus=False, d_per_channel=False) -> stree_scan_opts:
+    """Scan options (include/stree.h): dt_bias [H] f32 tensor or None, softplus of dt, D of shape [H][P]."""
+    return stree_scan_opts(_ptr(dt_bias), int(bool(dt_softplus)), int(bool(d_per_channel)))
+
+
 class stree_attn_dims(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
                 ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("cache_cap", ctypes.c_int32),
@@ -85,6 +94,9 @@ def lib():
             "stree_set_launch_flags": [ctypes.c_uint32],
             "stree_replay_scan": [vp] * 19,
             "stree_tree_scan_sharded": [vp] * 12,
+            "stree_tree_scan_ex": [vp] * 13,
+            "stree_commit_ex": [vp] * 13,
+            "stree_replay_scan_ex": [vp] * 20,
             "stree_replay_scan_sharded": [vp] * 19,
             "stree_scan_kernel_for": [vp],
             "stree_commit_kernel_for": [vp, i32],
@@ -212,6 +224,30 @@ def stree_replay_scan_sharded(x_prev, dt_prev, Bm_prev, parent_prev, path, path_
         ctypes.byref(dp), _ptr(x_prev), _ptr(dt_prev), _ptr(Bm_prev), _ptr(parent_prev), _ptr(path),
         _ptr(path_len), ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h),
         _ptr(parent), ctypes.byref(yout), _ptr(dev_status), _stream(stream)))
+
+
+def stree_tree_scan_ex(x, dt, A, Bm, Cm, D, h0, parent, y, opts, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_tree_scan_ex", lib().stree_tree_scan_ex(
+        ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h0), _ptr(parent), _ptr(y),
+        ctypes.byref(opts) if opts is not None else None, _ptr(dev_status), _stream(stream)))
+
+
+def stree_commit_ex(x, dt, A, Bm, h0, parent, path, path_len, h_new, opts, dev_status=None, stream=None, dims=None):
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_commit_ex", lib().stree_commit_ex(
+        ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(h0), _ptr(parent), _ptr(path), _ptr(path_len),
+        _ptr(h_new), ctypes.byref(opts) if opts is not None else None, _ptr(dev_status), _stream(stream)))
+
+
+def stree_replay_scan_ex(x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, x, dt, A, Bm, Cm, D, h, parent, y,
+                         opts, dev_status=None, stream=None, dims_prev=None, dims=None):
+    dp = dims_prev if dims_prev is not None else make_dims(x_prev, Bm_prev)
+    d = dims if dims is not None else make_dims(x, Bm)
+    _check("stree_replay_scan_ex", lib().stree_replay_scan_ex(
+        ctypes.byref(dp), _ptr(x_prev), _ptr(dt_prev), _ptr(Bm_prev), _ptr(parent_prev), _ptr(path),
+        _ptr(path_len), ctypes.byref(d), _ptr(x), _ptr(dt), _ptr(A), _ptr(Bm), _ptr(Cm), _ptr(D), _ptr(h),
+        _ptr(parent), _ptr(y), ctypes.byref(opts) if opts is not None else None, _ptr(dev_status), _stream(stream)))
 
 
 def stree_set_scan_impl(impl: int):

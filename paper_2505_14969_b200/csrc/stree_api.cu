@@ -73,6 +73,12 @@ std::atomic<uint32_t> g_launch_flags{STREE_LAUNCH_PDL};
 // two kernels (or whose operands the promise does not cover) clears the flag for that launch.
 thread_local uint32_t tl_flags_mask = ~0u;
 thread_local bool tl_replay_allowed = false;   // set by stree_replay_scan around its internal commit
+thread_local const stree_scan_opts* tl_opts = nullptr;   // options of the *_ex call in progress
+struct OptsScope {
+    const stree_scan_opts* saved;
+    explicit OptsScope(const stree_scan_opts* o) : saved(tl_opts) { tl_opts = o; }
+    ~OptsScope() { tl_opts = saved; }
+};
 struct FlagsMask {
     uint32_t saved;
     explicit FlagsMask(uint32_t clear) : saved(tl_flags_mask) { tl_flags_mask &= ~clear; }
@@ -118,6 +124,40 @@ extern "C" {
 const char* stree_version(void) { return "stree-b200 0.1 (sm_100a)"; }
 
 uint32_t stree_launch_flags_get() { return g_launch_flags.load(std::memory_order_relaxed) & tl_flags_mask; }
+
+const stree_scan_opts* stree_scan_opts_get() { return tl_opts; }
+
+namespace {
+bool opts_ok(const stree_scan_opts* o) { return !o || !o->dt_bias || (reinterpret_cast<uintptr_t>(o->dt_bias) & 3u) == 0; }
+}  // namespace
+
+stree_status stree_tree_scan_ex(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm,
+                                const void* Cm, const float* D, const float* h0, const int32_t* parent, void* y,
+                                const stree_scan_opts* opts, int32_t* dev_status, void* stream) {
+    if (!opts_ok(opts)) return STREE_ERR_ALIGN;
+    OptsScope sc(opts);
+    return stree_tree_scan(d, x, dt, A, Bm, Cm, D, h0, parent, y, dev_status, stream);
+}
+
+stree_status stree_commit_ex(const stree_dims* d, const void* x, const float* dt, const float* A, const void* Bm,
+                             const float* h0, const int32_t* parent, const int32_t* path, const int32_t* path_len,
+                             float* h_new, const stree_scan_opts* opts, int32_t* dev_status, void* stream) {
+    if (!opts_ok(opts)) return STREE_ERR_ALIGN;
+    OptsScope sc(opts);
+    return stree_commit(d, x, dt, A, Bm, h0, parent, path, path_len, h_new, dev_status, stream);
+}
+
+stree_status stree_replay_scan_ex(const stree_dims* d_prev, const void* x_prev, const float* dt_prev,
+                                  const void* Bm_prev, const int32_t* parent_prev, const int32_t* path,
+                                  const int32_t* path_len, const stree_dims* d, const void* x, const float* dt,
+                                  const float* A, const void* Bm, const void* Cm, const float* D, float* h,
+                                  const int32_t* parent, void* y, const stree_scan_opts* opts, int32_t* dev_status,
+                                  void* stream) {
+    if (!opts_ok(opts)) return STREE_ERR_ALIGN;
+    OptsScope sc(opts);
+    return stree_replay_scan(d_prev, x_prev, dt_prev, Bm_prev, parent_prev, path, path_len, d, x, dt, A, Bm, Cm, D,
+                             h, parent, y, dev_status, stream);
+}
 
 stree_status stree_set_launch_flags(uint32_t flags) {
     if (flags & ~(uint32_t)(STREE_LAUNCH_PDL | STREE_LAUNCH_EARLY_STATE | STREE_LAUNCH_EARLY_REPLAY |

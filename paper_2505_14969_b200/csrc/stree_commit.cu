@@ -60,6 +60,7 @@ struct CommitParams {
     int32_t* dev_status;
     unsigned long long* trace;   // debug: per-CTA globaltimer stamps (64 per CTA)
     int early_state;             // STREE_LAUNCH_EARLY_STATE: stream h0 before the PDL wait
+    DtX dtx;                     // *_ex options: effective dt
 };
 
 __device__ __forceinline__ unsigned long long c_gtimer() {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
                 const int m = m0 + lane;
                 float d = 0.f, a = 0.f;
                 if (m < r) {
-                    d = prm.dt[((size_t)b * T + spath[m]) * H + h];
+                    d = dt_eff(prm.dtx, prm.dt[((size_t)b * T + spath[m]) * H + h], h);
                     a = d * Ah;
                 }
 #pragma unroll
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
             } else {
                 __syncwarp();
                 for (int m = lane; m < r; m += 32)
-                    cl[m] = expf(last - cl[m]) * prm.dt[((size_t)b * T + spath[m]) * H + h];
+                    cl[m] = expf(last - cl[m]) * dt_eff(prm.dtx, prm.dt[((size_t)b * T + spath[m]) * H + h], h);
             }
         }
         if (staged)
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, 
                                                            const int32_t* __restrict__ parent,
                                                            const int32_t* __restrict__ path,
                                                            const int32_t* __restrict__ path_len, float* h_new,
-                                                           int32_t* dev_status) {
+                                                           int32_t* dev_status, DtX dtx) {
     __shared__ int s_path[kMaxNodes];
     __shared__ float s_coef[kMaxNodes];
     __shared__ float s_decay;
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, 
             float carry = 0.f;
             for (int base = 0; base < r0; base += 32) {
                 const int m = base + tid;
-                float a = (m < r0) ? dt[((size_t)b * T + s_path[m]) * H + h] * Ah : 0.f;
+                float a = (m < r0) ? dt_eff(dtx, dt[((size_t)b * T + s_path[m]) * H + h], h) * Ah : 0.f;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float t = __shfl_up_sync(0xffffffffu, a, o);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256) commit_block_kernel(int T, int H, int P, 
             }
             __syncwarp();
             for (int m = tid; m < r0; m += 32)
-                s_coef[m] = expf(carry - s_coef[m]) * dt[((size_t)b * T + s_path[m]) * H + h];
+                s_coef[m] = expf(carry - s_coef[m]) * dt_eff(dtx, dt[((size_t)b * T + s_path[m]) * H + h], h);
             if (tid == 0) s_decay = expf(carry);
         }
         if (tid == 0) s_r = ok ? r0 : 0;
@@ -381,7 +382,7 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
     if (!ring_ok) {
         return (int)stree::launch_k(stree::commit_block_kernel<IO>, dim3(H, B), dim3(256), 0, s, T, H, P, N, G,
                                     (const IO*)x, dt, A, (const IO*)Bm, h0, parent, path, path_len, h_new,
-                                    dev_status);
+                                    dev_status, stree::DtX::from(stree_scan_opts_get()));
     }
     const int hpg = H / G;
     int cpg = commit_sms() / (B * G);
@@ -395,6 +396,7 @@ int launch(const stree_dims* d, const void* x, const float* dt, const float* A, 
     stree::CommitParams prm{B, T, H, P, N, G, cpg, hpc, slots, x, dt, A, Bm, h0, parent, path, path_len,
                             h_new, dev_status, g_commit_trace,
                             (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0};
+    prm.dtx = stree::DtX::from(stree_scan_opts_get());
     size_t ustage = (size_t)stree::kCHPC * stree::kRMax * P * 4;
     const size_t lcoef = (size_t)stree::kCHPC * stree::kMaxNodes * 4;
     if (ustage < lcoef) ustage = lcoef;

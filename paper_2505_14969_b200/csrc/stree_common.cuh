@@ -26,6 +26,22 @@ __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// effective dt of the *_ex options (include/stree.h): dt + dt_bias[h], then softplus (PyTorch's threshold 20)
+struct DtX {
+    const float* bias;   // [H] or NULL
+    int softplus;
+    __host__ static DtX from(const stree_scan_opts* o) {
+        DtX x;
+        x.bias = o ? o->dt_bias : nullptr;
+        x.softplus = (o && o->dt_softplus) ? 1 : 0;
+        return x;
+    }
+};
+__device__ __forceinline__ float dt_eff(const DtX& x, float raw, int h) {
+    const float v = x.bias ? raw + x.bias[h] : raw;
+    return x.softplus ? (v > 20.f ? v : log1pf(__expf(v))) : v;
+}
+
 __device__ __forceinline__ void report(int32_t* dev_status, int code) {
     if (dev_status) atomicCAS(dev_status, 0, code);
 }
@@ -99,6 +115,8 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* rows, int W, int i, int
 
 // launch options (stree_set_launch_flags), read by every launcher
 extern "C" uint32_t stree_launch_flags_get();
+// scan options of the *_ex call in progress on this thread (NULL: plain call), read by the scan / commit launchers
+extern "C" const stree_scan_opts* stree_scan_opts_get();
 
 namespace stree {
 // cudaLaunchKernelEx with the programmatic-stream-serialization attribute when PDL is enabled

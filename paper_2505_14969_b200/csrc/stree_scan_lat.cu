@@ -101,6 +101,8 @@ struct Params {
     int has_h0, early_state, early_replay, early_tree;
     int early_dt;                // STREE_LAUNCH_EARLY_DT: the segsum runs before the dependency wait
     int dt_tma;                  // dt staged by TMA (needs H·4 % 16 == 0), else read by the row warps
+    DtX dtx;                     // *_ex options: effective dt (bias, softplus)
+    int d_pc;                    // *_ex options: D is [H][P]
     // replay (previous tree)
     int Tp;
     const __nv_bfloat16* x_prev;
@@ -299,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int i = lane + 32 * hf;
                 dtv[hf] = 0.f;
                 if (i < T)
-                    dtv[hf] = from_smem ? reinterpret_cast<const float*>(sm + L::DT)[4 * i + (h & 3)]
-                                        : prm.dt[((size_t)b * T + i) * H + h];
+                    dtv[hf] = dt_eff(prm.dtx, from_smem ? reinterpret_cast<const float*>(sm + L::DT)[4 * i + (h & 3)]
+                                                        : prm.dt[((size_t)b * T + i) * H + h], h);
                 lm[hf] = dtv[hf] * Ah;
             }
 #pragma unroll
@@ -391,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int rv = ok ? rr : 0;
                 // path-cumsum of log-decays: inclusive warp scans over m = lane, lane + 32, then 32-node chunks
                 const float Ahr = prm.A[h];
-                float a0 = lane < rv ? prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h] : 0.f;
-                float a1 = lane + 32 < rv ? prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h] : 0.f;
+                float a0 = lane < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h], h) : 0.f;
+                float a1 = lane + 32 < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h], h) : 0.f;
                 const float d0 = a0;
                 a0 *= Ahr;
                 a1 *= Ahr;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll 1
                     for (int m0 = 64; m0 < rv; m0 += 32) {
                         const int m = m0 + lane;
-                        float a = m < rv ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + h] * Ahr : 0.f;
+                        float a = m < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(m)) * H + h], h) * Ahr : 0.f;
 #pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
                             const float t = __shfl_up_sync(0xffffffffu, a, o);
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         for (int i = 0; i < 2; ++i) uu[i] = rcoef[m] * __bfloat162float(xprev[m * kP + (tid >> 3) + 32 * i]);
                     } else {   // long accepted paths: operands from L2, coefficients on the fly
                         const int s = rpath[m];
-                        const float dm = prm.dt_prev[((size_t)b * Tp + s) * H + h];
+                        const float dm = dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + s) * H + h], h);
                         lam_run += dm * Ak;
                         const float cm = __expf(last - lam_run) * dm;
                         const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + s) * G + g) * NS + 4 * pc;
@@ -605,7 +607,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
                         const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
                         const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
-                        o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(dh, xa, d0)), fmaf(s0, acc[p + 1], fmaf(dh, xb, d1)));
+                        float da = dh, db = dh;
+                        if (prm.d_pc && prm.D && !bad) {   // D[h][p]
+                            da = __ldg(prm.D + (size_t)h * kP + col + p);
+                            db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
+                        }
+                        o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(da, xa, d0)), fmaf(s0, acc[p + 1], fmaf(db, xb, d1)));
                     }
                 }
                 if (live && wi == 0 && lane == 0 && c16 == 1) stamp(18);
@@ -795,6 +802,8 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
         prm.y_head_off = 0;
     }
     prm.dt_tma = dt_tma ? 1 : 0;
+    prm.dtx = stree::DtX::from(stree_scan_opts_get());
+    prm.d_pc = (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0;
     prm.trace = g_lat_trace ? g_lat_trace + (size_t)(g_lat_trace_n++ % kTraceLaunches) * kTraceStride : nullptr;
     const uint32_t fl = stree_launch_flags_get();
     prm.early_state = (fl & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
                                                         const IO* __restrict__ Cm, const float* __restrict__ D,
                                                         const float* __restrict__ h0,
                                                         const int32_t* __restrict__ parent, IO* __restrict__ y,
-                                                        int32_t* dev_status) {
+                                                        int32_t* dev_status, DtX dtx, int d_pc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const SimtSmem L(T);
     int* sp = (int*)(smem_raw + L.sp);
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
         return;
     }
     const float Ah = A[h];
-    const float Dh = D ? D[h] : 0.f;
-    for (int i = tid; i < T; i += 256) dtv[i] = dt[((size_t)b * T + i) * H + h];
+    const float Dh = D ? D[h] : 0.f;   // (d_pc: D[h][p] per output column below)
+    for (int i = tid; i < T; i += 256) dtv[i] = dt_eff(dtx, dt[((size_t)b * T + i) * H + h], h);
     __syncthreads();
     // tree segsum Λ_i = Σ_{j∈path(i)} dt_j A_h   (A_tree = L A_log)
     for (int i = tid; i < T; i += 256) {
@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256) scan_simt_kernel(int T, int H, int P, int
                 for (int c = 0; c < 4; ++c) {
                     int p = pc + tx * 4 + c;
                     if (p < P) {
-                        float v = acc[r][c] + Dh * Xs[i * kPitch + tx * 4 + c];
+                        const float dd = d_pc ? (D ? D[(size_t)h * P + p] : 0.f) : Dh;
+                        float v = acc[r][c] + dd * Xs[i * kPitch + tx * 4 + c];
                         y[(((size_t)b * T + i) * H + h) * P + p] = from_f32<IO>(v);
                     }
                 }
@@ -229,7 +230,8 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
                             (const __nv_bfloat16*)x, dt, A, (const __nv_bfloat16*)Bm, (const __nv_bfloat16*)Cm, D, h0,
-                            parent, (__nv_bfloat16*)y, dev_status);
+                            parent, (__nv_bfloat16*)y, dev_status, stree::DtX::from(stree_scan_opts_get()),
+                            (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0);
         if (e != cudaSuccess) return (int)e;
     } else {
         auto k = stree::scan_simt_kernel<float>;
@@ -237,7 +239,8 @@ extern "C" int stree_launch_scan_simt(const stree_dims* d, const void* x, const 
         if (e != cudaSuccess) return (int)e;
         e = stree::launch_k(k, grid, dim3(256), smem, s, T, d->n_heads, d->head_dim, d->d_state, d->n_groups,
                             (const float*)x, dt, A, (const float*)Bm, (const float*)Cm, D, h0, parent, (float*)y,
-                            dev_status);
+                            dev_status, stree::DtX::from(stree_scan_opts_get()),
+                            (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0);
         if (e != cudaSuccess) return (int)e;
     }
     return (int)cudaGetLastError();

@@ -122,6 +122,8 @@ struct Params {
     int early_state;   // STREE_LAUNCH_EARLY_STATE: h0 may be streamed before the PDL wait
     int early_replay;  // STREE_LAUNCH_EARLY_REPLAY: the replay prologue may run before the PDL wait
     int early_tree;    // STREE_LAUNCH_EARLY_TREE: parent, A, D not written by the preceding kernel
+    DtX dtx;           // *_ex options: effective dt (bias, softplus)
+    int d_pc;          // *_ex options: D is [H][P]
     int early_dt;      // STREE_LAUNCH_EARLY_DT: dt not written by the preceding kernel (with early_tree: the
                        // whole tree prologue runs before the wait)
     int store_always;  // commit into a distinct h_new: store the state even when the path is invalid
@@ -197,8 +199,8 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
     for (int q = 0; q < kQ; ++q) {
         const int hh = uw + 4 * q;
         const bool hv = hh < nh;
-        dv[q][0] = (hv && lane < rr) ? prm.dt_prev[row0 + hh] : 0.f;
-        dv[q][1] = (hv && lane + 32 < rr) ? prm.dt_prev[row1 + hh] : 0.f;
+        dv[q][0] = (hv && lane < rr) ? dt_eff(prm.dtx, prm.dt_prev[row0 + hh], hbeg + hh) : 0.f;
+        dv[q][1] = (hv && lane + 32 < rr) ? dt_eff(prm.dtx, prm.dt_prev[row1 + hh], hbeg + hh) : 0.f;
         const uint32_t* xp = reinterpret_cast<const uint32_t*>(prm.x_prev) + lane;
 #pragma unroll
         for (int m = 0; m < kRStage; ++m) xv[q][m] = (hv && m < rs) ? xp[(rowm[m] + hh) * (kP / 2)] : 0u;
@@ -254,7 +256,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
 #pragma unroll 1
             for (int m0 = 64; m0 < r; m0 += 32) {
                 const int m = m0 + lane;
-                float a = (hv && m < r) ? prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh] * Ah : 0.f;
+                float a = (hv && m < r) ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(m)) * H + hbeg + hh], hbeg + hh) * Ah : 0.f;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const float t = __shfl_up_sync(0xffffffffu, a, o);
@@ -315,7 +317,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
                         uu[i] = cl[m] * __bfloat162float(xprev[(k * kRStage + m) * kP + (u >> 3) + 16 * i]);
                 } else {   // long accepted paths: operands and coefficients from L2 / on the fly
                     const int sm_ = rpath[m];
-                    const float dm = prm.dt_prev[((size_t)b * Tp + sm_) * H + hbeg + k];
+                    const float dm = dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + sm_) * H + hbeg + k], hbeg + k);
                     lam_run += dm * Ak;
                     const float cm = __expf(last - lam_run) * dm;
                     const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + sm_) * G + g) * NS + 4 * pc;
@@ -649,7 +651,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     const int i = lane + 32 * hf;
-                    dtr[q][hf] = (hv && i < T) ? prm.dt[((size_t)b * T + i) * H + hbeg + hh] : 0.f;
+                    dtr[q][hf] = (hv && i < T) ? dt_eff(prm.dtx, prm.dt[((size_t)b * T + i) * H + hbeg + hh], hbeg + hh) : 0.f;
                 }
             }
             if (e == 0) *sbad = 0;
@@ -915,14 +917,23 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                             const int ch = 4 * c + qc;
                             const uint4 xv = *reinterpret_cast<const uint4*>(xr + swz(row, ch));
                             const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+                            float dpc[8];   // D[h][p] of this chunk's 8 columns (d_pc), else D_h
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) dpc[q] = Dh;
+                            if (prm.d_pc && prm.D && !zero_out) {
+                                const float4* dr = reinterpret_cast<const float4*>(prm.D + (size_t)h * kP + 8 * ch);
+                                const float4 d0 = __ldg(dr), d1 = __ldg(dr + 1);
+                                dpc[0] = d0.x; dpc[1] = d0.y; dpc[2] = d0.z; dpc[3] = d0.w;
+                                dpc[4] = d1.x; dpc[5] = d1.y; dpc[6] = d1.z; dpc[7] = d1.w;
+                            }
                             uint32_t o[4];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 const float xa = __uint_as_float(xw[q] << 16), xb = __uint_as_float(xw[q] & 0xFFFF0000u);
                                 const int p = 8 * qc + 2 * q;
-                                const float ya = fmaf(s0, __uint_as_float(v0[cc][p]), fmaf(Dh, xa, __uint_as_float(v1[cc][p])));
-                                const float yb =
-                                    fmaf(s0, __uint_as_float(v0[cc][p + 1]), fmaf(Dh, xb, __uint_as_float(v1[cc][p + 1])));
+                                const float ya = fmaf(s0, __uint_as_float(v0[cc][p]), fmaf(dpc[2 * q], xa, __uint_as_float(v1[cc][p])));
+                                const float yb = fmaf(s0, __uint_as_float(v0[cc][p + 1]),
+                                                      fmaf(dpc[2 * q + 1], xb, __uint_as_float(v1[cc][p + 1])));
                                 o[q] = zero_out ? 0u : pack_bf16(ya, yb);
                             }
                             *reinterpret_cast<uint4*>(yr + swz(row, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
@@ -1069,6 +1080,8 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
     prm.early_tree = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_TREE) ? 1 : 0;
     prm.early_dt = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_DT) ? 1 : 0;
+    prm.dtx = stree::DtX::from(stree_scan_opts_get());
+    prm.d_pc = (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
     if (yo) {
@@ -1172,6 +1185,7 @@ extern "C" int stree_launch_commit_tc(const stree_dims* d, const void* x, const 
     prm.early_state = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
     prm.early_replay = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_REPLAY) ? 1 : 0;
     prm.store_always = h_new != h0;
+    prm.dtx = stree::DtX::from(stree_scan_opts_get());
     prm.Tp = d->n_nodes;
     prm.x_prev = (const __nv_bfloat16*)x;
     prm.dt_prev = dt;

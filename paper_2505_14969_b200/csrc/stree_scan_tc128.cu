@@ -77,6 +77,8 @@ struct Params {
     __nv_bfloat16* y;
     int32_t* dev_status;
     int B, T, H, G, cpg, hpc, has_h0;
+    DtX dtx;    // *_ex options: effective dt
+    int d_pc;   // *_ex options: D is [H][P]
 };
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -250,7 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pvv = (v < T && v < kT) ? prm.parent[(size_t)b * T + v] : -1;
         if (v < T && v < kT && (v == 0 ? pvv != -1 : (pvv < 0 || pvv >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
         if (v < kT)
-            for (int k = 0; k < nh; ++k) dts[k * kT + v] = v < T ? prm.dt[((size_t)b * T + v) * H + hbeg + k] : 0.f;
+            for (int k = 0; k < nh; ++k)
+                dts[k * kT + v] = v < T ? dt_eff(prm.dtx, prm.dt[((size_t)b * T + v) * H + hbeg + k], hbeg + k) : 0.f;
         mbar();
         const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);   // root error takes precedence
         if (badcode && tid == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             uint32_t y0[32], y1[32];
             const float li = laml[k * kT + i], ei = __expf(li), dh = ds[k];
+            const float* dpc = (prm.d_pc && prm.D) ? prm.D + (size_t)(hbeg + k) * kP : nullptr;   // D[h][p]
             const bool fac = (fmask >> k) & 1u;
             __nv_bfloat16* yrow = prm.y + (((size_t)b * T + i) * H + hbeg + k) * kP;
             {
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float a1 = __uint_as_float(y1[cc]);
                             const float xx = t2 ? bf_hi(xw[e]) : bf_lo(xw[e]);
                             const float base = fac ? ei * (a0 + a1) : fmaf(ei, a0, a1);
-                            v[t2] = valid ? fmaf(dh, xx, base) : 0.f;
+                            v[t2] = valid ? fmaf(dpc ? __ldg(dpc + col + 2 * e + t2) : dh, xx, base) : 0.f;
                         }
                         out[4 * q + e] = pack_bf16(v[0], v[1]);
                     }
@@ -542,5 +546,7 @@ extern "C" int stree_launch_scan_tc128(const stree_dims* d, const void* x, const
     Params prm{};
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.has_h0 = h0 != nullptr;
+    prm.dtx = stree::DtX::from(stree_scan_opts_get());
+    prm.d_pc = (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0;
     return T <= 128 ? launch_tc128<1>(d, mc, mb, mx, mh, prm, s) : launch_tc128<2>(d, mc, mb, mx, mh, prm, s);
 }

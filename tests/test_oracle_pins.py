@@ -648,3 +648,86 @@ def test_conv_commit_then_conv_equals_grafted_tree():
     pg = np.concatenate([p1, np.where(p2 < 0, k, p2 + T1)]).astype(np.int32)
     og, _ = oracle.tree_conv(np.concatenate([u1, u2], 1), weight, bias, state, pg[None])
     np.testing.assert_allclose(o2[0], og[0, T1:], rtol=1e-12, atol=1e-12)
+
+
+# ---- scan options (include/stree.h stree_scan_opts; SURVEY §8(f) unranked variants) ----
+def test_opts_softplus_inverse_and_bias_reduce_to_plain_scan():
+    """softplus(log(e^dt - 1)) = dt and (dt - b) + b = dt: the options fed the pre-images of dt give the plain
+    scan and commit (pins the transform's direction, its argument order and that it reaches every dt)."""
+    rng = np.random.default_rng(3)
+    x, dt, A, Bm, Cm, D, h0, par = rand_case(trees.random_recursive(9, 3, rng), H=3, P=2, N=3, seed=5)
+    bias = rng.uniform(-2, 2, 3)
+    raw = np.log(np.expm1(dt)) - bias[None, None, :]
+    y0, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, par)
+    y1, _ = oracle.tree_scan_ex(x, raw, A, Bm, Cm, D, h0, par, dt_bias=bias, dt_softplus=True)
+    y2, _ = oracle.tree_scan_ex(x, dt - bias[None, None, :], A, Bm, Cm, D, h0, par, dt_bias=bias)
+    assert relerr(y1, y0) < 1e-12 and relerr(y2, y0) < 1e-12
+    path = np.array([[0, 1, -1, -1, -1, -1, -1, -1, -1]], np.int32) if par[0, 1] == 0 else None
+    if path is not None:
+        pl = np.array([2], np.int32)
+        c0, _ = oracle.commit(x, dt, A, Bm, h0, path, pl, par)
+        c1, _ = oracle.commit_ex(x, raw, A, Bm, h0, path, pl, par, dt_bias=bias, dt_softplus=True)
+        assert relerr(c1, c0) < 1e-12
+
+
+def test_opts_single_node_closed_form():
+    """T = 1 from h0 = 0: y = softplus(dt + b)·x·(B·C) + D[h][p]·x, per head and channel — the recurrence
+    and the options written out by hand for one step (PAPER.md:44-45 per R1)."""
+    H, P, N = 2, 3, 4
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((1, 1, H, P))
+    raw = rng.uniform(-3, 3, (1, 1, H))
+    bias = rng.uniform(-1, 1, H)
+    A = -rng.uniform(1, 5, H)
+    Bm, Cm = rng.standard_normal((1, 1, 1, N)), rng.standard_normal((1, 1, 1, N))
+    Dhp = rng.standard_normal((H, P))
+    y, st = oracle.tree_scan_ex(x, raw, A, Bm, Cm, Dhp, None, np.array([[-1]], np.int32), dt_bias=bias,
+                                dt_softplus=True, d_per_channel=True)
+    bc = float(sum(Bm[0, 0, 0, n] * Cm[0, 0, 0, n] for n in range(N)))
+    for h in range(H):
+        sp = math.log1p(math.exp(raw[0, 0, h] + bias[h]))
+        for p in range(P):
+            want = sp * x[0, 0, h, p] * bc + Dhp[h, p] * x[0, 0, h, p]
+            assert abs(y[0, 0, h, p] - want) <= 1e-12 * max(1.0, abs(want))
+    assert not st.any()
+
+
+def test_opts_per_channel_d_reduces_and_is_linear():
+    """D[h][p] = D_h for every p equals the per-head D; y(D1 + D2) - y(D1) = D2 ∘ x (the skip term is
+    additive and per channel); invalid trees stay zero."""
+    rng = np.random.default_rng(7)
+    par = np.stack([trees.random_recursive(11, 3, rng), trees.chain(11)]).astype(np.int32)
+    cases = [rand_case(par[k], H=2, P=3, N=2, seed=8 + k) for k in range(2)]
+    x, dt, Bm, Cm, h0 = (np.concatenate([c[i] for c in cases]) for i in (0, 1, 3, 4, 6))
+    A, D = cases[0][2], cases[0][5]
+    Dhp = np.repeat(D[:, None], 3, axis=1)
+    ya, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, par)
+    yb, _ = oracle.tree_scan_ex(x, dt, A, Bm, Cm, Dhp, h0, par, d_per_channel=True)
+    assert relerr(yb, ya) < 1e-12
+    D2 = rng.standard_normal((2, 3))
+    yc, _ = oracle.tree_scan_ex(x, dt, A, Bm, Cm, Dhp + D2, h0, par, d_per_channel=True)
+    assert np.abs((yc - yb) - D2[None, None] * x).max() < 1e-12
+    bad = par.copy()
+    bad[1, 4] = 7
+    yz, st = oracle.tree_scan_ex(x, dt, A, Bm, Cm, Dhp, h0, bad, d_per_channel=True)
+    assert st[1] == 2 and not yz[1].any()
+
+
+def test_variable_T_by_padding_leaves():
+    """Variable T per tree: a tree of n < T nodes is padded with leaves under the root; every
+    real node's output is unchanged (outputs depend on ancestors only), and a padding leaf
+    whose token never matches is never accepted, so the committed state is unchanged too."""
+    rng = np.random.default_rng(21)
+    n, T = 9, 16
+    p9 = trees.random_recursive(n, 3, rng)
+    x, dt, A, Bm, Cm, D, h0, p16 = rand_case(np.concatenate([p9, np.zeros(T - n, np.int32)]), H=2, P=2, N=3,
+                                             seed=4)
+    y16, _ = oracle.tree_scan(x, dt, A, Bm, Cm, D, h0, p16)
+    y9, _ = oracle.tree_scan(x[:, :n], dt[:, :n], A, Bm[:, :n], Cm[:, :n], D, h0, p9[None])
+    assert np.array_equal(y16[:, :n], y9)
+    tok = np.concatenate([rng.integers(0, 50, n), -np.ones(T - n, np.int64)]).astype(np.int32)[None]
+    vt = tok.copy()
+    vt[0, :n] = rng.integers(0, 50, n)
+    path16, pl16, b16, _ = oracle.accept(tok, p16, vt)
+    path9, pl9, b9, _ = oracle.accept(tok[:, :n], p9[None], vt[:, :n])
+    assert pl16[0] == pl9[0] and b16[0] == b9[0] and np.array_equal(path16[0, :pl16[0]], path9[0, :pl9[0]])

@@ -21,7 +21,9 @@ def launches(path):
     return per
 
 
-API = {"scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "stree_replay_scan",
+API = {"lat_kernel<128, true>": "stree_replay_scan", "lat_kernel<64, true>": "stree_replay_scan",
+       "lat_kernel<128, false>": "stree_tree_scan", "lat_kernel<64, false>": "stree_tree_scan",
+       "scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "stree_replay_scan",
        "scan_tc_kernel<128, 0>": "stree_tree_scan", "scan_tc_kernel<64, 0>": "stree_tree_scan",
        "scan_tc_kernel<128, 2>": "stree_commit", "scan_tc_kernel<64, 2>": "stree_commit",
        "commit_ring_kernel": "stree_commit", "commit_block_kernel": "stree_commit",
@@ -124,5 +126,22 @@ for rep in ("prof_fused", "prof_scan", "prof_commit"):
 # L2 (under-counted), without flushing its replays hit L2 -- kept for reference only.
 print("traffic per launch (bytes, launch list):", json.dumps(traffic))
 print("--set full capture DRAM bytes (replayed, reference only):", json.dumps(full))
-json.dump({"c4": traffic, "source": "ncu launch list of bench.py, --cache-control none, mean read+write per launch"},
-          open(os.path.join(out, "traffic.json"), "w"), indent=1)
+res = {"c4": traffic, "source": "ncu launch list of bench.py, --cache-control none, mean read+write per launch"}
+# batch-1 configs (small-batch kernel): launch lists of bench.py --config c3 / c2
+for cfg in ("c3", "c2"):
+    pf = os.path.join(out, f"launches_{cfg}.csv")
+    if os.path.exists(pf):
+        print(f"== launch list, bench.py --config {cfg} ==")
+        pc = launches(pf)
+        tc_ = sum(sum(m["gpu__time_duration.sum"]) for m in pc.values())
+        tr = {}
+        for k, m in sorted(pc.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):
+            t = m["gpu__time_duration.sum"]
+            rd = sum(m["dram__bytes_read.sum"]) / len(t)
+            wr = sum(m["dram__bytes_write.sum"]) / len(t)
+            print(f"{k[:60]:60s} n={len(t):4d} mean={sum(t) / len(t) / 1e3:8.2f} us  share={sum(t) / tc_ * 100:5.1f}%  "
+                  f"dram r/w per launch {rd / 1e6:7.2f} / {wr / 1e6:7.2f} MB")
+            tr.setdefault(api_name(k), rd + wr)
+        res[cfg] = tr
+print("traffic.json:", json.dumps(res))
+json.dump(res, open(os.path.join(out, "traffic.json"), "w"), indent=1)
