@@ -281,6 +281,11 @@ def run_stree(args):
                                     binding.STREE_LAUNCH_EARLY_STATE | binding.STREE_LAUNCH_EARLY_REPLAY |
                                     binding.STREE_LAUNCH_EARLY_TREE | binding.STREE_LAUNCH_EARLY_DT))
     L = args.layers
+    base0 = inputs.config_problem(args.config)
+    # distinct per-layer buffers must exceed the 126 MB L2 (no flush needed): small layers get more of them
+    lb = scan_bytes(base0.dims) + base0.dims.batch * base0.dims.n_heads * base0.dims.head_dim * base0.dims.d_state * 4
+    if args.layers == 64 and lb * L < 2 * 126e6:
+        L = int(-(-2 * 126e6 // lb))
     # every rank verifies its own batch of trees (weak scaling; no data-path collective)
     from paper_2505_14969_b200 import dist as sdist
     base = inputs.config_problem(args.config)
@@ -531,8 +536,9 @@ def run_stree(args):
 
 
 def isolated_call_us(phase, layers, stream, L, reps=15):
-    """Median over `reps` trials of ONE layer's call of the phase's kernel, eager, with the device idle before
-    it (synchronize), timed with CUDA events on the launching stream."""
+    """Median over `reps` trials of ONE layer's call of the phase's kernel on its own: device time from the
+    event after a ~25 us spin kernel (which keeps the host launch overhead out of the interval) to the
+    kernel's completion — the kernel's full latency including its launch boundary, no PDL overlap."""
     import torch
     one = layers[:1]
     saved = list(layers)
@@ -543,6 +549,7 @@ def isolated_call_us(phase, layers, stream, L, reps=15):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
+                torch.cuda._sleep(50000)
                 e0.record(stream)
                 phase()
                 e1.record(stream)

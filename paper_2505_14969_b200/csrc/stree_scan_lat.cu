@@ -156,7 +156,7 @@ __device__ __forceinline__ void build_weights(uint32_t tq, int c0, uint64_t bits
     if (kTrace && tr) tr[27] = gtimer();
 }
 
-template <int NS, bool R>
+template <int NS, bool R, bool DPC = false>   // DPC: D is [H][P] (separate instantiation, no runtime branch)
 __global__ void __launch_bounds__(kThreads, 2)
     lat_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h,
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
                         const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
                         float da = dh, db = dh;
-                        if (prm.d_pc && prm.D && !bad) {   // D[h][p]
+                        if (DPC && prm.D && !bad) {   // D[h][p]
                             da = __ldg(prm.D + (size_t)h * kP + col + p);
                             db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
                         }
@@ -732,11 +732,11 @@ constexpr size_t kTraceStride = 1024 * stree::lat::kTraceWords;
 unsigned long long* g_lat_trace = nullptr;
 int g_lat_trace_n = 0;
 
-template <int NS, bool R>
+template <int NS, bool R, bool DPC = false>
 int launch_lat_inst(int B, int H, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb, const CUtensorMap& mx,
                     const CUtensorMap& mh, const CUtensorMap& mdt, const stree::lat::Params& prm) {
     using namespace stree::lat;
-    auto k = lat_kernel<NS, R>;
+    auto k = lat_kernel<NS, R, DPC>;
     size_t smem = Lay<NS, R>::TOTAL + 1024;
     static const bool one_cta = [] {   // debug knob (not part of the ABI): force one CTA per SM
         const char* e = std::getenv("STREE_LAT_ONE_CTA");
@@ -812,6 +812,12 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
     prm.early_dt = (fl & STREE_LAUNCH_EARLY_DT) ? 1 : 0;
     if (prm.early_tree && prm.early_dt) prm.dt_tma = 0;   // read before the wait by the row warps
     if (replay && !h0) return (int)cudaErrorInvalidValue;
+    if (prm.d_pc) {
+        if (N == 128) return replay ? launch_lat_inst<128, true, true>(B, H, s, mc, mb, mx, mh, mdt, prm)
+                                    : launch_lat_inst<128, false, true>(B, H, s, mc, mb, mx, mh, mdt, prm);
+        return replay ? launch_lat_inst<64, true, true>(B, H, s, mc, mb, mx, mh, mdt, prm)
+                      : launch_lat_inst<64, false, true>(B, H, s, mc, mb, mx, mh, mdt, prm);
+    }
     if (N == 128) return replay ? launch_lat_inst<128, true>(B, H, s, mc, mb, mx, mh, mdt, prm)
                                 : launch_lat_inst<128, false>(B, H, s, mc, mb, mx, mh, mdt, prm);
     return replay ? launch_lat_inst<64, true>(B, H, s, mc, mb, mx, mh, mdt, prm)

@@ -382,7 +382,9 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
 
 // MODE 0: tree scan; 1: replay of the previous tree's accepted path fused with the scan (in place);
 // 2: replay only (stree_commit): warps 0 (state producer), 6-9 (replay) and 10 (stores to tm_y = h_new)
-template <int NS, int MODE, typename YM = NoYPeers>
+// DPC: D is [H][P] (stree_scan_opts.d_per_channel) — a separate instantiation: a runtime branch in the
+// epilogue costs ~1 us per c4 layer even when not taken
+template <int NS, int MODE, typename YM = NoYPeers, bool DPC = false>
 __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
     scan_tc_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                         dy = tmem + kDirCol;
                         acc0 = 0;
                     }
-                    const uint64_t ad = sdesc(sb + S::MB + a * kAtom, 16, 1024);
+                    const uint64_t ad = sdesc(sb + S::MB + (a ^ 1) * kAtom, 16, 1024);   // (see mrow)
                     const uint64_t xd = sdesc(sb + S::xslot(sx), kAtom, 1024);
                     const int nk = (dbg & 2) ? 0 : Tp16 / 16;
 #pragma unroll
@@ -812,7 +814,10 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                 const float* lk = lam + k * 64;
                 const bool f = mode[k] != 0;
                 const float li = bown ? lk[brow] : 0.f;
-                unsigned char* mrow = sm + S::MB + a * kAtom;
+                // M'[a] lives at MB + (a^1)·kAtom: M'[0] (heads 0, 2, ..) over the C copy, which only the G MMA
+                // reads (done at BAR_G); M'[1] over C atom 0, which the C -> tf32 converters read (BAR_CTF)
+                if (k == 1) mbar_wait(BAR_CTF, 0);
+                unsigned char* mrow = sm + S::MB + (a ^ 1) * kAtom;
                 // split builders: half 0 takes columns j < 32, half 1 the rest
                 const int c16b = kSplit ? 2 * half : 0, c16e = kSplit ? min(Tp16 / 16, 2 * half + 2) : Tp16 / 16;
 #pragma unroll 1
@@ -920,7 +925,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
                             float dpc[8];   // D[h][p] of this chunk's 8 columns (d_pc), else D_h
 #pragma unroll
                             for (int q = 0; q < 8; ++q) dpc[q] = Dh;
-                            if (prm.d_pc && prm.D && !zero_out) {
+                            if (DPC && prm.D && !zero_out) {
                                 const float4* dr = reinterpret_cast<const float4*>(prm.D + (size_t)h * kP + 8 * ch);
                                 const float4 d0 = __ldg(dr), d1 = __ldg(dr + 1);
                                 dpc[0] = d0.x; dpc[1] = d0.y; dpc[2] = d0.z; dpc[3] = d0.w;
@@ -1017,12 +1022,12 @@ extern "C" int stree_tc_supports(const stree_dims* d) {
 
 namespace {
 
-template <int NS, int MODE, typename YM = stree::tc::NoYPeers>
+template <int NS, int MODE, typename YM = stree::tc::NoYPeers, bool DPC = false>
 cudaError_t launch_tc_inst(dim3 grid, cudaStream_t s, const CUtensorMap& mc, const CUtensorMap& mb,
                            const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& my,
                            const stree::tc::Params& prm, const YM& ym = YM{}) {
     using namespace stree::tc;
-    auto k = scan_tc_kernel<NS, MODE, YM>;
+    auto k = scan_tc_kernel<NS, MODE, YM, DPC>;
     const size_t smem = Smem<NS, (MODE >= 1)>::TOTAL + 1024;
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1084,6 +1089,7 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     prm.d_pc = (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0;
     dim3 grid(B * G * cpg);
     cudaError_t e;
+    if (yo && prm.d_pc) return (int)cudaErrorNotSupported;   // sharded calls take no scan options
     if (yo) {
         prm.n_ypeer = yo->n_peers;
         prm.y_head_off = yo->head_offset;
@@ -1094,11 +1100,15 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
             e = replay ? launch_tc_inst<64, 1>(grid, s, mc, mb, mx, mh, my, prm, ym)
                        : launch_tc_inst<64, 0>(grid, s, mc, mb, mx, mh, my, prm, ym);
     } else if (N == 128)
-        e = replay ? launch_tc_inst<128, 1>(grid, s, mc, mb, mx, mh, my, prm)
-                   : launch_tc_inst<128, 0>(grid, s, mc, mb, mx, mh, my, prm);
+        e = prm.d_pc ? (replay ? launch_tc_inst<128, 1, NoYPeers, true>(grid, s, mc, mb, mx, mh, my, prm)
+                               : launch_tc_inst<128, 0, NoYPeers, true>(grid, s, mc, mb, mx, mh, my, prm))
+                     : (replay ? launch_tc_inst<128, 1>(grid, s, mc, mb, mx, mh, my, prm)
+                               : launch_tc_inst<128, 0>(grid, s, mc, mb, mx, mh, my, prm));
     else
-        e = replay ? launch_tc_inst<64, 1>(grid, s, mc, mb, mx, mh, my, prm)
-                   : launch_tc_inst<64, 0>(grid, s, mc, mb, mx, mh, my, prm);
+        e = prm.d_pc ? (replay ? launch_tc_inst<64, 1, NoYPeers, true>(grid, s, mc, mb, mx, mh, my, prm)
+                               : launch_tc_inst<64, 0, NoYPeers, true>(grid, s, mc, mb, mx, mh, my, prm))
+                     : (replay ? launch_tc_inst<64, 1>(grid, s, mc, mb, mx, mh, my, prm)
+                               : launch_tc_inst<64, 0>(grid, s, mc, mb, mx, mh, my, prm));
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }

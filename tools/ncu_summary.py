@@ -21,8 +21,10 @@ def launches(path):
     return per
 
 
-API = {"lat_kernel<128, true>": "stree_replay_scan", "lat_kernel<64, true>": "stree_replay_scan",
-       "lat_kernel<128, false>": "stree_tree_scan", "lat_kernel<64, false>": "stree_tree_scan",
+API = {"lat_kernel<128, 1": "stree_replay_scan", "lat_kernel<64, 1": "stree_replay_scan",
+       "lat_kernel<128, 0": "stree_tree_scan", "lat_kernel<64, 0": "stree_tree_scan",
+       "lat_kernel<128, true": "stree_replay_scan", "lat_kernel<64, true": "stree_replay_scan",
+       "lat_kernel<128, false": "stree_tree_scan", "lat_kernel<64, false": "stree_tree_scan",
        "scan_tc_kernel<128, 1>": "stree_replay_scan", "scan_tc_kernel<64, 1>": "stree_replay_scan",
        "scan_tc_kernel<128, 0>": "stree_tree_scan", "scan_tc_kernel<64, 0>": "stree_tree_scan",
        "scan_tc_kernel<128, 2>": "stree_commit", "scan_tc_kernel<64, 2>": "stree_commit",
@@ -34,7 +36,8 @@ API = {"lat_kernel<128, true>": "stree_replay_scan", "lat_kernel<64, true>": "st
 
 def api_name(k):
     for pre, v in API.items():
-        if k.split("::")[-1].startswith(pre) or pre in k:
+        pre2 = pre.rstrip(">")   # templates may carry more arguments (scan_tc_kernel<128, 1, NoYPeers>)
+        if k.split("::")[-1].startswith(pre2) or pre in k or pre2 + "," in k:
             return v
     if "scan_simt" in k:
         return "stree_tree_scan"
