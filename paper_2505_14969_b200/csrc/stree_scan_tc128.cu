@@ -34,6 +34,12 @@ constexpr int kP = 64, kN = 128;
 constexpr int kThreads = 320;   // warps 0-7 math (two per TMEM lane quadrant), 8 TMA, 9 MMA
 constexpr int kTile = 16384;          // 128 rows x 128 bytes, swizzle-128B
 constexpr uint32_t kCols = 512;
+constexpr int kTraceWords = 64;   // debug timeline: u64 globaltimer stamps per CTA (STREE_TRACE builds)
+#ifdef STREE_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 
 template <int NKB>
 struct Sm {
@@ -79,12 +85,14 @@ struct Params {
     int B, T, H, G, cpg, hpc, has_h0;
     DtX dtx;    // *_ex options: effective dt
     int d_pc;   // *_ex options: D is [H][P]
+    unsigned long long* trace;   // [grid][kTraceWords] or NULL (STREE_TRACE builds only)
+    int early_tree, early_dt;    // STREE_LAUNCH_EARLY_TREE / _DT: the tree prologue before the dependency wait
 };
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-template <int NKB>
+template <int NKB, bool DPC = false>   // DPC: D is [H][P] (separate instantiation, no runtime branch)
 __global__ void __launch_bounds__(kThreads, 1)
     scan_tc128_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h0,
@@ -110,6 +118,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kcta = min(Tp16, 128 * (rt + 1));       // keys this tile's rows can see (multiple of 16)
     const int nkb = rt + 1;                           // key blocks of 128
 
+    unsigned long long* const trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
+    auto stamp = [&](int k) {
+        if (kTrace && trace && k < kTraceWords) trace[k] = gtimer();
+    };
+    if (threadIdx.x == 0) stamp(0);
     const uint32_t bar0 = sb + Sm::BAR;
     const uint32_t BAR_TREE = bar0, BAR_G = bar0 + 8, BAR_CTF = bar0 + 16;
     auto bar_hfull = [&](int s) { return bar0 + 24 + 8 * s; };
@@ -151,7 +164,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_wait();
+    // math warps with EARLY_TREE + EARLY_DT run the whole tree prologue (validation, ancestor bits, Λ, decay
+    // modes and coefficients) before their dependency wait
+    const bool early_tree = warp < 8 && prm.early_tree && prm.early_dt;
+    if (!early_tree) pdl_wait();
+    if (tid == 0) stamp(1);
 
     if (warp == 8) {
         // ================= TMA producer =================
@@ -182,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ================= MMA issuer (warp converged, elected lane issues) =================
         mbar_wait(BAR_TREE, 0);
         tc_fence_after();
+        if (lane == 0) stamp(2);
         // G = C_rows·Bᵀ, one N = 128 block per 128 keys (NKB == 1: N = Tp16)
         for (int kb = 0; kb < nkb; ++kb) {
             const uint32_t id_g = idesc(kFmtBF16, 0, 128, NKB == 1 ? Tp16 : 128);
@@ -212,9 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   id_y0, kk > 0);
                 tc_commit_w(bar_hempty(s));
             }
+            if (lane == 0 && k < 8) stamp(20 + 2 * k);   // Y0 of head k issued
             mbar_wait(bar_mfull(a), ua & 1);
             mbar_wait(bar_xfull(s), u & 1);
             tc_fence_after();
+            if (lane == 0 && k < 8) stamp(21 + 2 * k);   // M' and x of head k ready
             const uint64_t xd = sdesc(sb + Sm::xstage(s), kTile, 1024);
 #pragma unroll 1
             for (int kk = 0; kk < kcta / 16; ++kk)
@@ -251,12 +271,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int v = tid;                       // node of this thread in the prologue (v < kT iff active)
         const int pvv = (v < T && v < kT) ? prm.parent[(size_t)b * T + v] : -1;
         if (v < T && v < kT && (v == 0 ? pvv != -1 : (pvv < 0 || pvv >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
-        if (v < kT)
-            for (int k = 0; k < nh; ++k)
-                dts[k * kT + v] = v < T ? dt_eff(prm.dtx, prm.dt[((size_t)b * T + v) * H + hbeg + k], hbeg + k) : 0.f;
+        if (v < kT) {   // the chunk's dt of node v: all loads in flight together (one latency, not nh)
+            float dv[kHPC];
+#pragma unroll
+            for (int k = 0; k < kHPC; ++k) dv[k] = (k < nh && v < T) ? prm.dt[((size_t)b * T + v) * H + hbeg + k] : 0.f;
+#pragma unroll
+            for (int k = 0; k < kHPC; ++k)
+                if (k < nh) dts[k * kT + v] = v < T ? dt_eff(prm.dtx, dv[k], hbeg + k) : 0.f;
+        }
         mbar();
         const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);   // root error takes precedence
-        if (badcode && tid == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
+        if (badcode && tid == 0 && rem == 0 && rt == 0 && !early_tree) report(prm.dev_status, badcode);
         const bool valid = badcode == 0;
         int cur = 0;
         if (v < kT) {
@@ -321,6 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             wok[warp] = okm;
             ((uint32_t*)(sm + Sm::WRB))[warp] = rbm;
         }
+        if (early_tree) {
+            pdl_wait();   // every global write follows the dependency wait
+            if (badcode && tid == 0 && rem == 0 && rt == 0) report(prm.dev_status, badcode);
+        }
+        if (tid == 0) stamp(3);   // tree prologue done
         // C -> tf32 into TMEM columns [kCCol, kCCol + 128) (row t of this tile)
         mbar_wait(BAR_TREE, 0);
         {
@@ -352,17 +382,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int w = 0; w < kW; ++w) myanc[w] = anc[w * kT + i];
         tc_fence_before();
         mbar_arrive(BAR_CTF);   // (NKB == 2: the C tile is free for x stage 1 from here)
+        if (tid == 0) stamp(4);
         mbar_wait(BAR_G, 0);
         tc_fence_after();
+        if (tid == 0) stamp(5);
         const float* laml = lam + cur * kHPC * kT;
 
         auto epilogue = [&](int k) {
             const int a = NKB == 1 ? (k & 1) : 0, s = k & 1, u = k >> 1, ua = NKB == 1 ? u : k;
             mbar_wait(bar_accfull(a), ua & 1);
             tc_fence_after();
+            if (tid == 0 && k < 8) stamp(40 + 2 * k);   // accumulator of head k ready
             uint32_t y0[32], y1[32];
             const float li = laml[k * kT + i], ei = __expf(li), dh = ds[k];
-            const float* dpc = (prm.d_pc && prm.D) ? prm.D + (size_t)(hbeg + k) * kP : nullptr;   // D[h][p]
+            const float* dpc = (DPC && prm.D) ? prm.D + (size_t)(hbeg + k) * kP : nullptr;   // D[h][p]
             const bool fac = (fmask >> k) & 1u;
             __nv_bfloat16* yrow = prm.y + (((size_t)b * T + i) * H + hbeg + k) * kP;
             {
@@ -387,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const float a1 = __uint_as_float(y1[cc]);
                             const float xx = t2 ? bf_hi(xw[e]) : bf_lo(xw[e]);
                             const float base = fac ? ei * (a0 + a1) : fmaf(ei, a0, a1);
-                            v[t2] = valid ? fmaf(dpc ? __ldg(dpc + col + 2 * e + t2) : dh, xx, base) : 0.f;
+                            v[t2] = valid ? fmaf((DPC && dpc) ? __ldg(dpc + col + 2 * e + t2) : dh, xx, base) : 0.f;
                         }
                         out[4 * q + e] = pack_bf16(v[0], v[1]);
                     }
@@ -401,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(bar_accempty(a));
             mbar_arrive(bar_xempty(s));
+            if (tid == 0 && k < 8) stamp(41 + 2 * k);   // epilogue of head k done
         };
 
         for (int k = 0; k < nh; ++k) {
@@ -464,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // keys past kcta are never read by the MMA (K = kcta)
             fence_proxy_async();
             mbar_arrive(bar_mfull(a));
+            if (tid == 0 && k < 8) stamp(6 + k);   // M' of head k built
             if (NKB == 1) {
                 if (k > 0) epilogue(k - 1);
             } else {
@@ -474,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) stamp(63);
     if (warp == 9) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -484,6 +520,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace stree
 
 namespace {
+// debug timeline (not part of the ABI): launch i writes its per-CTA stamps to buf + (i % 16) * 1024 * 64
+unsigned long long* g_tc128_trace = nullptr;
+int g_tc128_trace_n = 0;
 bool map2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
            uint32_t box_inner, uint32_t box_outer) {
     return stree::host::tmap_2d(m, dt, base, inner, outer, row_bytes, box_inner, box_outer);
@@ -498,7 +537,7 @@ extern "C" int stree_tc128_supports(const stree_dims* d) {
 }
 
 namespace {
-template <int NKB>
+template <int NKB, bool DPC>
 int launch_tc128(const stree_dims* d, const CUtensorMap& mc, const CUtensorMap& mb, const CUtensorMap& mx,
                  const CUtensorMap& mh, const stree::tc128::Params& base, cudaStream_t s) {
     using namespace stree::tc128;
@@ -518,7 +557,7 @@ int launch_tc128(const stree_dims* d, const CUtensorMap& mc, const CUtensorMap& 
     prm.cpg = cpg;
     prm.hpc = hpc;
     const size_t smem = S::TOTAL + 1024;
-    auto k = scan_tc128_kernel<NKB>;
+    auto k = scan_tc128_kernel<NKB, DPC>;
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return (int)e;
     e = stree::launch_k(k, dim3(B * G * cpg * NKB), dim3(kThreads), smem, s, mc, mb, mx, mh, prm);
@@ -548,5 +587,15 @@ extern "C" int stree_launch_scan_tc128(const stree_dims* d, const void* x, const
     prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.has_h0 = h0 != nullptr;
     prm.dtx = stree::DtX::from(stree_scan_opts_get());
     prm.d_pc = (stree_scan_opts_get() && stree_scan_opts_get()->d_per_channel) ? 1 : 0;
-    return T <= 128 ? launch_tc128<1>(d, mc, mb, mx, mh, prm, s) : launch_tc128<2>(d, mc, mb, mx, mh, prm, s);
+    prm.trace = g_tc128_trace ? g_tc128_trace + (size_t)(g_tc128_trace_n++ % 16) * 1024 * kTraceWords : nullptr;
+    prm.early_tree = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_TREE) ? 1 : 0;
+    prm.early_dt = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_DT) ? 1 : 0;
+    if (prm.d_pc)
+        return T <= 128 ? launch_tc128<1, true>(d, mc, mb, mx, mh, prm, s) : launch_tc128<2, true>(d, mc, mb, mx, mh, prm, s);
+    return T <= 128 ? launch_tc128<1, false>(d, mc, mb, mx, mh, prm, s) : launch_tc128<2, false>(d, mc, mb, mx, mh, prm, s);
+}
+
+extern "C" void stree_debug_tc128_trace(unsigned long long* dev_buf) {
+    g_tc128_trace = dev_buf;
+    g_tc128_trace_n = 0;
 }

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out/r2
+STREE_TRACE=1 python -c "from paper_2505_14969_b200 import build; build.build(force=True)" > /dev/null 2>&1
+timeout 120 python tools/trace_tc128.py --B 16 --T 128 > gpurun_out/r2/trace128_b16.txt 2>&1; cat gpurun_out/r2/trace128_b16.txt
+timeout 120 python tools/trace_tc128.py --B 1 --T 128 > gpurun_out/r2/trace128_b1.txt 2>&1; head -30 gpurun_out/r2/trace128_b1.txt

@@ -98,7 +98,10 @@ def leaf_paths(par):
 
 def main():
     quick = "--quick" in sys.argv
-    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE)
+    # a stack of scan-only layers: the preceding kernel (the previous layer) writes none of a layer's state, tree,
+    # dt or parameters, so the EARLY promises hold (as in bench.py)
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE |
+                                   binding.STREE_LAUNCH_EARLY_TREE | binding.STREE_LAUNCH_EARLY_DT)
     cases = inputs.sweep_cases()
     if quick:
         cases = [c for c in cases if c[0] in ("heap2_T16", "heap2_T64", "heap4_T64", "chain_T64", "fullbin_L5",
