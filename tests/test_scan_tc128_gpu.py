@@ -57,12 +57,14 @@ def test_tc128_matches_oracle(B, T, H, G, kind):
     assert_y_close(y, ref, TOL_BF16)
 
 
-@pytest.mark.parametrize("variant", ["stress_decay", "no_decay", "large_x", "h0_none", "D_none"])
+@pytest.mark.parametrize("variant", ["stress_decay", "mixed_decay", "no_decay", "large_x", "h0_none", "D_none"])
 @pytest.mark.parametrize("T", [112, 240])
 def test_tc128_stress(variant, T):
     d = inputs.Dims(2, T, 8, 64, 128, 1, "bf16")
     par = np.stack([trees.heap_kary(T, 2), trees.chain(T)])
-    kw = dict(stress_decay=dict(dt_range=(0.5, 1.0), A_range=(16.0, 16.0)), no_decay=dict(dt_range=(1e-6, 1e-5)),
+    # mixed_decay: per-head A·dt spans factorised, chunk-rebased and direct-decay heads in one CTA
+    kw = dict(stress_decay=dict(dt_range=(0.5, 1.0), A_range=(16.0, 16.0)),
+              mixed_decay=dict(dt_range=(0.2, 1.0), A_range=(0.05, 16.0)), no_decay=dict(dt_range=(1e-6, 1e-5)),
               large_x=dict(x_scale=100.0), h0_none=dict(h0_zero=True), D_none=dict(D_none=True)).get(variant, {})
     prob = inputs.make_problem(d, par, seed=99, **kw)
     y, st = run(prob, h0=variant != "h0_none")

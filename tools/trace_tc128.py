@@ -61,10 +61,11 @@ print(f"B={args.B} T={args.T} H={args.H}: graph of {L} layers: {e0.elapsed_time(
 tr = buf.cpu().numpy().astype(np.int64)[:L]
 ncta = int((tr[0, :, 0] > 0).sum())
 tr = tr[:, :ncta]
-names = {0: "start", 1: "pdl wait passed", 2: "iss: C,B landed", 3: "math: tree prologue done", 4: "math: C->tf32 done",
+names = {0: "start", 1: "pdl wait passed", 14: "math: prologue loads landed", 15: "math: pointer jumping done",
+         16: "math: modes + coefficients done", 2: "iss: C,B landed", 3: "math: tree prologue done", 4: "math: C->tf32 done",
          5: "math: G ready", 63: "end"}
 for k in range(8):
-    names[6 + k] = f"bld: M' head {k} built"
+    names[6 + k] = f"bld: X' (M') head {k} ready"
     names[20 + 2 * k] = f"iss: Y0 head {k} issued"
     names[21 + 2 * k] = f"iss: M'+x head {k} ready"
     names[40 + 2 * k] = f"epi: acc head {k} ready"
