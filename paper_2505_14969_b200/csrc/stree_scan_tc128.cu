@@ -316,78 +316,129 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int v = tid;                       // node of this thread in the prologue (v < kT iff active)
         const int pvv = (v < T && v < kT) ? prm.parent[(size_t)b * T + v] : -1;
         if (v < T && v < kT && (v == 0 ? pvv != -1 : (pvv < 0 || pvv >= v))) atomicMax(sbad, v == 0 ? 2 : 1);
-        if (v < kT) {   // the chunk's dt of node v: all loads in flight together (one latency, not nh)
-            float dv[kHPC];
+        {   // dt of the chunk's heads, coalesced over (node, head) pairs: all loads in flight together
+            constexpr int kLd = (kT * kHPC + 255) / 256;
+            float dv[kLd];
 #pragma unroll
-            for (int k = 0; k < kHPC; ++k) dv[k] = (k < nh && v < T) ? prm.dt[((size_t)b * T + v) * H + hbeg + k] : 0.f;
+            for (int r = 0; r < kLd; ++r) {
+                const int idx = tid + 256 * r, row = idx / nh, k = idx - row * nh;
+                dv[r] = (idx < kT * nh && row < T) ? prm.dt[((size_t)b * T + row) * H + hbeg + k] : 0.f;
+            }
 #pragma unroll
-            for (int k = 0; k < kHPC; ++k)
-                if (k < nh) dts[k * kT + v] = v < T ? dt_eff(prm.dtx, dv[k], hbeg + k) : 0.f;
+            for (int r = 0; r < kLd; ++r) {
+                const int idx = tid + 256 * r, row = idx / nh, k = idx - row * nh;
+                if (idx < kT * nh) dts[k * kT + row] = row < T ? dt_eff(prm.dtx, dv[r], hbeg + k) : 0.f;
+            }
         }
         mbar();
         if (tid == 0) stamp(14);   // prologue loads landed
         const int badcode = *sbad == 2 ? 1 : (*sbad == 1 ? 2 : 0);   // root error takes precedence
         if (badcode && tid == 0 && rem == 0 && rt == 0 && !early_tree) report(prm.dev_status, badcode);
         const bool valid = badcode == 0;
-        int cur = 0;
-        if (v < kT) {
-            for (int w = 0; w < kW; ++w) anc[w * kT + v] = (v < T && (v >> 5) == w) ? (1u << (v & 31)) : 0u;
-            jmp[v] = (valid && v < T) ? pvv : -1;
-            for (int k = 0; k < nh; ++k) lam[k * kT + v] = dts[k * kT + v] * as[k];
+        const int cur = 0;   // Λ and jump pointers in one buffer (each round reads, barrier, then writes)
+        // NKB == 1 (128 nodes, 256 threads): thread (node t, half hh) handles the heads k ≡ hh (mod 2) and
+        // half of the ancestor words; NKB == 2: thread = node, all heads
+        constexpr int kSplit = NKB == 1 ? 2 : 1, kHS = kHPC / kSplit, kWS = kW / kSplit;
+        const int pv = NKB == 1 ? t : tid;             // prologue node
+        const int hsel = NKB == 1 ? hh : 0;
+        const bool pact = pv < kT;
+        float lv[kHS];       // Λ_v of this thread's heads k = m·kSplit + hsel, in registers
+#pragma unroll
+        for (int m = 0; m < kHS; ++m) {
+            const int k = m * kSplit + hsel;
+            lv[m] = (pact && k < nh) ? dts[k * kT + pv] * as[k] : 0.f;
+        }
+        if (pact) {
+#pragma unroll
+            for (int w2 = 0; w2 < kWS; ++w2) {
+                const int w = hsel * kWS + w2;
+                anc[w * kT + pv] = (pv < T && (pv >> 5) == w) ? (1u << (pv & 31)) : 0u;
+            }
+            if (hsel == 0) jmp[pv] = (valid && pv < T) ? pvv : -1;
+#pragma unroll
+            for (int m = 0; m < kHS; ++m) {
+                const int k = m * kSplit + hsel;
+                if (k < nh) lam[k * kT + pv] = lv[m];
+            }
         }
         mbar();
         for (int r = 0; r < 7 + NKB - 1; ++r) {
-            const int nx = cur ^ 1;
-            // ancestor sets: read row j of this round, barrier, then OR it in (no row is read while it is
-            // being written: race-free under compute-sanitizer racecheck)
-            uint32_t aj[kW];
-            const int j = v < kT ? jmp[cur * kT + v] : -1;
+            // read everything of jump target j for this round, barrier, then update this node (race-free
+            // under compute-sanitizer racecheck; all loads of a round in flight together)
+            uint32_t aj[kWS];
+            float lj[kHS];
+            const int j = pact ? jmp[pv] : -1;
 #pragma unroll
-            for (int w = 0; w < kW; ++w) aj[w] = j >= 0 ? anc[w * kT + j] : 0u;
-            mbar();
-            if (v < kT) {
+            for (int w2 = 0; w2 < kWS; ++w2) aj[w2] = j >= 0 ? anc[(hsel * kWS + w2) * kT + j] : 0u;
 #pragma unroll
-                for (int w = 0; w < kW; ++w) anc[w * kT + v] |= aj[w];
-                for (int k = 0; k < nh; ++k)
-                    lam[(nx * kHPC + k) * kT + v] =
-                        lam[(cur * kHPC + k) * kT + v] + (j >= 0 ? lam[(cur * kHPC + k) * kT + j] : 0.f);
-                jmp[nx * kT + v] = j >= 0 ? jmp[cur * kT + j] : -1;
+            for (int m = 0; m < kHS; ++m) {
+                const int k = m * kSplit + hsel;
+                lj[m] = (j >= 0 && k < nh) ? lam[k * kT + j] : 0.f;
             }
+            const int jj = j >= 0 ? jmp[j] : -1;
             mbar();
-            cur = nx;
+            if (pact) {
+#pragma unroll
+                for (int w2 = 0; w2 < kWS; ++w2) anc[(hsel * kWS + w2) * kT + pv] |= aj[w2];
+#pragma unroll
+                for (int m = 0; m < kHS; ++m) {
+                    const int k = m * kSplit + hsel;
+                    lv[m] += lj[m];
+                    if (k < nh) lam[k * kT + pv] = lv[m];
+                }
+                if (hsel == 0) jmp[pv] = jj;
+            }
+            // stop once no jump pointer is left (depth < 2^(r+1)): heap trees of 128 nodes need 3 rounds
+            if (!named_bar_or(1, 256, pact && hsel == 0 && jj >= 0)) break;
         }
         if (tid == 0) stamp(15);   // pointer jumping done
         // decay mode per head: factorised iff min Λ >= -64 over the tree (both factors within e^{±64});
-        // otherwise rebased per 32-key chunk (warp = chunk of keys 32w .. 32w+31): R_c = max Λ over the chunk,
+        // otherwise rebased per 32-key chunk (c = node / 32): R_c = max Λ over the chunk,
         // e^{Λi-Λj} = e^{Λi-R_c} · e^{R_c-Λj} with e^{R_c-Λj} <= e^{64} when the chunk's Λ range is <= 64
         // (the row factor may underflow only where the true weight is below e^{-64}); per-element
-        // exponentials remain only for heads with a chunk of wider range (stress inputs)
-        uint32_t okm = 0, rbm = 0;
+        // exponentials remain only for heads with a chunk of wider range (stress inputs).  All heads of the
+        // thread reduced together (independent shuffle chains).  The per-warp masks carry 1 for the heads
+        // the warp does not own, so the AND over the 8 warps is the tree's mask.
         float* rc = (float*)(sm + Sm::RC);
-        for (int k = 0; k < nh; ++k) {
-            bool ok = true;
-            float l = 0.f;
-            if (v < kT) {
-                l = lam[(cur * kHPC + k) * kT + v];
-                if (v < T && l < -64.f) ok = false;
-            }
-            const bool live = v < T && v < kT;
-            float mx = live ? l : -3.0e38f, mnv = live ? l : 3.0e38f;
+        const bool live = pv < T && pact;
+        float mx[kHS], mnv[kHS];
+        uint32_t badm = 0u, own = 0u;
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                mnv = fminf(mnv, __shfl_xor_sync(0xffffffffu, mnv, o));
+        for (int m = 0; m < kHS; ++m) {
+            const int k = m * kSplit + hsel;
+            mx[m] = live ? lv[m] : -3.0e38f;
+            mnv[m] = live ? lv[m] : 3.0e38f;
+            if (live && k < nh && lv[m] < -64.f) badm |= 1u << k;
+            if (k < nh) own |= 1u << k;
+        }
+#pragma unroll
+        for (int m = 0; m < kHS; ++m) {
+            mx[m] = warp_max_f32(mx[m]);
+            mnv[m] = warp_min_f32(mnv[m]);
+        }
+        const uint32_t okm = ~__reduce_or_sync(0xffffffffu, badm);
+        uint32_t rbm = ~own;
+#pragma unroll
+        for (int m = 0; m < kHS; ++m)
+            if (mx[m] - mnv[m] <= 64.f || mx[m] < -1.0e38f) rbm |= 1u << (m * kSplit + hsel);
+        if (lane == 0 && pact) {
+#pragma unroll
+            for (int m = 0; m < kHS; ++m) {
+                const int k = m * kSplit + hsel;
+                if (k < nh) rc[k * 8 + (pv >> 5)] = mx[m];
             }
-            const bool chunk_ok = mx - mnv <= 64.f || mx < -1.0e38f;   // (an empty chunk is fine)
-            ok = __all_sync(0xffffffffu, ok);
-            if (lane == 0 && warp < 8) rc[k * 8 + warp] = mx;
-            // both coefficient sets: whether the head factorises is known only once every warp has voted
-            if (v < kT) {
-                cj[k * kT + v] = live ? __expf(-l) * dts[k * kT + v] : 0.f;
-                ((float*)(sm + Sm::CR))[k * kT + v] = live ? __expf(fminf(mx - l, 64.f)) * dts[k * kT + v] : 0.f;
+        }
+        // both coefficient sets: whether the head factorises is known only once every warp has voted
+        if (pact) {
+#pragma unroll
+            for (int m = 0; m < kHS; ++m) {
+                const int k = m * kSplit + hsel;
+                if (k < nh) {
+                    const float dtv = dts[k * kT + pv];
+                    cj[k * kT + pv] = live ? __expf(-lv[m]) * dtv : 0.f;
+                    ((float*)(sm + Sm::CR))[k * kT + pv] = live ? __expf(fminf(mx[m] - lv[m], 64.f)) * dtv : 0.f;
+                }
             }
-            if (ok) okm |= 1u << k;
-            if (chunk_ok) rbm |= 1u << k;
         }
         if (lane == 0) {
             wok[warp] = okm;
