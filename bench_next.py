@@ -199,6 +199,8 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
     torch.cuda.synchronize()
     assert status.item() == 0, f"device status {status.item()}"
     out["c5_sweep"] = measure_c5()
+    k2b = out["c5_sweep"]["k2b_B16_T128"]
+    k2b["frac"] = k2b["GB/s"] / hbm_peak
     return out
 
 
@@ -208,6 +210,10 @@ def measure_c5():
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import sweep_c5
     from gen import trees
+    from paper_2505_14969_b200 import binding
+    # a stack of scan layers: no layer writes the next one's tree, dt, parameters or state (as sweep_c5.py)
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE |
+                                   binding.STREE_LAUNCH_EARLY_TREE | binding.STREE_LAUNCH_EARLY_DT)
     res = {}
     for T in (64, 128, 256):
         par = trees.heap_kary(T, 2)
@@ -217,6 +223,13 @@ def measure_c5():
         t_u, _ = sweep_c5.time_scan(np.stack([trees.chain(maxlen)] * len(paths)), L=16)
         res[f"heap2_T{T}"] = {"packed_us": t_p, "unrolled_us": t_u, "speedup_vs_unrolled": t_u / t_p,
                               "kernel": {1: "simt", 2: "tcgen05", 3: "tcgen05-128"}.get(k_p)}
+    # the 128-row kernel (K2b) at batch 16: HBM roofline of one scan call (state read once, x read, y written,
+    # B and C once per tree, dt, parent; 2.7B shape H=80 P=64 N=128 G=1)
+    B, T, H, P, N = 16, 128, 80, 64, 128
+    t16, k16 = sweep_c5.time_scan(np.stack([trees.heap_kary(T, 2)] * B), L=16)
+    nbytes = B * H * P * N * 4 + 2 * B * T * H * P * 2 + 2 * B * T * N * 2 + B * T * H * 4 + B * T * 4 + 2 * H * 4
+    res["k2b_B16_T128"] = {"us": t16, "bytes": nbytes, "GB/s": nbytes / t16 * 1e-3, "nodes_per_s": B * T / (t16 * 1e-6),
+                           "kernel": {1: "simt", 2: "tcgen05", 3: "tcgen05-128"}.get(k16), "bound": "hbm"}
     return res
 
 
