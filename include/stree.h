@@ -270,7 +270,8 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *                            accept kernel is followed by at least one other kernel — e.g. the next
  *                            iteration's stree_build_mask — before the first replay).  The replay
  *                            prologue (path validation, coefficients, staging) then runs before that
- *                            wait; every global write still follows it.  Only stree_replay_scan honours
+ *                            wait — with EARLY_STATE also the replay of the state tiles already in flight
+ *                            (on chip, in shared memory); every global write still follows it.  Only stree_replay_scan honours
  *                            this flag; stree_commit ignores it (its path normally comes from the accept
  *                            kernel just before it).  The replay also reads A under this promise.
  *  STREE_LAUNCH_EARLY_TREE   promise: the tree topology and the per-head parameters of a scan call

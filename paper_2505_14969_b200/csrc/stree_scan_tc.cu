@@ -231,8 +231,9 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
         }
     }
     named_bar(3, 128);
-    if (prm.early_replay) pdl_wait();   // global writes (status, committed state) follow the dependency
-    if (u == 0 && rinfo[1] && chunk == 0 && g == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+    // no global writes here: with EARLY_REPLAY (and EARLY_STATE) the whole replay of the state tiles already in
+    // flight runs before the dependency wait; the storer warp (after its wait) reports an invalid path and
+    // writes the committed state
     // r is read back from shared memory and broadcast, so every branch on it is provably warp-uniform
     // (no collective fix-up code around the shuffles below)
     const int r = __shfl_sync(0xffffffffu, rinfo[0], 0);
@@ -355,7 +356,7 @@ __device__ __forceinline__ void replay_updater(const Params& prm, unsigned char*
 // warps so they never stall on the store.
 template <int NS, bool R>
 __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* sm, uint32_t sb, const CUtensorMap* tm_h,
-                                             int b, int hbeg, int nh, uint32_t bar0) {
+                                             int b, int hbeg, int nh, uint32_t bar0, bool report_bad) {
     using S = Smem<NS, R>;
     constexpr int kSt = S::kSt;
     auto bar_empty = [&](int s) { return bar0 + 24 + 8 * kSt + 8 * s; };
@@ -363,10 +364,11 @@ __device__ __forceinline__ void state_storer(const Params& prm, unsigned char* s
     unsigned long long* trace = (kTrace && prm.trace) ? prm.trace + (size_t)blockIdx.x * kTraceWords : nullptr;
     const uint64_t pol = policy_evict_first();
     const int H = prm.H;
-    if (prm.early_replay) pdl_wait();   // stores follow the dependency wait
+    if (prm.early_replay) pdl_wait();   // stores (and the status report) follow the dependency wait
     for (int k = 0; k < nh; ++k) {
         const int s = k % kSt;
         mbar_wait(bar_upd(s), (k / kSt) & 1);
+        if (k == 0 && ((const int*)(sm + S::RINFO))[1] && report_bad) report(prm.dev_status, STREE_DEV_BAD_PATH);
         if (((const int*)(sm + S::RINFO))[0] > 0 || prm.store_always) {   // path length, published before bar_upd
 #pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
         tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h0); tma_prefetch(&tm_y);
         // the state of the first heads is streamed before the dependency wait (caller's promise)
         for (int k = 0; k < n_early; ++k) {
-            mbar_add_tx(bar_full(k), S::H0S);
+            mbar_expect_tx(bar_full(k), S::H0S);   // arrive now: the replay of this tile may start pre-wait
 #pragma unroll 1
             for (int a = 0; a < NS / 32; ++a)
                 tma_load_2d(sb + S::slot(k) + a * S::kSlotAtom, &tm_h0, bar_full(k), 32 * a,
@@ -505,8 +507,7 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
             for (int k = 0; k < nh; ++k) {
                 const int s = k % kStages;
                 const int h = hbeg + k;
-                if (k < n_early) {   // state already in flight: arrive
-                    mbar_expect_tx(bar_full(s), 0);
+                if (k < n_early) {   // state already in flight (arrived at issue)
                 } else {
                     mbar_wait(bar_empty(s), ((k / kStages) & 1) ^ 1);
                     if (trace && k < 32) trace[128 + k] = gtimer();   // state load k issued (slot released)
@@ -621,7 +622,8 @@ __global__ void __launch_bounds__(MODE ? kThreadsReplay : kThreadsScan, 1)
         }
     } else if (kReplay && warp == 10) {
         // fused: committed state in place (tm_h0); commit only: into h_new (tm_y)
-        if (lane == 0) state_storer<NS, kReplay>(prm, sm, sb, kScan ? &tm_h0 : &tm_y, b, hbeg, nh, bar0);
+        if (lane == 0) state_storer<NS, kReplay>(prm, sm, sb, kScan ? &tm_h0 : &tm_y, b, hbeg, nh, bar0,
+                                                 chunk == 0 && g == 0);
     } else if (kReplay && warp >= 6) {
         replay_updater<NS, kReplay>(prm, sm, sb, &tm_h0, b, g, chunk, hbeg, nh, bar0);
     } else {
@@ -1002,13 +1004,27 @@ bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
 }
 
 unsigned long long* g_trace = nullptr;
+int g_trace_ring = 0, g_trace_n = 0;   // ring mode: launch i writes slot i % g_trace_ring (1024 CTAs each)
+unsigned long long* trace_slot() {
+    if (!g_trace || !g_trace_ring) return g_trace;
+    return g_trace + (size_t)(g_trace_n++ % g_trace_ring) * 1024 * stree::tc::kTraceWords;
+}
 
 int num_sms() { return stree::host::num_sms(); }
 
 }  // namespace
 
 // Debug hook (not part of the ABI): per-CTA globaltimer phase stamps, 64 u64 per CTA.
-extern "C" void stree_debug_tc_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
+extern "C" void stree_debug_tc_trace(unsigned long long* dev_buf) {
+    g_trace = dev_buf;
+    g_trace_ring = 0;
+}
+// ring mode: launch i writes its stamps to dev_buf + (i % n) * 1024 * 256 (tools/trace_stack.py)
+extern "C" void stree_debug_tc_trace_ring(unsigned long long* dev_buf, int n) {
+    g_trace = dev_buf;
+    g_trace_ring = n;
+    g_trace_n = 0;
+}
 
 extern "C" int stree_tc_supports(const stree_dims* d) {
     if (!d) return 0;
@@ -1077,7 +1093,7 @@ int launch_tc(const stree_dims* d, const void* x, const float* dt, const float* 
     split_heads(B, H, G, &cpg, &hpc);
     stree::tc::Params prm{};
     if (rp) prm = *rp;
-    prm.trace = g_trace;
+    prm.trace = trace_slot();
     prm.B = B; prm.T = T; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc;
     prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.has_h0 = h0 != nullptr;
@@ -1188,7 +1204,7 @@ extern "C" int stree_launch_commit_tc(const stree_dims* d, const void* x, const 
     int cpg, hpc;
     split_heads(B, H, G, &cpg, &hpc);
     Params prm{};
-    prm.trace = g_trace;
+    prm.trace = trace_slot();
     prm.B = B; prm.T = d->n_nodes; prm.H = H; prm.G = G; prm.cpg = cpg; prm.hpc = hpc;
     prm.A = A; prm.dev_status = dev_status;
     prm.has_h0 = 1;
