@@ -4,8 +4,8 @@
 //   seq_i        = conv_state[b] (W-1 rows, oldest first) ++ u[b][root .. i]
 //   out[b][i][c] = act( bias[c] + sum_{w<W} weight[c][w] * seq_i[len - W + w][c] )
 //
-// HBM-bound (intensity ~W FLOP per 4 bytes).  One CTA per (tree, block of 32 16-byte channel
-// chunks): the tree's rows of that channel block (and the conv state) are read once, coalesced,
+// HBM-bound (intensity ~W FLOP per 4 bytes).  One CTA per (tree, block of 16 16-byte channel
+// chunks): the tree's rows of that channel block (and the conv state) are read once (cp.async),
 // into shared memory; every node then reads its W-1 ancestors from there (the ancestor chain is
 // walked in shared memory, stepping into the state rows above the root), and the output row is
 // written once, coalesced.
@@ -15,8 +15,11 @@
 namespace stree {
 namespace conv {
 
-constexpr int kThreads = 256;   // 8 warps: lane = channel chunk, warp = node (strided by 8)
-constexpr int kChunks = 32;     // 16-byte channel chunks per CTA
+constexpr int kChunks = 32;     // 16-byte channel chunks per conv-commit warp (lane = chunk)
+#ifndef STREE_CONV_KC
+#define STREE_CONV_KC 16
+#endif
+constexpr int kConvKC = STREE_CONV_KC;     // chunks per tree-conv CTA (tree_conv_kernel)
 
 template <typename IO>
 struct Pack;
@@ -53,137 +56,171 @@ struct Pack<float> {
     }
 };
 
-__host__ __device__ constexpr size_t tree_conv_smem(int T, int W) {
-    return (size_t)kMaxNodes * 4 + (size_t)((W - 1) + T) * kChunks * 16;
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-
-// SiLU: bf16 outputs take x·σ(x) with σ(x) = ½ tanh(x/2) + ½ (one MUFU op; tanh.approx's 2^-11 error is
-// far below the bf16 rounding of the output); fp32 outputs keep the exp + division form (the 1e-4 path)
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// packed fp32 pairs (FFMA2: two fused multiply-adds per instruction on sm_100a)
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// the 16-byte chunk as V/2 packed fp32 pairs (bf16: w << 16 is the low element, w & 0xffff0000 the high one)
 template <typename IO>
-__device__ __forceinline__ float silu(float z);
+__device__ __forceinline__ void unpack2(const uint4& v, uint64_t* p);
 template <>
-__device__ __forceinline__ float silu<__nv_bfloat16>(float z) {
-    float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
-    return z * fmaf(0.5f, t, 0.5f);
+__device__ __forceinline__ void unpack2<__nv_bfloat16>(const uint4& v, uint64_t* p) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) p[q] = f2pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xFFFF0000u));
 }
 template <>
-__device__ __forceinline__ float silu<float>(float z) { return __fdividef(z, 1.f + __expf(-z)); }
+__device__ __forceinline__ void unpack2<float>(const uint4& v, uint64_t* p) {
+    p[0] = f2pack(__uint_as_float(v.x), __uint_as_float(v.y));
+    p[1] = f2pack(__uint_as_float(v.z), __uint_as_float(v.w));
+}
 
-template <typename IO, int W>
-__global__ void __launch_bounds__(kThreads, 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
-                                                             const float* __restrict__ bias, const IO* __restrict__ state,
-                                                             const int32_t* __restrict__ parent, int act,
-                                                             IO* __restrict__ out, int T, int C, int32_t* dev_status) {
-    constexpr int V = Pack<IO>::V;
+__host__ __device__ constexpr size_t tree_conv_smem(int T, int W, int KC) {
+    return (size_t)kMaxNodes * 4 + (size_t)((W - 1) + T) * KC * 16;
+}
+
+// SiLU from h = z/2 (the kernel folds the exact factor 1/2 into the weights and bias): silu(z) = z·σ(z) =
+// h + h·tanh(h).  bf16 outputs: one MUFU op and one FMA (tanh.approx's 2^-11 error is far below the bf16
+// rounding of the output); fp32 outputs keep the exp + division form (the 1e-4 path)
+template <typename IO>
+__device__ __forceinline__ float silu_h(float h);
+template <>
+__device__ __forceinline__ float silu_h<__nv_bfloat16>(float h) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
+template <>
+__device__ __forceinline__ float silu_h<float>(float h) { return __fdividef(2.f * h, 1.f + __expf(-2.f * h)); }
+
+// One CTA per (tree, block of KC 16-byte channel chunks), 8·KC threads: thread = (chunk ch = tid % KC, node
+// slot ns = tid / KC); slot ns computes nodes ns, ns + 8, ...  KC = 16 (128 threads, 4.5 CTAs per SM at the
+// 2.7B shape) balances the SMs: with KC = 32 (336 CTAs) 40 SMs ran 3 CTAs and the rest 2.
+template <typename IO, int W, int KC>
+__global__ void __launch_bounds__(8 * KC, KC <= 8 ? 10 : KC <= 16 ? 5 : 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
+                                                                 const float* __restrict__ bias, const IO* __restrict__ state,
+                                                                 const int32_t* __restrict__ parent, int act,
+                                                                 IO* __restrict__ out, int T, int C, int32_t* dev_status) {
+    constexpr int V = Pack<IO>::V, NT = 8 * KC, kSlots = 8;
     extern __shared__ __align__(16) unsigned char sm[];
     int* sp = reinterpret_cast<int*>(sm);                                   // parent[T]
-    uint4* rows = reinterpret_cast<uint4*>(sm + kMaxNodes * 4);             // [(W-1) + T][kChunks]
+    unsigned char* rows = sm + kMaxNodes * 4;                               // [(W-1) + T][KC] 16-byte chunks
     __shared__ int s_bad;
-    const int b = blockIdx.y, c0 = blockIdx.x * kChunks * V;
-    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-    const bool cv = c0 + lane * V < C;                                     // this lane's chunk exists
+    const int b = blockIdx.y, c0 = blockIdx.x * KC * V;
+    const int tid = threadIdx.x, ch = tid % KC, ns = tid / KC;
+    const bool cv = c0 + ch * V < C;                                       // this thread's chunk exists
     if (tid == 0) s_bad = 0;
     // the block's weights and bias: coalesced loads issued together with the parent and staging loads below
-    // (one memory latency for all of them), then through shared memory, [w][v][lane] so the per-thread reads
+    // (one memory latency for all of them), then through shared memory, [w][v][chunk] so the per-thread reads
     // are conflict-free
-    __shared__ float s_w[4 * 8 * kChunks];
-    __shared__ float s_b[8 * kChunks];
+    __shared__ float s_w[4 * 8 * KC];
+    __shared__ float s_b[8 * KC];
     pdl_wait();
-    const int nc = min(kChunks * V, C - c0);   // channels of this block (nc * W <= 4 * kThreads)
+    const int nc = min(KC * V, C - c0);   // channels of this block (nc * W <= 4 * NT)
     float wv[4], bv;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const int k = tid + q * kThreads;
+        const int k = tid + q * NT;
         wv[q] = k < nc * W ? __ldg(weight + (size_t)c0 * W + k) : 0.f;
     }
     bv = (tid < nc && bias) ? __ldg(bias + c0 + tid) : 0.f;
-    for (int i = tid; i < T; i += kThreads) sp[i] = parent[(size_t)b * T + i];
-    // stage the state rows and the tree's rows of this channel block (one coalesced pass)
-    // batches of kBatch independent 16-byte loads per thread in flight (one latency per batch, not per
-    // row): addresses are clamped to valid rows so the loads are unconditional, zeros selected after
-    constexpr int kBatch = 9, kWy = kThreads / 32;   // 9 x 8 warps = 72 >= 3 + 64 rows: one batch at T = 64
+    for (int i = tid; i < T; i += NT) sp[i] = parent[(size_t)b * T + i];
+    // stage the state rows and the tree's rows of this channel block with cp.async (global -> shared, no
+    // register round trip); missing state rows and absent chunks are zero-filled (source size 0)
     const int nrows = (W - 1) + T;
-    const size_t cofs = (size_t)c0 + (cv ? lane * V : 0);
-    for (int r0 = wy; r0 < nrows; r0 += kWy * kBatch) {
-        uint4 v[kBatch];
-#pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
-            const int r = min(r0 + kWy * k, nrows - 1);
-            const IO* src = (r < W - 1) ? (state ? state + ((size_t)b * (W - 1) + r) * C : u + (size_t)b * T * C)
-                                        : u + ((size_t)b * T + (r - (W - 1))) * C;
-            v[k] = __ldg(reinterpret_cast<const uint4*>(src + cofs));
-        }
-#pragma unroll
-        for (int k = 0; k < kBatch; ++k) {
-            const int r = r0 + kWy * k;
-            const bool zero = !cv || (r < W - 1 && !state);
-            if (r < nrows) rows[r * kChunks + lane] = zero ? make_uint4(0, 0, 0, 0) : v[k];
-        }
+    const size_t cofs = (size_t)c0 + (cv ? ch * V : 0);
+    const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(rows) + ch * 16;
+    for (int r = ns; r < nrows; r += kSlots) {
+        const bool st = r < W - 1;
+        const IO* src = st ? (state ? state + ((size_t)b * (W - 1) + r) * C : u) : u + ((size_t)b * T + (r - (W - 1))) * C;
+        cp_async16(rbase + r * KC * 16, src + cofs, (!cv || (st && !state)) ? 0u : 16u);
     }
+    cp_async_commit();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const int k = tid + q * kThreads;
+        const int k = tid + q * NT;
         if (k < nc * W) {
             const int cl = k / W, w = k % W;
-            s_w[(w * V + cl % V) * kChunks + cl / V] = wv[q];
+            s_w[(w * V + cl % V) * KC + cl / V] = wv[q];
         }
     }
-    if (tid < nc) s_b[(tid % V) * kChunks + tid / V] = bv;
+    if (tid < nc) s_b[(tid % V) * KC + tid / V] = bv;
     __syncthreads();
-    float wt[W][V], bs[V];
+    // weights / bias as packed pairs; with the activation they carry the factor 1/2 of silu_h
+    const float hs = act ? 0.5f : 1.f;
+    uint64_t wt2[W][V / 2], bs2[V / 2];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
+    for (int q = 0; q < V / 2; ++q) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) wt[w][v] = cv ? s_w[(w * V + v) * kChunks + lane] : 0.f;
-        bs[v] = cv ? s_b[v * kChunks + lane] : 0.f;
+        for (int w = 0; w < W; ++w)
+            wt2[w][q] = cv ? f2pack(hs * s_w[(w * V + 2 * q) * KC + ch], hs * s_w[(w * V + 2 * q + 1) * KC + ch])
+                           : f2pack(0.f, 0.f);
+        bs2[q] = cv ? f2pack(hs * s_b[2 * q * KC + ch], hs * s_b[(2 * q + 1) * KC + ch]) : f2pack(0.f, 0.f);
     }
     // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i (root error takes precedence); the same
-    // pass tabulates every node's window rows (oldest first: ancestors at distance W-1 .. 1, then the node;
-    // above the root the chain continues into the state rows W-2, W-3, ...) so the main loop's shared-memory
-    // loads are independent
+    // pass tabulates every node's window rows as byte offsets (oldest first: ancestors at distance W-1 .. 1,
+    // then the node; above the root the chain continues into the state rows W-2, W-3, ...) so the main
+    // loop's shared-memory loads are independent
     __shared__ int s_win[kMaxNodes * 4];
-    for (int i = tid; i < T; i += kThreads) {
+    for (int i = tid; i < T; i += NT) {
         const int p = sp[i];
         if (i == 0 ? p != -1 : (p < 0 || p >= i)) atomicMax(&s_bad, i == 0 ? 2 : 1);
         int v = i, srow = W - 1;
-        s_win[i * W + W - 1] = (W - 1) + i;
+        s_win[i * W + W - 1] = ((W - 1) + i) * KC * 16;
 #pragma unroll
         for (int k = 1; k < W; ++k) {
             if (v >= 0) {
                 const int pv = sp[v];
                 v = (pv >= 0 && pv < v) ? pv : -1;
             }
-            s_win[i * W + W - 1 - k] = v >= 0 ? (W - 1) + v : --srow;
+            s_win[i * W + W - 1 - k] = (v >= 0 ? (W - 1) + v : --srow) * KC * 16;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     const int bad = s_bad;
     if (bad && tid == 0 && blockIdx.x == 0) report(dev_status, bad == 2 ? 1 : 2);
+    const unsigned char* rl = rows + ch * 16;   // this thread's chunk of every row
 #pragma unroll 2
-    for (int i = wy; i < T; i += kThreads / 32) {
-        int rw[W];
+    for (int i = ns; i < T; i += kSlots) {
+        int ro[W];
 #pragma unroll
-        for (int k = 0; k < W; ++k) rw[k] = s_win[i * W + k];
-        float z[V];
+        for (int k = 0; k < W; ++k) ro[k] = s_win[i * W + k];
+        uint64_t z2[V / 2];
 #pragma unroll
-        for (int q = 0; q < V; ++q) z[q] = bs[q];
+        for (int q = 0; q < V / 2; ++q) z2[q] = bs2[q];
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            float f[V];
-            Pack<IO>::unpack(rows[rw[w] * kChunks + lane], f);
+            uint64_t f2[V / 2];
+            unpack2<IO>(*reinterpret_cast<const uint4*>(rl + ro[w]), f2);
 #pragma unroll
-            for (int q = 0; q < V; ++q) z[q] = fmaf(wt[w][q], f[q], z[q]);
+            for (int q = 0; q < V / 2; ++q) z2[q] = ffma2(wt2[w][q], f2[q], z2[q]);
         }
+        float z[V];
+#pragma unroll
+        for (int q = 0; q < V / 2; ++q) f2unpack(z2[q], z[2 * q], z[2 * q + 1]);
         if (act) {
 #pragma unroll
-            for (int q = 0; q < V; ++q) z[q] = silu<IO>(z[q]);
+            for (int q = 0; q < V; ++q) z[q] = silu_h<IO>(z[q]);
         }
         if (bad) {
 #pragma unroll
             for (int q = 0; q < V; ++q) z[q] = 0.f;
         }
-        if (cv) *reinterpret_cast<uint4*>(out + ((size_t)b * T + i) * C + c0 + lane * V) = Pack<IO>::pack(z);
+        if (cv) *reinterpret_cast<uint4*>(out + ((size_t)b * T + i) * C + c0 + ch * V) = Pack<IO>::pack(z);
     }
 }
 
@@ -241,17 +278,17 @@ template <typename IO, int W>
 cudaError_t launch_conv(const stree_conv_dims* d, const void* u, const float* weight, const float* bias,
                         const void* state, const int32_t* parent, int act, void* out, int32_t* dev_status,
                         cudaStream_t s) {
-    constexpr int V = Pack<IO>::V;
+    constexpr int V = Pack<IO>::V, KC = kConvKC;
     const int C = d->channels, T = d->n_nodes;
-    dim3 grid((C / V + kChunks - 1) / kChunks, d->batch);
-    const size_t smem = tree_conv_smem(T, W);
-    auto k = tree_conv_kernel<IO, W>;
-    // one wave at the 2.7B shape (336 CTAs over 148 SMs needs 3 resident per SM): registers capped by the
-    // launch bounds, shared-memory carveout at its maximum
+    dim3 grid((C / V + KC - 1) / KC, d->batch);
+    const size_t smem = tree_conv_smem(T, W, KC);
+    auto k = tree_conv_kernel<IO, W, KC>;
+    // every CTA of the 2.7B shape resident at once (672 CTAs, <= 5 per SM): registers capped by the launch
+    // bounds, shared-memory carveout at its maximum
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    return launch_k(k, grid, dim3(kThreads), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent, act,
+    return launch_k(k, grid, dim3(8 * KC), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent, act,
                     (IO*)out, T, C, dev_status);
 }
 
