@@ -109,12 +109,13 @@ __device__ __forceinline__ float silu_h<float>(float h) { return __fdividef(2.f 
 // One CTA per (tree, block of KC 16-byte channel chunks), 8·KC threads: thread = (chunk ch = tid % KC, node
 // slot ns = tid / KC); slot ns computes nodes ns, ns + 8, ...  KC = 16 (128 threads, 4.5 CTAs per SM at the
 // 2.7B shape) balances the SMs: with KC = 32 (336 CTAs) 40 SMs ran 3 CTAs and the rest 2.
-template <typename IO, int W, int KC>
+template <typename IO, int W, int KC, bool ACT>
 __global__ void __launch_bounds__(8 * KC, KC <= 8 ? 10 : KC <= 16 ? 5 : 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
                                                                  const float* __restrict__ bias, const IO* __restrict__ state,
-                                                                 const int32_t* __restrict__ parent, int act,
+                                                                 const int32_t* __restrict__ parent,
                                                                  IO* __restrict__ out, int T, int C, int32_t* dev_status) {
     constexpr int V = Pack<IO>::V, NT = 8 * KC, kSlots = 8;
+    static_assert(W <= 4, "window");
     extern __shared__ __align__(16) unsigned char sm[];
     int* sp = reinterpret_cast<int*>(sm);                                   // parent[T]
     unsigned char* rows = sm + kMaxNodes * 4;                               // [(W-1) + T][KC] 16-byte chunks
@@ -123,96 +124,96 @@ __global__ void __launch_bounds__(8 * KC, KC <= 8 ? 10 : KC <= 16 ? 5 : 3) tree_
     const int tid = threadIdx.x, ch = tid % KC, ns = tid / KC;
     const bool cv = c0 + ch * V < C;                                       // this thread's chunk exists
     if (tid == 0) s_bad = 0;
-    // the block's weights and bias: coalesced loads issued together with the parent and staging loads below
-    // (one memory latency for all of them), then through shared memory, [w][v][chunk] so the per-thread reads
-    // are conflict-free
+    // the block's weights and bias (with ACT pre-scaled by the 1/2 of silu_h; zero for absent channels):
+    // coalesced loads issued together with the parent and staging loads below (one memory latency for all
+    // of them), then through shared memory, [w][v][chunk] so the per-thread reads are conflict-free
     __shared__ float s_w[4 * 8 * KC];
     __shared__ float s_b[8 * KC];
+    __shared__ __align__(16) int s_win[kMaxNodes * 4];   // per node: byte offsets of its W window rows
+    constexpr float hs = ACT ? 0.5f : 1.f;
     pdl_wait();
     const int nc = min(KC * V, C - c0);   // channels of this block (nc * W <= 4 * NT)
     float wv[4], bv;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int k = tid + q * NT;
-        wv[q] = k < nc * W ? __ldg(weight + (size_t)c0 * W + k) : 0.f;
+        wv[q] = k < nc * W ? hs * __ldg(weight + (size_t)c0 * W + k) : 0.f;
     }
-    bv = (tid < nc && bias) ? __ldg(bias + c0 + tid) : 0.f;
+    bv = (tid < nc && bias) ? hs * __ldg(bias + c0 + tid) : 0.f;
     for (int i = tid; i < T; i += NT) sp[i] = parent[(size_t)b * T + i];
     // stage the state rows and the tree's rows of this channel block with cp.async (global -> shared, no
     // register round trip); missing state rows and absent chunks are zero-filled (source size 0)
-    const int nrows = (W - 1) + T;
-    const size_t cofs = (size_t)c0 + (cv ? ch * V : 0);
-    const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(rows) + ch * 16;
-    for (int r = ns; r < nrows; r += kSlots) {
-        const bool st = r < W - 1;
-        const IO* src = st ? (state ? state + ((size_t)b * (W - 1) + r) * C : u) : u + ((size_t)b * T + (r - (W - 1))) * C;
-        cp_async16(rbase + r * KC * 16, src + cofs, (!cv || (st && !state)) ? 0u : 16u);
+    {
+        const uint32_t cbytes = cv ? 16u : 0u;
+        const size_t cofs = (size_t)c0 + (cv ? ch * V : 0);
+        const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(rows) + ch * 16;
+        if (ns < W - 1)
+            cp_async16(rbase + ns * KC * 16, (state ? state + ((size_t)b * (W - 1) + ns) * C : u) + cofs,
+                       state ? cbytes : 0u);
+        const IO* src = u + ((size_t)b * T + ns) * C + cofs;
+        uint32_t dst = rbase + ((W - 1) + ns) * KC * 16;
+        for (int n = ns; n < T; n += kSlots, src += (size_t)kSlots * C, dst += kSlots * KC * 16) cp_async16(dst, src, cbytes);
     }
     cp_async_commit();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int k = tid + q * NT;
-        if (k < nc * W) {
+        if (k < KC * V * W) {
             const int cl = k / W, w = k % W;
             s_w[(w * V + cl % V) * KC + cl / V] = wv[q];
         }
     }
-    if (tid < nc) s_b[(tid % V) * KC + tid / V] = bv;
-    __syncthreads();
-    // weights / bias as packed pairs; with the activation they carry the factor 1/2 of silu_h
-    const float hs = act ? 0.5f : 1.f;
-    uint64_t wt2[W][V / 2], bs2[V / 2];
-#pragma unroll
-    for (int q = 0; q < V / 2; ++q) {
-#pragma unroll
-        for (int w = 0; w < W; ++w)
-            wt2[w][q] = cv ? f2pack(hs * s_w[(w * V + 2 * q) * KC + ch], hs * s_w[(w * V + 2 * q + 1) * KC + ch])
-                           : f2pack(0.f, 0.f);
-        bs2[q] = cv ? f2pack(hs * s_b[2 * q * KC + ch], hs * s_b[(2 * q + 1) * KC + ch]) : f2pack(0.f, 0.f);
-    }
+    if (tid < KC * V) s_b[(tid % V) * KC + tid / V] = bv;
     // PAPER.md:90 precondition: parent[0] = -1, 0 <= parent[i] < i (root error takes precedence); the same
     // pass tabulates every node's window rows as byte offsets (oldest first: ancestors at distance W-1 .. 1,
     // then the node; above the root the chain continues into the state rows W-2, W-3, ...) so the main
     // loop's shared-memory loads are independent
-    __shared__ int s_win[kMaxNodes * 4];
+    __syncthreads();
     for (int i = tid; i < T; i += NT) {
         const int p = sp[i];
         if (i == 0 ? p != -1 : (p < 0 || p >= i)) atomicMax(&s_bad, i == 0 ? 2 : 1);
         int v = i, srow = W - 1;
-        s_win[i * W + W - 1] = ((W - 1) + i) * KC * 16;
+        s_win[i * 4 + W - 1] = ((W - 1) + i) * KC * 16;
 #pragma unroll
         for (int k = 1; k < W; ++k) {
             if (v >= 0) {
                 const int pv = sp[v];
                 v = (pv >= 0 && pv < v) ? pv : -1;
             }
-            s_win[i * W + W - 1 - k] = (v >= 0 ? (W - 1) + v : --srow) * KC * 16;
+            s_win[i * 4 + W - 1 - k] = (v >= 0 ? (W - 1) + v : --srow) * KC * 16;
         }
+    }
+    uint64_t wt2[W][V / 2], bs2[V / 2];
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) wt2[w][q] = f2pack(s_w[(w * V + 2 * q) * KC + ch], s_w[(w * V + 2 * q + 1) * KC + ch]);
+        bs2[q] = f2pack(s_b[2 * q * KC + ch], s_b[(2 * q + 1) * KC + ch]);
     }
     cp_async_wait_all();
     __syncthreads();
     const int bad = s_bad;
     if (bad && tid == 0 && blockIdx.x == 0) report(dev_status, bad == 2 ? 1 : 2);
     const unsigned char* rl = rows + ch * 16;   // this thread's chunk of every row
+    IO* op = out + ((size_t)b * T + ns) * C + c0 + ch * V;
 #pragma unroll 2
-    for (int i = ns; i < T; i += kSlots) {
-        int ro[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) ro[k] = s_win[i * W + k];
+    for (int i = ns; i < T; i += kSlots, op += (size_t)kSlots * C) {
+        const int4 ro = *reinterpret_cast<const int4*>(s_win + i * 4);
+        const int rw[4] = {ro.x, ro.y, ro.z, ro.w};
         uint64_t z2[V / 2];
 #pragma unroll
         for (int q = 0; q < V / 2; ++q) z2[q] = bs2[q];
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             uint64_t f2[V / 2];
-            unpack2<IO>(*reinterpret_cast<const uint4*>(rl + ro[w]), f2);
+            unpack2<IO>(*reinterpret_cast<const uint4*>(rl + rw[w]), f2);
 #pragma unroll
             for (int q = 0; q < V / 2; ++q) z2[q] = ffma2(wt2[w][q], f2[q], z2[q]);
         }
         float z[V];
 #pragma unroll
         for (int q = 0; q < V / 2; ++q) f2unpack(z2[q], z[2 * q], z[2 * q + 1]);
-        if (act) {
+        if (ACT) {
 #pragma unroll
             for (int q = 0; q < V; ++q) z[q] = silu_h<IO>(z[q]);
         }
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(8 * KC, KC <= 8 ? 10 : KC <= 16 ? 5 : 3) tree_
 #pragma unroll
             for (int q = 0; q < V; ++q) z[q] = 0.f;
         }
-        if (cv) *reinterpret_cast<uint4*>(out + ((size_t)b * T + i) * C + c0 + ch * V) = Pack<IO>::pack(z);
+        if (cv) *reinterpret_cast<uint4*>(op) = Pack<IO>::pack(z);
     }
 }
 
@@ -282,13 +283,13 @@ cudaError_t launch_conv(const stree_conv_dims* d, const void* u, const float* we
     const int C = d->channels, T = d->n_nodes;
     dim3 grid((C / V + KC - 1) / KC, d->batch);
     const size_t smem = tree_conv_smem(T, W, KC);
-    auto k = tree_conv_kernel<IO, W, KC>;
+    auto k = act ? tree_conv_kernel<IO, W, KC, true> : tree_conv_kernel<IO, W, KC, false>;
     // every CTA of the 2.7B shape resident at once (672 CTAs, <= 5 per SM): registers capped by the launch
     // bounds, shared-memory carveout at its maximum
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    return launch_k(k, grid, dim3(8 * KC), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent, act,
+    return launch_k(k, grid, dim3(8 * KC), smem, s, (const IO*)u, weight, bias, (const IO*)state, parent,
                     (IO*)out, T, C, dev_status);
 }
 
