@@ -31,15 +31,19 @@ def check(name, err, tol):
         raise SystemExit(f"{name}: rel-err {err} > {tol}")
 
 
-def scan_case(name, prob, tol, impl=binding.STREE_SCAN_AUTO):
+def scan_case(name, prob, tol, impl=binding.STREE_SCAN_AUTO, flags=binding.STREE_LAUNCH_PDL, h0=True):
     binding.stree_set_scan_impl(impl)
+    binding.stree_set_launch_flags(flags)
     try:
         t = api.upload(prob)
+        if not h0:
+            t["h0"] = None
         st = torch.zeros(1, dtype=torch.int32, device="cuda")
         y = api.tree_scan(t, st)
         torch.cuda.synchronize()
     finally:
         binding.stree_set_scan_impl(binding.STREE_SCAN_AUTO)
+        binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
     ry, _ = oracle.scan_problem(prob)
     assert st.item() == 0
     check(name, rel(y.float().cpu().numpy(), ry), tol)
@@ -108,6 +112,13 @@ def main():
     # K2b: a 256-node chain (two 128-row tiles, direct decay)
     d5 = inputs.Dims(1, 256, 8, 64, 128, 1, "bf16")
     scan_case("scan T256 chain (tcgen05 128-row)", inputs.make_problem(d5, trees.chain(256)[None], seed=9), 2e-2)
+    # K2b one tile (T <= 128): factorised, rebased and direct heads in one CTA; every EARLY promise; no h0
+    d6 = inputs.Dims(2, 112, 12, 64, 128, 1, "bf16")
+    p6 = inputs.make_problem(d6, np.stack([trees.heap_kary(112, 2), trees.chain(112)]), seed=13, dt_range=(0.2, 1.0),
+                             A_range=(0.05, 16.0))
+    scan_case("scan T112 mixed decay (128-row, early)", p6, 2e-2, flags=all_flags)
+    p7 = inputs.make_problem(d6, p6.parent, seed=14, dt_range=(0.2, 1.0), A_range=(0.05, 16.0), h0_zero=True)
+    scan_case("scan T112 mixed decay (128-row, no h0)", p7, 2e-2, h0=False)
     # fused replay + scan: small-batch and pipeline kernels, every EARLY promise
     replay_case("replay_scan B2 H16 (small-batch)", 2, 48, 40, 16, all_flags)
     replay_case("replay_scan B16 H8 (pipeline)", 16, 64, 64, 8, all_flags, binding.STREE_SCAN_TC_PIPELINE)
