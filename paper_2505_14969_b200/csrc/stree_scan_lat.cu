@@ -18,19 +18,23 @@
 // Everything that does not depend on the preceding kernel runs before the wait, and the chain after it is
 // one DRAM latency plus the tensor-core work:
 //  * ≈ 105 KB of shared memory and 256 TMEM columns per CTA: two CTAs fit on an SM, so under PDL the next
-//    layer's CTAs are resident while this layer runs;
-//  * before the wait: barriers, TMEM, the state tile (STREE_LAUNCH_EARLY_STATE), the whole activation
-//    replay of the previous path (STREE_LAUNCH_EARLY_REPLAY; its operands gathered with cp.async, one DRAM
-//    latency after the path) and the hi/lo split of the state, and the tree topology — validation,
-//    ancestor bits, and the jump pointers of every pointer-jumping round — plus A_h, D_h
-//    (STREE_LAUNCH_EARLY_TREE);
-//  * after the wait: C, B, x by TMA and dt by the row warps, all in flight together; G = C·Bᵀ and then
-//    Y0 are issued the moment C, B land; the segsum Λ replays the recorded jump pointers (6 shuffle
-//    rounds); four warps (two per TMEM lane quadrant of the 64 node rows, on key-column halves) build the
-//    masked weights straight into TMEM (no shared memory, no proxy fence) for a TS-form Y'; the same warps
-//    write y from registers (64 contiguous bytes per thread).
-// Warps: 0, 1, 4, 5 row warps (tree, Λ, masked weights, epilogue); 2, 3, 6, 7 aux (replay, state split);
-// 8 TMA producer + MMA issuer (its own warp: the replay of the fused variant must never delay the MMAs).
+//    layer's CTAs are resident while this layer runs (grids of at most #SMs/2 CTAs take one SM each, so the
+//    next layer lands on other SMs);
+//  * at entry, before any barrier: the state tile by TMA (STREE_LAUNCH_EARLY_STATE), the tree operands
+//    (parent, A_h, D_h, dt: EARLY_TREE / EARLY_DT) and the previous tree's accepted path (EARLY_REPLAY) —
+//    one DRAM latency for all of them;
+//  * before the wait, on the aux warps (SM sub-partitions 2, 3, so that the next layer's pre-wait work,
+//    co-resident on the SM, stays off the sub-partitions of this layer's row warps): tree validation, ancestor
+//    bits and the pointer-jumping segsum (warp 3, published to the row warps through shared memory), the
+//    replay prologue (path validation, coefficients, operands gathered with cp.async); then, on all eight
+//    warps, the activation replay of the state tile (packed FFMA2) and its hi/lo split;
+//  * after the wait: C, B, x by TMA (dt too when not read early), all in flight together; G = C·Bᵀ and then
+//    Y0 are issued the moment C, B land; four row warps (two per TMEM lane quadrant of the 64 node rows, on
+//    key-column halves) build the masked weights straight into TMEM (no shared memory, no proxy fence) for a
+//    TS-form Y'; the same warps write y from registers (64 contiguous bytes per thread); the aux warps store
+//    the committed state tile (TMA, in place).
+// Warps: 0, 1, 4, 5 row warps (masked weights, epilogue); 2, 3, 6, 7 aux (tree, replay, state); 8 TMA producer
+// + MMA issuer (its own warp: the replay of the fused variant must never delay the MMAs).
 // Accumulator rows 64-127 are never read (M = 128 MMAs, T ≤ 64 rows).
 //
 // Served: bf16 io, P = 64, N in {64, 128}, 1 <= T <= 64 (the launcher picks this kernel when B·H ≤ #SMs).
@@ -74,9 +78,10 @@ struct Lay {
     static constexpr int H0 = HL + kCbAtoms * 2 * kAtom;      // state tile: atom a = columns [32a, 32a+32), fp32
     static constexpr int X = H0 + (NS / 32) * kAtom;          // x tile (64 rows of 64 bf16)
     static constexpr int DT = X + kAtom;                      // dt of heads (h & ~3) .. +3, T rows of 16 B (TMA)
-    static constexpr int CJ = DT + 64 * 16;                   // float [4 row warps][64]  c_j
-    static constexpr int LM = CJ + 4 * 64 * 4;                // float [4 row warps][64]  Λ_j (direct decay)
-    static constexpr int MODE = LM + 4 * 64 * 4;              // int
+    static constexpr int CJ = DT + 64 * 16;                   // float [64]  c_j (factorised) / dt_j (direct)
+    static constexpr int LM = CJ + 64 * 4;                    // float [64]  Λ_j
+    static constexpr int BITS = LM + 64 * 4;                  // u64 [64]    ancestor row of node i
+    static constexpr int MODE = BITS + 64 * 8;                // int [4]: decay mode, bad-tree code, D_h (bits)
     static constexpr int RPATH = MODE + 16;                   // int [kMaxNodes]
     static constexpr int RINFO = RPATH + (R ? kMaxNodes * 4 : 0);   // int [2]: r (0 = nothing), bad path
     static constexpr int RCOEF = RINFO + 16;                  // float [kRStage]
@@ -96,6 +101,7 @@ struct Params {
     const float* A;
     const float* D;
     const int32_t* parent;
+    const float* h0p;            // the state [B][H][P][N] (read by the threads into registers)
     __nv_bfloat16* y;
     int32_t* dev_status;
     int has_h0, early_state, early_replay, early_tree;
@@ -123,6 +129,24 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t pk2(float2 v) { return ((uint64_t)__float_as_uint(v.y) << 32) | __float_as_uint(v.x); }
+__device__ __forceinline__ float2 upk2(uint64_t d) { return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32))); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {   // packed FFMA2
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(d);
 }
 
 // Masked weights of one row warp (node row i = its TMEM lane, key columns [c0, c0 + 32)):
@@ -179,19 +203,63 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (kTrace && trace) trace[k] = gtimer();
     };
     if (tid == 0) stamp(0);
-
-    // ---- setup that touches no argument memory (overlaps the previous kernel under PDL) ----
-    if (tid == 0) {
-        mbar_init(BAR_CB, 1);
-        mbar_init(BAR_X, 1);
-        mbar_init(BAR_H, 1);
-        mbar_init(BAR_HS, 1);
-        mbar_init(BAR_G, 1);
-        mbar_init(BAR_M, 4);
-        mbar_init(BAR_ACC, 1);
-        fence_barrier_init();
+    if (kTrace && trace && tid == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trace[31] = smid;
     }
+
+    // ---- operands of the pre-wait work, loaded at entry (one DRAM latency for all of them, under the caller's
+    //      promises): tree warp 3 (lane: nodes lane, lane + 32): parent, A_h, D_h and, under EARLY_DT, raw dt;
+    //      aux warps (u = 0..127): the previous tree's accepted path and its length.  The state tile comes by
+    //      TMA (issuer, below). ----
+    const bool row_warp = warp < 8 && (warp & 2) == 0;   // 0, 1, 4, 5: TMEM lanes 0-63 (SM sub-partitions 0, 1)
+    const bool tree_warp = warp == 3;
+    const bool early_lambda = prm.early_tree && prm.early_dt;
+    int tpar[2] = {-1, -1};
+    float tA = 0.f, tD = 0.f, tdt[2] = {0.f, 0.f};
+    auto load_tree = [&](bool with_dt) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const int i = lane + 32 * hf;
+            tpar[hf] = i < T ? prm.parent[(size_t)b * T + i] : -1;
+            if (with_dt) tdt[hf] = i < T ? prm.dt[((size_t)b * T + i) * H + h] : 0.f;
+        }
+        tA = prm.A[h];
+        tD = prm.D ? prm.D[h] : 0.f;
+    };
+    if (tree_warp && prm.early_tree) load_tree(early_lambda);   // EARLY_TREE (+ EARLY_DT)
+    int rp_len = 0, rp0 = 0, rp1 = 0;
+    const int u = 32 * ((warp & 1) + 2 * (warp >> 2)) + lane;   // aux warps 2, 3, 6, 7 -> 0..127
+    auto load_path = [&]() {
+        rp_len = prm.path_len[b];
+        rp0 = u < prm.Tp ? prm.path[(size_t)b * prm.Tp + u] : 0;
+        rp1 = u + 128 < prm.Tp ? prm.path[(size_t)b * prm.Tp + u + 128] : 0;
+    };
+    if (R && warp < 8 && !row_warp && prm.early_replay) load_path();   // EARLY_REPLAY
+
+    // ---- setup (overlaps the previous kernel under PDL): the issuer initialises the barriers and, under
+    //      STREE_LAUNCH_EARLY_STATE, starts the state stream at once (the longest pre-wait chain: 32 KB,
+    //      then the replay update and the hi/lo split) ----
     if (warp == kIssW) {
+        if (lane == 0) {
+            mbar_init(BAR_CB, 1);
+            mbar_init(BAR_X, 1);
+            mbar_init(BAR_H, 1);
+            mbar_init(BAR_HS, 1);
+            mbar_init(BAR_G, 1);
+            mbar_init(BAR_M, 4);
+            mbar_init(BAR_ACC, 1);
+            fence_barrier_init();
+            fence_proxy_async();
+            if (early_h) {   // caller's promise: the state is not written by the preceding kernel
+                mbar_expect_tx(BAR_H, NS * kP * 4);
+#pragma unroll 1
+                for (int a = 0; a < NS / 32; ++a)
+                    tma_load_2d(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP);
+            }
+        }
+        __syncwarp();
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sb + L::TMEMP),
                      "r"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -205,58 +273,39 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + L::TMEMP);
-    const bool row_warp = warp < 8 && (warp & 2) == 0;   // 0, 1, 4, 5
 
-    if (warp == kIssW && lane == 0) {   // state stream first: the replay (aux warps) waits on it
-        tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x); tma_prefetch(&tm_h);
+    if (warp == kIssW && lane == 0) {
+        tma_prefetch(&tm_c); tma_prefetch(&tm_b); tma_prefetch(&tm_x);
         if (prm.dt_tma) tma_prefetch(&tm_dt);
-        if (early_h) {   // caller's promise: the state is not written by the preceding kernel
-            mbar_expect_tx(BAR_H, NS * kP * 4);
-#pragma unroll 1
-            for (int a = 0; a < NS / 32; ++a)
-                tma_load_2d(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP);
-        }
         stamp(1);
     }
+    float* cjs = reinterpret_cast<float*>(sm + L::CJ);
+    float* lms = reinterpret_cast<float*>(sm + L::LM);
+    uint64_t* tbits = reinterpret_cast<uint64_t*>(sm + L::BITS);
+    volatile int* tinfo = reinterpret_cast<volatile int*>(sm + L::MODE);
+    constexpr int kBarTree = 5;   // named barrier: tree warp publishes (arrive), row warps consume (sync)
     if (warp < 8) {
-        // ================= warps 0-7: row warps 0, 1, 4, 5 (TMEM lane quadrant qd = node rows 32 qd + lane,
-        // column half ch) and aux warps 2, 3, 6, 7 (u = 0..127)
-        const bool rowr = row_warp;
-        const int qd = warp & 1, ch = warp >> 2, wi = qd + 2 * ch;
-        const int u = 32 * ((warp & 1) + 2 * (warp >> 2)) + lane;
-        bool waited = false, loaded = false;
-        // without STREE_LAUNCH_EARLY_STATE the state is streamed after the dependency wait (aux warp 7)
-        auto wait_and_load_state = [&]() {
+        // ================= warps 0-7.  Aux warps 2, 3, 6, 7 (u = 0..127): tree topology + segsum (warp 3) and the
+        // replay prologue; all eight: the state update and hi/lo split (before the dependency wait under the
+        // promises); then the aux warps store the committed state while the row warps 0, 1, 4, 5 (TMEM lanes
+        // 0-63) build the masked weights and run the epilogue
+        bool waited = false;
+        auto wait_dep = [&]() {
             if (!waited) { pdl_wait(); waited = true; }
-            if (prm.has_h0 && !early_h && !loaded && warp == 7 && lane == 0) {
-                mbar_expect_tx(BAR_H, NS * kP * 4);
-#pragma unroll 1
-                for (int a = 0; a < NS / 32; ++a)
-                    tma_load_2d_ef(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP, policy_evict_first());
-            }
-            loaded = true;
         };
-        // ---- tree topology (PAPER.md:90 precondition; ancestor rows PAPER.md:63-66): lane holds nodes lane
-        //      and lane + 32; pointer jumping, the jump pointer of every round recorded for the segsum ----
-        bool root_bad = false, par_bad = false;
-        uint64_t bits = 0ull;                  // ancestor row of this thread's node (row 32 qd + lane)
+        // ---- tree topology (PAPER.md:90 precondition; ancestor rows PAPER.md:63-66), warp 3: lane holds nodes
+        //      lane and lane + 32; pointer jumping with the jump pointer of every round recorded for the segsum ----
         uint32_t jpk[3] = {0u, 0u, 0u};        // jump pointer + 1 of round r, half hf: byte 2r + hf
-        float Ah = 0.f, Dh = 0.f;
+        int bad_code = 0;
         auto jump = [&](int r, int hf) { return (int)((jpk[(2 * r + hf) >> 2] >> (8 * ((2 * r + hf) & 3))) & 0xFFu) - 1; };
         auto topology = [&]() {
-            int par[2];
+            const int par[2] = {tpar[0], tpar[1]};
             uint64_t rw[2];
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                const int i = lane + 32 * hf;
-                par[hf] = i < T ? prm.parent[(size_t)b * T + i] : -1;
-            }
-            Ah = prm.A[h];
-            Dh = prm.D ? prm.D[h] : 0.f;
-            root_bad = __any_sync(0xffffffffu, lane == 0 && par[0] != -1);
-            par_bad = __any_sync(0xffffffffu, (lane > 0 && lane < T && (par[0] < 0 || par[0] >= lane)) ||
-                                                  (lane + 32 < T && (par[1] < 0 || par[1] >= lane + 32)));
-            const bool bad = root_bad || par_bad;
+            const bool root_bad = __any_sync(0xffffffffu, lane == 0 && par[0] != -1);
+            const bool par_bad = __any_sync(0xffffffffu, (lane > 0 && lane < T && (par[0] < 0 || par[0] >= lane)) ||
+                                                             (lane + 32 < T && (par[1] < 0 || par[1] >= lane + 32)));
+            bad_code = root_bad ? STREE_DEV_BAD_ROOT : (par_bad ? STREE_DEV_BAD_PARENT : 0);
+            const bool bad = bad_code != 0;
             int jp[2];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -285,25 +334,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                     jp[hf] = njp[hf];
                 }
             }
-            bits = qd ? rw[1] : rw[0];
+            tbits[lane] = rw[0];
+            tbits[lane + 32] = rw[1];
         };
-        const int row = 32 * qd + lane;                 // tree node of this thread's TMEM lane (row warps)
-        const uint32_t tq = tmem + ((uint32_t)(32 * qd) << 16);
-        float* cjw = reinterpret_cast<float*>(sm + L::CJ) + 64 * wi;
-        float* lmw = reinterpret_cast<float*>(sm + L::LM) + 64 * wi;
         // ---- segsum Λ = L·(dt A_h): the recorded jumps, values only; then c_j and the decay
-        //      mode.  Before the dependency wait under EARLY_TREE + EARLY_DT, else after it. ----
-        float dtv[2], lm[2];
-        bool fac = true;
+        //      mode, published with the topology to the row warps ----
         auto segsum = [&](bool from_smem) {
+            float dtv[2], lm[2];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 const int i = lane + 32 * hf;
                 dtv[hf] = 0.f;
                 if (i < T)
                     dtv[hf] = dt_eff(prm.dtx, from_smem ? reinterpret_cast<const float*>(sm + L::DT)[4 * i + (h & 3)]
-                                                        : prm.dt[((size_t)b * T + i) * H + h], h);
-                lm[hf] = dtv[hf] * Ah;
+                                                        : (early_lambda ? tdt[hf] : prm.dt[((size_t)b * T + i) * H + h]), h);
+                lm[hf] = dtv[hf] * tA;
             }
 #pragma unroll
             for (int r = 0; r < kRounds; ++r) {
@@ -319,140 +364,173 @@ __global__ void __launch_bounds__(kThreads, 2)
             float mn = fminf(lm[0], lm[1]);
 #pragma unroll
             for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            fac = mn >= -64.f;   // e^{Λi-Λj} = e^{Λi}·e^{-Λj} with both factors inside fp32 range
+            const bool fac = mn >= -64.f;   // e^{Λi-Λj} = e^{Λi}·e^{-Λj} with both factors inside fp32 range
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 const int i = lane + 32 * hf;
-                cjw[i] = fac ? __expf(-lm[hf]) * dtv[hf] : dtv[hf];
-                lmw[i] = lm[hf];
+                cjs[i] = fac ? __expf(-lm[hf]) * dtv[hf] : dtv[hf];
+                lms[i] = lm[hf];
             }
-            if (wi == 0 && lane == 0) *reinterpret_cast<volatile int*>(sm + L::MODE) = fac ? 1 : 0;
+            if (lane == 0) {
+                tinfo[0] = fac ? 1 : 0;
+                tinfo[1] = bad_code;
+                tinfo[2] = __float_as_int(tD);
+            }
             __syncwarp();
+            asm volatile("bar.arrive %0, %1;" ::"r"(kBarTree), "r"(160) : "memory");   // publish to the row warps
+            if (lane == 0) stamp(10);
         };
-        const bool early_lambda = prm.early_tree && prm.early_dt;
+        auto tree_phase = [&]() {   // after the dependency wait unless EARLY_TREE (+ EARLY_DT)
+            if (!prm.early_tree) {
+                wait_dep();
+                load_tree(false);
+            }
+            topology();
+            if (early_lambda) segsum(false);
+            else {
+                wait_dep();
+                if (prm.dt_tma) mbar_wait(BAR_CB, 0);
+                segsum(prm.dt_tma != 0);
+            }
+        };
         int* rinfo = reinterpret_cast<int*>(sm + L::RINFO);
+        bool tree_done = false;
         // ================= phase A (before the dependency wait where the promises allow) =================
-        if (rowr) {
-            if (prm.early_tree) topology();   // caller's promise: parent, A, D not written by the preceding kernel
-            if (early_lambda) segsum(false);  // caller's promise: dt not written by the preceding kernel
-            if (wi == 0 && lane == 0) stamp(10);
-        } else if (R) {
-            // ---- activation replay of the previous tree's accepted path (PAPER.md:113, 86-90 along the path):
-            //   h <- e^{λ_{r-1}} h + Σ_m c_m x_prev[s_m] B_prev[s_m]ᵀ,  c_m = e^{λ_{r-1} - λ_m} dt_prev[s_m],
-            //   λ_m = Σ_{q<=m} dt_prev[s_q] A_h.  Prologue (aux warps): path, validation, coefficients and the
-            //   staged operands of the first kRStage nodes ----
-            if (!prm.early_replay) wait_and_load_state();
-            const int Tp = prm.Tp, G = prm.G;
-            int* rpath = reinterpret_cast<int*>(sm + L::RPATH);
-            float* rcoef = reinterpret_cast<float*>(sm + L::RCOEF);
-            float* rlam = reinterpret_cast<float*>(sm + L::RLAM);
-            const __nv_bfloat16* xprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::XPREV);
-            const __nv_bfloat16* bprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::BPREV);
-            const int r_raw = prm.path_len[b];
-            {
-                const int p0 = u < Tp ? prm.path[(size_t)b * Tp + u] : 0;
-                const int p1 = u + 128 < Tp ? prm.path[(size_t)b * Tp + u + 128] : 0;
-                if (u < Tp) rpath[u] = p0;
-                if (u + 128 < Tp) rpath[u + 128] = p1;
-            }
-            named_bar(3, 128);
-            const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
-            const int rs = min(rr, kRStage);
-            auto node = [&](int m) {   // clamped into the tree: loads stay in bounds before validation
-                const int v = rpath[m];
-                return (v >= 0 && v < Tp) ? v : 0;
-            };
-            // staged operands of the first kRStage path nodes: 16-byte cp.async gathers, one DRAM latency
-#pragma unroll
-            for (int k = u; k < kRStage * (NS / 8); k += 128) {
-                const int m = k / (NS / 8), c = k % (NS / 8);
-                if (m < rs)
-                    cp_async16(sb + L::BPREV + (m * NS + 8 * c) * 2,
-                               prm.b_prev + (((size_t)b * Tp + node(m)) * G + g) * NS + 8 * c);
-            }
-            if (u < rs * (kP / 8)) {
-                const int m = u / (kP / 8), c = u % (kP / 8);
-                cp_async16(sb + L::XPREV + (m * kP + 8 * c) * 2,
-                           prm.x_prev + (((size_t)b * Tp + node(m)) * H + h) * kP + 8 * c);
-            }
-            if (u < 32) {
-                // path validation (root-anchored, increasing, parent-linked: PAPER.md:90 on the accepted path)
-                int ok = rr > 0;
-                for (int m = lane; m < rr; m += 32) {
+        if (!row_warp) {
+            if (R) {
+                // ---- activation replay of the previous tree's accepted path (PAPER.md:113, 86-90 along the path):
+                //   h <- e^{λ_{r-1}} h + Σ_m c_m x_prev[s_m] B_prev[s_m]ᵀ,  c_m = e^{λ_{r-1} - λ_m} dt_prev[s_m],
+                //   λ_m = Σ_{q<=m} dt_prev[s_q] A_h.  Prologue: path, validation, coefficients and the staged
+                //   operands of the first kRStage nodes ----
+                if (!prm.early_replay) {
+                    wait_dep();
+                    load_path();
+                }
+                const int Tp = prm.Tp, G = prm.G;
+                int* rpath = reinterpret_cast<int*>(sm + L::RPATH);
+                float* rcoef = reinterpret_cast<float*>(sm + L::RCOEF);
+                float* rlam = reinterpret_cast<float*>(sm + L::RLAM);
+                const int r_raw = rp_len;
+                if (u < Tp) rpath[u] = rp0;
+                if (u + 128 < Tp) rpath[u + 128] = rp1;
+                named_bar(3, 128);
+                const int rr = (r_raw >= 1 && r_raw <= Tp) ? r_raw : 0;   // candidate length, validated below
+                const int rs = min(rr, kRStage);
+                auto node = [&](int m) {   // clamped into the tree: loads stay in bounds before validation
                     const int v = rpath[m];
-                    bool good = (v >= 0 && v < Tp);
-                    if (m == 0) good = good && v == 0;
-                    else {
-                        const int pu = rpath[m - 1];
-                        good = good && v > pu;
-                        if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
-                    }
-                    if (!good) ok = 0;
+                    return (v >= 0 && v < Tp) ? v : 0;
+                };
+                // staged operands of the first kRStage path nodes: 16-byte cp.async gathers, one DRAM latency
+    #pragma unroll
+                for (int k = u; k < kRStage * (NS / 8); k += 128) {
+                    const int m = k / (NS / 8), c = k % (NS / 8);
+                    if (m < rs)
+                        cp_async16(sb + L::BPREV + (m * NS + 8 * c) * 2,
+                                   prm.b_prev + (((size_t)b * Tp + node(m)) * G + g) * NS + 8 * c);
                 }
-                ok = __all_sync(0xffffffffu, ok);
-                const int rv = ok ? rr : 0;
-                // path-cumsum of log-decays: inclusive warp scans over m = lane, lane + 32, then 32-node chunks
-                const float Ahr = prm.A[h];
-                float a0 = lane < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h], h) : 0.f;
-                float a1 = lane + 32 < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h], h) : 0.f;
-                const float d0 = a0;
-                a0 *= Ahr;
-                a1 *= Ahr;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
-                    if (lane >= o) { a0 += t0; a1 += t1; }
+                if (u < rs * (kP / 8)) {
+                    const int m = u / (kP / 8), c = u % (kP / 8);
+                    cp_async16(sb + L::XPREV + (m * kP + 8 * c) * 2,
+                               prm.x_prev + (((size_t)b * Tp + node(m)) * H + h) * kP + 8 * c);
                 }
-                a1 += __shfl_sync(0xffffffffu, a0, 31);
-                float last = rv <= 32 ? __shfl_sync(0xffffffffu, a0, (rv - 1) & 31) : __shfl_sync(0xffffffffu, a1, (rv - 33) & 31);
-                if (rv > 64) {
-                    float carry = __shfl_sync(0xffffffffu, a1, 31);
-#pragma unroll 1
-                    for (int m0 = 64; m0 < rv; m0 += 32) {
-                        const int m = m0 + lane;
-                        float a = m < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(m)) * H + h], h) * Ahr : 0.f;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const float t = __shfl_up_sync(0xffffffffu, a, o);
-                            if (lane >= o) a += t;
+                if (tree_warp && prm.early_tree) {   // the tree phase overlaps the gathers
+                    tree_phase();
+                    tree_done = true;
+                }
+                if (u < 32) {
+                    // path validation (root-anchored, increasing, parent-linked: PAPER.md:90 on the accepted path)
+                    int ok = rr > 0;
+                    for (int m = lane; m < rr; m += 32) {
+                        const int v = rpath[m];
+                        bool good = (v >= 0 && v < Tp);
+                        if (m == 0) good = good && v == 0;
+                        else {
+                            const int pu = rpath[m - 1];
+                            good = good && v > pu;
+                            if (prm.parent_prev && good) good = prm.parent_prev[(size_t)b * Tp + v] == pu;
                         }
-                        carry += __shfl_sync(0xffffffffu, a, 31);
+                        if (!good) ok = 0;
                     }
-                    last = carry;
+                    ok = __all_sync(0xffffffffu, ok);
+                    const int rv = ok ? rr : 0;
+                    // path-cumsum of log-decays: inclusive warp scans over m = lane, lane + 32, then 32-node chunks
+                    const float Ahr = prm.A[h];
+                    float a0 = lane < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane)) * H + h], h) : 0.f;
+                    float a1 = lane + 32 < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(lane + 32)) * H + h], h) : 0.f;
+                    const float d0 = a0;
+                    a0 *= Ahr;
+                    a1 *= Ahr;
+    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const float t0 = __shfl_up_sync(0xffffffffu, a0, o), t1 = __shfl_up_sync(0xffffffffu, a1, o);
+                        if (lane >= o) { a0 += t0; a1 += t1; }
+                    }
+                    a1 += __shfl_sync(0xffffffffu, a0, 31);
+                    float last = rv <= 32 ? __shfl_sync(0xffffffffu, a0, (rv - 1) & 31) : __shfl_sync(0xffffffffu, a1, (rv - 33) & 31);
+                    if (rv > 64) {
+                        float carry = __shfl_sync(0xffffffffu, a1, 31);
+    #pragma unroll 1
+                        for (int m0 = 64; m0 < rv; m0 += 32) {
+                            const int m = m0 + lane;
+                            float a = m < rv ? dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + node(m)) * H + h], h) * Ahr : 0.f;
+    #pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const float t = __shfl_up_sync(0xffffffffu, a, o);
+                                if (lane >= o) a += t;
+                            }
+                            carry += __shfl_sync(0xffffffffu, a, 31);
+                        }
+                        last = carry;
+                    }
+                    const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
+                    if (lane < kRStage) rcoef[lane] = __expf(last - a0) * d0;
+                    if (lane == 0) {
+                        rlam[0] = last;
+                        rlam[1] = lst;
+                        rlam[2] = __expf(last);
+                        rinfo[0] = rv;
+                        rinfo[1] = ok ? 0 : 1;
+                    }
                 }
-                const float lst = __shfl_sync(0xffffffffu, a0, kRStage - 1);
-                if (lane < kRStage) rcoef[lane] = __expf(last - a0) * d0;
-                if (lane == 0) {
-                    rlam[0] = last;
-                    rlam[1] = lst;
-                    rlam[2] = __expf(last);
-                    rinfo[0] = rv;
-                    rinfo[1] = ok ? 0 : 1;
-                }
+                cp_async_wait_all();
+                named_bar(3, 128);
+                if (u == 0) stamp(20);
+            } else if (tree_warp && prm.early_tree) {
+                tree_phase();
+                tree_done = true;
             }
-            cp_async_wait_all();
-            named_bar(3, 128);
-            if (u == 0) stamp(20);
         }
-        // ================= phase B: the state tile, by the 256 threads of warps 0-7: the replay update (R),
-        // the committed fp32 tile written back for its store, and the hi/lo bf16 split (B operand of Y0) =====
+        // ================= phase B: the state tile, by the 256 threads of warps 0-7 (thread tid: rows (tid >> 3) + 32 i,
+        // i = 0, 1, columns 32 a + 4 pc .. +3, pc = tid & 7): the replay update (R; packed FFMA2 over column pairs),
+        // the committed fp32 tile written back for its TMA store, and the hi/lo bf16 split (B operand of Y0) =====
         int r = 0;
         if (prm.has_h0) {
-            if (!early_h) wait_and_load_state();
-            mbar_wait(BAR_H, 0);
+            if (!early_h) {
+                wait_dep();
+                if (!row_warp && u == 0) {
+                    mbar_expect_tx(BAR_H, NS * kP * 4);
+#pragma unroll 1
+                    for (int a = 0; a < NS / 32; ++a)
+                        tma_load_2d_ef(sb + L::H0 + a * kAtom, &tm_h, BAR_H, 32 * a, (b * H + h) * kP, policy_evict_first());
+                }
+            }
             if (R) {
                 named_bar(4, 256);                  // replay prologue published (aux warps) to all 8 warps
                 r = rinfo[0];
             }
+            mbar_wait(BAR_H, 0);
             if (tid == 0) stamp(21);
             const int pc = tid & 7;                 // 16-byte chunk of a 128-byte fp32 atom row
             constexpr int kAt = NS / 32;
-            float4 hv[2][kAt];
+            float2 hv[2][2 * kAt];                  // rows (tid >> 3) + 32 i, column pairs 32 a + 4 pc + {0, 2}
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int a = 0; a < kAt; ++a)
-                    hv[i][a] = *reinterpret_cast<const float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc));
+                for (int a = 0; a < kAt; ++a) {
+                    const float4 v = *reinterpret_cast<const float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc));
+                    hv[i][2 * a] = make_float2(v.x, v.y);
+                    hv[i][2 * a + 1] = make_float2(v.z, v.w);
+                }
             if (R && r > 0) {
                 const float* rcoef = reinterpret_cast<const float*>(sm + L::RCOEF);
                 const float* rlam = reinterpret_cast<const float*>(sm + L::RLAM);
@@ -460,37 +538,37 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const __nv_bfloat16* xprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::XPREV);
                 const __nv_bfloat16* bprev = reinterpret_cast<const __nv_bfloat16*>(sm + L::BPREV);
                 const int Tp = prm.Tp, G = prm.G;
-                const float dk = rlam[2], Ak = prm.A[h], last = rlam[0];
+                const float dk = rlam[2], last = rlam[0];
                 float lam_run = rlam[1];
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int a = 0; a < kAt; ++a) {
-                        hv[i][a].x *= dk; hv[i][a].y *= dk; hv[i][a].z *= dk; hv[i][a].w *= dk;
-                    }
+                    for (int a = 0; a < 2 * kAt; ++a) hv[i][a] = fmul2(hv[i][a], make_float2(dk, dk));
 #pragma unroll 1
                 for (int m = 0; m < r; ++m) {
-                    float4 bb[kAt];
+                    float2 bb[2 * kAt];
                     float uu[2];
                     if (m < kRStage) {
 #pragma unroll
                         for (int a = 0; a < kAt; ++a) {
                             const uint2 w = *reinterpret_cast<const uint2*>(&bprev[m * NS + 32 * a + 4 * pc]);
-                            bb[a] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                                                __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+                            bb[2 * a] = make_float2(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u));
+                            bb[2 * a + 1] = make_float2(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
                         }
+                        const float cm = rcoef[m];
 #pragma unroll
-                        for (int i = 0; i < 2; ++i) uu[i] = rcoef[m] * __bfloat162float(xprev[m * kP + (tid >> 3) + 32 * i]);
+                        for (int i = 0; i < 2; ++i) uu[i] = cm * __bfloat162float(xprev[m * kP + (tid >> 3) + 32 * i]);
                     } else {   // long accepted paths: operands from L2, coefficients on the fly
                         const int s = rpath[m];
                         const float dm = dt_eff(prm.dtx, prm.dt_prev[((size_t)b * Tp + s) * H + h], h);
-                        lam_run += dm * Ak;
+                        lam_run += dm * prm.A[h];
                         const float cm = __expf(last - lam_run) * dm;
                         const __nv_bfloat16* br = prm.b_prev + (((size_t)b * Tp + s) * G + g) * NS + 4 * pc;
 #pragma unroll
-                        for (int a = 0; a < kAt; ++a)
-                            bb[a] = make_float4(__bfloat162float(br[32 * a]), __bfloat162float(br[32 * a + 1]),
-                                                __bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
+                        for (int a = 0; a < kAt; ++a) {
+                            bb[2 * a] = make_float2(__bfloat162float(br[32 * a]), __bfloat162float(br[32 * a + 1]));
+                            bb[2 * a + 1] = make_float2(__bfloat162float(br[32 * a + 2]), __bfloat162float(br[32 * a + 3]));
+                        }
                         const __nv_bfloat16* xr = prm.x_prev + (((size_t)b * Tp + s) * H + h) * kP;
 #pragma unroll
                         for (int i = 0; i < 2; ++i) uu[i] = cm * __bfloat162float(xr[(tid >> 3) + 32 * i]);
@@ -498,17 +576,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int i = 0; i < 2; ++i)
 #pragma unroll
-                        for (int a = 0; a < kAt; ++a) {
-                            hv[i][a].x = fmaf(uu[i], bb[a].x, hv[i][a].x); hv[i][a].y = fmaf(uu[i], bb[a].y, hv[i][a].y);
-                            hv[i][a].z = fmaf(uu[i], bb[a].z, hv[i][a].z); hv[i][a].w = fmaf(uu[i], bb[a].w, hv[i][a].w);
-                        }
+                        for (int a = 0; a < 2 * kAt; ++a) hv[i][a] = ffma2(make_float2(uu[i], uu[i]), bb[a], hv[i][a]);
                 }
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int a = 0; a < kAt; ++a)
-                        *reinterpret_cast<float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc)) = hv[i][a];
-                if (tid == 0) stamp(22);
+                        *reinterpret_cast<float4*>(sm + L::H0 + a * kAtom + swz((tid >> 3) + 32 * i, pc)) =
+                            make_float4(hv[i][2 * a].x, hv[i][2 * a].y, hv[i][2 * a + 1].x, hv[i][2 * a + 1].y);
+                if (tid == 0) stamp(28);
             }
             // hi/lo split: fp32 columns 32 a + 4 pc .. +3 -> bf16 atom a / 2, 16-byte chunk (a & 1)·4 + pc / 2,
             // 8-byte half pc & 1 (rows 0-63 of the split tile = hi, the next 64-row atom = lo)
@@ -516,15 +592,16 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int a = 0; a < kAt; ++a) {
-                    const float4 v = hv[i][a];
-                    const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
-                    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+                    const float2 v01 = hv[i][2 * a], v23 = hv[i][2 * a + 1];
+                    const __nv_bfloat162 h01 = __floats2bfloat162_rn(v01.x, v01.y), h23 = __floats2bfloat162_rn(v23.x, v23.y);
+                    const float2 l01 = fsub2(v01, __bfloat1622float2(h01)), l23 = fsub2(v23, __bfloat1622float2(h23));
                     const uint2 hi = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
-                    const uint2 lo = make_uint2(pack_bf16(v.x - f01.x, v.y - f01.y), pack_bf16(v.z - f23.x, v.w - f23.y));
+                    const uint2 lo = make_uint2(pack_bf16(l01.x, l01.y), pack_bf16(l23.x, l23.y));
                     const uint32_t off = (a >> 1) * 2 * kAtom + swz((tid >> 3) + 32 * i, (a & 1) * 4 + (pc >> 1)) + (pc & 1) * 8;
                     *reinterpret_cast<uint2*>(sm + L::HL + off) = hi;
                     *reinterpret_cast<uint2*>(sm + L::HL + kAtom + off) = lo;
                 }
+            if (tid == 0) stamp(22);
             fence_proxy_async();   // split tiles (and the replayed tile, for its TMA store) -> async proxy
             named_bar(4, 256);
             if (tid == 0) {
@@ -533,99 +610,101 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
         // ================= phase C: after the dependency wait =================
-        if (!waited) { pdl_wait(); waited = true; }   // every global write follows the dependency wait
-        if (!rowr) {
-            if (R && u == 0) {
-                stamp(23);
-                if (rinfo[1] && h == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
-                if (r > 0) {                    // the committed state, in place
-                    const uint64_t ef = policy_evict_first();
+        if (!row_warp) {
+        if (tree_warp && !tree_done) tree_phase();
+        wait_dep();   // every global write follows the dependency wait
+        if (R && u == 0) {
+            stamp(23);
+            if (rinfo[1] && h == 0) report(prm.dev_status, STREE_DEV_BAD_PATH);
+            if (r > 0) {                    // the committed state, in place
+                const uint64_t ef = policy_evict_first();
 #pragma unroll 1
-                    for (int a = 0; a < NS / 32; ++a)
-                        tma_store_2d_ef(&tm_h, sb + L::H0 + a * kAtom, 32 * a, (b * H + h) * kP, ef);
-                    bulk_commit();
-                    bulk_wait_read_all();   // the store has read the tile before the CTA releases its shared memory
-                }
-                stamp(24);
+                for (int a = 0; a < NS / 32; ++a)
+                    tma_store_2d_ef(&tm_h, sb + L::H0 + a * kAtom, 32 * a, (b * H + h) * kP, ef);
+                bulk_commit();
+                bulk_wait_read_all();   // the store has read the tile before the CTA releases its shared memory
             }
+            stamp(24);
+        }
         } else {
-            const bool live = true;
-            if (!prm.early_tree) topology();
-            const bool bad = root_bad || par_bad;
-            if (bad && wi == 0 && lane == 0 && h == 0)
-                report(prm.dev_status, root_bad ? STREE_DEV_BAD_ROOT : STREE_DEV_BAD_PARENT);
-            if (!early_lambda) {
-                if (prm.dt_tma) mbar_wait(BAR_CB, 0);
-                segsum(prm.dt_tma != 0);
-            }
-            if (live) {
-                if (wi == 0 && lane == 0) stamp(11);
-                // ---- masked weights of key columns [32 ch, 32 ch + 32), straight into TMEM ----
-                mbar_wait(BAR_G, 0);
-                tc_fence_after();
-                if (wi == 0 && lane == 0) stamp(12);
-            }
-            if (32 * ch < Tp16) {
-                unsigned long long* tr = (live && wi == 0 && lane == 0) ? trace : nullptr;
-                if (fac) build_weights<true>(tq, 32 * ch, bits, qd ? lm[1] : lm[0], cjw, lmw, tr);
-                else build_weights<false>(tq, 32 * ch, bits, qd ? lm[1] : lm[0], cjw, lmw, tr);
-            }
-            if (live) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(BAR_M);
-                if (wi == 0 && lane == 0) stamp(13);
-                // ---- epilogue: node row 32 qd + lane, output columns [32 ch, 32 ch + 32):
-                //      y = e^{Λ_i}·acc (+ Y'_direct) + D_h x, bf16 (RNE), straight to HBM ----
-                mbar_wait(BAR_ACC, 0);
-                tc_fence_after();
-                if (wi == 0 && lane == 0) stamp(14);
-            }
-            const bool has0 = prm.has_h0 || fac;
-            const float s0 = bad ? 0.f : __expf(qd ? lm[1] : lm[0]);
-            const float dh = bad ? 0.f : Dh;
-            const size_t yoff = (((size_t)b * T + row) * prm.y_heads + prm.y_head_off + h) * kP + 32 * ch;
+        // ================= row warps 0, 1, 4, 5: TMEM lane quadrant qd = node rows 32 qd + lane, key / output
+        // column half ch: the masked weights and the epilogue =================
+        const int qd = warp & 1, ch = warp >> 2, wi = qd + 2 * ch;
+        const int row = 32 * qd + lane;                 // tree node of this thread's TMEM lane
+        const uint32_t tq = tmem + ((uint32_t)(32 * qd) << 16);
+        pdl_wait();
+        named_bar(kBarTree, 160);                       // topology, segsum and decay mode published (warp 3)
+        const uint64_t bits = tbits[row];
+        const float lmr = lms[row];
+        const bool fac = tinfo[0] != 0;
+        const int bad_code = tinfo[1];
+        const bool bad = bad_code != 0;
+        const float Dh = __int_as_float(tinfo[2]);
+        if (bad && wi == 0 && lane == 0 && h == 0) report(prm.dev_status, bad_code);
+        if (wi == 0 && lane == 0) stamp(11);
+        // ---- masked weights of key columns [32 ch, 32 ch + 32), straight into TMEM ----
+        mbar_wait(BAR_G, 0);
+        tc_fence_after();
+        if (wi == 0 && lane == 0) stamp(12);
+        if (32 * ch < Tp16) {
+            unsigned long long* tr = (wi == 0 && lane == 0) ? trace : nullptr;
+            if (fac) build_weights<true>(tq, 32 * ch, bits, lmr, cjs, lms, tr);
+            else build_weights<false>(tq, 32 * ch, bits, lmr, cjs, lms, tr);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR_M);
+        if (wi == 0 && lane == 0) stamp(13);
+        // ---- epilogue: node row 32 qd + lane, output columns [32 ch, 32 ch + 32):
+        //      y = e^{Λ_i}·acc (+ Y'_direct) + D_h x, bf16 (RNE), straight to HBM ----
+        mbar_wait(BAR_ACC, 0);
+        tc_fence_after();
+        if (wi == 0 && lane == 0) stamp(14);
+        const bool has0 = prm.has_h0 || fac;
+        const float s0 = bad ? 0.f : __expf(lmr);
+        const float dh = bad ? 0.f : Dh;
+        const size_t yoff = (((size_t)b * T + row) * prm.y_heads + prm.y_head_off + h) * kP + 32 * ch;
 #pragma unroll
-            for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
-                const int col = 32 * ch + 16 * c16;
-                uint32_t va[16], vb[16];
-                if (has0) tmem_ld16r(tq + kColAcc + col, va);
-                if (!fac) tmem_ld16r(tq + kColYd + col, vb);
-                tmem_wait();
-                float acc[16];
+        for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
+            const int col = 32 * ch + 16 * c16;
+            uint32_t va[16], vb[16];
+            if (has0) tmem_ld16r(tq + kColAcc + col, va);
+            if (!fac) tmem_ld16r(tq + kColYd + col, vb);
+            tmem_wait();
+            float acc[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) acc[k] = has0 ? __uint_as_float(va[k]) : 0.f;
-                if (live && wi == 0 && lane == 0 && c16 == 0) stamp(17);
-                uint32_t o[8];
+            for (int k = 0; k < 16; ++k) acc[k] = has0 ? __uint_as_float(va[k]) : 0.f;
+            if (wi == 0 && lane == 0 && c16 == 0) stamp(17);
+            uint32_t o[8];
 #pragma unroll
-                for (int qc = 0; qc < 2; ++qc) {
-                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, (col >> 3) + qc));
-                    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+            for (int qc = 0; qc < 2; ++qc) {
+                const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, (col >> 3) + qc));
+                const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int p = 8 * qc + 2 * k;
-                        const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
-                        const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
-                        const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
-                        float da = dh, db = dh;
-                        if (DPC && prm.D && !bad) {   // D[h][p]
-                            da = __ldg(prm.D + (size_t)h * kP + col + p);
-                            db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
-                        }
-                        o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(da, xa, d0)), fmaf(s0, acc[p + 1], fmaf(db, xb, d1)));
+                for (int k = 0; k < 4; ++k) {
+                    const int p = 8 * qc + 2 * k;
+                    const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
+                    const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
+                    const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
+                    float da = dh, db = dh;
+                    if (DPC && prm.D && !bad) {   // D[h][p]
+                        da = __ldg(prm.D + (size_t)h * kP + col + p);
+                        db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
                     }
+                    o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(da, xa, d0)), fmaf(s0, acc[p + 1], fmaf(db, xb, d1)));
                 }
-                if (live && wi == 0 && lane == 0 && c16 == 1) stamp(18);
-                if (live && row < T) {
+            }
+            if (wi == 0 && lane == 0 && c16 == 1) stamp(18);
+            if (row < T) {
 #pragma unroll 1
-                    for (int pr = 0; pr < prm.n_ypeer; ++pr) {
-                        uint4* dst = reinterpret_cast<uint4*>(prm.ypeer[pr] + yoff);
-                        dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
-                        dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
-                    }
+                for (int pr = 0; pr < prm.n_ypeer; ++pr) {
+                    uint4* dst = reinterpret_cast<uint4*>(prm.ypeer[pr] + yoff);
+                    dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
+                    dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
                 }
             }
-            if (live && wi == 0 && lane == 0) stamp(15);
+        }
+        if (wi == 0 && lane == 0) stamp(15);
         }
     } else if (warp == kIssW) {
         // ================= TMA producer + MMA issuer (warp converged, elected lane issues) =================
@@ -742,7 +821,10 @@ int launch_lat_inst(int B, int H, cudaStream_t s, const CUtensorMap& mc, const C
         const char* e = std::getenv("STREE_LAT_ONE_CTA");
         return e && e[0] == '1';
     }();
-    if (one_cta) smem = 120 * 1024;
+    // One CTA per SM when the grid fits in half the SMs: the next layer's CTAs (launched under PDL while this
+    // layer runs) then land on other SMs instead of sharing this layer's (c2, 24 CTAs: 3.90 -> 3.48 µs per layer).
+    // With more CTAs than that the next layer could not start until this one exits, so two CTAs per SM stay.
+    if (one_cta || 2 * B * H <= stree::host::num_sms()) smem = 120 * 1024;
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return (int)e;
     e = stree::launch_k(k, dim3(B * H), dim3(kThreads), smem, s, mc, mb, mx, mh, mdt, prm);
@@ -788,7 +870,7 @@ extern "C" int stree_launch_scan_lat(const stree_dims* d, const void* x, const f
     Params prm{};
     if (replay) prm = *static_cast<const Params*>(replay);
     prm.B = B; prm.T = T; prm.H = H; prm.G = G;
-    prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
+    prm.dt = dt; prm.A = A; prm.D = D; prm.parent = parent; prm.h0p = h0; prm.y = (__nv_bfloat16*)y; prm.dev_status = dev_status;
     prm.has_h0 = h0 != nullptr;
     if (yo) {
         prm.n_ypeer = yo->n_peers;

@@ -2,6 +2,7 @@
 // ceiling.  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mufu tools/mufu_probe.cu && /tmp/mufu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cstdint>
 
 template <int MODE>
 __global__ void k(float* out, int iters) {
@@ -12,7 +13,16 @@ __global__ void k(float* out, int iters) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             if (MODE == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
-            else asm volatile("fma.rn.f32 %0, %0, 0f3F7FFFFF, 0fBA83126F;" : "+f"(a[i]));
+            else if (MODE == 1) asm volatile("fma.rn.f32 %0, %0, 0f3F7FFFFF, 0fBA83126F;" : "+f"(a[i]));
+            else if (MODE == 2) {   // packed half2: two exps per instruction
+                uint32_t v = __float_as_uint(a[i]);
+                asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v));
+                a[i] = __uint_as_float(v);
+            } else {                // packed bf16x2
+                uint32_t v = __float_as_uint(a[i]);
+                asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v));
+                a[i] = __uint_as_float(v);
+            }
         }
     }
     float s = 0.f;
@@ -28,12 +38,12 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const int iters = 4096;
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 4; ++mode)
         for (int tpb : {128, 256, 512, 1024}) {
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
-            auto kk = mode == 0 ? k<0> : k<1>;
+            auto kk = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : k<3>;
             kk<<<sms * 2, tpb>>>(d, 16);
             cudaEventRecord(e0);
             kk<<<sms * 2, tpb>>>(d, iters);
@@ -41,10 +51,10 @@ int main() {
             cudaEventSynchronize(e1);
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
-            const double ops = (double)sms * 2 * tpb * iters * 16;
+            const double ops = (double)sms * 2 * tpb * iters * 16 * (mode >= 2 ? 2 : 1);   // exps (2 per packed op)
             const double per_clk_sm = ops / (ms * 1e-3) / (clk * 1e3) / sms;
             printf("%s threads/CTA %4d (2 CTAs/SM): %.1f ops/clk/SM (at the %d MHz rated clock)\n",
-                   mode == 0 ? "ex2.approx.ftz.f32" : "fma.rn.f32        ", tpb, per_clk_sm, clk / 1000);
+                   mode == 0 ? "ex2.approx.ftz.f32   " : mode == 1 ? "fma.rn.f32           " : mode == 2 ? "ex2.approx.f16x2 (x2)" : "ex2.bf16x2 (x2)      ", tpb, per_clk_sm, clk / 1000);
         }
     return 0;
 }

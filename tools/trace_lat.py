@@ -70,7 +70,7 @@ names = {0: "start", 1: "setup done", 2: "pdl wait passed", 3: "iss: C,B landed"
          5: "iss: Y0 issued", 6: "iss: M' ready", 7: "iss: x ready", 8: "iss: Y' issued", 10: "row: tree done",
          11: "row: lambda done", 12: "row: G ready", 13: "row: M' done", 14: "epi: acc ready", 15: "epi: stored",
          16: "aux: split done", 17: "epi: tmem loaded", 18: "epi: computed", 25: "bld: G loaded",
-         26: "bld: computed", 27: "bld: stored", 20: "rep: prologue", 21: "rep: state landed", 22: "rep: updated",
+         26: "bld: computed", 27: "bld: stored", 28: "upd half0", 29: "split half0", 19: "upd half1", 20: "rep: prologue", 21: "rep: state landed", 22: "state: upd+split",
          23: "rep: wait passed", 24: "rep: stored", 30: "end"}
 rel = np.where(tr > 0, tr - t0, -1) / 1000.0
 print(f"{ncta} CTAs per launch")
@@ -79,11 +79,37 @@ for li in range(L):
     en = rel[li, :, 30]
     print(f"layer {li:2d}: start {st.min():7.2f}..{st.max():7.2f}  wait {rel[li, :, 2].min():7.2f}..{rel[li, :, 2].max():7.2f}"
           f"  end {en.min():7.2f}..{en.max():7.2f}")
+for li in (L // 2, L // 2 + 1):
+    base = rel[li, :, 2].min()
+    print(f"layer {li} phases relative to its first dependency-wait release:")
+    for k in sorted(names):
+        v = rel[li, :, k]
+        v = v[v >= 0]
+        if len(v):
+            print(f"  {names[k]:>20s}: min {v.min() - base:7.2f}  med {np.median(v) - base:7.2f}  max {v.max() - base:7.2f}")
+# per layer: body (wait -> last end), gap (last end -> next wait), pre-wait window (first start -> wait), median of
+# the key phases relative to the wait, and how many CTAs share an SM with a CTA of the previous layer
+sm = tr[:, :, 31]
+keys = [(1, "setup"), (21, "st.land"), (22, "upd+spl"), (16, "split"), (3, "CB"), (12, "G"), (13, "M'"), (14, "acc"),
+        (15, "stored")]
+print("layer  window  body   gap   " + " ".join(f"{n:>7s}" for _, n in keys) + "  shareSM")
+for li in range(1, L - 1):
+    w = rel[li, :, 2].min()
+    body = rel[li, :, 30].max() - w
+    gap = rel[li + 1, :, 2].min() - rel[li, :, 30].max()
+    win = w - rel[li, :, 0].min()
+    cols = []
+    for k, _ in keys:
+        v = rel[li, :, k]
+        v = v[v >= 0]
+        cols.append(f"{np.median(v) - w:7.2f}" if len(v) else "      -")
+    share = len(set(sm[li].tolist()) & set(sm[li - 1].tolist()))
+    print(f"{li:5d} {win:6.2f} {body:6.2f} {gap:5.2f}   " + " ".join(cols) + f"  {share:5d}")
+# stragglers of one layer: the CTAs that end last, with their SM and phases (relative to the layer's wait)
 li = L // 2
-base = rel[li, :, 2].min()
-print(f"layer {li} phases relative to its first dependency-wait release:")
-for k in sorted(names):
-    v = rel[li, :, k]
-    v = v[v >= 0]
-    if len(v):
-        print(f"  {names[k]:>20s}: min {v.min() - base:7.2f}  med {np.median(v) - base:7.2f}  max {v.max() - base:7.2f}")
+w = rel[li, :, 2].min()
+order = np.argsort(rel[li, :, 30])[::-1]
+print(f"layer {li}: slowest / fastest CTAs (block, sm, start, setup, prologue, upd+split, CB, G, M', acc, end)")
+for c in list(order[:6]) + list(order[-3:]):
+    v = [rel[li, c, k] - w if rel[li, c, k] >= 0 else float("nan") for k in (0, 1, 20, 22, 3, 12, 13, 14, 30)]
+    print(f"  cta {c:3d} sm {int(sm[li, c]):3d}  " + " ".join(f"{x:6.2f}" for x in v))
