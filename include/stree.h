@@ -260,7 +260,8 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *                            immediately preceding the call in its stream (true in a decode loop: the
  *                            state was committed an iteration earlier).  Covered operands:
  *                              stree_tree_scan, stree_commit, stree_replay_scan: h0 / h;
- *                              stree_tree_attn: k_cache, v_cache and cache_len.
+ *                              stree_tree_attn: k_cache, v_cache and cache_len;
+ *                              stree_tree_conv: conv_state (with EARLY_TREE).
  *                            The kernels then start streaming them before the dependency wait.  A call
  *                            that launches two kernels (stree_replay_scan on shapes the fused kernel does
  *                            not serve: commit, then scan) applies the promise to its first kernel only.
@@ -281,6 +282,8 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *                            then validate the tree and run the pointer-jumping rounds of the ancestor
  *                            mask before the dependency wait, so only the segsum of dt
  *                            and the contractions remain after it.  x, B, C are never read early.
+ *                            stree_tree_conv: parent, weight and bias (read, and every node's window
+ *                            tabulated, before the wait; only u is read after it).
  *  STREE_LAUNCH_EARLY_DT     promise (with EARLY_TREE): dt of a scan call is not written by the kernel
  *                            immediately preceding it.  True in a Mamba-2 layer, where dt comes from the
  *                            input projection and the causal conv1d kernel (which produces x, B, C) runs

@@ -153,3 +153,32 @@ def test_conv_two_iterations_equal_grafted_tree():
     pg = np.concatenate([par1[0], np.where(par2[0] < 0, k, par2[0] + 24)]).astype(np.int32)
     ref, _ = oracle.tree_conv(np.concatenate([u1, u2], 1), weight, bias, state, pg[None])
     assert_conv_close(got[0][None], ref[:, 24:], TOL_F32)
+
+
+@pytest.mark.parametrize("flags", [1, 1 | 8, 1 | 2 | 8, 31])
+@pytest.mark.parametrize("shape", [(16, 64, MAMBA2_CONV, 4), (2, 256, 520, 3), (3, 37, 264, 4), (2, 5, 64, 2)])
+def test_tree_conv_launch_promises(flags, shape):
+    """EARLY_TREE (weights, bias, parents and windows before the dependency wait) and EARLY_STATE (conv-state
+    rows too), as a chain of dependent calls: each layer's input is the previous layer's output (written by the
+    kernel immediately before it), so any read of u before the wait would see stale rows."""
+    B, T, C, W = shape
+    io = "bf16"
+    par, u, weight, bias, state = make_conv(B, T, C, W, io, seed=T + C)
+    binding.stree_set_launch_flags(flags)
+    try:
+        L = 4
+        bufs = [dev(u, io)] + [torch.empty_like(dev(u, io)) for _ in range(L)]
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for i in range(L):
+            binding.stree_tree_conv(bufs[i], dev(weight), dev(bias), dev(state, io), dev(par), bufs[i + 1], act=True,
+                                    dev_status=st)
+        torch.cuda.synchronize()
+        x = u
+        for i in range(L):
+            ref, _ = oracle.tree_conv(x, weight, bias, state, par)
+            got = bufs[i + 1].float().cpu().numpy()
+            assert_conv_close(got, ref, TOL_BF16)
+            x = got   # the next layer reads exactly what the kernel wrote (bf16 values)
+        assert int(st.item()) == 0
+    finally:
+        binding.stree_set_launch_flags(1)

@@ -1,6 +1,5 @@
 """Tree conv at the bench shape (c4 trees, conv_dim 5376, W = 4, bf16, 64 layers in one CUDA graph): time
-per call, or a few eager calls for ncu (--ncu).  (Round 2 used it to compare a persistent TMA-ring variant
-selected by STREE_CONV_PIPE; that variant measured no faster and was dropped — see DESIGN.md §12.)"""
+per call under the launch flags PDL / + EARLY_TREE / all promises, or a few eager calls for ncu (--ncu)."""
 import argparse
 import os
 import sys
@@ -31,7 +30,6 @@ cl = [{"u": torch.randn((B, T, C), generator=gen, device=dev).to(bf),
        "out": torch.empty((B, T, C), dtype=bf, device=dev)} for _ in range(args.layers)]
 cdims = binding.make_conv_dims(cl[0]["u"], cl[0]["w"])
 st = torch.zeros(1, dtype=torch.int32, device=dev)
-binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
 
 
 def run():
@@ -40,8 +38,8 @@ def run():
 
 
 vbytes = 2 * B * T * C * 2 + B * (W - 1) * C * 2 + C * W * 4 + C * 4 + B * T * 4
-for pipe in ("1", "0"):
-    os.environ["STREE_CONV_PIPE"] = pipe
+for flags in (1, 1 | 8, 31):
+    binding.stree_set_launch_flags(flags)
     if args.ncu:
         for _ in range(3):
             run()
@@ -64,4 +62,4 @@ for pipe in ("1", "0"):
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (10 * len(cl))
-    print(f"pipe={pipe}: {us:.2f} us per call, {vbytes / us / 1e3:.0f} GB/s")
+    print(f"flags={flags}: {us:.2f} us per call, {vbytes / us / 1e3:.0f} GB/s")
