@@ -17,9 +17,13 @@ namespace conv {
 
 constexpr int kChunks = 32;     // 16-byte channel chunks per conv-commit warp (lane = chunk)
 #ifndef STREE_CONV_KC
-#define STREE_CONV_KC 16
+#define STREE_CONV_KC 8
 #endif
 constexpr int kConvKC = STREE_CONV_KC;     // chunks per tree-conv CTA (tree_conv_kernel)
+#ifndef STREE_CONV_GROUPS
+#define STREE_CONV_GROUPS 4
+#endif
+constexpr int kConvGroups = STREE_CONV_GROUPS;   // cp.async node groups per tree-conv CTA
 
 template <typename IO>
 struct Pack;
@@ -107,8 +111,8 @@ template <>
 __device__ __forceinline__ float silu_h<float>(float h) { return __fdividef(2.f * h, 1.f + __expf(-2.f * h)); }
 
 // One CTA per (tree, block of KC 16-byte channel chunks), 8·KC threads: thread = (chunk ch = tid % KC, node
-// slot ns = tid / KC); slot ns computes nodes ns, ns + 8, ...  KC = 16 (128 threads, 4.5 CTAs per SM at the
-// 2.7B shape) balances the SMs: with KC = 32 (336 CTAs) 40 SMs ran 3 CTAs and the rest 2.
+// slot ns = tid / KC); slot ns computes nodes ns, ns + 8, ...  KC = 8 (64 threads, 1344 CTAs at the 2.7B
+// shape, all resident): tools/conv_sweep.sh measured KC = 8 / 16 / 32 at 6.5 / 6.7 / 8.3 µs per call (4 groups).
 // Under STREE_LAUNCH_EARLY_TREE the weights, bias and parents are read, and every node's window tabulated,
 // before the dependency wait (EARLY_STATE: the conv-state rows too), so only the tree's rows remain after it.
 // The rows arrive in kGroups cp.async groups of consecutive nodes; group k is computed and stored while the
@@ -323,8 +327,8 @@ cudaError_t launch_conv(const stree_conv_dims* d, const void* u, const float* we
     const int C = d->channels, T = d->n_nodes;
     dim3 grid((C / V + KC - 1) / KC, d->batch);
     const size_t smem = tree_conv_smem(T, W, KC);
-    // 4 row groups per CTA (8 groups measured slower at the 2.7B shape: 7.1 vs 6.8 µs per call)
-    auto k = act ? tree_conv_kernel<IO, W, KC, true, 4> : tree_conv_kernel<IO, W, KC, false, 4>;
+    // row groups per CTA (8 groups measured slower at the 2.7B shape: 7.1 vs 6.8 µs per call)
+    auto k = act ? tree_conv_kernel<IO, W, KC, true, kConvGroups> : tree_conv_kernel<IO, W, KC, false, kConvGroups>;
     // every CTA of the 2.7B shape resident at once (672 CTAs, <= 5 per SM): registers capped by the launch
     // bounds, shared-memory carveout at its maximum
     cudaError_t e = stree::host::smem_attr((const void*)k, (int)smem);
