@@ -102,7 +102,7 @@ names = {"Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throu
          "Dynamic Shared Memory Per Block", "Grid Size", "Block Size", "L2 Hit Rate", "Achieved Active Warps Per SM",
          "Issued Warp Per Scheduler", "No Eligible"}
 full = {}
-for rep in ("prof_fused", "prof_scan", "prof_commit"):
+for rep in ("prof_fused", "prof_scan", "prof_commit", "prof_lat_c3", "prof_attn", "prof_conv"):
     p = os.path.join(out, rep + ".ncu-rep")
     if os.path.exists(p):
         print(f"== ncu --set full: {rep} ==")

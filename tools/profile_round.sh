@@ -26,5 +26,7 @@ ncu --metrics $M,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed
     --log-file $OUT/launches_next.csv python tools/prof_attn.py > $OUT/ncu_launches_next.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 4 -c 1 -o $OUT/prof_attn \
     python tools/prof_attn.py > $OUT/ncu_attn.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tree_conv -s 8 -c 1 -o $OUT/prof_conv \
+    python tools/prof_conv.py --ncu > $OUT/ncu_conv.log 2>&1
 python tools/ncu_summary.py $OUT > $OUT/profile_summary.txt 2>&1
 tail -40 $OUT/profile_summary.txt

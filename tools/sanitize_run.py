@@ -121,6 +121,8 @@ def main():
     scan_case("scan T112 mixed decay (128-row, no h0)", p7, 2e-2, h0=False)
     # fused replay + scan: small-batch and pipeline kernels, every EARLY promise
     replay_case("replay_scan B2 H16 (small-batch)", 2, 48, 40, 16, all_flags)
+    replay_case("replay_scan B2 H16 (small-batch, PDL only)", 2, 48, 40, 16, binding.STREE_LAUNCH_PDL)
+    replay_case("replay_scan B1 H80 (small-batch, c3)", 1, 64, 64, 80, all_flags)
     replay_case("replay_scan B16 H8 (pipeline)", 16, 64, 64, 8, all_flags, binding.STREE_SCAN_TC_PIPELINE)
     if args.quick:
         return
@@ -129,7 +131,7 @@ def main():
     rc = pytest.main(["-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
                       "tests/test_conv_gpu.py", "tests/test_attn_gpu.py", "tests/test_mss_gpu.py", "-k",
                       "(conv_matches_oracle and 264) or conv_commit_bit_exact or bf16_ragged or "
-                      "kv_commit_bitexact or (random_trees and 1000)"])
+                      "kv_commit_bitexact or (random_trees and 1000) or (launch_promises and 37)"])
     if rc != 0:
         raise SystemExit(f"§8(f) tests failed under the sanitizer (pytest rc {rc})")
 
