@@ -220,7 +220,7 @@ def run_reference(args):
             "config": workload_desc(args.config, prob, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -529,7 +529,7 @@ def run_stree(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(base, tok, vt)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
@@ -660,7 +660,25 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": K}
 
 
+_JSON_FD = None   # the real stdout, reserved for the one JSON line (see main)
+
+
+def emit(line):
+    """Write the bench line to the real stdout: libraries (NCCL prints its version banner on rank 0, torch
+    warnings) write to fd 1 too, so main() points fd 1 at stderr and keeps the original for this line only."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)

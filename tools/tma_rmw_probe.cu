@@ -92,6 +92,66 @@ __global__ void __launch_bounds__(32, 1) k_rmw(const __grid_constant__ CUtensorM
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// Mixed variant: the 32 KB state of each unit through the LSU (cp.async 16-byte chunks into a STAGES-deep shared
+// ring by NW warps, then read back and stored with st.global, in place), the x tile / y tile through TMA by one
+// extra thread — the TMA engine carries only ~20 % of the bytes.
+template <int STAGES, int NW>
+__global__ void __launch_bounds__(32 * NW + 32, 1) k_mixed(const __grid_constant__ CUtensorMap mx,
+                                                           const __grid_constant__ CUtensorMap my, float* hbase,
+                                                           int units) {
+    extern __shared__ __align__(1024) unsigned char smr[];
+    unsigned char* sm = smr + ((1024u - (su32(smr) & 1023u)) & 1023u);
+    __shared__ __align__(8) unsigned long long bars[8];
+    const int tid = threadIdx.x, NT = 32 * NW;
+    const int u0 = blockIdx.x * units;
+    const uint32_t SZ = 32768;
+    unsigned char* xs = sm + STAGES * SZ;   // x ring: STAGES x 8 KB
+    if (tid == NT) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(su32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        auto issue = [&](int k) {
+            const int s = k % STAGES, unit = u0 + k, b = unit / H, h = unit % H;
+            expect_tx(su32(&bars[s]), 8192);
+            tld(su32(xs + s * 8192), &mx, su32(&bars[s]), h * P, b * T);
+        };
+        for (int k = 0; k < STAGES && k < units; ++k) issue(k);
+        for (int j = 0; j < units; ++j) {
+            const int s = j % STAGES, unit = u0 + j, b = unit / H, h = unit % H;
+            mwait(su32(&bars[s]), (j / STAGES) & 1);
+            tst(&my, su32(xs + s * 8192), h * P, b * T);
+            asm volatile("cp.async.bulk.commit_group;");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if (j + STAGES < units) issue(j + STAGES);
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        return;
+    }
+    if (tid > NT) return;
+    auto load = [&](int k) {
+        const int s = k % STAGES, unit = u0 + k, b = unit / H, h = unit % H;
+        const char* src = reinterpret_cast<const char*>(hbase + ((size_t)(b * H + h) * P) * N);
+        for (int c = tid; c < 2048; c += NT)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(sm + s * SZ + c * 16)), "l"(src + c * 16) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int k = 0; k < STAGES - 1; ++k) {
+        if (k < units) load(k);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int j = 0; j < units; ++j) {
+        if (j + STAGES - 1 < units) load(j + STAGES - 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");   // this thread's chunks of unit j
+        const int s = j % STAGES, unit = u0 + j, b = unit / H, h = unit % H;
+        float4* dst = reinterpret_cast<float4*>(hbase + ((size_t)(b * H + h) * P) * N);
+        for (int c = tid; c < 2048; c += NT) {
+            const float4 v = *reinterpret_cast<const float4*>(sm + s * SZ + c * 16);
+            __stcs(dst + c, v);
+        }
+    }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -157,5 +217,28 @@ int main() {
     run(k_rmw<4, false, 3>, 4, "  evict_first loads + stores");
     run(k_rmw<2, false, 0>, 2, "  2 stages");
     run(k_rmw<1, false, 0>, 1, "  1 stage");
+    auto run_mixed = [&](auto k, int stages, int nw, const char* name) {
+        size_t smem = (size_t)stages * 40960 + 1024;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        for (int w = 0; w < 2; ++w)
+            for (int l = 0; l < layers; ++l) k<<<ctas, 32 * nw + 32, smem>>>(mx[l], my[l], hs[l], units);
+        cudaEventRecord(e0);
+        const int reps = 5;
+        for (int r = 0; r < reps; ++r)
+            for (int l = 0; l < layers; ++l) k<<<ctas, 32 * nw + 32, smem>>>(mx[l], my[l], hs[l], units);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double us = ms * 1e3 / (reps * layers);
+        printf("%-46s stages=%d %8.2f us/launch  %7.1f GB/s\n", name, stages, us, bytes / (us * 1e-6) / 1e9);
+        cudaError_t err = cudaGetLastError();
+        if (err) printf("  error %s\n", cudaGetErrorString(err));
+    };
+    run_mixed(k_mixed<3, 4>, 3, 4, "LSU state (4 warps) + TMA x/y");
+    run_mixed(k_mixed<4, 4>, 4, 4, "LSU state (4 warps) + TMA x/y");
+    run_mixed(k_mixed<3, 8>, 3, 8, "LSU state (8 warps) + TMA x/y");
+    run_mixed(k_mixed<4, 8>, 4, 8, "LSU state (8 warps) + TMA x/y");
+    run_mixed(k_mixed<5, 8>, 5, 8, "LSU state (8 warps) + TMA x/y");
     return 0;
 }
