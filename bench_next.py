@@ -151,6 +151,10 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
                    "st": torch.randn((B, W - 1, C), generator=gen, device=dev).to(bf),
                    "out": torch.empty((B, T, C), dtype=bf, device=dev)})
     cdims = binding.make_conv_dims(cl[0]["u"], cl[0]["w"])
+    # decode-loop promises for the conv (as the scan bench uses them): the tree, the conv weights / bias and the
+    # conv state are not written by the kernel right before a layer's conv (EARLY_TREE + EARLY_STATE)
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE |
+                                   binding.STREE_LAUNCH_EARLY_TREE)
 
     def conv_all():
         for t in cl:
