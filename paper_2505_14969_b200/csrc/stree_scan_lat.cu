@@ -155,24 +155,27 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 template <bool FAC>
 __device__ __forceinline__ void build_weights(uint32_t tq, int c0, uint64_t bits, float li, const float* cjw,
                                               const float* lmw, unsigned long long* tr) {
-    uint32_t o[16];
+    uint32_t o[16], gv[32];
+    tmem_ld32(tq + kColG + c0, gv);   // the 32 key columns in one load (one TMEM round trip)
+    const uint32_t bw = (uint32_t)(bits >> c0);   // c0 in {0, 32}: this half's ancestor bits
+    float cj[32];
 #pragma unroll
-    for (int h16 = 0; h16 < 2; ++h16) {   // 16 key columns at a time (registers)
-        uint32_t gv[16];
-        tmem_ld16r(tq + kColG + c0 + 16 * h16, gv);
-        tmem_wait();
-        if (kTrace && tr && h16 == 0) tr[25] = gtimer();
+    for (int k4 = 0; k4 < 8; ++k4) {   // c_j of the 32 keys: 8 broadcast 16-byte loads while the TMEM load is in flight
+        const float4 v = reinterpret_cast<const float4*>(cjw + c0)[k4];
+        cj[4 * k4] = v.x; cj[4 * k4 + 1] = v.y; cj[4 * k4 + 2] = v.z; cj[4 * k4 + 3] = v.w;
+    }
+    tmem_wait();
+    if (kTrace && tr) tr[25] = gtimer();
 #pragma unroll
-        for (int k = 0; k < 16; k += 2) {
-            const int j = c0 + 16 * h16 + k;
-            float v0 = cjw[j] * __uint_as_float(gv[k]);
-            float v1 = cjw[j + 1] * __uint_as_float(gv[k + 1]);
-            if (!FAC) {
-                v0 *= __expf(fminf(li - lmw[j], 0.f));
-                v1 *= __expf(fminf(li - lmw[j + 1], 0.f));
-            }
-            o[8 * h16 + (k >> 1)] = pack_bf16(((bits >> j) & 1ull) ? v0 : 0.f, ((bits >> (j + 1)) & 1ull) ? v1 : 0.f);
+    for (int k = 0; k < 32; k += 2) {
+        const int j = c0 + k;
+        float v0 = cj[k] * __uint_as_float(gv[k]);
+        float v1 = cj[k + 1] * __uint_as_float(gv[k + 1]);
+        if (!FAC) {
+            v0 *= __expf(fminf(li - lmw[j], 0.f));
+            v1 *= __expf(fminf(li - lmw[j + 1], 0.f));
         }
+        o[k >> 1] = pack_bf16((bw & (1u << k)) ? v0 : 0.f, (bw & (2u << k)) ? v1 : 0.f);
     }
     if (kTrace && tr) tr[26] = gtimer();
     tmem_st16(tq + kColM + (c0 >> 1), o);
@@ -664,43 +667,73 @@ __global__ void __launch_bounds__(kThreads, 2)
         const float s0 = bad ? 0.f : __expf(lmr);
         const float dh = bad ? 0.f : Dh;
         const size_t yoff = (((size_t)b * T + row) * prm.y_heads + prm.y_head_off + h) * kP + 32 * ch;
-#pragma unroll
-        for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
-            const int col = 32 * ch + 16 * c16;
-            uint32_t va[16], vb[16];
-            if (has0) tmem_ld16r(tq + kColAcc + col, va);
-            if (!fac) tmem_ld16r(tq + kColYd + col, vb);
+        if (fac && !DPC) {
+            // factorised decay: the 32 accumulator columns in one TMEM load, 64 contiguous bytes per thread
+            uint32_t va[32];
+            tmem_ld32(tq + kColAcc + 32 * ch, va);
             tmem_wait();
-            float acc[16];
+            if (wi == 0 && lane == 0) stamp(17);
+            uint32_t o[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) acc[k] = has0 ? __uint_as_float(va[k]) : 0.f;
-            if (wi == 0 && lane == 0 && c16 == 0) stamp(17);
-            uint32_t o[8];
-#pragma unroll
-            for (int qc = 0; qc < 2; ++qc) {
-                const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, (col >> 3) + qc));
+            for (int qc = 0; qc < 4; ++qc) {
+                const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, 4 * ch + qc));
                 const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int p = 8 * qc + 2 * k;
                     const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
-                    const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
-                    const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
-                    float da = dh, db = dh;
-                    if (DPC && prm.D && !bad) {   // D[h][p]
-                        da = __ldg(prm.D + (size_t)h * kP + col + p);
-                        db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
-                    }
-                    o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(da, xa, d0)), fmaf(s0, acc[p + 1], fmaf(db, xb, d1)));
+                    o[4 * qc + k] = pack_bf16(fmaf(s0, __uint_as_float(va[p]), dh * xa),
+                                              fmaf(s0, __uint_as_float(va[p + 1]), dh * xb));
                 }
             }
-            if (wi == 0 && lane == 0 && c16 == 1) stamp(18);
+            if (wi == 0 && lane == 0) stamp(18);
             if (row < T) {
 #pragma unroll 1
                 for (int pr = 0; pr < prm.n_ypeer; ++pr) {
                     uint4* dst = reinterpret_cast<uint4*>(prm.ypeer[pr] + yoff);
-                    dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
-                    dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                }
+            }
+        } else {
+    #pragma unroll
+            for (int c16 = 0; c16 < 2; ++c16) {   // 16 output columns at a time (registers: no spills)
+                const int col = 32 * ch + 16 * c16;
+                uint32_t va[16], vb[16];
+                if (has0) tmem_ld16r(tq + kColAcc + col, va);
+                if (!fac) tmem_ld16r(tq + kColYd + col, vb);
+                tmem_wait();
+                float acc[16];
+    #pragma unroll
+                for (int k = 0; k < 16; ++k) acc[k] = has0 ? __uint_as_float(va[k]) : 0.f;
+                if (wi == 0 && lane == 0 && c16 == 0) stamp(17);
+                uint32_t o[8];
+    #pragma unroll
+                for (int qc = 0; qc < 2; ++qc) {
+                    const uint4 xv = *reinterpret_cast<const uint4*>(sm + L::X + swz(row, (col >> 3) + qc));
+                    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+    #pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int p = 8 * qc + 2 * k;
+                        const float xa = __uint_as_float(xw[k] << 16), xb = __uint_as_float(xw[k] & 0xFFFF0000u);
+                        const float d0 = (!fac && !bad) ? __uint_as_float(vb[p]) : 0.f;
+                        const float d1 = (!fac && !bad) ? __uint_as_float(vb[p + 1]) : 0.f;
+                        float da = dh, db = dh;
+                        if (DPC && prm.D && !bad) {   // D[h][p]
+                            da = __ldg(prm.D + (size_t)h * kP + col + p);
+                            db = __ldg(prm.D + (size_t)h * kP + col + p + 1);
+                        }
+                        o[4 * qc + k] = pack_bf16(fmaf(s0, acc[p], fmaf(da, xa, d0)), fmaf(s0, acc[p + 1], fmaf(db, xb, d1)));
+                    }
+                }
+                if (wi == 0 && lane == 0 && c16 == 1) stamp(18);
+                if (row < T) {
+    #pragma unroll 1
+                    for (int pr = 0; pr < prm.n_ypeer; ++pr) {
+                        uint4* dst = reinterpret_cast<uint4*>(prm.ypeer[pr] + yoff);
+                        dst[2 * c16] = make_uint4(o[0], o[1], o[2], o[3]);
+                        dst[2 * c16 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+                    }
                 }
             }
         }
