@@ -15,6 +15,7 @@
 // hold) use the simple per-(tree, head) kernel below.
 #include "stree_common.cuh"
 #include "stree_host.cuh"
+#include "stree_tc_ptx.cuh"
 
 namespace stree {
 
@@ -24,23 +25,12 @@ constexpr int kCThreads = 288;       // 1 producer warp + 8 compute warps
 constexpr int kCompute = 256;
 constexpr int kRingBytes = 128 * 1024;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void c_mbar_init(uint32_t b, uint32_t c) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c));
-}
-__device__ __forceinline__ void c_mbar_arrive(uint32_t b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
-}
-__device__ __forceinline__ void c_mbar_expect_tx(uint32_t b, uint32_t n) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n) : "memory");
-}
-__device__ __forceinline__ void c_mbar_wait(uint32_t b, uint32_t ph) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(b),
-        "r"(ph)
-        : "memory");
-}
-__device__ __forceinline__ void c_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+using stree::tc::mbar_arrive;
+using stree::tc::mbar_expect_tx;
+using stree::tc::mbar_init;
+using stree::tc::mbar_wait;
+using stree::tc::smem_u32;
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                  : "memory");
@@ -93,7 +83,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
     int* spath = (int*)(decay + kCHPC);                 // [kMaxNodes]
     int* sr = spath + kMaxNodes;                        // [1]
     unsigned long long* bars = (unsigned long long*)(((uintptr_t)(sr + 1) + 7) & ~(uintptr_t)7);
-    const uint32_t bar0 = su32(bars);
+    const uint32_t bar0 = smem_u32(bars);
     auto bar_full = [&](int s) { return bar0 + 8 * s; };
     auto bar_empty = [&](int s) { return bar0 + 8 * (prm.slots + s); };
     const size_t base = ((size_t)b * H + hbeg) * (size_t)blk;
@@ -102,8 +92,8 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
 
     if (tid == 0) {
         for (int s = 0; s < prm.slots; ++s) {
-            c_mbar_init(bar_full(s), 1);
-            c_mbar_init(bar_empty(s), kCompute / 32);
+            mbar_init(bar_full(s), 1);
+            mbar_init(bar_empty(s), kCompute / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -115,15 +105,15 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
             int k = 0;
             if (prm.early_state)   // the state is not written by the preceding kernel: stream it now
                 for (; k < nh && k < prm.slots; ++k) {
-                    c_mbar_expect_tx(bar_full(k), blk_bytes);
-                    c_bulk_load(su32(ring + (size_t)k * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(k));
+                    mbar_expect_tx(bar_full(k), blk_bytes);
+                    bulk_load_1d(smem_u32(ring + (size_t)k * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(k));
                 }
             pdl_wait();
             for (; k < nh; ++k) {
                 const int s = k % prm.slots;
-                c_mbar_wait(bar_empty(s), ((k / prm.slots) & 1) ^ 1);
-                c_mbar_expect_tx(bar_full(s), blk_bytes);
-                c_bulk_load(su32(ring + (size_t)s * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(s));
+                mbar_wait(bar_empty(s), ((k / prm.slots) & 1) ^ 1);
+                mbar_expect_tx(bar_full(s), blk_bytes);
+                bulk_load_1d(smem_u32(ring + (size_t)s * blk), prm.h0 + base + (size_t)k * blk, blk_bytes, bar_full(s));
             }
         }
         return;
@@ -218,7 +208,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
         float* dst = prm.h_new + base + (size_t)k * blk;
         float4 v[8];
         if (prm.h0) {
-            c_mbar_wait(bar_full(s), (k / prm.slots) & 1);
+            mbar_wait(bar_full(s), (k / prm.slots) & 1);
             if (tr && tid == 32 && k < 16) tr[4 + 2 * k] = c_gtimer();
             const float4* src = reinterpret_cast<const float4*>(ring + (size_t)s * blk);
 #pragma unroll
@@ -227,7 +217,7 @@ __global__ void __launch_bounds__(kCThreads, 1) commit_ring_kernel(const CommitP
                 v[q] = e < nvec ? src[e] : make_float4(0, 0, 0, 0);
             }
             __syncwarp();
-            if (lane == 0) c_mbar_arrive(bar_empty(s));
+            if (lane == 0) mbar_arrive(bar_empty(s));
         } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = make_float4(0, 0, 0, 0);

@@ -15,13 +15,17 @@
 // epilogue applies the single row factor e^{Λ_i}.  Heads with deeper decay use
 // the direct per-element e^{Λ_i-Λ_j} with Y' in separate TMEM columns.
 //
-// One CTA = one tree and a range of heads of one group (grid = B x G x chunks),
-// 192 threads, warp-specialised:
-//   warp 0      TMA producer: C, B once; then per head h0_h (4 boxes) + x_h, NSTAGE-deep ring
-//   warp 1      tcgen05.mma issuer (one elected thread) + TMEM allocator
-//   warps 2-5   tree / segsum prologue, C -> tf32 conversion; then warps 2,3 build the
-//               masked weights of head k+1 while warps 4,5 (TMEM lanes 0..63) run the
-//               TMEM -> register epilogue of head k and the TMA store of y
+// One CTA = one tree and a range of heads of one group (grid = B x G x chunks, <= #SMs CTAs),
+// warp-specialised, 320 threads (scan) / 352 threads (fused replay + scan, MODE 1; commit only, MODE 2):
+//   warp 0        TMA producer: C, B once; then per head the 32 KB state (4 boxes) into a 4-slot ring and
+//                 the x tile into the x ring
+//   warp 1        tcgen05.mma issuer (one elected lane of a converged warp) + TMEM allocator (512 columns)
+//   warps 2-3     (+ 6-7 in the scan) masked weights M' of head k+1 from G rows in TMEM lanes 64-127
+//   warps 4-5     (+ 8-9 in the scan) epilogue of head k (TMEM lanes 0-63 = tree nodes) and the x stream
+//   warps 6-9     (MODE 1/2) activation replay of the previous tree's accepted path on each state slot
+//   warp 10       (MODE 1/2) TMA store of the committed state slot (in place)
+// The tree / segsum prologue runs on the builder and epilogue warps before the first head (before the
+// dependency wait under the STREE_LAUNCH_EARLY_* promises).  DESIGN.md §6 (K2, K2f, K4p) has the details.
 // Rows are the tree nodes (M = 128 with rows >= T ignored; every MMA row is
 // independent so the unused rows may read arbitrary shared memory).
 //

@@ -8,13 +8,14 @@
 //     y_i = e^{Λ_i} Y0_i + Y'_i + D_h x_i     (direct decay, M'_ij = e^{min(Λ_i-Λ_j,0)} dt_j G_ij, otherwise)
 // but with the tree's nodes in all 128 TMEM lanes (K2 puts them in lanes 0-63 and a copy of G in 64-127),
 // so trees of up to 128 nodes stay on the tensor cores instead of the FP32 SIMT kernel.  A simpler pipeline
-// than K2: one CTA per (tree, chunk of <= 10 heads of one group), 192 threads —
-//   warps 0-3  thread = node = TMEM lane: tree prologue (validation, ancestor bits and Λ of every head by
-//              pointer jumping), C -> tf32 into TMEM, then per head the masked weights M' (G row from TMEM
-//              -> bf16 swizzle-128B K-major smem tile) and the epilogue of the previous head
-//   warp 4     TMA producer: C, B once; per head the 32 KB fp32 state (4 boxes) and the x tile, 2-stage rings
-//   warp 5     tcgen05.mma issuer + TMEM allocator (512 columns: G 0-127, C tf32 128-255, two head slots of
+// than K2: one CTA per (tree, chunk of <= 10 heads of one group, 128-row tile of nodes), 352 threads —
+//   warps 0-7  math, two per TMEM lane quadrant (thread = node = TMEM lane, the pair split over column halves):
+//              tree prologue (validation, ancestor bits and Λ of every head by pointer jumping), C -> tf32 into
+//              TMEM, then per head the masked weights and the epilogue of the previous head
+//   warp 8     TMA producer: C, B once; per head the 32 KB fp32 state (4 boxes) and the x tile, 2-stage rings
+//   warp 9     tcgen05.mma issuer + TMEM allocator (512 columns: G 0-127, C tf32 128-255, two head slots of
 //              Y0 / Y' accumulators 256-511)
+//   warp 10    y tiles staged in shared memory, TMA-stored
 // Served: bf16 io, P = 64, N = 128, 1 <= T <= 256 (dispatched for T > 64).  NKB = 2 (128 < T <= 256): each
 // CTA owns one 128-row tile of nodes (rt = 0, 1); its keys are the nodes 0 .. 128·rt + 127 (topological order:
 // every ancestor precedes its descendants), G = C_rows·Bᵀ takes 256 TMEM columns, so one accumulator slot,

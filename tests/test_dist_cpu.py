@@ -72,3 +72,45 @@ def test_gloo_world2_gather_and_max():
     assert [r[1] for r in res] == [True, True]
     assert [r[2] for r in res] == [2.5, 2.5]
     assert [r[3] for r in res] == [(0, 8), (8, 16)]
+
+
+def _scan_worker(rank, world, port, q):
+    """Head-sharded layer on the CPU oracle: each rank scans its shard of heads (with its groups' B / C), the
+    shards are all-gathered over gloo and re-laid out as [B][T][H][P] — must equal the unsharded scan."""
+    import numpy as np
+
+    import oracle
+    from gen import inputs, trees
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        B, T, H, P, N, G = 2, 9, 8, 4, 8, 2
+        par = np.stack([trees.random_recursive(T, 3, rng) for _ in range(B)])
+        prob = inputs.make_problem(inputs.Dims(B, T, H, P, N, G, "f32"), par, seed=21)
+        y_full, _ = oracle.tree_scan(prob.x, prob.dt, prob.A, prob.Bm, prob.Cm, prob.D, prob.h0, par, n_groups=G)
+        lo, hi = sd.shard_heads(H, G, world, rank)
+        hpg = H // G
+        glo, ghi = lo // hpg, hi // hpg   # the shard's groups (heads of a group are contiguous, never split)
+        y_sh, _ = oracle.tree_scan(prob.x[:, :, lo:hi], prob.dt[:, :, lo:hi], prob.A[lo:hi], prob.Bm[:, :, glo:ghi],
+                                   prob.Cm[:, :, glo:ghi], prob.D[lo:hi], prob.h0[:, lo:hi], par, n_groups=ghi - glo)
+        g = sd.gather_heads(torch.from_numpy(np.ascontiguousarray(y_sh)))
+        y = sd.heads_to_layer(g).numpy()
+        q.put((rank, bool(np.array_equal(y, y_full)), (lo, hi)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_head_sharded_scan_equals_unsharded():
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_scan_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [True, True]
+    assert [r[2] for r in res] == [(0, 4), (4, 8)]
