@@ -18,10 +18,20 @@ __global__ void k(float* out, int iters) {
                 uint32_t v = __float_as_uint(a[i]);
                 asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v));
                 a[i] = __uint_as_float(v);
-            } else {                // packed bf16x2
+            } else if (MODE == 3) {   // packed bf16x2
                 uint32_t v = __float_as_uint(a[i]);
                 asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v));
                 a[i] = __uint_as_float(v);
+            } else if (MODE == 4) {   // cvt.rn.bf16x2.f32 (the attention softmax's P packing): pipe and rate
+                uint32_t v;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(a[i]), "f"(a[(i + 1) & 15]));
+                a[i] = __uint_as_float(v ^ 0x3f800000u);
+            } else {                  // one ex2 + one bf16x2 cvt per element: do they share a pipe?
+                float e;
+                asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a[i]));
+                uint32_t v;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(v) : "f"(e), "f"(a[(i + 1) & 15]));
+                a[i] = __uint_as_float(v ^ 0x3f800000u);
             }
         }
     }
@@ -38,12 +48,12 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const int iters = 4096;
-    for (int mode = 0; mode < 4; ++mode)
+    for (int mode = 0; mode < 6; ++mode)
         for (int tpb : {128, 256, 512, 1024}) {
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
-            auto kk = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : k<3>;
+            auto kk = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : mode == 3 ? k<3> : mode == 4 ? k<4> : k<5>;
             kk<<<sms * 2, tpb>>>(d, 16);
             cudaEventRecord(e0);
             kk<<<sms * 2, tpb>>>(d, iters);
@@ -51,10 +61,10 @@ int main() {
             cudaEventSynchronize(e1);
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
-            const double ops = (double)sms * 2 * tpb * iters * 16 * (mode >= 2 ? 2 : 1);   // exps (2 per packed op)
+            const double ops = (double)sms * 2 * tpb * iters * 16 * (mode == 2 || mode == 3 ? 2 : 1);   // exps (2 per packed op); mode 4: cvt instructions
             const double per_clk_sm = ops / (ms * 1e-3) / (clk * 1e3) / sms;
             printf("%s threads/CTA %4d (2 CTAs/SM): %.1f ops/clk/SM (at the %d MHz rated clock)\n",
-                   mode == 0 ? "ex2.approx.ftz.f32   " : mode == 1 ? "fma.rn.f32           " : mode == 2 ? "ex2.approx.f16x2 (x2)" : "ex2.bf16x2 (x2)      ", tpb, per_clk_sm, clk / 1000);
+                   mode == 0 ? "ex2.approx.ftz.f32   " : mode == 1 ? "fma.rn.f32           " : mode == 2 ? "ex2.approx.f16x2 (x2)" : mode == 3 ? "ex2.bf16x2 (x2)      " : mode == 4 ? "cvt.rn.bf16x2.f32    " : "ex2 + cvt (ex2 rate) ", tpb, per_clk_sm, clk / 1000);
         }
     return 0;
 }
