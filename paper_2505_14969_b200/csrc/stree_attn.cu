@@ -6,7 +6,10 @@
 //   o[b][i][h] = softmax_j( scale <q_i,h , key_j> ) value_j,
 //   keys(i)    = k_cache[b][0 : cache_len[b]]  ++  k_new[b][path(i)]        (kv head h / (Hq/Hkv))
 //
-// Two kernels serve stree_tree_attn:
+// Kernels serving stree_tree_attn:
+//   attn_db_kernel   (default for bf16, head dim 128) the layout below with 64-key K/V tiles and two score
+//                    buffers per query tile, so S_w(j+2) is computed while the softmax works on S_w(j+1)
+//                    (K7b, further down; STREE_ATTN_DB=0 selects attn_tc_kernel).
 //   attn_tc_kernel   bf16, head dim 128, (Hq/Hkv) | 128: flash attention on tcgen05.  One CTA per
 //                    (tree, kv head, pair of 128-row query tiles); query rows are (node, q head of
 //                    the group) so the GQA group shares every K/V tile.  Warp 0: TMA producer
@@ -625,6 +628,351 @@ __global__ void __launch_bounds__(SPLIT ? kThreadsSplit : kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// K7b attn_db_kernel (bf16, D = 128): 64-key K/V tiles with double-buffered scores.  Same rows, mask and
+// online softmax as attn_tc_kernel, but every query tile owns two 64-column score buffers in TMEM (tile w:
+// columns [128w, 128w + 64) and [128w + 64, 128w + 128); O at [256 + 128w, +128)), so the tensor core
+// computes S_w(j+2) into the buffer just released by P_w(j)·V while the softmax works on S_w(j+1): the
+// softmax never waits for its next scores, and the MUFU-bound exp phases of the two tiles overlap the
+// tensor core instead of alternating with it.  Per KV tile j and query tile w the MMA warp issues
+//   [wait P_w(j)] O_w += P_w(j)·V_j (4 MMAs, K = 64), commit odone_w;  S_w(j+2) = Q_w·K_{j+2}ᵀ (8 MMAs,
+//   N = 64) into buffer j & 1, commit sfull_w[j & 1]
+// (in-order tensor pipe: S_w(j+2) overwrites P_w(j) only after the PV has read it).  The lazy O rescale of
+// iteration j first waits odone_w for PV_w(j-1) (the only PV that can still be in flight).
+// ---------------------------------------------------------------------------
+constexpr int kBN2 = 64;                 // keys per K/V tile
+constexpr int kStages2 = 4;              // K/V ring depth (same bytes as 2 x 128 keys)
+constexpr int kHalfK2 = kBN2 * 128;      // 64 keys x 64 elements (128 B rows), swizzle-128B = 8 KB
+constexpr int kTileK2 = 2 * kHalfK2;     // 64 keys x 128 elements
+
+struct Smem2 {
+    static constexpr int Q = 0;                          // 2 query tiles (kTile each)
+    static constexpr int K = Q + 2 * kTile;              // kStages2 key tiles
+    static constexpr int V = K + kStages2 * kTileK2;     // kStages2 value tiles
+    static constexpr int PAR = V + kStages2 * kTileK2;   // parent[256] int
+    static constexpr int ANC = PAR + kMaxNodes * 4;      // ancestor bits of each softmax row: [8 words][256 rows]
+    static constexpr int BAR = ANC + kMaxWords * 256 * 4;
+    // barriers: q, kfull[4], kempty[4], vfull[4], vempty[4], sfull[2 tiles][2 bufs], pfull[2][2], odone[2], ofull[2]
+    static constexpr int NBAR = 1 + 4 * kStages2 + 4 + 4 + 2 + 2;
+    static constexpr int TMEMP = BAR + NBAR * 8;
+    static constexpr int TOTAL = TMEMP + 16;
+    static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_db_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
+                   const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
+                   const __grid_constant__ CUtensorMap tm_vn, const AttnParams prm) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sb = smem_u32(sm);
+    const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+    const int T = prm.T, Hq = prm.Hq, Hkv = prm.Hkv, grp = Hq / Hkv;
+    const int b = blockIdx.x / (Hkv * prm.npairs);
+    const int rem = blockIdx.x % (Hkv * prm.npairs);
+    const int kvh = rem / prm.npairs, pr = rem % prm.npairs;
+    const int nmt = (T * grp + kBM - 1) / kBM;
+    const int nw = min(2, nmt - 2 * pr);               // query tiles of this CTA (1 or 2)
+
+    const uint32_t bar0 = sb + Smem2::BAR;
+    const uint32_t BAR_Q = bar0;
+    auto bar_kfull = [&](int s) { return bar0 + 8 + 8 * s; };
+    auto bar_kempty = [&](int s) { return bar0 + 8 + 8 * kStages2 + 8 * s; };
+    auto bar_vfull = [&](int s) { return bar0 + 8 + 16 * kStages2 + 8 * s; };
+    auto bar_vempty = [&](int s) { return bar0 + 8 + 24 * kStages2 + 8 * s; };
+    const uint32_t bar1 = bar0 + 8 + 32 * kStages2;
+    auto bar_sfull = [&](int w, int u) { return bar1 + 8 * (2 * w + u); };
+    auto bar_pfull = [&](int w, int u) { return bar1 + 32 + 8 * (2 * w + u); };
+    auto bar_odone = [&](int w) { return bar1 + 64 + 8 * w; };
+    auto bar_ofull = [&](int w) { return bar1 + 80 + 8 * w; };
+    uint32_t* tmem_slot = (uint32_t*)(sm + Smem2::TMEMP);
+    int* sp = (int*)(sm + Smem2::PAR);
+
+    if (tid == 0) {
+        mbar_init(BAR_Q, 1);
+        for (int s = 0; s < kStages2; ++s) {   // a K / V stage is free once every query tile has consumed it
+            mbar_init(bar_kfull(s), 1);
+            mbar_init(bar_kempty(s), nw);
+            mbar_init(bar_vfull(s), 1);
+            mbar_init(bar_vempty(s), nw);
+        }
+        for (int w = 0; w < 2; ++w) {
+            for (int u = 0; u < 2; ++u) {
+                mbar_init(bar_sfull(w, u), 1);
+                mbar_init(bar_pfull(w, u), 128);
+            }
+            mbar_init(bar_odone(w), 1);
+            mbar_init(bar_ofull(w), 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    int n_early = 0;
+    auto issue_kv = [&](int j, bool pre, int key0) {
+        const int s = j % kStages2;
+        mbar_expect_tx(bar_kfull(s), kTileK2);
+        for (int hf = 0; hf < 2; ++hf)
+            tma_load_4d(sb + Smem2::K + s * kTileK2 + hf * kHalfK2, pre ? &tm_kc : &tm_kn, bar_kfull(s), 64 * hf, kvh, key0, b);
+        mbar_expect_tx(bar_vfull(s), kTileK2);
+        for (int hf = 0; hf < 2; ++hf)
+            tma_load_4d(sb + Smem2::V + s * kTileK2 + hf * kHalfK2, pre ? &tm_vc : &tm_vn, bar_vfull(s), 64 * hf, kvh, key0, b);
+    };
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_q); tma_prefetch(&tm_kc); tma_prefetch(&tm_vc); tma_prefetch(&tm_kn); tma_prefetch(&tm_vn);
+        if (prm.early) {   // EARLY_STATE: the first prefix tiles before the dependency wait (as attn_tc_kernel)
+            const int Le = prm.cache_len[b];
+            if (Le > 0 && Le <= prm.S) {
+                n_early = min(kStages2, (Le + kBN2 - 1) / kBN2);
+                for (int j = 0; j < n_early; ++j) issue_kv(j, true, j * kBN2);
+            }
+        }
+    }
+    pdl_wait();
+    // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length
+    int bad = 0;
+    for (int v = tid; v < T; v += (int)blockDim.x) {
+        const int p = prm.parent[(size_t)b * T + v];
+        sp[v] = p;
+        if (v == 0 ? p != -1 : (p < 0 || p >= v)) bad = v == 0 ? 1 : 2;
+    }
+    const int L = prm.cache_len[b];
+    const int any1 = __syncthreads_or(bad == 1);
+    const int any2 = __syncthreads_or(bad == 2);
+    int code = any1 ? 1 : (any2 ? 2 : ((L < 0 || L > prm.S) ? kDev_Capacity : 0));
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int npre = code ? 0 : (L + kBN2 - 1) / kBN2;   // prefix tiles
+    const int ntr = (T + kBN2 - 1) / kBN2;               // tree tiles
+    const int nt = npre + ntr;
+
+    if (code) {
+        if (tid == 0 && rem == 0) report(prm.dev_status, code);
+        if (warp == 0 && lane == 0)   // drain the early loads before the CTA exits
+            for (int j = 0; j < n_early; ++j) {
+                mbar_wait(bar_kfull(j), 0);
+                mbar_wait(bar_vfull(j), 0);
+            }
+        if (warp >= 2) {   // zero this CTA's output rows
+            const int w = (warp - 2) >> 2, r = 32 * (warp & 3) + lane;
+            if (w < nw) {
+                const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
+                if (i < T) {
+                    uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD);
+#pragma unroll
+                    for (int c = 0; c < kD / 8; ++c) orow[c] = make_uint4(0, 0, 0, 0);
+                }
+            }
+        }
+    } else if (warp == 0) {
+        // ---- TMA producer ----
+        if (lane == 0) {
+            mbar_expect_tx(BAR_Q, nw * kTile);
+            for (int w = 0; w < nw; ++w) {
+                const int node0 = (2 * pr + w) * (kBM / grp);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(sb + Smem2::Q + w * kTile + hf * kHalf, &tm_q, BAR_Q, 64 * hf, kvh * grp, node0, b);
+            }
+            for (int j = n_early; j < nt; ++j) {
+                const int s = j % kStages2, u = j / kStages2;
+                const bool pre = j < npre;
+                const int key0 = pre ? j * kBN2 : (j - npre) * kBN2;
+                mbar_wait(bar_kempty(s), (u & 1) ^ 1);
+                mbar_wait(bar_vempty(s), (u & 1) ^ 1);
+                issue_kv(j, pre, key0);
+            }
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer (whole warp converged, one elected lane issues) ----
+        const uint32_t id_s = idesc(kFmtBF16, 0, kBM, kBN2);   // S = Q·Kᵀ: A, B K-major, N = 64 keys
+        const uint32_t id_o = idesc(kFmtBF16, 1, kBM, kD);     // O += P·V: A in TMEM, B (V) MN-major
+        auto issue_s = [&](int w, int j) {   // S_w(j) into score buffer j & 1 of tile w
+            const int s = j % kStages2;
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint64_t ad = sdesc(sb + Smem2::Q + w * kTile + (kk >> 2) * kHalf, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                const uint64_t bd = sdesc(sb + Smem2::K + s * kTileK2 + (kk >> 2) * kHalfK2, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                mma_f16_w(tmem + 128 * w + 64 * (j & 1), ad, bd, id_s, kk > 0);
+            }
+            tc_commit_w(bar_sfull(w, j & 1));
+        };
+        mbar_wait(BAR_Q, 0);
+        for (int j = 0; j < 2 && j < nt; ++j) {   // the first two score tiles of both query tiles
+            mbar_wait(bar_kfull(j % kStages2), (j / kStages2) & 1);
+            tc_fence_after();
+            for (int w = 0; w < nw; ++w) {
+                issue_s(w, j);
+                tc_commit_w(bar_kempty(j % kStages2));
+            }
+        }
+        // the tiles in turn (a first-ready order with non-blocking barrier tests measured slower: 42.8 vs 31.8 µs,
+        // the polling issuer takes issue slots from the softmax warps of its sub-partition)
+        for (int j = 0; j < nt; ++j) {
+            const int s = j % kStages2, u = j / kStages2;
+            const int j2 = j + 2, s2 = j2 % kStages2, u2 = j2 / kStages2;
+            for (int w = 0; w < nw; ++w) {
+                mbar_wait(bar_pfull(w, j & 1), (j >> 1) & 1);
+                if (w == 0) mbar_wait(bar_vfull(s), u & 1);
+                tc_fence_after();
+                const uint64_t vd = sdesc(sb + Smem2::V + s * kTileK2, kHalfK2, 1024);
+#pragma unroll
+                for (int kk = 0; kk < kBN2 / 16; ++kk)
+                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 64 * (j & 1) + 8 * kk, vd + (uint64_t)(kk * 128), id_o,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+                tc_commit_w(bar_odone(w));
+                tc_commit_w(bar_vempty(s));
+                if (j == nt - 1) tc_commit_w(bar_ofull(w));
+                if (j2 < nt) {
+                    if (w == 0) {
+                        mbar_wait(bar_kfull(s2), u2 & 1);
+                        tc_fence_after();
+                    }
+                    issue_s(w, j2);
+                    tc_commit_w(bar_kempty(s2));
+                }
+            }
+        }
+    } else {
+        // ---- softmax: thread = query row = TMEM lane ----
+        const int w = (warp - 2) >> 2, q4 = warp & 3, r = 32 * q4 + lane;
+        if (w < nw) {
+            const int rr = (2 * pr + w) * kBM + r, i = rr / grp, hg = rr % grp;
+            const bool vrow = i < T;
+            // ancestor bits of the row's node, word-major in smem (conflict-free reads)
+            uint32_t* sanc = (uint32_t*)(sm + Smem2::ANC) + 128 * w + r;
+            {
+                uint32_t anc[kMaxWords];
+#pragma unroll
+                for (int q = 0; q < kMaxWords; ++q) anc[q] = 0u;
+                if (vrow)
+                    for (int v = i; v >= 0; v = sp[v]) {
+#pragma unroll
+                        for (int q = 0; q < kMaxWords; ++q) anc[q] |= ((v >> 5) == q) ? (1u << (v & 31)) : 0u;
+                    }
+#pragma unroll
+                for (int q = 0; q < kMaxWords; ++q) sanc[256 * q] = anc[q];
+            }
+            const uint32_t lane_base = tmem + ((uint32_t)(32 * q4) << 16);
+            const uint32_t t_o = lane_base + 256 + 128 * w;
+            const float sl2 = prm.scale_log2;
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < nt; ++j) {
+                const int buf = j & 1;
+                const uint32_t t_s = lane_base + 128 * w + 64 * buf;
+                mbar_wait(bar_sfull(w, buf), (j >> 1) & 1);
+                tc_fence_after();
+                // valid-key bits of this row in the tile, one word per 32-column chunk: committed prefix keys
+                // [0, lim), or tree nodes on the row's root path
+                const bool pre = j < npre;
+                const int lim = pre ? L - j * kBN2 : T - (j - npre) * kBN2;
+                const uint32_t* aw = sanc + 256 * 2 * (pre ? 0 : j - npre);
+                const bool full = pre && lim >= kBN2;   // full prefix tile: no masking
+                auto valid_word = [&](int cg) -> uint32_t {
+                    const int n = lim - 32 * cg;
+                    uint32_t vw = n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+                    if (!pre) vw &= aw[256 * cg];
+                    return vw;
+                };
+                uint32_t sr[64];
+                tmem_ld32(t_s, sr);
+                tmem_ld32(t_s + 32, sr + 32);
+                tmem_wait();
+                if (!full) {   // partial tile: masked scores -> -inf
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const uint32_t vw = valid_word(c);
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) sr[32 * c + e] = ((vw >> e) & 1u) ? sr[32 * c + e] : 0xff800000u;
+                    }
+                }
+                // row max: 8 independent FMNMX3 chains
+                float m8[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) m8[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+                for (int e = 16; e < 64; e += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2)
+                        m8[k >> 1] = fmax3(m8[k >> 1], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+#pragma unroll
+                for (int e = 24; e < 64; e += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2)
+                        m8[4 + (k >> 1)] = fmax3(m8[4 + (k >> 1)], __uint_as_float(sr[e + k]), __uint_as_float(sr[e + k + 1]));
+                float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+                mx *= sl2;   // scale > 0
+                // lazy rescaling: keep the running max unless the new one exceeds it by > 8 (log2 units); the
+                // rescale of O waits for PV_w(j-1), the only P·V that can still be accumulating into O
+                const bool need = mx > m_run + 8.f;
+                const float alpha = need ? (m_run == -INFINITY ? 0.f : ex2(m_run - mx)) : 1.f;
+                if (need) m_run = mx;
+                l_run *= alpha;
+                if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+                    mbar_wait(bar_odone(w), (j - 1) & 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < kD / 32; ++c) {
+                        uint32_t orr[32];
+                        tmem_ld32(t_o + 32 * c, orr);
+                        tmem_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+                        tmem_st32(t_o + 32 * c, orr);
+                    }
+                    tmem_st_wait();
+                }
+                const float mu = m_run == -INFINITY ? 0.f : m_run;
+                // p = 2^(s·scale·log2e - m) (masked: 2^-inf = 0); paired FFMA2, 4 FADD2 sum chains; bf16 P packed
+                // in place over the consumed scores, then written over the buffer's first 32 columns
+                const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(-mu, -mu);
+                uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const uint64_t a2 = ffma2(f2pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nm2);
+                    const float p0 = ex2(__uint_as_float((uint32_t)a2));
+                    const float p1 = ex2(__uint_as_float((uint32_t)(a2 >> 32)));
+                    acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
+                    sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
+                }
+                tmem_st32(t_s, sr);
+                const uint64_t a01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                l_run += __uint_as_float((uint32_t)a01) + __uint_as_float((uint32_t)(a01 >> 32));
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(bar_pfull(w, buf));
+            }
+            // epilogue: O / l -> bf16 -> global
+            mbar_wait(bar_ofull(w), 0);
+            tc_fence_after();
+            const float inv = 1.f / l_run;
+            uint4* orow = (uint4*)(prm.o + (((size_t)b * T + i) * Hq + kvh * grp + hg) * kD);
+#pragma unroll 1
+            for (int c = 0; c < kD / 32; ++c) {
+                uint32_t orr[32];
+                tmem_ld32(t_o + 32 * c, orr);
+                tmem_wait();
+                if (vrow) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float* f = reinterpret_cast<const float*>(orr + 8 * e);
+                        orow[4 * c + e] = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                                                     pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K8 KV commit: append the accepted path's K/V rows to the cache (one CTA per tree)
 // ---------------------------------------------------------------------------
 template <typename W>
@@ -721,6 +1069,23 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
         prm.scale_log2 = scale * 1.4426950408889634f;
         prm.trace = g_attn_trace;
         prm.early = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
+        static const int dbuf = [] {
+            const char* v = std::getenv("STREE_ATTN_DB");   // 1 (default): 64-key double-buffered kernel
+            return v && v[0] ? std::atoi(v) : 1;
+        }();
+        if (dbuf) {
+            CUtensorMap mkc2, mvc2, mkn2, mvn2;
+            if (!(make_map4(&mkc2, k_cache, D, Hkv, S, B, 1, kBN2) && make_map4(&mvc2, v_cache, D, Hkv, S, B, 1, kBN2) &&
+                  make_map4(&mkn2, k_new, D, Hkv, T, B, 1, kBN2) && make_map4(&mvn2, v_new, D, Hkv, T, B, 1, kBN2)))
+                return (int)cudaErrorInvalidValue;
+            const size_t smem2 = Smem2::TOTAL + 1024;
+            e = stree::host::smem_attr((const void*)attn_db_kernel, (int)smem2);
+            if (e != cudaSuccess) return (int)e;
+            e = stree::launch_k(attn_db_kernel, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem2, s, mq, mkc2, mvc2,
+                                mkn2, mvn2, prm);
+            if (e != cudaSuccess) return (int)e;
+            return (int)cudaGetLastError();
+        }
         const size_t smem = Smem::TOTAL + 1024;
         static const int poly = [] {
             const char* v = std::getenv("STREE_ATTN_POLY");   // tuning knob; default 0 (measured best)

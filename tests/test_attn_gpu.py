@@ -251,3 +251,26 @@ def test_early_kv_prefetch_flag():
         check(o[1:], ref[1:], TOL_BF16)
     finally:
         binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
+
+
+def test_tc_128key_kernel_still_matches(tmp_path):
+    """The default tcgen05 kernel is the 64-key double-buffered one (attn_db_kernel); the 128-key kernel stays
+    selectable (STREE_ATTN_DB=0, read once per process), so check it in a child process."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, tests.test_attn_gpu as t\n"
+        "from paper_2505_14969_b200 import binding\n"
+        "binding.lib()\n"
+        "for seed, (B, T, L) in enumerate([(2, 64, 900), (3, 37, 0), (1, 200, 300)]):\n"
+        "    p = t.make_case(B, T, 32, 8, 128, 1280, 'bf16', 40 + seed, cache_len=[L] * B)\n"
+        "    o, st = t.run_gpu(p)\n"
+        "    ref, _ = t.run_oracle(p)\n"
+        "    assert st == 0\n"
+        "    t.check(o, ref, t.TOL_BF16)\n"
+        "print('ok')\n")
+    env = dict(os.environ, STREE_ATTN_DB="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
