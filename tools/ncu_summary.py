@@ -31,7 +31,8 @@ API = {"lat_kernel<128, 1": "stree_replay_scan", "lat_kernel<64, 1": "stree_repl
        "commit_ring_kernel": "stree_commit", "commit_block_kernel": "stree_commit",
        "build_mask_kernel": "stree_build_mask", "accept_kernel": "stree_accept",
        "attn_tc_kernel": "stree_tree_attn", "attn_simt_kernel": "stree_tree_attn", "kv_commit_kernel": "stree_kv_commit",
-       "tree_conv_kernel": "stree_tree_conv", "conv_commit_kernel": "stree_conv_commit", "mss_kernel": "stree_accept_mss"}
+       "tree_conv_kernel": "stree_tree_conv", "conv_commit_kernel": "stree_conv_commit", "mss_kernel": "stree_accept_mss",
+       "attn_db_kernel": "stree_tree_attn"}
 
 
 def api_name(k):
