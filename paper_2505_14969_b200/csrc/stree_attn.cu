@@ -986,21 +986,33 @@ __global__ void __launch_bounds__(256) kv_commit_kernel(const W* __restrict__ k_
     __shared__ int s_path[kMaxNodes];
     pdl_wait();
     const int b = blockIdx.x, tid = threadIdx.x;
-    if (tid == 0) {
+    // path validation in parallel (root-anchored, parent-linked: warp 0, 32 path nodes per round, all loads of a
+    // round in flight together) — a serial walk cost two dependent DRAM latencies per path node
+    if (tid < 32) {
         const int r = path_len[b], L = cache_len[b];
         int ok = (r >= 1 && r <= T) ? 1 : 0;
-        for (int s = 0; ok && s < r; ++s) {
-            const int v = path[(size_t)b * T + s];
-            if (v < 0 || v >= T) ok = 0;
-            else if (s == 0 ? v != 0 : (parent && parent[(size_t)b * T + v] != s_path[s - 1])) ok = 0;
-            else s_path[s] = v;
+        if (ok) {
+            for (int s0 = 0; s0 < r; s0 += 32) {
+                const int s = s0 + tid;
+                int v = -1, pv = -1, par = -2;
+                if (s < r) {
+                    v = path[(size_t)b * T + s];
+                    pv = s > 0 ? path[(size_t)b * T + s - 1] : -1;
+                    if (v >= 0 && v < T) par = parent ? parent[(size_t)b * T + v] : pv;
+                }
+                bool good = s >= r || (v >= 0 && v < T && (s == 0 ? v == 0 : par == pv));
+                if (s < r && good) s_path[s] = v;
+                if (!__all_sync(0xffffffffu, good)) { ok = 0; break; }
+            }
         }
-        int code = ok ? 0 : STREE_DEV_BAD_PATH;
-        if (ok && (L < 0 || L + r > S)) code = kDev_Capacity;
-        if (code) report(dev_status, code);
-        s_ok = code == 0;
-        s_L = L;
-        s_r = r;
+        if (tid == 0) {
+            int code = ok ? 0 : STREE_DEV_BAD_PATH;
+            if (ok && (L < 0 || L + r > S)) code = kDev_Capacity;
+            if (code) report(dev_status, code);
+            s_ok = code == 0;
+            s_L = L;
+            s_r = r;
+        }
     }
     __syncthreads();
     if (!s_ok) return;

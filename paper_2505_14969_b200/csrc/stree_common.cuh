@@ -37,9 +37,12 @@ struct DtX {
         return x;
     }
 };
+// softplus out of line: log1pf inlined at every dt_eff call site was ≈ 450 SASS instructions of the small-batch
+// scan kernel's 4100 (instruction-fetch bound at batch 1), for an option the common path never takes
+static __device__ __noinline__ float softplus_f(float v) { return v > 20.f ? v : log1pf(__expf(v)); }
 __device__ __forceinline__ float dt_eff(const DtX& x, float raw, int h) {
     const float v = x.bias ? raw + x.bias[h] : raw;
-    return x.softplus ? (v > 20.f ? v : log1pf(__expf(v))) : v;
+    return x.softplus ? softplus_f(v) : v;
 }
 
 __device__ __forceinline__ void report(int32_t* dev_status, int code) {

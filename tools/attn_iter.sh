@@ -6,5 +6,5 @@ import bench_next
 from bench import load_peaks
 hbm, bf16, _ = load_peaks()
 r = bench_next.measure(torch.device('cuda',0), hbm, bf16)
-print('db=$db', json.dumps(r['tree_attn']))
+print('db=$db', json.dumps(r['tree_attn']), 'kv_commit', r['kv_commit']['us'])
 "; done
