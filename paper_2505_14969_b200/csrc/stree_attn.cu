@@ -658,7 +658,8 @@ struct Smem2 {
     static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kThreadsDb = 352;   // warp 0 TMA, warps 1 / 10 MMA issuers of query tile 0 / 1, warps 2-9 softmax
+__global__ void __launch_bounds__(kThreadsDb, 1)
     attn_db_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                    const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kn,
                    const __grid_constant__ CUtensorMap tm_vn, const AttnParams prm) {
@@ -784,52 +785,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 issue_kv(j, pre, key0);
             }
         }
-    } else if (warp == 1) {
-        // ---- MMA issuer (whole warp converged, one elected lane issues) ----
-        const uint32_t id_s = idesc(kFmtBF16, 0, kBM, kBN2);   // S = Q·Kᵀ: A, B K-major, N = 64 keys
-        const uint32_t id_o = idesc(kFmtBF16, 1, kBM, kD);     // O += P·V: A in TMEM, B (V) MN-major
-        auto issue_s = [&](int w, int j) {   // S_w(j) into score buffer j & 1 of tile w
-            const int s = j % kStages2;
+    } else if (warp == 1 || warp == 10) {
+        // ---- MMA issuers, one warp per query tile (warp 1: tile 0, warp 10: tile 1; converged, one elected lane
+        // issues): each tile's MMAs are issued and committed by its own thread, so a tile waits only for its own
+        // P and for the K / V ring, never for the other tile (tcgen05.commit tracks the issuing thread's MMAs) ----
+        const int w = warp == 1 ? 0 : 1;
+        if (w < nw) {
+            const uint32_t id_s = idesc(kFmtBF16, 0, kBM, kBN2);   // S = Q·Kᵀ: A, B K-major, N = 64 keys
+            const uint32_t id_o = idesc(kFmtBF16, 1, kBM, kD);     // O += P·V: A in TMEM, B (V) MN-major
+            auto issue_s = [&](int j) {   // S_w(j) into score buffer j & 1 of tile w
+                const int s = j % kStages2;
 #pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk) {
-                const uint64_t ad = sdesc(sb + Smem2::Q + w * kTile + (kk >> 2) * kHalf, 16, 1024) + (uint64_t)((kk & 3) * 2);
-                const uint64_t bd = sdesc(sb + Smem2::K + s * kTileK2 + (kk >> 2) * kHalfK2, 16, 1024) + (uint64_t)((kk & 3) * 2);
-                mma_f16_w(tmem + 128 * w + 64 * (j & 1), ad, bd, id_s, kk > 0);
-            }
-            tc_commit_w(bar_sfull(w, j & 1));
-        };
-        mbar_wait(BAR_Q, 0);
-        for (int j = 0; j < 2 && j < nt; ++j) {   // the first two score tiles of both query tiles
-            mbar_wait(bar_kfull(j % kStages2), (j / kStages2) & 1);
-            tc_fence_after();
-            for (int w = 0; w < nw; ++w) {
-                issue_s(w, j);
+                for (int kk = 0; kk < kD / 16; ++kk) {
+                    const uint64_t ad = sdesc(sb + Smem2::Q + w * kTile + (kk >> 2) * kHalf, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                    const uint64_t bd = sdesc(sb + Smem2::K + s * kTileK2 + (kk >> 2) * kHalfK2, 16, 1024) + (uint64_t)((kk & 3) * 2);
+                    mma_f16_w(tmem + 128 * w + 64 * (j & 1), ad, bd, id_s, kk > 0);
+                }
+                tc_commit_w(bar_sfull(w, j & 1));
+            };
+            mbar_wait(BAR_Q, 0);
+            for (int j = 0; j < 2 && j < nt; ++j) {   // the first two score tiles
+                mbar_wait(bar_kfull(j % kStages2), (j / kStages2) & 1);
+                tc_fence_after();
+                issue_s(j);
                 tc_commit_w(bar_kempty(j % kStages2));
             }
-        }
-        // the tiles in turn (a first-ready order with non-blocking barrier tests measured slower: 42.8 vs 31.8 µs,
-        // the polling issuer takes issue slots from the softmax warps of its sub-partition)
-        for (int j = 0; j < nt; ++j) {
-            const int s = j % kStages2, u = j / kStages2;
-            const int j2 = j + 2, s2 = j2 % kStages2, u2 = j2 / kStages2;
-            for (int w = 0; w < nw; ++w) {
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % kStages2, u = j / kStages2;
+                const int j2 = j + 2, s2 = j2 % kStages2, u2 = j2 / kStages2;
                 mbar_wait(bar_pfull(w, j & 1), (j >> 1) & 1);
-                if (w == 0) mbar_wait(bar_vfull(s), u & 1);
+                mbar_wait(bar_vfull(s), u & 1);
                 tc_fence_after();
                 const uint64_t vd = sdesc(sb + Smem2::V + s * kTileK2, kHalfK2, 1024);
 #pragma unroll
                 for (int kk = 0; kk < kBN2 / 16; ++kk)
-                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 64 * (j & 1) + 8 * kk, vd + (uint64_t)(kk * 128), id_o,
-                                 (j > 0 || kk > 0) ? 1u : 0u);
+                    mma_f16_ts_w(tmem + 256 + 128 * w, tmem + 128 * w + 64 * (j & 1) + 8 * kk, vd + (uint64_t)(kk * 128),
+                                 id_o, (j > 0 || kk > 0) ? 1u : 0u);
                 tc_commit_w(bar_odone(w));
                 tc_commit_w(bar_vempty(s));
                 if (j == nt - 1) tc_commit_w(bar_ofull(w));
                 if (j2 < nt) {
-                    if (w == 0) {
-                        mbar_wait(bar_kfull(s2), u2 & 1);
-                        tc_fence_after();
-                    }
-                    issue_s(w, j2);
+                    mbar_wait(bar_kfull(s2), u2 & 1);
+                    tc_fence_after();
+                    issue_s(j2);
                     tc_commit_w(bar_kempty(s2));
                 }
             }
@@ -1093,7 +1091,7 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
             const size_t smem2 = Smem2::TOTAL + 1024;
             e = stree::host::smem_attr((const void*)attn_db_kernel, (int)smem2);
             if (e != cudaSuccess) return (int)e;
-            e = stree::launch_k(attn_db_kernel, dim3(B * Hkv * prm.npairs), dim3(kThreads), smem2, s, mq, mkc2, mvc2,
+            e = stree::launch_k(attn_db_kernel, dim3(B * Hkv * prm.npairs), dim3(kThreadsDb), smem2, s, mq, mkc2, mvc2,
                                 mkn2, mvn2, prm);
             if (e != cudaSuccess) return (int)e;
             return (int)cudaGetLastError();
