@@ -73,8 +73,10 @@ def measure(dev, hbm_peak, bf16_peak, layers_attn=32, layers_ssm=64):
 
     stream = torch.cuda.Stream(device=dev)
     out = {}
-    # decode-loop launch promise: a layer's KV cache / conv state is not written by the kernel right before it
-    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE)
+    # decode-loop launch promises: a layer's KV cache / conv state and the iteration's tree are not written by the
+    # kernel right before it
+    binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL | binding.STREE_LAUNCH_EARLY_STATE |
+                                   binding.STREE_LAUNCH_EARLY_TREE)
 
     # ---------------- tree attention + KV commit ----------------
     prob = attn_config("hyb8b")

@@ -283,7 +283,8 @@ stree_status stree_set_scan_impl(stree_scan_impl impl);
  *                            mask before the dependency wait, so only the segsum of dt
  *                            and the contractions remain after it.  x, B, C are never read early.
  *                            stree_tree_conv: parent, weight and bias (read, and every node's window
- *                            tabulated, before the wait; only u is read after it).
+ *                            tabulated, before the wait; only u is read after it).  stree_tree_attn (with
+ *                            EARLY_STATE): parent, validated before the wait; q, k_new, v_new after it.
  *  STREE_LAUNCH_EARLY_DT     promise (with EARLY_TREE): dt of a scan call is not written by the kernel
  *                            immediately preceding it.  True in a Mamba-2 layer, where dt comes from the
  *                            input projection and the causal conv1d kernel (which produces x, B, C) runs

@@ -222,6 +222,7 @@ struct AttnParams {
     __nv_bfloat16* o;
     int32_t* dev_status;
     int T, Hq, Hkv, S, npairs, early;
+    int early_tree;   // STREE_LAUNCH_EARLY_TREE with EARLY_STATE: tree validation before the dependency wait (K7b)
     unsigned long long* trace;
     float scale_log2;
 };
@@ -731,8 +732,10 @@ __global__ void __launch_bounds__(kThreadsDb, 1)
             }
         }
     }
-    pdl_wait();
-    // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length
+    // tree validation (PAPER.md:90 ordering, R5) and the committed prefix length: before the dependency
+    // wait under EARLY_TREE + EARLY_STATE (the tree and the cache length are not written by the preceding kernel)
+    const bool early_prologue = prm.early && prm.early_tree;
+    if (!early_prologue) pdl_wait();
     int bad = 0;
     for (int v = tid; v < T; v += (int)blockDim.x) {
         const int p = prm.parent[(size_t)b * T + v];
@@ -742,6 +745,7 @@ __global__ void __launch_bounds__(kThreadsDb, 1)
     const int L = prm.cache_len[b];
     const int any1 = __syncthreads_or(bad == 1);
     const int any2 = __syncthreads_or(bad == 2);
+    if (early_prologue) pdl_wait();
     int code = any1 ? 1 : (any2 ? 2 : ((L < 0 || L > prm.S) ? kDev_Capacity : 0));
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
@@ -1079,6 +1083,7 @@ extern "C" int stree_launch_tree_attn(const stree_attn_dims* d, const void* q, c
         prm.scale_log2 = scale * 1.4426950408889634f;
         prm.trace = g_attn_trace;
         prm.early = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_STATE) ? 1 : 0;
+        prm.early_tree = (stree_launch_flags_get() & STREE_LAUNCH_EARLY_TREE) ? 1 : 0;
         static const int dbuf = [] {
             const char* v = std::getenv("STREE_ATTN_DB");   // 1 (default): 64-key double-buffered kernel
             return v && v[0] ? std::atoi(v) : 1;

@@ -274,3 +274,33 @@ def test_tc_128key_kernel_still_matches(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("flags", [1 | 2, 1 | 2 | 8])
+def test_attn_chain_under_launch_promises(flags):
+    """A chain of dependent calls: each call's q is the previous call's output, written by the kernel right before
+    it.  Under EARLY_STATE (K/V prefetch) + EARLY_TREE (tree validation before the dependency wait) q must still
+    be read after the wait; parity with the oracle chain proves it."""
+    binding.stree_set_launch_flags(flags)
+    try:
+        prob = make_case(3, 64, 32, 8, 128, 1024, "bf16", 71, cache_len=[900, 64, 0])
+        q, kn, vn, kc, vc = (_dev(prob, n) for n in ("q", "k_new", "v_new", "k_cache", "v_cache"))
+        cl = torch.from_numpy(prob.cache_len.astype(np.int32)).cuda()
+        par = torch.from_numpy(prob.parent.astype(np.int32)).cuda()
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        outs = [q]
+        for _ in range(3):
+            o = torch.empty_like(q)
+            binding.stree_tree_attn(outs[-1], kn, vn, kc, vc, cl, par, prob.scale, o, dev_status=st)
+            outs.append(o)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        qi = _f64(prob, "q")
+        for i in range(3):
+            ref, _ = oattn.tree_attn(qi, _f64(prob, "k_new"), _f64(prob, "v_new"), _f64(prob, "k_cache"),
+                                     _f64(prob, "v_cache"), prob.cache_len, prob.parent, prob.scale)
+            got = outs[i + 1].float().cpu().numpy().astype(np.float64)
+            check(got, ref, TOL_BF16)
+            qi = got   # the next call reads exactly what this one wrote (bf16 values)
+    finally:
+        binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
