@@ -640,6 +640,10 @@ __global__ void __launch_bounds__(SPLIT ? kThreadsSplit : kThreads, 1)
 // (in-order tensor pipe: S_w(j+2) overwrites P_w(j) only after the PV has read it).  The lazy O rescale of
 // iteration j first waits odone_w for PV_w(j-1) (the only PV that can still be in flight).
 // ---------------------------------------------------------------------------
+#ifndef STREE_ATTN_DB_POLY
+#define STREE_ATTN_DB_POLY 0
+#endif
+constexpr int kDbPoly = STREE_ATTN_DB_POLY;   // every kDbPoly-th exp pair on the FMA pipe (0: all on the MUFU)
 constexpr int kBN2 = 64;                 // keys per K/V tile
 constexpr int kStages2 = 4;              // K/V ring depth (same bytes as 2 x 128 keys)
 constexpr int kHalfK2 = kBN2 * 128;      // 64 keys x 64 elements (128 B rows), swizzle-128B = 8 KB
@@ -933,8 +937,17 @@ __global__ void __launch_bounds__(kThreadsDb, 1)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const uint64_t a2 = ffma2(f2pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, nm2);
-                    const float p0 = ex2(__uint_as_float((uint32_t)a2));
-                    const float p1 = ex2(__uint_as_float((uint32_t)(a2 >> 32)));
+                    float p0, p1;
+                    if (kDbPoly > 0 && e % kDbPoly == kDbPoly - 1) {   // this pair's 2^x on the FMA pipe
+                        ex2_poly2(a2, p0, p1);
+                        if (!full) {   // the polynomial does not map -inf to 0
+                            p0 = sr[2 * e] == 0xff800000u ? 0.f : p0;
+                            p1 = sr[2 * e + 1] == 0xff800000u ? 0.f : p1;
+                        }
+                    } else {
+                        p0 = ex2(__uint_as_float((uint32_t)a2));
+                        p1 = ex2(__uint_as_float((uint32_t)(a2 >> 32)));
+                    }
                     acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
                     sr[e] = pack_bf16(p0, p1);   // in place: sr[2e], sr[2e+1] are consumed (e <= 2e)
                 }
