@@ -20,6 +20,9 @@ constexpr int kChunks = 32;     // 16-byte channel chunks per conv-commit warp (
 #define STREE_CONV_KC 8
 #endif
 constexpr int kConvKC = STREE_CONV_KC;     // chunks per tree-conv CTA (tree_conv_kernel)
+#ifndef STREE_CONV_MINB
+#define STREE_CONV_MINB 10   // min CTAs per SM at KC = 8 (register cap; 13 / 16, which would let two layers be resident, measured 9.3 / 9.4 vs 6.5 us)
+#endif
 #ifndef STREE_CONV_GROUPS
 #define STREE_CONV_GROUPS 4
 #endif
@@ -131,7 +134,7 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {   // n is a compile-tim
     }
 }
 template <typename IO, int W, int KC, bool ACT, int kGroups>
-__global__ void __launch_bounds__(8 * KC, KC <= 8 ? 10 : KC <= 16 ? 5 : 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
+__global__ void __launch_bounds__(8 * KC, KC <= 8 ? STREE_CONV_MINB : KC <= 16 ? 5 : 3) tree_conv_kernel(const IO* __restrict__ u, const float* __restrict__ weight,
                                                                  const float* __restrict__ bias, const IO* __restrict__ state,
                                                                  const int32_t* __restrict__ parent,
                                                                  IO* __restrict__ out, int T, int C, int32_t* dev_status,
