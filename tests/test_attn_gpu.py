@@ -304,3 +304,35 @@ def test_attn_chain_under_launch_promises(flags):
             qi = got   # the next call reads exactly what this one wrote (bf16 values)
     finally:
         binding.stree_set_launch_flags(binding.STREE_LAUNCH_PDL)
+
+
+@pytest.mark.parametrize("kernel_env", ["1", "0"])
+def test_online_softmax_rescale_mid_stream(kernel_env):
+    """Key tiles whose scores jump far above the running row max (x16 in the score scale, i.e. > 8 in log2
+    units) after the first tiles: the lazy O rescale must run mid-stream — in K7b it first waits for the one
+    P·V that can still be accumulating into O.  Run for both tcgen05 kernels (the 128-key one in a child
+    process: the kernel choice is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, tests.test_attn_gpu as t\n"
+        "from gen.attn import _io\n"
+        "from paper_2505_14969_b200 import binding\n"
+        "binding.lib()\n"
+        "for seed, (T, L) in enumerate([(64, 700), (33, 130), (200, 90)]):\n"
+        "    p = t.make_case(2, T, 32, 8, 128, 1280, 'bf16', 80 + seed, cache_len=[L, L // 2])\n"
+        "    kc = p.as_f32('k_cache').copy()\n"
+        "    for b in range(2):\n"
+        "        hot = slice(int(p.cache_len[b]) // 2, int(p.cache_len[b]))\n"
+        "        kc[b, hot] *= 16.0                    # later prefix keys: scores x16\n"
+        "    p.k_cache = _io(kc, 'bf16')\n"
+        "    o, st = t.run_gpu(p)\n"
+        "    ref, _ = t.run_oracle(p)\n"
+        "    assert st == 0 and np.isfinite(o).all()\n"
+        "    t.check(o, ref, t.TOL_BF16)\n"
+        "print('ok')\n")
+    env = dict(os.environ, STREE_ATTN_DB=kernel_env)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
