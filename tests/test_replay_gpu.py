@@ -156,3 +156,21 @@ def test_replay_equals_separate_commit_then_scan():
     ys = api.tree_scan(tn).float().cpu().numpy()
     assert_h_close(hf, hs.cpu().numpy(), 1e-5)
     assert_y_close(yf, ys, 1e-2)
+
+
+def test_replay_kernel_selection_boundaries():
+    """Around the small-batch kernel's grid limits (one head per CTA: B·H <= #SMs; one CTA per SM when
+    2·B·H <= #SMs, two per SM above): the fused call at B·H = #SMs/2, #SMs/2 + 2, #SMs and #SMs + 2 (the last
+    one on the pipeline kernel), each against the oracle."""
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    for units, expect in ((nsm // 2, 4), (nsm // 2 + 2, 4), (nsm, 4), (nsm + 2, 2)):
+        B = 2
+        H = units // B
+        prev, new, path, plen = make_pair(B, 40, 48, H, 64, 128, 1, "bf16", seed=units)
+        d = binding.stree_dims(B, 48, H, 64, 128, 1, 1)
+        assert binding.stree_scan_kernel_for(d) == expect, (units, expect)
+        y, h, st = run_fused(prev, new, path, plen)
+        yr, hr, hst, yst = oracle_pair(prev, new, path, plen)
+        assert st == 0 and not hst.any() and not yst.any()
+        assert_h_close(h, hr, TOL_F32)
+        assert_y_close(y, yr, TOL_BF16)
