@@ -1,5 +1,6 @@
-"""Timeline of CTA 0 of the tcgen05 tree-attention kernel (globaltimer stamps; debug hook
-stree_debug_attn_trace).  Prints per-KV-tile event times relative to the first stamp (us)."""
+"""Timeline of CTA 0 of the 128-key tcgen05 tree-attention kernel K7 (globaltimer stamps; debug hook
+stree_debug_attn_trace).  Prints per-KV-tile event times relative to the first stamp (us).  The default kernel
+is K7b (attn_db_kernel), which has no trace hook: run with STREE_ATTN_DB=0."""
 import ctypes
 import os
 import sys
