@@ -16,7 +16,8 @@ import torch  # noqa: E402
 from gen import inputs  # noqa: E402
 from paper_2505_14969_b200 import api, binding  # noqa: E402
 
-binding.stree_set_launch_flags(31)
+binding.stree_set_launch_flags(int(os.environ.get("FLAGS", "31")))
+FUSED = os.environ.get("FUSED", "1") == "1"   # 0: stree_tree_scan only
 base = inputs.config_problem("c3")
 tok, vt = inputs.make_accept_inputs(base.parent, seed=3, p_match=0.9)
 L = 64
@@ -30,7 +31,10 @@ for H in [int(x) for x in os.environ.get("HEADS", "8,24,40,64,74,80,96,128").spl
 
     def run():
         for t, y in zip(lay, ys):
-            api.replay_scan(t, path, plen, t, t["h0"], y=y)
+            if FUSED:
+                api.replay_scan(t, path, plen, t, t["h0"], y=y)
+            else:
+                api.tree_scan(t, y=y)
 
     with torch.cuda.stream(s):
         run()
