@@ -1,5 +1,5 @@
 mkdir -p gpurun_out/attn
-timeout 600 python -m pytest tests/test_attn_gpu.py -x -q > gpurun_out/attn/pytest.log 2>&1; tail -3 gpurun_out/attn/pytest.log
+timeout 240 python -m pytest tests/test_attn_gpu.py -x -q > gpurun_out/attn/pytest.log 2>&1; tail -3 gpurun_out/attn/pytest.log
 for db in 1 0; do STREE_ATTN_DB=$db timeout 300 python -c "
 import sys, json, torch; sys.path.insert(0,'.')
 import bench_next
