@@ -569,22 +569,55 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
     import torch.distributed as dist
     from paper_2505_14969_b200 import binding
 
-    host = []
+    # each layer's inputs (x, dt, B, C) live in ONE pinned host block and ONE device block (256-byte aligned views),
+    # so a layer is one host->device copy (many small copies cost more per byte on PCIe than one large one)
+    keys = ("x", "dt", "Bm", "Cm")
+
+    def layout(t):
+        offs, o = {}, 0
+        for k in keys:
+            offs[k] = o
+            o += -(-t[k].numel() * t[k].element_size() // 256) * 256
+        return offs, o
+
+    def views(block, t, offs):
+        return {k: block[offs[k]:offs[k] + t[k].numel() * t[k].element_size()].view(t[k].dtype).view(t[k].shape)
+                for k in keys}
+
+    host, hblk, dblk = [], [], [[]]
     for t in layers:
-        host.append({k: t[k].cpu().pin_memory() for k in ("x", "dt", "Bm", "Cm")})
+        offs, nbytes = layout(t)
+        hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        hv = views(hb, t, offs)
+        for k in keys:
+            hv[k].copy_(t[k].cpu())
+        host.append(hv)
+        hblk.append(hb)
+        db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        dv = views(db, t, offs)
+        for k in keys:
+            dv[k].copy_(t[k])
+        dblk[0].append((db, dv))
     # the verified tree's x, dt, B are the cache the next step's replay reads, so the
     # fused loop double-buffers them: step k uploads into set k % 2 and replays from set (k - 1) % 2
-    bufs = [[{k: t[k] for k in ("x", "dt", "Bm", "Cm")} for t in layers]]
+    bufs = [[dv for _, dv in dblk[0]]]
     if fused:
-        bufs.append([{k: (t[k].clone() if k != "Cm" else t[k]) for k in ("x", "dt", "Bm", "Cm")} for t in layers])
+        dblk.append([])
+        for t in layers:
+            offs, nbytes = layout(t)
+            db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            dv = views(db, t, offs)
+            for k in keys:
+                dv[k].copy_(t[k])
+            dblk[1].append((db, dv))
+        bufs.append([dv for _, dv in dblk[1]])
     it = [0]
     hp = parent.cpu().pin_memory()
     htok, hvt = tok_d.cpu().pin_memory(), vt_d.cpu().pin_memory()
     out = [torch.empty(path.shape, dtype=torch.int32).pin_memory(),
            torch.empty(plen.shape, dtype=torch.int32).pin_memory(),
            torch.empty(bonus.shape, dtype=torch.int32).pin_memory()]
-    h2d = sum(v.numel() * v.element_size() for hh in host for v in hh.values()) + \
-        (hp.numel() + htok.numel() + hvt.numel()) * 4
+    h2d = sum(hb.numel() for hb in hblk) + (hp.numel() + htok.numel() + hvt.numel()) * 4   # incl. alignment padding
     d2h = sum(o.numel() * 4 for o in out)
 
     # host->device copies run on their own stream, layer by layer, so layer l's kernel overlaps the copy
@@ -602,9 +635,9 @@ def run_e2e(args, layers, parent, tok_d, vt_d, path, plen, bonus, status, dims, 
             tok_d.copy_(htok, non_blocking=True)
             vt_d.copy_(hvt, non_blocking=True)
             evs[-1].record(cstream)
-            for c, hh, ev in zip(cur, host, evs):
-                for k, v in hh.items():
-                    c[k].copy_(v, non_blocking=True)
+            cb = dblk[(it[0] - 1) % len(dblk)]
+            for (db, _), hb, ev in zip(cb, hblk, evs):
+                db.copy_(hb, non_blocking=True)   # the layer's x, dt, B, C in one transfer
                 ev.record(cstream)
         with torch.cuda.stream(stream):
             stream.wait_event(evs[-1])
